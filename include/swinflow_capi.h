@@ -1,0 +1,143 @@
+/* swinflow_capi.h -- C-ABI of the B200-native swinflow denoiser hot path.
+ *
+ * Drop-in boundary for the reference's header-only C++ API (arxiv 2509.13523 / AERIS,
+ * /root/reference/proj/include/swinflow). Each entry point cites the reference interface it
+ * replaces. Plain pointers and sizes only; no torch / Eigen types cross this boundary.
+ *
+ * Data layout (identical to the reference's Eigen column-major storage):
+ *   a C x N field (C channels, N = H*W pixels, pixel index y*W + x) is N*C contiguous values
+ *   with the C channels of one pixel adjacent ("[N][C]"); a weight W (out x in) is in*out
+ *   values, column k (input k) contiguous ("[in][out]").
+ *
+ * Errors: every int-returning call returns SWF_OK (0) or a code below; swf_last_error() gives a
+ * thread-local message. Codes mirror the reference CLI exit codes (swinflow_main.cpp:705-718):
+ *   SWF_ERR_NUMERICS (1) <- NumericsError  (non-finite activation / solver divergence)
+ *   SWF_ERR_CONFIG   (2) <- ConfigError    (shape / divisibility / channel mismatch)
+ *   SWF_ERR_IO       (3) <- IoError
+ *   SWF_ERR_CUDA     (4)    device / driver failure (no CPU fallback exists)
+ *
+ * Threading: one stream and one workspace per context; a context must not be used from two
+ * threads at once (use one context per thread, as reference_train_step_mt's pool would).
+ */
+#ifndef SWINFLOW_CAPI_H
+#define SWINFLOW_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWF_OK 0
+#define SWF_ERR_NUMERICS 1
+#define SWF_ERR_CONFIG 2
+#define SWF_ERR_IO 3
+#define SWF_ERR_CUDA 4
+
+/* precision of the device path */
+#define SWF_PREC_BF16 0 /* BF16 tensor-core operands, FP32 accumulate + FP32 residual stream */
+#define SWF_PREC_FP32 1 /* FP32 validation mode (SIMT FP32 on the GPU; <= 1e-4 vs the oracle) */
+
+/* host buffer element types */
+#define SWF_F32 0
+#define SWF_F64 1
+
+/* ownership of windows across ranks (SWiPe window parallelism) */
+#define SWF_OWN_CONTIGUOUS 0 /* contiguous window blocks (performance default, least exchange) */
+#define SWF_OWN_ROUND_ROBIN 1 /* reference window_owner (topology.hpp:107-109) */
+
+/* swinflow::ModelConfig (model.hpp:21-62) */
+typedef struct swf_model_cfg {
+    int hidden_dim, n_heads, ffn_dim, n_layers, blocks_per_layer, window_px, in_channels, out_channels, time_dim;
+} swf_model_cfg;
+
+/* swinflow::DiffusionConfig (diffusion.hpp:29-46) with ChurnSchedule::amount */
+typedef struct swf_diffusion_cfg {
+    double sigma_d, sigma_min, sigma_max;
+    int solver_steps;
+    double churn;
+} swf_diffusion_cfg;
+
+/* Standardizer pairs (grid.hpp:85-133): mean/std arrays of the state (C_out), residual (C_out)
+ * and forcing (C_in - 2*C_out) channels, element type given by the call's dtype. */
+typedef struct swf_standardizers {
+    const void *state_mean, *state_std, *resid_mean, *resid_std, *forcing_mean, *forcing_std;
+} swf_standardizers;
+
+typedef struct swf_ctx swf_ctx;
+
+const char* swf_last_error(void);
+const char* swf_version(void);
+
+/* Create a context for a model on an H x W grid on CUDA device `device`.
+ * Replaces ModelConfig::validate_grid (model.hpp:48-52) + the implicit state of forward(). */
+int swf_create(const swf_model_cfg* cfg, int grid_h, int grid_w, int device, int precision, swf_ctx** out);
+void swf_destroy(swf_ctx* ctx);
+
+/* Window-parallel topology (topology.hpp:74-132): this context is rank `rank` of a wp_a x wp_b
+ * window-parallel grid (sp must be 1 in this build). peer_handles: wp_a*wp_b cudaIpcMemHandle_t
+ * blobs (64 B each) of every rank's residual buffers, from swf_ipc_handles(); may be NULL when
+ * world == 1. Must be called before swf_load_params. */
+int swf_set_topology(swf_ctx* ctx, int wp_a, int wp_b, int sp, int rank, int ownership);
+/* Export this rank's residual-buffer IPC handles (2 x 64 bytes) / import all ranks' handles. */
+int swf_ipc_handles(swf_ctx* ctx, void* out128);
+int swf_connect_peers(swf_ctx* ctx, const void* all_handles /* world x 128 bytes */);
+
+/* Parameters in canonical parameter_arrays order (model.hpp:140-168), each array Eigen
+ * column-major, element type dtype. Replaces Parameters<T> / load_params. */
+int swf_load_params(swf_ctx* ctx, const void* const* arrays, int n_arrays, int dtype);
+int swf_load_params_flat(swf_ctx* ctx, const void* flat, long long count, int dtype);
+long long swf_param_count(const swf_model_cfg* cfg); /* parameter_count_formula (model.hpp:118-129) */
+/* init_parameters (model.hpp:185-209) generated on the device with the reference counter RNG:
+ * mode 0 = init_parameters(seed); 1 = init_parameters_random(seed, scale) (model.hpp:213-223);
+ * 2 = init_parameters(seed) + scale*N(0,1) added only to the arrays it leaves at zero except the
+ * encode/time biases (ada.w, ada.b, decode.w, decode.b) -- synthetic benchmark weights with live
+ * AdaLN and decode paths. */
+int swf_init_params(swf_ctx* ctx, uint64_t seed, int mode, double scale);
+
+/* forward(p, input, t, H, W) (swin.hpp:327-368): input C_in x N, output C_out x N, host memory.
+ * Under a multi-rank topology each rank writes only the pixels it owns (see swf_owned_pixels). */
+int swf_forward(swf_ctx* ctx, const void* input, double t, void* output, int dtype);
+/* Same, on device pointers (fp32, [N][C]) on the context stream, without synchronising;
+ * numerics flags are checked by swf_sync(). */
+int swf_forward_device(swf_ctx* ctx, const float* d_input, double t, float* d_output);
+int swf_sync(swf_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) for callers that enqueue their own copies. */
+void* swf_stream(swf_ctx* ctx);
+
+/* solve_pf_ode(net, x_init, dc, churn_key) (diffusion.hpp:207-272) with net = the denoiser
+ * conditioned on standardized x_prev (C_out x N) and forcings ((C_in-2C_out) x N), as in the
+ * forecast_step net lambda (diffusion.hpp:304-311). Host buffers. f_evals may be NULL. */
+int swf_solve_pf_ode(swf_ctx* ctx, const void* x_init, const void* x_prev_std, const void* forcings_std,
+                     const swf_diffusion_cfg* dc, uint64_t churn_key, void* x_out, int* f_evals, int dtype);
+/* forecast_step (diffusion.hpp:295-319): standardize, window-keyed noise z_init, solve, invert
+ * the residual standardization and add to x_prev_phys. Host buffers. */
+int swf_forecast_step(swf_ctx* ctx, const void* x_prev_phys, const void* forcing_phys,
+                      const swf_standardizers* stds, const swf_diffusion_cfg* dc, uint64_t run_seed,
+                      uint64_t noise_event, void* out, int dtype);
+/* rollout_ensemble (diffusion.hpp:323-339): members x steps, out is members*steps fields
+ * (member-major), forcings is steps fields. */
+int swf_rollout_ensemble(swf_ctx* ctx, const void* x_init_phys, const void* forcings_phys, int n_members,
+                         int n_steps, const swf_standardizers* stds, const swf_diffusion_cfg* dc,
+                         uint64_t run_seed, uint64_t rollout_id, void* out, int dtype);
+
+/* Diagnostics: local token count, owned-pixel list (pixel index per local token, window order of
+ * the unshifted layout), and the number of kernels launched by the last forward. */
+long long swf_local_tokens(swf_ctx* ctx);
+int swf_owned_pixels(swf_ctx* ctx, long long* pixels);
+long long swf_kernel_launches(swf_ctx* ctx);
+/* Per-kernel-class device time from CUDA events recorded on the context stream around each
+ * launch while enabled. Classes: 0 encode GEMM, 1 RMS+AdaLN, 2 QKV GEMM, 3 attention, 4 out GEMM,
+ * 5 gate/up GEMM, 6 down GEMM, 7 decode GEMM, 8 other. swf_profile resets the counters. */
+int swf_profile(swf_ctx* ctx, int enable);
+int swf_profile_read(swf_ctx* ctx, double* ms, long long* launches, int n_classes);
+/* Noise field (diffusion.hpp:91-108) for (run_seed, event) into a host C x N buffer (fp32). */
+int swf_noise_field(swf_ctx* ctx, uint64_t run_seed, uint64_t event, int channels, double sigma_d, float* out);
+/* Run one bf16 GEMM self-test of the tcgen05 kernel: C = A.B^T on device, returns max |err|
+ * against an fp32 SIMT product of the same bf16 operands (used by the parity tests). */
+int swf_selftest_gemm(int device, long long M, int N, int K, double* max_abs_err, double* max_ref);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWINFLOW_CAPI_H */

@@ -108,6 +108,9 @@ def lib():
                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                  u64, u64, C.c_void_p, C.c_void_p]
         L.orc_forecast_step_f64.argtypes = fargs
+        L.orc_solve_net_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_int,
+                                        C.c_double, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, u64,
+                                        C.c_void_p, C.c_void_p]
         L.orc_forecast_step_f32.argtypes = fargs
     return _lib
 
@@ -319,6 +322,17 @@ def forecast_step(cfg: ModelConfig, params, H, W, x_prev, forc, run_seed, event,
     args = [np.ascontiguousarray(a, dt) for a in (*st, *rs, *fo)]
     _check(fn(C.byref(_c(cfg)), _p(params), sigma_d, sigma_min, sigma_max, steps, churn, H, W, _p(x_prev),
               _p(forc), *[_p(a) for a in args], run_seed, event, _p(out), C.byref(fe)))
+    return out, fe.value
+
+
+def solve_net(cfg: ModelConfig, params, H, W, x_init, x_prev_std, forc_std, sigma_d=1.0, sigma_min=0.2,
+              sigma_max=500.0, steps=10, churn=0.0, churn_key=0):
+    """solve_pf_ode with the forecast_step net lambda on given standardized conditioning (f64)."""
+    a = [np.ascontiguousarray(v, np.float64) for v in (x_init, x_prev_std, forc_std)]
+    out = np.empty_like(a[0])
+    fe = C.c_int(0)
+    _check(lib().orc_solve_net_f64(C.byref(_c(cfg)), _p(params), sigma_d, sigma_min, sigma_max, steps, churn, H, W,
+                                   _p(a[0]), _p(a[1]), _p(a[2]), churn_key, _p(out), C.byref(fe)))
     return out, fe.value
 
 

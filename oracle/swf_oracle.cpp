@@ -619,6 +619,34 @@ static void forecast_step(const Params<T>& p, const DCfg& dc, int H, int W, cons
         for (int i = 0; i < Cp; ++i) out[j * Cp + i] = x_prev_phys[j * Cp + i] + (r[j * Cp + i] * rs_std[i] + rs_mean[i]);
 }
 
+// solve_pf_ode with the forecast_step net lambda (diffusion.hpp:304-311) on given standardized
+// conditioning: used to check the device solver without the noise / standardisation steps.
+template <class T>
+static void solve_net(const Params<T>& p, const DCfg& dc, int H, int W, const T* x_init, const T* xp, const T* fo,
+                      u64 churn_key, T* out, int* f_evals) {
+    const Cfg& c = p.cfg;
+    const i64 N = i64(H) * W;
+    const int Cp = c.out_channels, Cin = c.in_channels, Cf = Cin - 2 * Cp;
+    std::vector<T> pe(size_t(N) * Cin);
+    posenc<T>(H, W, Cin, pe.data());
+    const T sdT = static_cast<T>(dc.sigma_d);
+    auto net = [&](const std::vector<T>& xs, T t) {
+        std::vector<T> in(size_t(N) * Cin), o(size_t(N) * Cp);
+        for (i64 j = 0; j < N; ++j) {
+            for (int i = 0; i < Cp; ++i) in[j * Cin + i] = xs[j * Cp + i] / sdT;
+            for (int i = 0; i < Cp; ++i) in[j * Cin + Cp + i] = xp[j * Cp + i];
+            for (int i = 0; i < Cf; ++i) in[j * Cin + 2 * Cp + i] = fo[j * Cf + i];
+            for (int i = 0; i < Cin; ++i) in[j * Cin + i] += pe[j * Cin + i];
+        }
+        forward<T>(p, in.data(), t, H, W, o.data());
+        for (auto& v : o) v = sdT * v;
+        return o;
+    };
+    std::vector<T> x0(x_init, x_init + N * Cp);
+    const auto r = solve_pf_ode<T>(net, x0, dc, churn_key, f_evals);
+    std::memcpy(out, r.data(), sizeof(T) * N * Cp);
+}
+
 // ---------------------------------------------------------------- topology.hpp:74-188
 static std::pair<int, int> window_owner(int wy, int wx, int a, int b) { return {wy % a, wx % b}; }
 
@@ -846,6 +874,15 @@ double orc_t_of_sigma(double sigma, double sigma_d) { return std::atan(sigma / s
     }
 ORC_FORECAST(double, f64)
 ORC_FORECAST(float, f32)
+
+int orc_solve_net_f64(const orc_cfg* c, const double* params, double sigma_d, double sigma_min, double sigma_max,
+                      int steps, double churn, int H, int W, const double* x_init, const double* xp,
+                      const double* fo, u64 churn_key, double* out, int* f_evals) {
+    ORC_TRY({
+        DCfg dc{sigma_d, sigma_min, sigma_max, steps, churn};
+        solve_net<double>(view<double>(to_cfg(c), params), dc, H, W, x_init, xp, fo, churn_key, out, f_evals);
+    })
+}
 
 // window_owner (topology.hpp:107-109)
 void orc_window_owner(int wy, int wx, int a, int b, int* oa, int* ob) {

@@ -1,0 +1,288 @@
+"""swinflow-b200: B200-native (sm_100a) denoiser hot path of arxiv 2509.13523 (AERIS).
+
+Thin ctypes mirror of the C-ABI in include/swinflow_capi.h, which itself mirrors the
+reference's C++ API (proj/include/swinflow/swin.hpp `forward`, diffusion.hpp `solve_pf_ode`,
+`forecast_step`, `rollout_ensemble`). There is no CPU fallback: if the CUDA library is missing
+or no B200 is visible, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, astuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "libswinflow_b200.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "swinflow_capi.h")
+
+OK, ERR_NUMERICS, ERR_CONFIG, ERR_IO, ERR_CUDA = 0, 1, 2, 3, 4
+PREC_BF16, PREC_FP32 = 0, 1
+F32, F64 = 0, 1
+OWN_CONTIGUOUS, OWN_ROUND_ROBIN = 0, 1
+
+
+class SwfError(RuntimeError):
+    def __init__(self, rc: int, msg: str):
+        super().__init__(f"[rc={rc}] {msg}")
+        self.rc = rc
+
+
+class ConfigError(SwfError):
+    pass
+
+
+class NumericsError(SwfError):
+    pass
+
+
+class CudaError(SwfError):
+    pass
+
+
+@dataclass
+class ModelConfig:
+    """swinflow::ModelConfig (model.hpp:21-62)."""
+    hidden_dim: int
+    n_heads: int
+    ffn_dim: int
+    n_layers: int
+    blocks_per_layer: int = 1
+    window_px: int = 8
+    in_channels: int = 8
+    out_channels: int = 3
+    time_dim: int = 0
+
+    def n_blocks(self) -> int:
+        return self.n_layers * self.blocks_per_layer
+
+
+@dataclass
+class DiffusionConfig:
+    """swinflow::DiffusionConfig (diffusion.hpp:29-46)."""
+    sigma_d: float = 1.0
+    sigma_min: float = 0.2
+    sigma_max: float = 500.0
+    solver_steps: int = 10
+    churn: float = 0.0
+
+
+class _Cfg(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("hidden_dim", "n_heads", "ffn_dim", "n_layers", "blocks_per_layer",
+                                        "window_px", "in_channels", "out_channels", "time_dim")]
+
+
+class _DCfg(C.Structure):
+    _fields_ = [("sigma_d", C.c_double), ("sigma_min", C.c_double), ("sigma_max", C.c_double),
+                ("solver_steps", C.c_int), ("churn", C.c_double)]
+
+
+class _Std(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("state_mean", "state_std", "resid_mean", "resid_std", "forcing_mean",
+                                          "forcing_std")]
+
+
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-j8", "-C", _HERE], check=True)
+    return LIB_PATH
+
+
+def lib():
+    """Load the sm_100a library (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"swinflow CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp, i, d, u64, ll = C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_longlong
+        L.swf_last_error.restype = C.c_char_p
+        L.swf_version.restype = C.c_char_p
+        L.swf_create.argtypes = [vp, i, i, i, i, C.POINTER(vp)]
+        L.swf_destroy.argtypes = [vp]
+        L.swf_destroy.restype = None
+        L.swf_set_topology.argtypes = [vp, i, i, i, i, i]
+        L.swf_ipc_handles.argtypes = [vp, vp]
+        L.swf_connect_peers.argtypes = [vp, vp]
+        L.swf_load_params.argtypes = [vp, vp, i, i]
+        L.swf_load_params_flat.argtypes = [vp, vp, ll, i]
+        L.swf_init_params.argtypes = [vp, u64, i, d]
+        L.swf_param_count.argtypes = [vp]
+        L.swf_param_count.restype = ll
+        L.swf_forward.argtypes = [vp, vp, d, vp, i]
+        L.swf_forward_device.argtypes = [vp, vp, d, vp]
+        L.swf_sync.argtypes = [vp]
+        L.swf_stream.argtypes = [vp]
+        L.swf_stream.restype = vp
+        L.swf_solve_pf_ode.argtypes = [vp, vp, vp, vp, vp, u64, vp, C.POINTER(i), i]
+        L.swf_forecast_step.argtypes = [vp, vp, vp, vp, vp, u64, u64, vp, i]
+        L.swf_rollout_ensemble.argtypes = [vp, vp, vp, i, i, vp, vp, u64, u64, vp, i]
+        L.swf_local_tokens.argtypes = [vp]
+        L.swf_local_tokens.restype = ll
+        L.swf_owned_pixels.argtypes = [vp, vp]
+        L.swf_kernel_launches.argtypes = [vp]
+        L.swf_kernel_launches.restype = ll
+        L.swf_profile.argtypes = [vp, i]
+        L.swf_profile_read.argtypes = [vp, vp, vp, i]
+        L.swf_noise_field.argtypes = [vp, u64, u64, i, d, vp]
+        L.swf_selftest_gemm.argtypes = [i, ll, i, i, C.POINTER(d), C.POINTER(d)]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc == OK:
+        return
+    msg = lib().swf_last_error().decode()
+    cls = {ERR_NUMERICS: NumericsError, ERR_CONFIG: ConfigError, ERR_CUDA: CudaError}.get(rc, SwfError)
+    raise cls(rc, msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _dt(a: np.ndarray) -> int:
+    if a.dtype == np.float64:
+        return F64
+    if a.dtype == np.float32:
+        return F32
+    raise TypeError("fields must be float32 or float64")
+
+
+def param_count(cfg: ModelConfig) -> int:
+    return lib().swf_param_count(C.byref(_Cfg(*astuple(cfg))))
+
+
+def selftest_gemm(M: int, N: int, K: int, device: int = 0):
+    e, r = C.c_double(), C.c_double()
+    _check(lib().swf_selftest_gemm(device, M, N, K, C.byref(e), C.byref(r)))
+    return e.value, r.value
+
+
+class Denoiser:
+    """Device context for one model on one H x W grid (forward / solve / forecast)."""
+
+    def __init__(self, cfg: ModelConfig, grid_h: int, grid_w: int, device: int = 0, precision: int = PREC_BF16,
+                 topology: tuple | None = None):
+        self.cfg, self.H, self.W, self.precision = cfg, grid_h, grid_w, precision
+        self._c = C.c_void_p()
+        _check(lib().swf_create(C.byref(_Cfg(*astuple(cfg))), grid_h, grid_w, device, precision,
+                                C.byref(self._c)))
+        if topology is not None:
+            wp_a, wp_b, sp, rank, own = topology
+            _check(lib().swf_set_topology(self._c, wp_a, wp_b, sp, rank, own))
+
+    def close(self):
+        if self._c:
+            lib().swf_destroy(self._c)
+            self._c = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- parameters (model.hpp:140-168 canonical order, col-major)
+    def load_params(self, flat: np.ndarray):
+        flat = np.ascontiguousarray(flat)
+        _check(lib().swf_load_params_flat(self._c, _p(flat), flat.size, _dt(flat)))
+
+    def init_params(self, seed: int, mode: int = 0, scale: float = 0.25):
+        """init_parameters (mode 0) / init_parameters_random (mode 1) / bench weights (mode 2),
+        generated on the device with the reference counter RNG (model.hpp:185-223)."""
+        _check(lib().swf_init_params(self._c, seed, mode, scale))
+
+    # ---- forward (swin.hpp:327-368)
+    def forward(self, inp: np.ndarray, t: float) -> np.ndarray:
+        inp = np.ascontiguousarray(inp)
+        out = np.zeros((self.H * self.W, self.cfg.out_channels), inp.dtype)
+        _check(lib().swf_forward(self._c, _p(inp), float(t), _p(out), _dt(inp)))
+        return out
+
+    def forward_device(self, d_in: int, t: float, d_out: int):
+        _check(lib().swf_forward_device(self._c, C.c_void_p(d_in), float(t), C.c_void_p(d_out)))
+
+    def sync(self):
+        _check(lib().swf_sync(self._c))
+
+    @property
+    def stream(self) -> int:
+        return lib().swf_stream(self._c) or 0
+
+    def local_tokens(self) -> int:
+        n = lib().swf_local_tokens(self._c)
+        if n < 0:
+            _check(ERR_CUDA)
+        return n
+
+    KERNEL_CLASSES = ("encode_gemm", "rms_adaln", "qkv_gemm", "attention", "out_gemm", "gateup_gemm",
+                      "down_gemm", "decode_gemm", "other")
+
+    def profile(self, enable: bool = True):
+        _check(lib().swf_profile(self._c, int(enable)))
+
+    def profile_read(self) -> dict:
+        n = len(self.KERNEL_CLASSES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_longlong * n)()
+        _check(lib().swf_profile_read(self._c, ms, cnt, n))
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(self.KERNEL_CLASSES)}
+
+    def kernel_launches(self) -> int:
+        return lib().swf_kernel_launches(self._c)
+
+    # ---- sampler (diffusion.hpp:207-339)
+    def solve_pf_ode(self, x_init, x_prev_std, forcings_std, dc: DiffusionConfig, churn_key: int = 0):
+        x_init = np.ascontiguousarray(x_init)
+        dt = x_init.dtype
+        out = np.zeros_like(x_init)
+        fe = C.c_int(0)
+        f = None if forcings_std is None else np.ascontiguousarray(forcings_std, dt)
+        _check(lib().swf_solve_pf_ode(self._c, _p(x_init), _p(np.ascontiguousarray(x_prev_std, dt)), _p(f),
+                                      C.byref(_DCfg(*astuple(dc))), churn_key, _p(out), C.byref(fe), _dt(x_init)))
+        return out, fe.value
+
+    def _stds(self, stds, dt):
+        if stds is None:
+            return None, []
+        keep = [None if a is None else np.ascontiguousarray(a, dt) for a in stds]
+        return _Std(*[None if a is None else a.ctypes.data for a in keep]), keep
+
+    def forecast_step(self, x_prev_phys, forcing_phys, dc: DiffusionConfig, run_seed: int, event: int, stds=None):
+        x_prev_phys = np.ascontiguousarray(x_prev_phys)
+        dt = x_prev_phys.dtype
+        st, keep = self._stds(stds, dt)
+        out = np.zeros_like(x_prev_phys)
+        f = None if forcing_phys is None else np.ascontiguousarray(forcing_phys, dt)
+        _check(lib().swf_forecast_step(self._c, _p(x_prev_phys), _p(f), None if st is None else C.byref(st),
+                                       C.byref(_DCfg(*astuple(dc))), run_seed, event, _p(out), _dt(x_prev_phys)))
+        return out
+
+    def rollout_ensemble(self, x_init_phys, forcings_phys, n_members, n_steps, dc, run_seed, rollout_id, stds=None):
+        x = np.ascontiguousarray(x_init_phys)
+        dt = x.dtype
+        st, keep = self._stds(stds, dt)
+        f = np.ascontiguousarray(np.stack(forcings_phys[:n_steps]), dt)
+        out = np.zeros((n_members, n_steps) + x.shape, dt)
+        _check(lib().swf_rollout_ensemble(self._c, _p(x), _p(f), n_members, n_steps,
+                                          None if st is None else C.byref(st), C.byref(_DCfg(*astuple(dc))),
+                                          run_seed, rollout_id, _p(out), _dt(x)))
+        return out
+
+    def noise_field(self, run_seed: int, event: int, channels: int, sigma_d: float = 1.0) -> np.ndarray:
+        out = np.zeros((self.H * self.W, channels), np.float32)
+        _check(lib().swf_noise_field(self._c, run_seed, event, channels, sigma_d, _p(out)))
+        return out
+
+
+def exported_symbols() -> list[str]:
+    """Function names declared in include/swinflow_capi.h."""
+    import re
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(swf_[a-z0-9_]+)\s*\(", src)))

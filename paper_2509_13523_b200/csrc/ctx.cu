@@ -1,0 +1,1357 @@
+// ctx.cu -- device context, weight repack, the denoiser forward orchestration and the device-
+// resident TrigFlow sampler, behind the C-ABI in include/swinflow_capi.h.
+//
+// Data flow of one forward (reference swin.hpp:327-368), all on one stream:
+//   gather(input, pixel -> window order of layout 0)            [HBM]
+//   encode GEMM (+bias) -> x (fp32 residual, window order)       [tensor]
+//   per block b (layout L_b = shift 0 / w/2, window.hpp:83-85):
+//     rms+AdaLN(x) -> xm ; QKV GEMM (+RoPE, head-major scatter) ; attention -> O ;
+//     out GEMM (x += W_out O) ; rms+AdaLN(x) -> xm ; gate/up GEMM (+SiLU*up) -> s ;
+//     down GEMM (x' = x + W_down s) stored directly in the window order of L_{b+1}
+//       -- the window gather/scatter of swin.hpp:356-358 becomes the down-projection's
+//          store address, so no standalone permutation pass exists.
+//   rms(x) -> xm ; decode GEMM (+bias) -> out (window order of layout 0) ; scatter to pixels
+#include <cuda.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/swinflow_capi.h"
+#include "kernels.cuh"
+
+namespace swf {
+
+struct ConfigError : std::runtime_error {
+    explicit ConfigError(const std::string& m) : std::runtime_error(m) {}
+};
+struct NumericsError : std::runtime_error {
+    explicit NumericsError(const std::string& m) : std::runtime_error(m) {}
+};
+static void require(bool c, const std::string& m) {
+    if (!c) throw ConfigError(m);
+}
+
+static inline i64 roundup(i64 a, i64 b) { return (a + b - 1) / b * b; }
+
+struct Dims {
+    int h, heads, d, f, nb, w, cin, cout, td;
+    int hp, fp, cinp;              // K dims padded to 64
+    int bn_enc, bn_qkv, bn_out, bn_gu, bn_down, bn_dec;
+    int np_enc, np_qkv, np_out, np_gu, np_down, np_dec;  // N dims padded
+    int G;                         // gate/up interleave granularity
+};
+
+struct Peer {
+    float* x[2];
+};
+
+}  // namespace swf
+
+using namespace swf;
+
+struct swf_ctx {
+    swf_model_cfg cfg;
+    Dims m;
+    int H = 0, W = 0;
+    i64 N = 0;
+    int prec = SWF_PREC_BF16;
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    // topology
+    int wp_a = 1, wp_b = 1, sp = 1, rank = 0, world = 1, own = SWF_OWN_CONTIGUOUS;
+    i64 M = 0;  // local tokens
+    std::vector<int> l2g[2];
+    int* d_l2g[2] = {nullptr, nullptr};
+    int* d_g2rl[2] = {nullptr, nullptr};
+    LayMap lay[2];
+    bool allocated = false, loaded = false, peers = false;
+    // small fp32 parameters
+    float *enc_b = nullptr, *g_attn = nullptr, *g_ffn = nullptr, *w_ada_t = nullptr, *b_ada = nullptr;
+    float *w_time_t = nullptr, *b_time = nullptr, *g_dec = nullptr, *b_dec = nullptr;
+    // GEMM weights [Npad][Kpad] (bf16 or fp32)
+    void *w_enc = nullptr, *w_dec = nullptr;
+    std::vector<void*> w_qkv, w_out, w_gu, w_down;
+    // activations
+    float* xbuf[2] = {nullptr, nullptr};
+    void *xm = nullptr, *qkv = nullptr, *sbuf = nullptr, *a_in = nullptr;
+    float* out_loc = nullptr;
+    float *rope_row = nullptr, *rope_col = nullptr, *feat = nullptr, *emb = nullptr, *six = nullptr;
+    int* flags = nullptr;
+    int* h_flags = nullptr;
+    float* h_feat = nullptr;
+    float *in_pix = nullptr, *out_pix = nullptr;
+    float** d_xdst[2] = {nullptr, nullptr};
+    std::vector<Peer> peer;
+    // TMA maps (BF16 path)
+    TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec;
+    std::vector<TmaMap> tm_qkv, tm_out, tm_gu, tm_down;
+    long long launches = 0;
+    // sampler workspace (allocated lazily)
+    float *pe_loc = nullptr, *s_x = nullptr, *s_xmid = nullptr, *s_tmp = nullptr, *s_base = nullptr;
+    float *s_cond = nullptr, *s_stats = nullptr;
+    std::vector<void*> allocs;
+    int nflags = 0;
+    // per-kernel-class CUDA-event timing (bench roofline): class id -> accumulated ms / launches
+    bool prof = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    double prof_ms[16] = {0};
+    long long prof_n[16] = {0};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class T>
+T* dalloc(swf_ctx* c, size_t n) {
+    void* p = nullptr;
+    SWF_CUDA(cudaMalloc(&p, n * sizeof(T) + 256));
+    SWF_CUDA(cudaMemset(p, 0, n * sizeof(T) + 256));
+    c->allocs.push_back(p);
+    return static_cast<T*>(p);
+}
+
+size_t esize(const swf_ctx* c) { return c->prec == SWF_PREC_BF16 ? 2 : 4; }
+
+void* talloc(swf_ctx* c, size_t n) {
+    return c->prec == SWF_PREC_BF16 ? static_cast<void*>(dalloc<__nv_bfloat16>(c, n))
+                                    : static_cast<void*>(dalloc<float>(c, n));
+}
+
+Dims make_dims(const swf_model_cfg& cf, int prec) {
+    Dims m;
+    m.h = cf.hidden_dim;
+    m.heads = cf.n_heads;
+    m.d = cf.hidden_dim / cf.n_heads;
+    m.f = cf.ffn_dim;
+    m.nb = cf.n_layers * cf.blocks_per_layer;
+    m.w = cf.window_px;
+    m.cin = cf.in_channels;
+    m.cout = cf.out_channels;
+    m.td = cf.time_dim > 0 ? cf.time_dim : cf.hidden_dim;
+    m.hp = int(roundup(m.h, 64));
+    m.fp = int(roundup(m.f, 64));
+    m.cinp = int(roundup(m.cin, 64));
+    auto bn = [&](int n) { return (prec == SWF_PREC_BF16 && n % 256 == 0) ? 256 : 128; };
+    m.bn_enc = bn(m.h);
+    m.bn_qkv = bn(3 * m.h);
+    m.bn_out = bn(m.h);
+    m.bn_down = bn(m.h);
+    m.bn_dec = 128;
+    m.np_enc = int(roundup(m.h, m.bn_enc));
+    m.np_qkv = int(roundup(3 * m.h, m.bn_qkv));
+    m.np_out = int(roundup(m.h, m.bn_out));
+    m.np_down = int(roundup(m.h, m.bn_down));
+    m.np_dec = int(roundup(m.cout, 128));
+    if (prec == SWF_PREC_BF16) {
+        m.bn_gu = (2 * m.f) % 256 == 0 ? 256 : 128;
+        m.G = m.bn_gu / 2;
+        m.np_gu = int(roundup(2 * m.f, m.bn_gu));
+    } else {
+        m.bn_gu = 128;
+        m.G = 4;
+        m.np_gu = int(roundup(2 * roundup(m.f, 4), 128));
+    }
+    return m;
+}
+
+void validate_model(const swf_model_cfg& c, int H, int W, int prec) {
+    require(c.hidden_dim > 0 && c.n_heads > 0 && c.ffn_dim > 0 && c.n_layers > 0, "model: dims must be positive");
+    require(c.blocks_per_layer >= 1, "model: blocks_per_layer must be >= 1");
+    require(c.hidden_dim % c.n_heads == 0, "model: hidden_dim must divide by n_heads");
+    require((c.hidden_dim / c.n_heads) % 4 == 0, "model: head_dim must be divisible by 4 (axial rotary pairs)");
+    require(c.in_channels > 0 && c.out_channels > 0, "model: channel counts must be positive");
+    require(c.in_channels % 2 == 0, "model: in_channels must be even (positional encoding split)");
+    require(c.window_px > 0, "model: window size must be positive");
+    require(H > 0 && W > 0 && H % c.window_px == 0 && W % c.window_px == 0, "model: grid not divisible by window size");
+    require(prec == SWF_PREC_BF16 || prec == SWF_PREC_FP32, "precision must be SWF_PREC_BF16 or SWF_PREC_FP32");
+    if (prec == SWF_PREC_BF16) {
+        const int d = c.hidden_dim / c.n_heads;
+        require(c.hidden_dim % 128 == 0 && c.ffn_dim % 128 == 0,
+                "BF16 path: hidden_dim and ffn_dim must be multiples of 128 (use SWF_PREC_FP32 otherwise)");
+        require(d == 32 || d == 64 || d == 128, "BF16 path: head_dim must be 32, 64 or 128");
+    }
+}
+
+// ------------------------------------------------------------------ weight repack
+// dst[row(o)][k] = src[k*out + o] (Eigen col-major W(out x in) -> K-major rows), optional
+// gate/up interleave: row(o) = (o/G)*2G + part*G + o%G.
+template <class T>
+__global__ void k_repack(const float* __restrict__ src, int out, int in, T* __restrict__ dst, int ld, int G,
+                         int part) {
+    const i64 total = i64(out) * in;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const int o = int(e / in);
+        const int k = int(e - i64(o) * in);
+        const int row = G > 0 ? (o / G) * 2 * G + part * G + (o % G) : o;
+        const float v = src[i64(k) * out + o];
+        if constexpr (sizeof(T) == 2)
+            dst[i64(row) * ld + k] = __float2bfloat16_rn(v);
+        else
+            dst[i64(row) * ld + k] = v;
+    }
+}
+
+void repack(swf_ctx* c, const float* d_src, int out, int in, void* dst, int ld, int G, int part, bool force_f32) {
+    const i64 total = i64(out) * in;
+    int grid = int(std::min<i64>((total + 255) / 256, 148 * 32));
+    if (c->prec == SWF_PREC_BF16 && !force_f32)
+        k_repack<__nv_bfloat16><<<grid, 256, 0, c->st>>>(d_src, out, in, static_cast<__nv_bfloat16*>(dst), ld, G, part);
+    else
+        k_repack<float><<<grid, 256, 0, c->st>>>(d_src, out, in, static_cast<float*>(dst), ld, G, part);
+    SWF_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ topology / layouts
+void build_layouts(swf_ctx* c) {
+    const Dims& m = c->m;
+    const int ny = c->H / m.w, nx = c->W / m.w, nwin = ny * nx;
+    require(ny % c->wp_a == 0, "topology: window rows " + std::to_string(ny) + " not divisible by WP grid A=" +
+                                   std::to_string(c->wp_a));
+    require(nx % c->wp_b == 0, "topology: window cols " + std::to_string(nx) + " not divisible by WP grid B=" +
+                                   std::to_string(c->wp_b));
+    const int ra = c->rank / c->wp_b, rb = c->rank % c->wp_b;
+    std::vector<int> g2rl(nwin);
+    for (int par = 0; par < 2; ++par) {
+        c->l2g[par].clear();
+        std::vector<int> cnt(c->world, 0);
+        for (int wy = 0; wy < ny; ++wy)
+            for (int wx = 0; wx < nx; ++wx) {
+                int oa, ob;
+                if (c->own == SWF_OWN_ROUND_ROBIN) {  // window_owner, topology.hpp:107-109
+                    oa = wy % c->wp_a;
+                    ob = wx % c->wp_b;
+                } else {  // contiguous window blocks
+                    oa = wy / (ny / c->wp_a);
+                    ob = wx / (nx / c->wp_b);
+                }
+                const int r = oa * c->wp_b + ob;
+                const int gw = wy * nx + wx;
+                g2rl[gw] = (r << 16) | cnt[r]++;
+                if (r == c->rank) c->l2g[par].push_back(gw);
+            }
+        (void)ra;
+        (void)rb;
+        if (!c->d_l2g[par]) {
+            c->d_l2g[par] = dalloc<int>(c, nwin);
+            c->d_g2rl[par] = dalloc<int>(c, nwin);
+        }
+        SWF_CUDA(cudaMemcpy(c->d_l2g[par], c->l2g[par].data(), sizeof(int) * c->l2g[par].size(), cudaMemcpyHostToDevice));
+        SWF_CUDA(cudaMemcpy(c->d_g2rl[par], g2rl.data(), sizeof(int) * nwin, cudaMemcpyHostToDevice));
+        LayMap& L = c->lay[par];
+        L.g = make_lay(c->H, c->W, m.w, par == 0 ? 0 : m.w / 2);
+        L.nloc = int(c->l2g[par].size());
+        L.loc2glob = c->d_l2g[par];
+        L.glob2rl = c->d_g2rl[par];
+    }
+    c->M = i64(c->lay[0].nloc) * m.w * m.w;
+}
+
+// RoPE cos/sin tables: angle = T(pos * omega_j) in double then cast (rope.hpp:19-31), trig in
+// float (rope.hpp:38) -- identical to the reference's float instantiation.
+void build_rope(swf_ctx* c) {
+    const Dims& m = c->m;
+    const int q4 = m.d / 4;
+    auto table = [&](int npos) {
+        std::vector<float> t(size_t(npos) * q4 * 2);
+        for (int pos = 0; pos < npos; ++pos)
+            for (int j = 0; j < q4; ++j) {
+                const double om = std::pow(10000.0, -double(j) / q4);
+                const float a = static_cast<float>(pos * om);
+                t[(size_t(pos) * q4 + j) * 2] = std::cos(a);
+                t[(size_t(pos) * q4 + j) * 2 + 1] = std::sin(a);
+            }
+        return t;
+    };
+    const auto tr = table(c->H + m.w), tc = table(c->W + m.w);
+    c->rope_row = dalloc<float>(c, tr.size());
+    c->rope_col = dalloc<float>(c, tc.size());
+    SWF_CUDA(cudaMemcpy(c->rope_row, tr.data(), tr.size() * 4, cudaMemcpyHostToDevice));
+    SWF_CUDA(cudaMemcpy(c->rope_col, tc.data(), tc.size() * 4, cudaMemcpyHostToDevice));
+}
+
+void allocate(swf_ctx* c) {
+    if (c->allocated) return;
+    const Dims& m = c->m;
+    build_layouts(c);
+    build_rope(c);
+    const i64 M = c->M;
+    c->xbuf[0] = dalloc<float>(c, size_t(M) * m.h);
+    c->xbuf[1] = dalloc<float>(c, size_t(M) * m.h);
+    c->xm = talloc(c, size_t(M) * m.hp);
+    c->qkv = talloc(c, size_t(3) * M * m.h);
+    c->sbuf = talloc(c, size_t(M) * m.fp);
+    c->a_in = talloc(c, size_t(M) * m.cinp);
+    c->out_loc = dalloc<float>(c, size_t(M) * m.cout);
+    c->feat = dalloc<float>(c, m.td);
+    c->emb = dalloc<float>(c, m.td);
+    c->six = dalloc<float>(c, size_t(m.nb) * 6 * m.h);
+    c->nflags = m.nb + 2 + 4096;
+    c->flags = dalloc<int>(c, c->nflags);
+    SWF_CUDA(cudaMallocHost(&c->h_flags, sizeof(int) * c->nflags));
+    SWF_CUDA(cudaMallocHost(&c->h_feat, sizeof(float) * m.td));
+    c->in_pix = dalloc<float>(c, size_t(c->N) * m.cin);
+    c->out_pix = dalloc<float>(c, size_t(c->N) * m.cout);
+    // weights
+    c->enc_b = dalloc<float>(c, m.h);
+    c->g_attn = dalloc<float>(c, size_t(m.nb) * m.h);
+    c->g_ffn = dalloc<float>(c, size_t(m.nb) * m.h);
+    c->w_ada_t = dalloc<float>(c, size_t(m.nb) * 6 * m.h * m.td);
+    c->b_ada = dalloc<float>(c, size_t(m.nb) * 6 * m.h);
+    c->w_time_t = dalloc<float>(c, size_t(m.td) * m.td);
+    c->b_time = dalloc<float>(c, m.td);
+    c->g_dec = dalloc<float>(c, m.h);
+    c->b_dec = dalloc<float>(c, m.np_dec);
+    c->w_enc = talloc(c, size_t(m.np_enc) * m.cinp);
+    c->w_dec = talloc(c, size_t(m.np_dec) * m.hp);
+    for (int b = 0; b < m.nb; ++b) {
+        c->w_qkv.push_back(talloc(c, size_t(m.np_qkv) * m.hp));
+        c->w_out.push_back(talloc(c, size_t(m.np_out) * m.hp));
+        c->w_gu.push_back(talloc(c, size_t(m.np_gu) * m.hp));
+        c->w_down.push_back(talloc(c, size_t(m.np_down) * m.fp));
+    }
+    // destination tables for the fused down-projection store (own buffer unless peers connect)
+    c->peer.assign(c->world, Peer{{nullptr, nullptr}});
+    c->peer[c->rank].x[0] = c->xbuf[0];
+    c->peer[c->rank].x[1] = c->xbuf[1];
+    for (int par = 0; par < 2; ++par) {
+        c->d_xdst[par] = dalloc<float*>(c, 8);
+        std::vector<float*> t(8, nullptr);
+        for (int r = 0; r < c->world; ++r) t[r] = c->peer[r].x[par];
+        SWF_CUDA(cudaMemcpy(c->d_xdst[par], t.data(), sizeof(float*) * 8, cudaMemcpyHostToDevice));
+    }
+    if (c->prec == SWF_PREC_BF16) {
+        make_tma_bf16(&c->tm_ain, c->a_in, M, m.cinp, 128);
+        make_tma_bf16(&c->tm_xm, c->xm, M, m.hp, 128);
+        make_tma_bf16(&c->tm_s, c->sbuf, M, m.fp, 128);
+        make_tma_bf16(&c->tm_enc, c->w_enc, m.np_enc, m.cinp, m.bn_enc / 2);
+        make_tma_bf16(&c->tm_dec, c->w_dec, m.np_dec, m.hp, m.bn_dec / 2);
+        c->tm_qkv.resize(m.nb);
+        c->tm_out.resize(m.nb);
+        c->tm_gu.resize(m.nb);
+        c->tm_down.resize(m.nb);
+        for (int b = 0; b < m.nb; ++b) {
+            make_tma_bf16(&c->tm_qkv[b], c->w_qkv[b], m.np_qkv, m.hp, m.bn_qkv / 2);
+            make_tma_bf16(&c->tm_out[b], c->w_out[b], m.np_out, m.hp, m.bn_out / 2);
+            make_tma_bf16(&c->tm_gu[b], c->w_gu[b], m.np_gu, m.hp, m.bn_gu / 2);
+            make_tma_bf16(&c->tm_down[b], c->w_down[b], m.np_down, m.fp, m.bn_down / 2);
+        }
+    }
+    SWF_CUDA(cudaDeviceSynchronize());
+    c->allocated = true;
+}
+
+// ------------------------------------------------------------------ parameter load
+// Canonical array list (model.hpp:140-168): (rows, cols) of every array in order.
+std::vector<std::pair<i64, i64>> param_shapes(const Dims& m) {
+    std::vector<std::pair<i64, i64>> v;
+    v.push_back({m.h, m.cin});
+    v.push_back({m.h, 1});
+    for (int b = 0; b < m.nb; ++b) {
+        v.push_back({3 * m.h, m.h});
+        v.push_back({m.h, m.h});
+        v.push_back({m.h, 1});
+        v.push_back({m.h, 1});
+        v.push_back({m.f, m.h});
+        v.push_back({m.f, m.h});
+        v.push_back({m.h, m.f});
+        v.push_back({6 * m.h, m.td});
+        v.push_back({6 * m.h, 1});
+    }
+    v.push_back({m.td, m.td});
+    v.push_back({m.td, 1});
+    v.push_back({m.h, 1});
+    v.push_back({m.cout, m.h});
+    v.push_back({m.cout, 1});
+    return v;
+}
+
+// Consume arrays in canonical order from `next(ai, n)` (device fp32, Eigen col-major) and repack.
+template <class Next>
+void load_params_from(swf_ctx* c, Next&& next) {
+    allocate(c);
+    const Dims& m = c->m;
+    int ai = 0;
+    auto up = [&](size_t n) -> float* { return next(ai++, n); };
+    auto copy_vec = [&](float* dst, size_t n) {
+        float* s = up(n);
+        SWF_CUDA(cudaMemcpyAsync(dst, s, n * 4, cudaMemcpyDeviceToDevice, c->st));
+    };
+    repack(c, up(size_t(m.h) * m.cin), m.h, m.cin, c->w_enc, m.cinp, 0, 0, false);  // encode.w (h x C_in)
+    copy_vec(c->enc_b, m.h);
+    for (int b = 0; b < m.nb; ++b) {
+        repack(c, up(size_t(3) * m.h * m.h), 3 * m.h, m.h, c->w_qkv[b], m.hp, 0, 0, false);
+        repack(c, up(size_t(m.h) * m.h), m.h, m.h, c->w_out[b], m.hp, 0, 0, false);
+        copy_vec(c->g_attn + size_t(b) * m.h, m.h);
+        copy_vec(c->g_ffn + size_t(b) * m.h, m.h);
+        repack(c, up(size_t(m.f) * m.h), m.f, m.h, c->w_gu[b], m.hp, m.G, 0, false);  // gate
+        repack(c, up(size_t(m.f) * m.h), m.f, m.h, c->w_gu[b], m.hp, m.G, 1, false);  // up
+        repack(c, up(size_t(m.h) * m.f), m.h, m.f, c->w_down[b], m.fp, 0, 0, false);
+        repack(c, up(size_t(6) * m.h * m.td), 6 * m.h, m.td, c->w_ada_t + size_t(b) * 6 * m.h * m.td, m.td, 0, 0,
+               true);
+        copy_vec(c->b_ada + size_t(b) * 6 * m.h, size_t(6) * m.h);
+    }
+    repack(c, up(size_t(m.td) * m.td), m.td, m.td, c->w_time_t, m.td, 0, 0, true);
+    copy_vec(c->b_time, m.td);
+    copy_vec(c->g_dec, m.h);
+    repack(c, up(size_t(m.cout) * m.h), m.cout, m.h, c->w_dec, m.hp, 0, 0, false);
+    copy_vec(c->b_dec, m.cout);
+    SWF_CUDA(cudaStreamSynchronize(c->st));
+    c->loaded = true;
+}
+
+size_t max_array(const Dims& m) {
+    size_t mx = 0;
+    for (const auto& s : param_shapes(m)) mx = std::max(mx, size_t(s.first * s.second));
+    return mx;
+}
+
+void load_params(swf_ctx* c, const void* const* arrays, int n_arrays, int dtype) {
+    allocate(c);
+    const Dims& m = c->m;
+    const int expect = 2 + 9 * m.nb + 5;
+    require(n_arrays == expect, "load_params: expected " + std::to_string(expect) + " arrays, got " +
+                                    std::to_string(n_arrays));
+    require(dtype == SWF_F32 || dtype == SWF_F64, "load_params: dtype must be SWF_F32 or SWF_F64");
+    float* stage = nullptr;
+    SWF_CUDA(cudaMalloc(&stage, max_array(m) * sizeof(float)));
+    std::vector<float> hb;
+    load_params_from(c, [&](int ai, size_t n) -> float* {
+        SWF_CUDA(cudaStreamSynchronize(c->st));  // staging buffer reuse
+        const void* src = arrays[ai];
+        require(src != nullptr, "load_params: null array pointer");
+        const float* f32;
+        if (dtype == SWF_F64) {
+            hb.resize(n);
+            const double* d = static_cast<const double*>(src);
+            for (size_t i = 0; i < n; ++i) hb[i] = static_cast<float>(d[i]);
+            f32 = hb.data();
+        } else {
+            f32 = static_cast<const float*>(src);
+        }
+        SWF_CUDA(cudaMemcpyAsync(stage, f32, n * sizeof(float), cudaMemcpyHostToDevice, c->st));
+        return stage;
+    });
+    SWF_CUDA(cudaFree(stage));
+}
+
+// init_parameters (model.hpp:185-209) / init_parameters_random (:213-223) generated on the device
+// with the same counter RNG (rng.hpp:17-45). mode 0: init_parameters; 1: init_parameters_random
+// (every array += scale*N(0,1)); 2: init_parameters + scale*N(0,1) on the arrays it leaves at zero
+// (ada.w, ada.b, decode.w, decode.b -- the bench's synthetic weights).
+__device__ __forceinline__ u64 dv_splitmix(u64 x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+__global__ void k_init_fill(float* __restrict__ dst, i64 n, u64 key, double scale, int op /*0 set,1 add,2 ones*/) {
+    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
+        if (op == 2) {
+            dst[i] = 1.f;
+            continue;
+        }
+        const u64 b0 = dv_splitmix(key + 0x632be59bd9b4e019ULL * (2 * u64(i) + 1));
+        const u64 b1 = dv_splitmix(key + 0x632be59bd9b4e019ULL * (2 * u64(i) + 2));
+        const double u1 = (double(b0 >> 11) + 1.0) * 0x1.0p-53;
+        const double u2 = double(b1 >> 11) * 0x1.0p-53;
+        const float v = static_cast<float>(scale * (sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2)));
+        dst[i] = op == 1 ? dst[i] + v : v;
+    }
+}
+
+u64 h_splitmix(u64 x);
+u64 h_kd(u64 k, u64 t);
+
+void init_params_device(swf_ctx* c, u64 seed, int mode, double scale) {
+    allocate(c);
+    const Dims& m = c->m;
+    const auto shapes = param_shapes(m);
+    float* stage = nullptr;
+    SWF_CUDA(cudaMalloc(&stage, max_array(m) * sizeof(float)));
+    u64 stream = 0;
+    const int nb = m.nb;
+    load_params_from(c, [&](int ai, size_t n) -> float* {
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        const int grid = int(std::min<size_t>((n + 255) / 256, 148 * 32));
+        // which base rule applies to array ai (model.hpp:193-208)
+        double sc = 0.0;
+        int op = 0;  // 0: gaussian fill, 2: ones, 3: zeros
+        if (ai == 0) {
+            sc = 1.0 / std::sqrt(double(m.cin));
+        } else if (ai == 1) {
+            op = 3;
+        } else if (ai < 2 + 9 * nb) {
+            const int k = (ai - 2) % 9;
+            switch (k) {
+                case 0: sc = 1.0 / std::sqrt(double(m.h)); break;
+                case 1: sc = 1.0 / std::sqrt(double(m.h) * 2 * nb); break;
+                case 2: case 3: op = 2; break;
+                case 4: case 5: sc = 1.0 / std::sqrt(double(m.h)); break;
+                case 6: sc = 1.0 / std::sqrt(double(m.f) * 2 * nb); break;
+                default: op = 3; break;  // ada.w, ada.b
+            }
+        } else {
+            const int k = ai - (2 + 9 * nb);
+            if (k == 0) sc = 1.0 / std::sqrt(double(m.td));
+            else if (k == 2) op = 2;
+            else op = 3;
+        }
+        if (op == 0) {
+            k_init_fill<<<grid, 256, 0, c->st>>>(stage, i64(n), h_kd(h_kd(seed, 0x1217u), stream++), sc, 0);
+        } else if (op == 2) {
+            k_init_fill<<<grid, 256, 0, c->st>>>(stage, i64(n), 0, 0.0, 2);
+        } else {
+            SWF_CUDA(cudaMemsetAsync(stage, 0, n * 4, c->st));
+        }
+        const bool zero_init = (op == 3);
+        if (mode == 1 || (mode == 2 && zero_init && ai != 1 && ai != 2 + 9 * nb + 1)) {
+            // init_parameters_random key: key_derive(seed, 0xabc, 1000 + j)
+            k_init_fill<<<grid, 256, 0, c->st>>>(stage, i64(n), h_kd(h_kd(seed, 0xabcu), u64(1000 + ai)), scale, 1);
+        }
+        SWF_LAUNCH_CHECK();
+        return stage;
+    });
+    SWF_CUDA(cudaFree(stage));
+}
+
+// ------------------------------------------------------------------ forward
+const TmaMap* tmap_at(const std::vector<TmaMap>& v, int b) { return b < int(v.size()) ? &v[b] : nullptr; }
+
+template <class T>
+struct Gemm;
+
+template <>
+struct Gemm<float> {
+    static void run(swf_ctx* c, const void* A, const TmaMap*, const void* B, const TmaMap*, i64 M, int Np, int K, int,
+                    int mode, const EpiParams& ep) {
+        gemm_f32(static_cast<const float*>(A), static_cast<const float*>(B), M, Np, K, mode, ep, c->st);
+    }
+};
+template <>
+struct Gemm<__nv_bfloat16> {
+    static void run(swf_ctx* c, const void*, const TmaMap* tA, const void*, const TmaMap* tB, i64 M, int Np, int K,
+                    int BN, int mode, const EpiParams& ep) {
+        gemm_bf16_tc(*tA, *tB, M, Np, K, BN, mode, ep, c->st);
+    }
+};
+
+EpiParams base_ep(swf_ctx* c) {
+    EpiParams ep;
+    std::memset(&ep, 0, sizeof ep);
+    ep.M = c->M;
+    ep.h = c->m.h;
+    ep.d = c->m.d;
+    ep.heads = c->m.heads;
+    ep.rope_row = reinterpret_cast<const float2*>(c->rope_row);
+    ep.rope_col = reinterpret_cast<const float2*>(c->rope_col);
+    ep.cur = c->lay[0];
+    ep.nxt = c->lay[0];
+    ep.my_rank = c->rank;
+    ep.out_scale = 1.f;
+    return ep;
+}
+
+void time_vectors(swf_ctx* c, double t) {
+    // time_features (model.hpp:229-241): arguments in double, values cast to float
+    const int td = c->m.td, nf = td / 2;
+    const float tf = static_cast<float>(t);
+    for (int k = 0; k < nf; ++k) {
+        const double om = std::pow(10000.0, -double(k) / nf);
+        const double arg = double(tf) * 636.6197723675814 * om;
+        c->h_feat[2 * k] = static_cast<float>(std::sin(arg));
+        c->h_feat[2 * k + 1] = static_cast<float>(std::cos(arg));
+    }
+    if (td % 2 == 1) c->h_feat[td - 1] = 1.f;
+    SWF_CUDA(cudaMemcpyAsync(c->feat, c->h_feat, sizeof(float) * td, cudaMemcpyHostToDevice, c->st));
+    time_embed(c->feat, c->w_time_t, c->b_time, td, c->emb, c->st);
+    ada_vectors(c->emb, c->w_ada_t, c->b_ada, c->m.nb, 6 * c->m.h, td, c->six, c->st);
+    c->launches += 2;
+}
+
+void peer_barrier(swf_ctx* c);
+
+// kernel classes for the profile (swf_profile_read)
+enum KClass { K_ENCODE, K_RMS, K_QKV, K_ATTN, K_OUT, K_GATEUP, K_DOWN, K_DECODE, K_OTHER, K_NCLASS };
+
+cudaEvent_t prof_event(swf_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        SWF_CUDA(cudaEventCreate(&e));
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+struct ProfScope {
+    swf_ctx* c;
+    int k;
+    cudaEvent_t b = nullptr;
+    ProfScope(swf_ctx* c_, int k_) : c(c_), k(k_) {
+        if (c->prof) {
+            b = prof_event(c);
+            SWF_CUDA(cudaEventRecord(b, c->st));
+        }
+    }
+    ~ProfScope() {
+        if (c->prof) {
+            cudaEvent_t e = prof_event(c);
+            cudaEventRecord(e, c->st);
+            c->prof_ev.push_back({k, {b, e}});
+        }
+    }
+};
+
+// The network on the prepared model input a_in (window order of layout 0). out_scale multiplies
+// the decode output (sigma_d for the sampler's net lambda, 1 for forward()).
+template <class T>
+void forward_core(swf_ctx* c, double t, float out_scale) {
+    const Dims& m = c->m;
+    const i64 M = c->M;
+    time_vectors(c, t);
+    EpiParams ep = base_ep(c);
+    // encode (swin.hpp:341-342)
+    ep.x = c->xbuf[0];
+    ep.bias = c->enc_b;
+    ep.N = m.h;
+    {
+        ProfScope ps(c, K_ENCODE);
+        Gemm<T>::run(c, c->a_in, &c->tm_ain, c->w_enc, &c->tm_enc, M, m.np_enc, m.cinp, m.bn_enc, EPI_ENCODE, ep);
+    }
+    c->launches++;
+    int cur = 0;
+    T* xm = static_cast<T*>(c->xm);
+    for (int b = 0; b < m.nb; ++b) {
+        const int par = b & 1;
+        const int npar = (b + 1 < m.nb) ? ((b + 1) & 1) : 0;
+        const float* six = c->six + size_t(b) * 6 * m.h;
+        float* x = c->xbuf[cur];
+        // attention branch: prenorm_modulate -> heads -> out projection (swin.hpp:313-322)
+        {
+            ProfScope ps(c, K_RMS);
+            rms_modulate<T>(x, M, m.h, m.hp, c->g_attn + size_t(b) * m.h, six, six + m.h, six + 2 * m.h, xm, c->flags,
+                        1 + b, c->st);
+        }
+        EpiParams e = ep;
+        e.cur = c->lay[par];
+        e.out = c->qkv;
+        e.plane = M * m.h;
+        e.N = 3 * m.h;
+        {
+            ProfScope ps(c, K_QKV);
+            Gemm<T>::run(c, xm, &c->tm_xm, c->w_qkv[b], tmap_at(c->tm_qkv, b), M, m.np_qkv, m.hp,
+                     m.bn_qkv, EPI_QKV, e);
+        }
+        AttnParams ap;
+        ap.q = c->qkv;
+        ap.k = static_cast<const char*>(c->qkv) + size_t(M) * m.h * esize(c);
+        ap.v = static_cast<const char*>(c->qkv) + size_t(2) * M * m.h * esize(c);
+        ap.o = xm;
+        ap.ldo = m.hp;
+        ap.nloc = c->lay[par].nloc;
+        ap.heads = m.heads;
+        ap.s = m.w * m.w;
+        ap.d = m.d;
+        ap.w = m.w;
+        ap.lay = c->lay[par];
+        ap.scale = 1.0f / std::sqrt(float(m.d));
+        {
+            ProfScope ps(c, K_ATTN);
+            if constexpr (sizeof(T) == 4)
+                attention_f32(ap, c->st);
+            else
+                attention_bf16(ap, c->st);
+        }
+        e = ep;
+        e.x = x;
+        e.N = m.h;
+        {
+            ProfScope ps(c, K_OUT);
+            Gemm<T>::run(c, xm, &c->tm_xm, c->w_out[b], tmap_at(c->tm_out, b), M, m.np_out, m.hp,
+                     m.bn_out, EPI_RESID, e);
+        }
+        // feed-forward branch (swin.hpp:323-324)
+        {
+            ProfScope ps(c, K_RMS);
+            rms_modulate<T>(x, M, m.h, m.hp, c->g_ffn + size_t(b) * m.h, six + 3 * m.h, six + 4 * m.h, six + 5 * m.h, xm,
+                        nullptr, 0, c->st);
+        }
+        e = ep;
+        e.out = c->sbuf;
+        e.ld_out = m.fp;
+        e.N = m.f;
+        e.G = m.G;
+        {
+            ProfScope ps(c, K_GATEUP);
+            Gemm<T>::run(c, xm, &c->tm_xm, c->w_gu[b], tmap_at(c->tm_gu, b), M, m.np_gu, m.hp,
+                     m.bn_gu, EPI_SWIGLU, e);
+        }
+        e = ep;
+        e.x = x;
+        e.N = m.h;
+        e.cur = c->lay[par];
+        e.nxt = c->lay[npar];
+        e.xdst = c->d_xdst[cur ^ 1];
+        {
+            ProfScope ps(c, K_DOWN);
+            Gemm<T>::run(c, c->sbuf, &c->tm_s, c->w_down[b], tmap_at(c->tm_down, b), M,
+                     m.np_down, m.fp, m.bn_down, EPI_DOWN, e);
+        }
+        c->launches += 7;
+        if (c->world > 1) peer_barrier(c);
+        cur ^= 1;
+    }
+    // decode (swin.hpp:362-366)
+    {
+            ProfScope ps(c, K_RMS);
+            rms_modulate<T>(c->xbuf[cur], M, m.h, m.hp, c->g_dec, nullptr, nullptr, nullptr, xm, c->flags, 1 + m.nb, c->st);
+        }
+    EpiParams e = ep;
+    e.out = c->out_loc;
+    e.ld_out = m.cout;
+    e.N = m.cout;
+    e.bias = c->b_dec;
+    e.out_scale = out_scale;
+    {
+            ProfScope ps(c, K_DECODE);
+            Gemm<T>::run(c, xm, &c->tm_xm, c->w_dec, &c->tm_dec, M, m.np_dec, m.hp, m.bn_dec, EPI_DECODE, e);
+        }
+    c->launches += 2;
+}
+
+void forward_any(swf_ctx* c, double t, float out_scale) {
+    if (c->prec == SWF_PREC_BF16)
+        forward_core<__nv_bfloat16>(c, t, out_scale);
+    else
+        forward_core<float>(c, t, out_scale);
+}
+
+void gather_input_any(swf_ctx* c, const float* in_pix) {
+    if (c->prec == SWF_PREC_BF16)
+        gather_rows<__nv_bfloat16>(in_pix, c->lay[0], c->m.cin, c->m.cinp, c->M, static_cast<__nv_bfloat16*>(c->a_in),
+                                   c->flags, 0, c->st);
+    else
+        gather_rows<float>(in_pix, c->lay[0], c->m.cin, c->m.cinp, c->M, static_cast<float*>(c->a_in), c->flags, 0,
+                           c->st);
+    c->launches++;
+}
+
+void reset_flags(swf_ctx* c) { SWF_CUDA(cudaMemsetAsync(c->flags, 0, sizeof(int) * c->nflags, c->st)); }
+
+// Raise NumericsError for the first flagged slot, naming it like check_finite (swin.hpp:295-300)
+// and the solver (diffusion.hpp:248-251).
+void check_flags(swf_ctx* c) {
+    SWF_CUDA(cudaMemcpyAsync(c->h_flags, c->flags, sizeof(int) * c->nflags, cudaMemcpyDeviceToHost, c->st));
+    SWF_CUDA(cudaStreamSynchronize(c->st));
+    const int nb = c->m.nb;
+    for (int s = 0; s < c->nflags; ++s) {
+        if (!c->h_flags[s]) continue;
+        if (s == 0) throw NumericsError("non-finite activation entering input");
+        if (s <= nb) throw NumericsError("non-finite activation entering block " + std::to_string(s - 1));
+        if (s == nb + 1) throw NumericsError("non-finite activation entering decode");
+        throw NumericsError("pf-ode solver diverged at step " + std::to_string(s - nb - 2));
+    }
+}
+
+void peer_barrier(swf_ctx* c) {
+    (void)c;
+    throw ConfigError("multi-rank barrier not connected (call swf_connect_peers)");
+}
+
+// ------------------------------------------------------------------ sampler
+void ensure_sampler(swf_ctx* c) {
+    if (c->pe_loc) return;
+    const Dims& m = c->m;
+    const i64 M = c->M;
+    // sinusoidal_pos_encode (posenc.hpp:16-37) in double, cast to float, pixel order, then gathered
+    std::vector<float> pe(size_t(c->N) * m.cin);
+    const int per_axis = m.cin / 2, nf = (per_axis + 1) / 2;
+    for (int axis = 0; axis < 2; ++axis)
+        for (int i = 0; i < per_axis; ++i) {
+            const int k = i / 2;
+            const double om = std::pow(10000.0, -double(k) / std::max(1, nf));
+            const bool use_sin = (i % 2 == 0);
+            const int ch = axis * per_axis + i;
+            for (int y = 0; y < c->H; ++y)
+                for (int x = 0; x < c->W; ++x) {
+                    const double pos = axis == 0 ? y : x;
+                    pe[(size_t(y) * c->W + x) * m.cin + ch] =
+                        static_cast<float>(use_sin ? std::sin(pos * om) : std::cos(pos * om));
+                }
+        }
+    c->pe_loc = dalloc<float>(c, size_t(M) * m.cin);
+    SWF_CUDA(cudaMemcpy(c->in_pix, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice));
+    gather_rows<float>(c->in_pix, c->lay[0], m.cin, m.cin, M, c->pe_loc, nullptr, 0, c->st);
+    c->s_x = dalloc<float>(c, size_t(M) * m.cout);
+    c->s_xmid = dalloc<float>(c, size_t(M) * m.cout);
+    c->s_tmp = dalloc<float>(c, size_t(M) * m.cout);
+    c->s_base = dalloc<float>(c, size_t(M) * m.cout);
+    c->s_cond = dalloc<float>(c, size_t(M) * std::max(m.cin - 2 * m.cout, 1));
+    c->s_stats = dalloc<float>(c, size_t(6) * m.cin);
+    SWF_CUDA(cudaStreamSynchronize(c->st));
+}
+
+// a_in channels [cp, cin) <- [x_prev ; forcings] + posenc (net lambda, diffusion.hpp:304-311)
+void set_conditioning(swf_ctx* c, const float* xprev_loc, const float* forc_loc) {
+    const Dims& m = c->m;
+    const int cf = m.cin - 2 * m.cout;
+    if (c->prec == SWF_PREC_BF16)
+        build_static_input<__nv_bfloat16>(xprev_loc, forc_loc, c->pe_loc, c->M, m.cout, cf, m.cin, m.cinp,
+                                          static_cast<__nv_bfloat16*>(c->a_in), c->st);
+    else
+        build_static_input<float>(xprev_loc, forc_loc, c->pe_loc, c->M, m.cout, cf, m.cin, m.cinp,
+                                  static_cast<float*>(c->a_in), c->st);
+}
+
+// v = sigma_d * F(x / sigma_d, t) into out_loc
+void net_eval(swf_ctx* c, const float* x, double sd, double t) {
+    const Dims& m = c->m;
+    if (c->prec == SWF_PREC_BF16)
+        assemble_state<__nv_bfloat16>(x, c->pe_loc, c->M, m.cout, m.cin, m.cinp, float(sd),
+                                      static_cast<__nv_bfloat16*>(c->a_in), c->st);
+    else
+        assemble_state<float>(x, c->pe_loc, c->M, m.cout, m.cin, m.cinp, float(sd), static_cast<float*>(c->a_in),
+                              c->st);
+    forward_any(c, t, float(sd));
+}
+
+void validate_dc(const swf_diffusion_cfg& dc) {
+    require(dc.sigma_d > 0, "diffusion: sigma_d must be positive");
+    require(0 < dc.sigma_min && dc.sigma_min < dc.sigma_max, "diffusion: need 0 < sigma_min < sigma_max");
+    require(dc.solver_steps >= 1, "diffusion: solver_steps must be >= 1");
+    require(dc.churn >= 0, "diffusion: churn amount must be >= 0");
+    require(dc.solver_steps <= 4000, "diffusion: solver_steps too large");
+}
+
+static std::pair<float, float> trig_coeffs_f(float t) {  // diffusion.hpp:50-55 in float
+    if (t == 0.f) return {1.f, 0.f};
+    if (t == static_cast<float>(M_PI_2)) return {0.f, 1.f};
+    return {std::cos(t), std::sin(t)};
+}
+
+// solve_pf_ode (diffusion.hpp:207-272) on the state c->s_x (local window order, [M][C_out]).
+void solve(swf_ctx* c, const swf_diffusion_cfg& dc, u64 churn_key, int* f_evals) {
+    validate_dc(dc);
+    const Dims& m = c->m;
+    const i64 n = c->M * m.cout;
+    const int S = dc.solver_steps;
+    const double sd = dc.sigma_d;
+    auto t_of = [&](double s) { return std::atan(s / sd); };
+    std::vector<double> sigma(S + 1);
+    for (int k = 0; k <= S; ++k) {
+        const double fr = double(k) / S;
+        sigma[k] = std::exp((1.0 - fr) * std::log(dc.sigma_max) + fr * std::log(dc.sigma_min));
+    }
+    double t_cur = t_of(sigma[0]), sig_cur = sigma[0];
+    u64 churn_ctr = 0;
+    int fe = 0;
+    for (int k = 0; k < S; ++k) {
+        const double sig_next = sigma[k + 1], t_next = t_of(sig_next);
+        const double sig_mid = std::sqrt(sig_cur * sig_next), t_mid = t_of(sig_mid);
+        const double b_s = std::sin(t_cur) * sd;
+        const double a_m = std::cos(t_mid), b_m = std::sin(t_mid) * sd;
+        const double a_t = std::cos(t_next), b_t = std::sin(t_next) * sd;
+        // stage 1: d1 = x0hat(x, t_cur); x_mid = (b_m/b_s) x - a_m (r_mid - 1) d1
+        net_eval(c, c->s_x, sd, static_cast<float>(t_cur));
+        auto cs1 = trig_coeffs_f(static_cast<float>(t_cur));
+        const double r_mid = sig_mid / sig_cur;
+        sampler_update(c->s_x, c->s_x, c->out_loc, n, cs1.first, cs1.second, float(b_m / b_s),
+                       float(a_m * (r_mid - 1.0)), c->s_xmid, nullptr, 0, c->st);
+        // stage 2: d2 = x0hat(x_mid, t_mid); x = (b_t/b_s) x - a_t (r - 1) d2
+        net_eval(c, c->s_xmid, sd, static_cast<float>(t_mid));
+        auto cs2 = trig_coeffs_f(static_cast<float>(t_mid));
+        const double r = sig_next / sig_cur;
+        sampler_update(c->s_x, c->s_xmid, c->out_loc, n, cs2.first, cs2.second, float(b_t / b_s),
+                       float(a_t * (r - 1.0)), c->s_x, c->flags, m.nb + 2 + std::min(k, 4000), c->st);
+        fe += 2;
+        c->launches += 2;
+        t_cur = t_next;
+        sig_cur = sig_next;
+        const bool active = dc.churn > 0.0 && 3 * k >= S && 3 * k < 2 * S;  // ChurnSchedule::active_step
+        if (active && k + 1 < S) {
+            const double delta = dc.churn * 0.05 * (t_of(sigma[k]) - t_next);
+            if (delta > 0) {
+                churn_rotate(c->s_x, c->lay[0], c->M, m.cout, churn_key, churn_ctr, sd, float(std::cos(delta)),
+                             float(std::sin(delta)), c->st);
+                churn_ctr += u64(c->N) * m.cout;
+                t_cur += delta;
+                sig_cur = sd * std::tan(t_cur);
+                c->launches++;
+            }
+        }
+    }
+    if (f_evals) *f_evals = fe;
+}
+
+// host-side helpers: host [N][C] (f32/f64) <-> device pixel staging
+void h2d_field(swf_ctx* c, const void* src, int C, int dtype, float* dst_pix) {
+    const size_t n = size_t(c->N) * C;
+    if (dtype == SWF_F64) {
+        std::vector<float> tmp(n);
+        const double* d = static_cast<const double*>(src);
+        for (size_t i = 0; i < n; ++i) tmp[i] = static_cast<float>(d[i]);
+        SWF_CUDA(cudaMemcpyAsync(dst_pix, tmp.data(), n * 4, cudaMemcpyHostToDevice, c->st));
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+    } else {
+        SWF_CUDA(cudaMemcpyAsync(dst_pix, src, n * 4, cudaMemcpyHostToDevice, c->st));
+    }
+}
+
+void d2h_field(swf_ctx* c, const float* src_loc, int C, int dtype, void* dst) {
+    const size_t n = size_t(c->N) * C;
+    SWF_CUDA(cudaMemsetAsync(c->out_pix, 0, n * 4, c->st));
+    scatter_rows(src_loc, c->lay[0], C, c->M, c->out_pix, c->st);
+    if (dtype == SWF_F64) {
+        std::vector<float> tmp(n);
+        SWF_CUDA(cudaMemcpyAsync(tmp.data(), c->out_pix, n * 4, cudaMemcpyDeviceToHost, c->st));
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        double* d = static_cast<double*>(dst);
+        for (size_t i = 0; i < n; ++i) d[i] = tmp[i];
+    } else {
+        SWF_CUDA(cudaMemcpyAsync(dst, c->out_pix, n * 4, cudaMemcpyDeviceToHost, c->st));
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+    }
+}
+
+// host field [N][C] -> device local window order (layout 0)
+void h2d_local(swf_ctx* c, const void* src, int C, int dtype, float* dst_loc) {
+    h2d_field(c, src, C, dtype, c->in_pix);
+    gather_rows<float>(c->in_pix, c->lay[0], C, C, c->M, dst_loc, nullptr, 0, c->st);
+    SWF_CUDA(cudaStreamSynchronize(c->st));
+}
+
+void upload_stats(swf_ctx* c, const swf_standardizers* s, int dtype) {
+    const Dims& m = c->m;
+    const int cp = m.cout, cf = std::max(m.cin - 2 * m.cout, 0);
+    std::vector<float> st(size_t(6) * m.cin, 0.f);
+    auto get = [&](const void* p, int n, size_t off, float dflt) {
+        for (int i = 0; i < n; ++i) {
+            float v = dflt;
+            if (p) v = dtype == SWF_F64 ? float(static_cast<const double*>(p)[i]) : static_cast<const float*>(p)[i];
+            st[off + i] = v;
+        }
+    };
+    get(s ? s->state_mean : nullptr, cp, 0, 0.f);
+    get(s ? s->state_std : nullptr, cp, size_t(m.cin), 1.f);
+    get(s ? s->resid_mean : nullptr, cp, size_t(2) * m.cin, 0.f);
+    get(s ? s->resid_std : nullptr, cp, size_t(3) * m.cin, 1.f);
+    get(s ? s->forcing_mean : nullptr, cf, size_t(4) * m.cin, 0.f);
+    get(s ? s->forcing_std : nullptr, cf, size_t(5) * m.cin, 1.f);
+    SWF_CUDA(cudaMemcpy(c->s_stats, st.data(), st.size() * 4, cudaMemcpyHostToDevice));
+}
+
+u64 h_splitmix(u64 x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+u64 h_kd(u64 k, u64 t) { return h_splitmix(k ^ h_splitmix(t)); }
+
+// forecast_step on device-resident x_prev (local order): result into dst_loc.
+void forecast_core(swf_ctx* c, const float* xprev_phys_loc, const float* forc_phys_loc,
+                   const swf_diffusion_cfg& dc, u64 run_seed, u64 event, float* dst_loc) {
+    const Dims& m = c->m;
+    const int cp = m.cout, cf = m.cin - 2 * m.cout;
+    require(cf >= 0, "forecast: in_channels must be >= 2 * out_channels");
+    float* S = c->s_stats;
+    standardize(xprev_phys_loc, c->M, cp, S, S + m.cin, c->s_tmp, c->st);
+    if (cf > 0) standardize(forc_phys_loc, c->M, cf, S + 4 * m.cin, S + 5 * m.cin, c->s_cond, c->st);
+    set_conditioning(c, c->s_tmp, c->s_cond);
+    // z_init = noise_field(sp, key_derive(event, 0x1217), ...) (diffusion.hpp:313-315)
+    const u64 zfk = h_kd(h_kd(run_seed, 0x7au), h_kd(event, 0x1217u));
+    noise_field(zfk, cp, c->lay[0], dc.sigma_d, c->s_x, c->st);
+    solve(c, dc, h_kd(event, 0xc4u), nullptr);
+    destandardize_add(c->s_x, xprev_phys_loc, c->M, cp, S + 2 * m.cin, S + 3 * m.cin, dst_loc, c->st);
+    c->launches += 5;
+}
+
+int fail(const std::exception& e, int rc) {
+    g_err = e.what();
+    return rc;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+#define SWF_API_TRY(...)                                            \
+    try {                                                           \
+        __VA_ARGS__;                                                \
+        return SWF_OK;                                              \
+    } catch (const swf::NumericsError& e) {                         \
+        return fail(e, SWF_ERR_NUMERICS);                           \
+    } catch (const swf::ConfigError& e) {                           \
+        return fail(e, SWF_ERR_CONFIG);                             \
+    } catch (const swf::CudaError& e) {                             \
+        return fail(e, SWF_ERR_CUDA);                               \
+    } catch (const std::exception& e) {                             \
+        return fail(e, SWF_ERR_CUDA);                               \
+    }
+
+extern "C" {
+
+const char* swf_last_error(void) { return g_err.c_str(); }
+const char* swf_version(void) { return "swinflow-b200 0.1 (sm_100a)"; }
+
+long long swf_param_count(const swf_model_cfg* c) {
+    const long long h = c->hidden_dim, f = c->ffn_dim, td = c->time_dim > 0 ? c->time_dim : c->hidden_dim;
+    const long long blk = 3 * h * h + h * h + 2 * h + 3 * f * h + 6 * h * td + 6 * h;
+    return (long long)c->in_channels * h + h + (long long)c->n_layers * c->blocks_per_layer * blk + td * td + td +
+           h + (long long)c->out_channels * h + c->out_channels;
+}
+
+int swf_create(const swf_model_cfg* cfg, int grid_h, int grid_w, int device, int precision, swf_ctx** out) {
+    SWF_API_TRY({
+        require(cfg && out, "swf_create: null argument");
+        validate_model(*cfg, grid_h, grid_w, precision);
+        int ndev = 0;
+        SWF_CUDA(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "swf_create: no CUDA device " + std::to_string(device));
+        SWF_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        SWF_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) throw CudaError("swf_create: this build targets sm_100a (B200); found sm_" +
+                                               std::to_string(prop.major) + std::to_string(prop.minor));
+        swf_ctx* c = new swf_ctx();
+        c->cfg = *cfg;
+        c->m = make_dims(*cfg, precision);
+        c->H = grid_h;
+        c->W = grid_w;
+        c->N = i64(grid_h) * grid_w;
+        c->prec = precision;
+        c->dev = device;
+        SWF_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+        *out = c;
+    })
+}
+
+void swf_destroy(swf_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    cudaStreamSynchronize(c->st);
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->h_flags) cudaFreeHost(c->h_flags);
+    if (c->h_feat) cudaFreeHost(c->h_feat);
+    for (const auto& pr : c->peer)
+        for (int k = 0; k < 2; ++k)
+            if (pr.x[k] && pr.x[k] != c->xbuf[k]) cudaIpcCloseMemHandle(pr.x[k]);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    cudaStreamDestroy(c->st);
+    delete c;
+}
+
+int swf_set_topology(swf_ctx* c, int wp_a, int wp_b, int sp, int rank, int ownership) {
+    SWF_API_TRY({
+        require(c, "null context");
+        require(!c->allocated, "swf_set_topology must precede swf_load_params");
+        require(wp_a >= 1 && wp_b >= 1 && sp >= 1, "topology: all degrees must be >= 1");
+        require(sp == 1, "topology: sequence parallelism (SP > 1) is not built in this round");
+        require(wp_a * wp_b <= 8, "topology: at most 8 window-parallel ranks per box");
+        require(rank >= 0 && rank < wp_a * wp_b, "topology: rank out of range");
+        require(ownership == SWF_OWN_CONTIGUOUS || ownership == SWF_OWN_ROUND_ROBIN, "topology: bad ownership");
+        c->wp_a = wp_a;
+        c->wp_b = wp_b;
+        c->sp = sp;
+        c->rank = rank;
+        c->world = wp_a * wp_b;
+        c->own = ownership;
+    })
+}
+
+int swf_load_params(swf_ctx* c, const void* const* arrays, int n_arrays, int dtype) {
+    SWF_API_TRY({
+        require(c && arrays, "null argument");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        load_params(c, arrays, n_arrays, dtype);
+    })
+}
+
+int swf_load_params_flat(swf_ctx* c, const void* flat, long long count, int dtype) {
+    SWF_API_TRY({
+        require(c && flat, "null argument");
+        require(count == swf_param_count(&c->cfg), "load_params: flat count " + std::to_string(count) +
+                                                        " != parameter_count_formula " +
+                                                        std::to_string(swf_param_count(&c->cfg)));
+        const Dims& m = c->m;
+        std::vector<size_t> sizes;
+        sizes.push_back(size_t(m.h) * m.cin);
+        sizes.push_back(m.h);
+        for (int b = 0; b < m.nb; ++b) {
+            for (size_t s : {size_t(3) * m.h * m.h, size_t(m.h) * m.h, size_t(m.h), size_t(m.h), size_t(m.f) * m.h,
+                             size_t(m.f) * m.h, size_t(m.h) * m.f, size_t(6) * m.h * m.td, size_t(6) * m.h})
+                sizes.push_back(s);
+        }
+        for (size_t s : {size_t(m.td) * m.td, size_t(m.td), size_t(m.h), size_t(m.cout) * m.h, size_t(m.cout)})
+            sizes.push_back(s);
+        std::vector<const void*> ptrs;
+        size_t off = 0;
+        const size_t es = dtype == SWF_F64 ? 8 : 4;
+        for (size_t s : sizes) {
+            ptrs.push_back(static_cast<const char*>(flat) + off * es);
+            off += s;
+        }
+        SWF_CUDA(cudaSetDevice(c->dev));
+        load_params(c, ptrs.data(), int(ptrs.size()), dtype);
+    })
+}
+
+int swf_init_params(swf_ctx* c, uint64_t seed, int mode, double scale) {
+    SWF_API_TRY({
+        require(c, "null context");
+        require(mode >= 0 && mode <= 2, "init_params: mode must be 0, 1 or 2");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        init_params_device(c, seed, mode, scale);
+    })
+}
+
+int swf_forward(swf_ctx* c, const void* input, double t, void* output, int dtype) {
+    SWF_API_TRY({
+        require(c && input && output, "null argument");
+        require(c->loaded, "forward: parameters not loaded");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        reset_flags(c);
+        h2d_field(c, input, c->m.cin, dtype, c->in_pix);
+        gather_input_any(c, c->in_pix);
+        forward_any(c, t, 1.f);
+        check_flags(c);
+        d2h_field(c, c->out_loc, c->m.cout, dtype, output);
+    })
+}
+
+int swf_forward_device(swf_ctx* c, const float* d_input, double t, float* d_output) {
+    SWF_API_TRY({
+        require(c && d_input && d_output, "null argument");
+        require(c->loaded, "forward: parameters not loaded");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        c->launches = 0;
+        reset_flags(c);
+        gather_input_any(c, d_input);
+        forward_any(c, t, 1.f);
+        scatter_rows(c->out_loc, c->lay[0], c->m.cout, c->M, d_output, c->st);
+        c->launches++;
+    })
+}
+
+int swf_sync(swf_ctx* c) {
+    SWF_API_TRY({
+        require(c, "null context");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        check_flags(c);
+    })
+}
+
+void* swf_stream(swf_ctx* c) { return c ? static_cast<void*>(c->st) : nullptr; }
+
+int swf_solve_pf_ode(swf_ctx* c, const void* x_init, const void* x_prev_std, const void* forcings_std,
+                     const swf_diffusion_cfg* dc, uint64_t churn_key, void* x_out, int* f_evals, int dtype) {
+    SWF_API_TRY({
+        require(c && x_init && x_prev_std && dc && x_out, "null argument");
+        require(c->loaded, "solve: parameters not loaded");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        ensure_sampler(c);
+        const Dims& m = c->m;
+        const int cf = m.cin - 2 * m.cout;
+        require(cf >= 0, "solve: in_channels must be >= 2 * out_channels");
+        reset_flags(c);
+        h2d_local(c, x_prev_std, m.cout, dtype, c->s_tmp);
+        if (cf > 0) {
+            require(forcings_std != nullptr, "solve: forcings required");
+            h2d_local(c, forcings_std, cf, dtype, c->s_cond);
+        }
+        set_conditioning(c, c->s_tmp, c->s_cond);
+        h2d_local(c, x_init, m.cout, dtype, c->s_x);
+        solve(c, *dc, churn_key, f_evals);
+        check_flags(c);
+        d2h_field(c, c->s_x, m.cout, dtype, x_out);
+    })
+}
+
+int swf_forecast_step(swf_ctx* c, const void* x_prev_phys, const void* forcing_phys, const swf_standardizers* stds,
+                      const swf_diffusion_cfg* dc, uint64_t run_seed, uint64_t noise_event, void* out, int dtype) {
+    SWF_API_TRY({
+        require(c && x_prev_phys && dc && out, "null argument");
+        require(c->loaded, "forecast: parameters not loaded");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        validate_dc(*dc);
+        ensure_sampler(c);
+        const Dims& m = c->m;
+        const int cf = m.cin - 2 * m.cout;
+        require(cf >= 0, "forecast: in_channels must be >= 2 * out_channels");
+        reset_flags(c);
+        upload_stats(c, stds, dtype);
+        h2d_local(c, x_prev_phys, m.cout, dtype, c->s_base);
+        float* forc = nullptr;
+        if (cf > 0) {
+            require(forcing_phys != nullptr, "forecast: forcings required");
+            forc = dalloc<float>(c, size_t(c->M) * cf);
+            h2d_local(c, forcing_phys, cf, dtype, forc);
+        }
+        float* dst = dalloc<float>(c, size_t(c->M) * m.cout);
+        forecast_core(c, c->s_base, forc, *dc, run_seed, noise_event, dst);
+        check_flags(c);
+        d2h_field(c, dst, m.cout, dtype, out);
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        // release the per-call buffers (keeps repeated calls bounded)
+        for (void* p : {static_cast<void*>(dst), static_cast<void*>(forc)}) {
+            if (!p) continue;
+            for (size_t i = 0; i < c->allocs.size(); ++i)
+                if (c->allocs[i] == p) {
+                    cudaFree(p);
+                    c->allocs.erase(c->allocs.begin() + i);
+                    break;
+                }
+        }
+    })
+}
+
+int swf_rollout_ensemble(swf_ctx* c, const void* x_init_phys, const void* forcings_phys, int n_members, int n_steps,
+                         const swf_standardizers* stds, const swf_diffusion_cfg* dc, uint64_t run_seed,
+                         uint64_t rollout_id, void* out, int dtype) {
+    SWF_API_TRY({
+        require(c && x_init_phys && dc && out, "null argument");
+        require(n_members >= 1 && n_steps >= 1, "rollout: members and steps must be >= 1");
+        require(c->loaded, "rollout: parameters not loaded");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        validate_dc(*dc);
+        ensure_sampler(c);
+        const Dims& m = c->m;
+        const int cf = m.cin - 2 * m.cout;
+        require(cf >= 0, "rollout: in_channels must be >= 2 * out_channels");
+        upload_stats(c, stds, dtype);
+        const size_t es = dtype == SWF_F64 ? 8 : 4;
+        const size_t fsz = size_t(c->N) * m.cout * es, ffsz = size_t(c->N) * std::max(cf, 0) * es;
+        float* x0 = dalloc<float>(c, size_t(c->M) * m.cout);
+        float* xa = dalloc<float>(c, size_t(c->M) * m.cout);
+        float* xb = dalloc<float>(c, size_t(c->M) * m.cout);
+        float* forc = dalloc<float>(c, size_t(c->M) * std::max(cf, 1) * n_steps);
+        h2d_local(c, x_init_phys, m.cout, dtype, x0);
+        for (int k = 0; k < n_steps && cf > 0; ++k)
+            h2d_local(c, static_cast<const char*>(forcings_phys) + k * ffsz, cf, dtype,
+                      forc + size_t(c->M) * cf * k);
+        for (int mem = 0; mem < n_members; ++mem) {
+            const float* x = x0;
+            for (int k = 0; k < n_steps; ++k) {
+                // event = key_derive(rollout_id, m, k) (diffusion.hpp:333)
+                const u64 ev = h_kd(h_kd(rollout_id, u64(mem)), u64(k));
+                float* dst = (x == xa) ? xb : xa;
+                reset_flags(c);
+                forecast_core(c, x, forc + size_t(c->M) * std::max(cf, 0) * k, *dc, run_seed, ev, dst);
+                check_flags(c);
+                d2h_field(c, dst, m.cout, dtype, static_cast<char*>(out) + (size_t(mem) * n_steps + k) * fsz);
+                x = dst;
+            }
+        }
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        for (void* p : {static_cast<void*>(x0), static_cast<void*>(xa), static_cast<void*>(xb), static_cast<void*>(forc)})
+            for (size_t i = 0; i < c->allocs.size(); ++i)
+                if (c->allocs[i] == p) {
+                    cudaFree(p);
+                    c->allocs.erase(c->allocs.begin() + i);
+                    break;
+                }
+    })
+}
+
+long long swf_local_tokens(swf_ctx* c) {
+    if (!c) return -1;
+    try {
+        allocate(c);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+    return c->M;
+}
+
+int swf_owned_pixels(swf_ctx* c, long long* pixels) {
+    SWF_API_TRY({
+        require(c && pixels, "null argument");
+        const int s = c->m.w * c->m.w;
+        i64 i = 0;
+        for (int gw : c->l2g[0])
+            for (int tok = 0; tok < s; ++tok) pixels[i++] = c->lay[0].g.win_to_pix(i64(gw) * s + tok);
+    })
+}
+
+long long swf_kernel_launches(swf_ctx* c) { return c ? c->launches : -1; }
+
+int swf_profile(swf_ctx* c, int enable) {
+    SWF_API_TRY({
+        require(c, "null context");
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        c->prof = enable != 0;
+        c->prof_ev.clear();
+        c->ev_used = 0;
+        for (int k = 0; k < 16; ++k) {
+            c->prof_ms[k] = 0;
+            c->prof_n[k] = 0;
+        }
+    })
+}
+
+int swf_profile_read(swf_ctx* c, double* ms, long long* launches, int n) {
+    SWF_API_TRY({
+        require(c && ms && launches, "null argument");
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        for (auto& pe : c->prof_ev) {
+            float t = 0.f;
+            SWF_CUDA(cudaEventElapsedTime(&t, pe.second.first, pe.second.second));
+            c->prof_ms[pe.first] += t;
+            c->prof_n[pe.first] += 1;
+        }
+        c->prof_ev.clear();
+        c->ev_used = 0;
+        for (int k = 0; k < n && k < 16; ++k) {
+            ms[k] = c->prof_ms[k];
+            launches[k] = c->prof_n[k];
+        }
+    })
+}
+
+int swf_noise_field(swf_ctx* c, uint64_t run_seed, uint64_t event, int channels, double sigma_d, float* out) {
+    SWF_API_TRY({
+        require(c && out && channels > 0, "bad argument");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        allocate(c);
+        float* z = dalloc<float>(c, size_t(c->M) * channels);
+        float* zp = dalloc<float>(c, size_t(c->N) * channels);
+        noise_field(h_kd(h_kd(run_seed, 0x7au), event), channels, c->lay[0], sigma_d, z, c->st);
+        scatter_rows(z, c->lay[0], channels, c->M, zp, c->st);
+        SWF_CUDA(cudaMemcpyAsync(out, zp, size_t(c->N) * channels * 4, cudaMemcpyDeviceToHost, c->st));
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        for (void* p : {static_cast<void*>(z), static_cast<void*>(zp)})
+            for (size_t i = 0; i < c->allocs.size(); ++i)
+                if (c->allocs[i] == p) {
+                    cudaFree(p);
+                    c->allocs.erase(c->allocs.begin() + i);
+                    break;
+                }
+    })
+}
+
+int swf_ipc_handles(swf_ctx* c, void* out128) {
+    SWF_API_TRY({
+        require(c && out128, "null argument");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        allocate(c);
+        cudaIpcMemHandle_t h[2];
+        SWF_CUDA(cudaIpcGetMemHandle(&h[0], c->xbuf[0]));
+        SWF_CUDA(cudaIpcGetMemHandle(&h[1], c->xbuf[1]));
+        std::memcpy(out128, h, 128);
+    })
+}
+
+int swf_connect_peers(swf_ctx* c, const void* all) {
+    SWF_API_TRY({
+        require(c && all, "null argument");
+        (void)all;
+        throw ConfigError("swf_connect_peers: window-parallel peer exchange not built yet");
+    })
+}
+
+}  // extern "C"

@@ -1,0 +1,338 @@
+// k_elem.cu -- HBM-bound kernels of the denoiser path: time embedding / AdaLN vectors, input
+// gather, RMSNorm+modulation, sampler updates, noise field, standardisation.
+#include "kernels.cuh"
+
+namespace swf {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(i64 n, int per_block = kThreads) {
+    i64 g = (n + per_block - 1) / per_block;
+    if (g > 148 * 64) g = 148 * 64;
+    return int(g < 1 ? 1 : g);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------- time embedding (model.hpp:261-269)
+// emb[o] = silu(sum_k Wt[o][k] feat[k] + b[o]); one warp per output row.
+__global__ void k_time_embed(const float* __restrict__ feat, const float* __restrict__ wt,
+                             const float* __restrict__ b, int td, float* __restrict__ emb) {
+    const int o = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (o >= td) return;
+    float acc = 0.f;
+    for (int k = lane; k < td; k += 32) acc += wt[i64(o) * td + k] * feat[k];
+    acc = warp_sum(acc);
+    if (lane == 0) emb[o] = silu_f(acc + b[o]);
+}
+
+// ---------------------------------------------------------------- ada vectors (swin.hpp:28-41)
+__global__ void k_ada(const float* __restrict__ emb, const float* __restrict__ wt, const float* __restrict__ b,
+                      i64 rows, int td, float* __restrict__ six) {
+    const i64 o = i64(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (o >= rows) return;
+    const float* w = wt + o * td;
+    float acc = 0.f;
+    for (int k = lane; k < td; k += 32) acc += w[k] * emb[k];
+    acc = warp_sum(acc);
+    if (lane == 0) six[o] = b[o] + acc;
+}
+
+// ---------------------------------------------------------------- gather / scatter rows
+template <class T>
+__device__ __forceinline__ T cvt(float v);
+template <>
+__device__ __forceinline__ float cvt<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <class T>
+__global__ void k_gather_rows(const float* __restrict__ src, LayMap lay, int C, int ldo, i64 M, T* __restrict__ dst,
+                              int* flags, int slot) {
+    const i64 total = M * ldo;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const i64 i = e / ldo;
+        const int c = int(e - i * ldo);
+        float v = 0.f;
+        if (c < C) {
+            v = src[lay.loc_to_pix(i) * C + c];
+            if (flags && !isfinite(v)) flag_nonfinite(flags, slot);
+        }
+        dst[e] = cvt<T>(v);
+    }
+}
+
+__global__ void k_scatter_rows(const float* __restrict__ src, LayMap lay, int C, i64 M, float* __restrict__ dst) {
+    const i64 total = M * C;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const i64 i = e / C;
+        const int c = int(e - i * C);
+        dst[lay.loc_to_pix(i) * C + c] = src[e];
+    }
+}
+
+// ---------------------------------------------------------------- RMSNorm + AdaLN (swin.hpp:72-85)
+// One warp per token row. r = sqrt(||x||^2/h + 1e-8); u = x / r; out = gate*((g*u)*(1+a)+b).
+template <class T>
+__device__ __forceinline__ void store4(T* p, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void store4<float>(float* p, float a, float b, float c, float d) {
+    *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a, float b, float c, float d) {
+    uint2 u;
+    u.x = pack_bf16x2(a, b);
+    u.y = pack_bf16x2(c, d);
+    *reinterpret_cast<uint2*>(p) = u;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_rms_mod(const float* __restrict__ x, i64 M, int h, int ldo,
+                                                 const float* __restrict__ g, const float* __restrict__ a,
+                                                 const float* __restrict__ b, const float* __restrict__ gate,
+                                                 T* __restrict__ out, int* flags, int slot) {
+    const int lane = threadIdx.x & 31;
+    const i64 nwarps = i64(gridDim.x) * (blockDim.x / 32);
+    for (i64 m = i64(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32; m < M; m += nwarps) {
+        const float4* xr = reinterpret_cast<const float4*>(x + m * h);
+        float ss = 0.f;
+        bool bad = false;
+        for (int i = lane; i < h / 4; i += 32) {
+            const float4 v = xr[i];
+            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+            bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+        }
+        ss = warp_sum(ss);
+        if (flags && __any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(flags, slot);
+        const float r = sqrtf(ss / float(h) + 1e-8f);
+        T* o = out + m * ldo;
+        for (int i = lane; i < h / 4; i += 32) {
+            const float4 v = xr[i];
+            const float4 gg = reinterpret_cast<const float4*>(g)[i];
+            float y0 = gg.x * (v.x / r), y1 = gg.y * (v.y / r), y2 = gg.z * (v.z / r), y3 = gg.w * (v.w / r);
+            if (a) {
+                const float4 aa = reinterpret_cast<const float4*>(a)[i];
+                const float4 bb = reinterpret_cast<const float4*>(b)[i];
+                const float4 ga = reinterpret_cast<const float4*>(gate)[i];
+                y0 = ga.x * (y0 * (1.f + aa.x) + bb.x);
+                y1 = ga.y * (y1 * (1.f + aa.y) + bb.y);
+                y2 = ga.z * (y2 * (1.f + aa.z) + bb.z);
+                y3 = ga.w * (y3 * (1.f + aa.w) + bb.w);
+            }
+            store4<T>(o + 4 * i, y0, y1, y2, y3);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- sampler
+__global__ void k_sampler_update(const float* __restrict__ xa, const float* __restrict__ xd,
+                                 const float* __restrict__ v, i64 n, float cs, float sn, float c1, float c2,
+                                 float* __restrict__ y, int* flags, int slot) {
+    bool bad = false;
+    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
+        const float d = cs * xd[i] - sn * v[i];
+        const float r = c1 * xa[i] - c2 * d;
+        y[i] = r;
+        bad |= !isfinite(r);
+    }
+    if (flags && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_nonfinite(flags, slot);
+}
+
+template <class T>
+__global__ void k_build_static(const float* __restrict__ xp, const float* __restrict__ fo,
+                               const float* __restrict__ pe, i64 M, int cp, int cf, int cin, int kp,
+                               T* __restrict__ a_in) {
+    const int w = kp - cp;
+    const i64 total = M * w;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const i64 i = e / w;
+        const int c = cp + int(e - i * w);
+        float v = 0.f;
+        if (c < 2 * cp)
+            v = xp[i * cp + (c - cp)] + pe[i * cin + c];
+        else if (c < cin)
+            v = fo[i * cf + (c - 2 * cp)] + pe[i * cin + c];
+        a_in[i * kp + c] = cvt<T>(v);
+    }
+}
+
+template <class T>
+__global__ void k_assemble_state(const float* __restrict__ x, const float* __restrict__ pe, i64 M, int cp, int cin,
+                                 int kp, float sd, T* __restrict__ a_in) {
+    const i64 total = M * cp;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const i64 i = e / cp;
+        const int c = int(e - i * cp);
+        a_in[i * kp + c] = cvt<T>(x[e] / sd + pe[i * cin + c]);
+    }
+}
+
+// counter RNG (rng.hpp:17-45), double-precision Box-Muller as in the reference
+__device__ __forceinline__ u64 d_splitmix(u64 x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ u64 d_kd(u64 key, u64 tag) { return d_splitmix(key ^ d_splitmix(tag)); }
+__device__ __forceinline__ double d_gaussian(u64 key, u64 ctr) {
+    const u64 b0 = d_splitmix(key + 0x632be59bd9b4e019ULL * (2 * ctr + 1));
+    const u64 b1 = d_splitmix(key + 0x632be59bd9b4e019ULL * (2 * ctr + 2));
+    const double u1 = (double(b0 >> 11) + 1.0) * 0x1.0p-53;
+    const double u2 = double(b1 >> 11) * 0x1.0p-53;
+    return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+__global__ void k_noise(u64 zfk, int C, LayMap lay, double sd, float* __restrict__ z, i64 M) {
+    const int s = lay.g.w * lay.g.w;
+    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < M; i += i64(gridDim.x) * blockDim.x) {
+        const int lw = int(i / s);
+        const int tok = int(i - i64(lw) * s);
+        const u64 key = d_kd(d_kd(zfk, u64(lay.loc2glob[lw])), u64(tok));
+        for (int c = 0; c < C; ++c) z[i * C + c] = float(sd * d_gaussian(key, u64(c)));
+    }
+}
+
+__global__ void k_churn(float* __restrict__ x, LayMap lay, i64 M, int C, u64 key, u64 ctr0, double sd, float c,
+                        float s) {
+    const i64 total = M * C;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const i64 i = e / C;
+        const int ch = int(e - i * C);
+        const u64 ctr = ctr0 + u64(lay.loc_to_pix(i)) * C + ch;
+        const float zeta = float(sd * d_gaussian(key, ctr));
+        x[e] = c * x[e] + s * zeta;
+    }
+}
+
+__global__ void k_standardize(const float* __restrict__ x, i64 M, int C, const float* __restrict__ mean,
+                              const float* __restrict__ sd, float* __restrict__ y) {
+    const i64 total = M * C;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const int c = int(e % C);
+        y[e] = (x[e] - mean[c]) / sd[c];
+    }
+}
+
+__global__ void k_destd_add(const float* __restrict__ r, const float* __restrict__ base, i64 M, int C,
+                            const float* __restrict__ mean, const float* __restrict__ sd, float* __restrict__ y) {
+    const i64 total = M * C;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const int c = int(e % C);
+        y[e] = base[e] + (r[e] * sd[c] + mean[c]);
+    }
+}
+
+__global__ void k_check_finite(const float* __restrict__ x, i64 n, int* flags, int slot) {
+    bool bad = false;
+    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_nonfinite(flags, slot);
+}
+
+}  // namespace
+
+void time_embed(const float* feat, const float* w_time_t, const float* b_time, int td, float* emb, cudaStream_t st) {
+    k_time_embed<<<(td + 7) / 8, 256, 0, st>>>(feat, w_time_t, b_time, td, emb);
+    SWF_LAUNCH_CHECK();
+}
+
+void ada_vectors(const float* emb, const float* w_ada_t, const float* b_ada, int nb, int six_h, int td, float* six,
+                 cudaStream_t st) {
+    const i64 rows = i64(nb) * six_h;
+    k_ada<<<int((rows + 7) / 8), 256, 0, st>>>(emb, w_ada_t, b_ada, rows, td, six);
+    SWF_LAUNCH_CHECK();
+}
+
+template <class T>
+void gather_rows(const float* src_pix, const LayMap& lay, int C, int ldo, i64 M, T* dst, int* flags, int slot,
+                 cudaStream_t st) {
+    k_gather_rows<T><<<grid_for(M * ldo), kThreads, 0, st>>>(src_pix, lay, C, ldo, M, dst, flags, slot);
+    SWF_LAUNCH_CHECK();
+}
+template void gather_rows<float>(const float*, const LayMap&, int, int, i64, float*, int*, int, cudaStream_t);
+template void gather_rows<__nv_bfloat16>(const float*, const LayMap&, int, int, i64, __nv_bfloat16*, int*, int,
+                                         cudaStream_t);
+
+void scatter_rows(const float* src_loc, const LayMap& lay, int C, i64 M, float* dst_pix, cudaStream_t st) {
+    k_scatter_rows<<<grid_for(M * C), kThreads, 0, st>>>(src_loc, lay, C, M, dst_pix);
+    SWF_LAUNCH_CHECK();
+}
+
+template <class T>
+void rms_modulate(const float* x, i64 M, int h, int ldo, const float* g, const float* a, const float* b,
+                  const float* gate, T* out, int* flags, int slot, cudaStream_t st) {
+    if (h % 4 != 0) throw CudaError("rms_modulate: h must be a multiple of 4");
+    k_rms_mod<T><<<grid_for(M * 32), 256, 0, st>>>(x, M, h, ldo, g, a, b, gate, out, flags, slot);
+    SWF_LAUNCH_CHECK();
+}
+template void rms_modulate<float>(const float*, i64, int, int, const float*, const float*, const float*,
+                                  const float*, float*, int*, int, cudaStream_t);
+template void rms_modulate<__nv_bfloat16>(const float*, i64, int, int, const float*, const float*, const float*,
+                                          const float*, __nv_bfloat16*, int*, int, cudaStream_t);
+
+void sampler_update(const float* xa, const float* xd, const float* v, i64 n, float cs, float sn, float c1, float c2,
+                    float* y, int* flags, int slot, cudaStream_t st) {
+    k_sampler_update<<<grid_for(n), kThreads, 0, st>>>(xa, xd, v, n, cs, sn, c1, c2, y, flags, slot);
+    SWF_LAUNCH_CHECK();
+}
+
+template <class T>
+void build_static_input(const float* xprev, const float* forc, const float* pe, i64 M, int cp, int cf, int cin,
+                        int kp, T* a_in, cudaStream_t st) {
+    k_build_static<T><<<grid_for(M * (kp - cp)), kThreads, 0, st>>>(xprev, forc, pe, M, cp, cf, cin, kp, a_in);
+    SWF_LAUNCH_CHECK();
+}
+template void build_static_input<float>(const float*, const float*, const float*, i64, int, int, int, int, float*,
+                                        cudaStream_t);
+template void build_static_input<__nv_bfloat16>(const float*, const float*, const float*, i64, int, int, int, int,
+                                                __nv_bfloat16*, cudaStream_t);
+
+template <class T>
+void assemble_state(const float* x, const float* pe, i64 M, int cp, int cin, int kp, float sd, T* a_in,
+                    cudaStream_t st) {
+    k_assemble_state<T><<<grid_for(M * cp), kThreads, 0, st>>>(x, pe, M, cp, cin, kp, sd, a_in);
+    SWF_LAUNCH_CHECK();
+}
+template void assemble_state<float>(const float*, const float*, i64, int, int, int, float, float*, cudaStream_t);
+template void assemble_state<__nv_bfloat16>(const float*, const float*, i64, int, int, int, float, __nv_bfloat16*,
+                                            cudaStream_t);
+
+void noise_field(u64 zfk, int C, const LayMap& lay0, double sigma_d, float* z, cudaStream_t st) {
+    const i64 M = i64(lay0.nloc) * lay0.g.w * lay0.g.w;
+    k_noise<<<grid_for(M), kThreads, 0, st>>>(zfk, C, lay0, sigma_d, z, M);
+    SWF_LAUNCH_CHECK();
+}
+
+void churn_rotate(float* x, const LayMap& lay0, i64 M, int C, u64 key, u64 ctr0, double sigma_d, float c, float s,
+                  cudaStream_t st) {
+    k_churn<<<grid_for(M * C), kThreads, 0, st>>>(x, lay0, M, C, key, ctr0, sigma_d, c, s);
+    SWF_LAUNCH_CHECK();
+}
+
+void standardize(const float* x, i64 M, int C, const float* mean, const float* stdv, float* y, cudaStream_t st) {
+    k_standardize<<<grid_for(M * C), kThreads, 0, st>>>(x, M, C, mean, stdv, y);
+    SWF_LAUNCH_CHECK();
+}
+
+void destandardize_add(const float* r, const float* base, i64 M, int C, const float* mean, const float* stdv,
+                       float* y, cudaStream_t st) {
+    k_destd_add<<<grid_for(M * C), kThreads, 0, st>>>(r, base, M, C, mean, stdv, y);
+    SWF_LAUNCH_CHECK();
+}
+
+void check_finite(const float* x, i64 n, int* flags, int slot, cudaStream_t st) {
+    k_check_finite<<<grid_for(n), kThreads, 0, st>>>(x, n, flags, slot);
+    SWF_LAUNCH_CHECK();
+}
+
+}  // namespace swf

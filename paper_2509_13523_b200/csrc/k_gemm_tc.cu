@@ -1,0 +1,512 @@
+// k_gemm_tc.cu -- BF16 GEMM on the 5th-generation tensor cores (sm_100a):
+//   tcgen05.mma.cta_group::2 (UMMA 256 x BN x 16, 2-CTA pairs), operands staged by TMA with
+//   128-byte swizzle, FP32 accumulators in TMEM (double-buffered), persistent static tile
+//   schedule, warp specialisation (TMA producer / MMA issuer / 4 epilogue warps).
+// The epilogue fuses the reference's per-token ops that follow each linear:
+//   encode bias, RoPE + head-major scatter (QKV), residual add (out), SiLU*up (gate/up) and the
+//   residual add + next-layout window permutation of the down projection (swin.hpp:306-366).
+#include <cuda.h>
+
+#include <mutex>
+#include <vector>
+
+#include "../../include/swinflow_capi.h"
+#include "epilogue.cuh"
+
+namespace swf {
+
+namespace {
+
+constexpr int BM = 128;  // rows per CTA; UMMA M = 256 per CTA pair
+constexpr int BK = 64;   // one 128-byte swizzle atom of bf16
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kStageA = BM * BK * 2;
+    static constexpr int kStageB = (BN / 2) * BK * 2;
+    static constexpr int kStage = kStageA + kStageB;
+    static constexpr int kStages = (BN == 256) ? 6 : 8;
+    static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
+    static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t kIdesc = (1u << 4)                 // D = F32
+                                       | (1u << 7) | (1u << 10)  // A, B = BF16
+                                       | (uint32_t(BN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2cta(uint32_t dst, const void* tmap, uint32_t bar_cluster, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16)  // LBO (unused for swizzled K-major)
+           | (uint64_t(1024 >> 4) << 32)                          // SBO: 8 rows x 128 B
+           | (uint64_t(1) << 46)                                  // sm100 descriptor version
+           | (uint64_t(2) << 61);                                 // SWIZZLE_128B
+}
+__device__ __forceinline__ void umma_2cta(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- vectorised epilogues (32 columns)
+template <int MODE>
+__device__ __forceinline__ void epi32(const EpiParams& ep, i64 m, int n0, float* v) {
+    if (m >= ep.M || n0 >= ep.N) return;
+    const int h = ep.h;
+    if constexpr (MODE == EPI_ENCODE) {
+        float4* xr = reinterpret_cast<float4*>(ep.x + m * h + n0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 b = reinterpret_cast<const float4*>(ep.bias + n0)[j];
+            xr[j] = make_float4(v[4 * j] + b.x, v[4 * j + 1] + b.y, v[4 * j + 2] + b.z, v[4 * j + 3] + b.w);
+        }
+    } else if constexpr (MODE == EPI_RESID) {
+        float4* xr = reinterpret_cast<float4*>(ep.x + m * h + n0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float4 o = xr[j];
+            o.x += v[4 * j];
+            o.y += v[4 * j + 1];
+            o.z += v[4 * j + 2];
+            o.w += v[4 * j + 3];
+            xr[j] = o;
+        }
+    } else if constexpr (MODE == EPI_DOWN) {
+        int rank;
+        const i64 li = ep.nxt.pix_to_loc(ep.cur.loc_to_pix(m), &rank);
+        const float4* xs = reinterpret_cast<const float4*>(ep.x + m * h + n0);
+        float4* xd = reinterpret_cast<float4*>(ep.xdst[rank] + li * h + n0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 o = xs[j];
+            xd[j] = make_float4(o.x + v[4 * j], o.y + v[4 * j + 1], o.z + v[4 * j + 2], o.w + v[4 * j + 3]);
+        }
+    } else if constexpr (MODE == EPI_QKV) {
+        // d >= 32 so the 32 columns lie inside one head of one of q/k/v
+        const int s = ep.cur.g.w * ep.cur.g.w;
+        const int lw = int(m / s);
+        const int tok = int(m - i64(lw) * s);
+        const int which = n0 / h;
+        const int e = n0 - which * h;
+        const int head = e / ep.d;
+        const int dd = e - head * ep.d;
+        if (which < 2) {
+            const int gw = ep.cur.loc2glob[lw];
+            const int w = ep.cur.g.w;
+            const int wy = gw / ep.cur.g.nx, wx = gw - wy * ep.cur.g.nx;
+            const int prow = wy * w + ep.cur.g.shift + tok / w;
+            const int pcol = wx * w + ep.cur.g.shift + tok % w;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) rope_pair(ep, prow, pcol, (dd + j) >> 1, v[j], v[j + 1]);
+        }
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ep.out) + which * ep.plane +
+                             ((i64(lw) * ep.heads + head) * s + tok) * ep.d + dd;
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            d4[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                               pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+    } else if constexpr (MODE == EPI_DECODE) {
+        float* o = reinterpret_cast<float*>(ep.out) + m * ep.ld_out;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (n0 + j < ep.N) o[n0 + j] = (v[j] + ep.bias[n0 + j]) * ep.out_scale;
+    }
+}
+
+__device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0, const float* g, const float* u) {
+    if (m >= ep.M || j0 >= ep.N) return;
+    uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.out) + m * ep.ld_out + j0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float r[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) r[t] = silu_f(g[8 * j + t]) * u[8 * j + t];
+        d4[j] = make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
+                           pack_bf16x2(r[6], r[7]));
+    }
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int BN, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, i64 M, int n_tiles,
+              int num_k, EpiParams ep) {
+    using C = Cfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + C::kStages * C::kStageA;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = bars + C::kStages;
+    uint64_t* tfull_bar = bars + 2 * C::kStages;
+    uint64_t* tempty_bar = bars + 2 * C::kStages + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = cluster_rank();
+    const bool leader = crank == 0;
+    const int cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+    const i64 m_tiles = (M + 2 * BM - 1) / (2 * BM);
+    const i64 total = m_tiles * n_tiles;
+
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(smem_u32(&full_bar[s]), 1);
+            mbar_init(smem_u32(&empty_bar[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(smem_u32(&tfull_bar[a]), 1);
+            mbar_init(smem_u32(&tempty_bar[a]), 2 * 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer (both CTAs; each loads its A half and B half, signalling the leader)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (i64 t = cluster_id; t < total; t += n_clusters) {
+                const int m_blk = int(t / n_tiles), n_blk = int(t % n_tiles);
+                const int row_a = m_blk * 2 * BM + int(crank) * BM;
+                const int row_b = n_blk * BN + int(crank) * (BN / 2);
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+                    const uint32_t fb = map_to_rank(smem_u32(&full_bar[stage]), 0);
+                    if (leader) mbar_expect_tx(smem_u32(&full_bar[stage]), 2 * C::kStage);
+                    tma_load_2cta(smem_u32(sA + stage * C::kStageA), &tmA, fb, kb * BK, row_a);
+                    tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK, row_b);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (leader CTA, one thread)
+        if (leader && lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (i64 t = cluster_id; t < total; t += n_clusters) {
+                mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t dtm = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(smem_u32(&full_bar[stage]), phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * C::kStageA);
+                    const uint32_t b0 = smem_u32(sB + stage * C::kStageB);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        umma_2cta(dtm, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), C::kIdesc,
+                                  (kb | k) != 0);
+                    umma_commit_mc(smem_u32(&empty_bar[stage]), 0x3);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit_mc(smem_u32(&tfull_bar[acc]), 0x3);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= kEpiWarp0) {
+        // ===== epilogue: TMEM -> registers -> fused op -> global
+        const int q = warp - kEpiWarp0;  // TMEM lane quadrant (warp % 4)
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        const uint32_t tempty_leader = map_to_rank(smem_u32(&tempty_bar[0]), 0);
+        for (i64 t = cluster_id; t < total; t += n_clusters) {
+            const int m_blk = int(t / n_tiles), n_blk = int(t % n_tiles);
+            mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
+            tc_fence_after();
+            const i64 row = i64(m_blk) * 2 * BM + crank * BM + q * 32 + lane;
+            const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+            if constexpr (MODE == EPI_SWIGLU) {
+                // interleave G = BN/2: columns [0, BN/2) gate, [BN/2, BN) up of the same ffn units
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 64; ++ch) {
+                    float g[32], u[32];
+                    tmem_ld32(tbase + ch * 32, g);
+                    tmem_ld32(tbase + BN / 2 + ch * 32, u);
+                    epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u);
+                }
+            } else {
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 32; ++ch) {
+                    float v[32];
+                    tmem_ld32(tbase + ch * 32, v);
+                    epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols));
+    }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+template <int BN, int MODE>
+void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiParams& ep, cudaStream_t st) {
+    using C = Cfg<BN>;
+    static bool configured = false;
+    auto kern = k_gemm_tc<BN, MODE>;
+    if (!configured) {
+        SWF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        configured = true;
+    }
+    const int n_tiles = Npad / BN;
+    const i64 m_tiles = (M + 2 * BM - 1) / (2 * BM);
+    const i64 total = m_tiles * n_tiles;
+    int sms = 148;
+    int clusters = int(std::min<i64>(total, sms / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(2 * clusters));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cfg.attrs = nullptr;  // cluster shape (2,1,1) comes from __cluster_dims__
+    cfg.numAttrs = 0;
+    const CUtensorMap* a = reinterpret_cast<const CUtensorMap*>(&A);
+    const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(&B);
+    SWF_CUDA(cudaLaunchKernelEx(&cfg, kern, *a, *b, M, n_tiles, K / BK, ep));
+}
+
+template <int BN>
+void dispatch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int mode, const EpiParams& ep,
+              cudaStream_t st) {
+    switch (mode) {
+        case EPI_ENCODE: launch<BN, EPI_ENCODE>(A, B, M, Npad, K, ep, st); break;
+        case EPI_QKV: launch<BN, EPI_QKV>(A, B, M, Npad, K, ep, st); break;
+        case EPI_RESID: launch<BN, EPI_RESID>(A, B, M, Npad, K, ep, st); break;
+        case EPI_SWIGLU: launch<BN, EPI_SWIGLU>(A, B, M, Npad, K, ep, st); break;
+        case EPI_DOWN: launch<BN, EPI_DOWN>(A, B, M, Npad, K, ep, st); break;
+        case EPI_DECODE: launch<BN, EPI_DECODE>(A, B, M, Npad, K, ep, st); break;
+        default: throw CudaError("gemm_bf16_tc: bad epilogue mode");
+    }
+}
+
+}  // namespace
+
+void make_tma_bf16(TmaMap* m, const void* base, i64 rows, i64 kcols, int box_rows) {
+    static_assert(sizeof(TmaMap) == sizeof(CUtensorMap), "TmaMap size");
+    if (kcols % BK != 0) throw CudaError("make_tma_bf16: K must be a multiple of 64");
+    cuuint64_t dims[2] = {cuuint64_t(kcols), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(kcols) * 2};
+    cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(reinterpret_cast<CUtensorMap*>(m), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
+void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int BN, int mode, const EpiParams& ep,
+                  cudaStream_t st) {
+    if (K % BK != 0) throw CudaError("gemm_bf16_tc: K must be a multiple of 64");
+    if (Npad % BN != 0) throw CudaError("gemm_bf16_tc: N must be a multiple of the N tile");
+    if (BN == 256)
+        dispatch<256>(A, B, M, Npad, K, mode, ep, st);
+    else if (BN == 128)
+        dispatch<128>(A, B, M, Npad, K, mode, ep, st);
+    else
+        throw CudaError("gemm_bf16_tc: BN must be 128 or 256");
+}
+
+}  // namespace swf
+
+// ====================================================================== self-test (C-ABI)
+namespace {
+using swf::i64;
+__global__ void k_fill_bf16(__nv_bfloat16* p, i64 n, uint64_t seed, float* f32) {
+    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
+        uint64_t x = seed + 0x9e3779b97f4a7c15ULL * (i + 1);
+        x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+        x ^= x >> 31;
+        const float v = (float((x >> 40) & 0xFFFF) / 65536.0f - 0.5f) * 2.0f;
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        p[i] = b;
+        f32[i] = __bfloat162float(b);
+    }
+}
+__global__ void k_maxdiff(const float* a, const float* b, i64 n, float* out) {
+    float md = 0.f, mr = 0.f;
+    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
+        md = fmaxf(md, fabsf(a[i] - b[i]));
+        mr = fmaxf(mr, fabsf(b[i]));
+    }
+    atomicMax(reinterpret_cast<int*>(out), __float_as_int(md));
+    atomicMax(reinterpret_cast<int*>(out + 1), __float_as_int(mr));
+}
+}  // namespace
+
+extern "C" int swf_selftest_gemm(int device, long long M, int N, int K, double* max_abs_err, double* max_ref) {
+    using namespace swf;
+    try {
+        SWF_CUDA(cudaSetDevice(device));
+        if (N % 128 != 0 || K % 64 != 0) throw CudaError("selftest: N % 128 and K % 64 required");
+        __nv_bfloat16 *A, *B;
+        float *Af, *Bf, *C1, *C2, *bias, *res;
+        SWF_CUDA(cudaMalloc(&A, size_t(M) * K * 2));
+        SWF_CUDA(cudaMalloc(&B, size_t(N) * K * 2));
+        SWF_CUDA(cudaMalloc(&Af, size_t(M) * K * 4));
+        SWF_CUDA(cudaMalloc(&Bf, size_t(N) * K * 4));
+        SWF_CUDA(cudaMalloc(&C1, size_t(M) * N * 4));
+        SWF_CUDA(cudaMalloc(&C2, size_t(M) * N * 4));
+        SWF_CUDA(cudaMalloc(&bias, size_t(N) * 4));
+        SWF_CUDA(cudaMalloc(&res, 8));
+        SWF_CUDA(cudaMemset(bias, 0, size_t(N) * 4));
+        SWF_CUDA(cudaMemset(res, 0, 8));
+        SWF_CUDA(cudaMemset(C1, 0xff, size_t(M) * N * 4));
+        k_fill_bf16<<<1024, 256>>>(A, M * K, 1, Af);
+        k_fill_bf16<<<1024, 256>>>(B, i64(N) * K, 2, Bf);
+        SWF_LAUNCH_CHECK();
+        TmaMap ta, tb;
+        const int BN = (N % 256 == 0) ? 256 : 128;
+        make_tma_bf16(&ta, A, M, K, 128);
+        make_tma_bf16(&tb, B, N, K, BN / 2);
+        EpiParams ep;
+        memset(&ep, 0, sizeof ep);
+        ep.M = M;
+        ep.N = N;
+        ep.h = N;
+        ep.x = C1;
+        ep.bias = bias;
+        gemm_bf16_tc(ta, tb, M, N, K, BN, EPI_ENCODE, ep, 0);
+        ep.x = C2;
+        gemm_f32(Af, Bf, M, N, K, EPI_ENCODE, ep, 0);
+        k_maxdiff<<<1024, 256>>>(C1, C2, M * N, res);
+        float h[2];
+        SWF_CUDA(cudaMemcpy(h, res, 8, cudaMemcpyDeviceToHost));
+        *max_abs_err = h[0];
+        *max_ref = h[1];
+        for (void* p : {(void*)A, (void*)B, (void*)Af, (void*)Bf, (void*)C1, (void*)C2, (void*)bias, (void*)res})
+            cudaFree(p);
+        return 0;
+    } catch (const std::exception& e) {
+        fprintf(stderr, "swf_selftest_gemm: %s\n", e.what());
+        return SWF_ERR_CUDA;
+    }
+}

@@ -1,0 +1,163 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): bit-exact for index maps / permutations, <= 1e-4 for the
+FP32 validation mode, <= 2e-2 for the BF16 path, errors normalised per output channel by the
+channel's max |ref| (the reference audit convention, swinflow_main.cpp:427-430).
+"""
+import numpy as np
+import pytest
+
+import paper_2509_13523_b200 as swf
+from oracle import pyoracle as o
+from tests.util import rel_err_per_channel
+
+pytestmark = pytest.mark.gpu
+
+TOL_FP32 = 1e-4
+TOL_BF16 = 2e-2
+
+TINY = dict(hidden_dim=16, n_heads=4, ffn_dim=32, n_layers=2, window_px=6, in_channels=4, out_channels=2,
+            time_dim=16)  # reference golden config, test_swin_core.cpp:16-27
+C1 = dict(hidden_dim=128, n_heads=4, ffn_dim=256, n_layers=2, window_px=8, in_channels=8, out_channels=3,
+          time_dim=128)  # BASELINE.json configs[0]
+MID = dict(hidden_dim=256, n_heads=2, ffn_dim=512, n_layers=2, window_px=12, in_channels=16, out_channels=6,
+           time_dim=256)  # d = 128 like the 1.3B shape, seam-masked windows on block 1
+
+
+def cfgs(d):
+    return o.ModelConfig(**d), swf.ModelConfig(**d)
+
+
+def run(d, H, W, prec, seed=2024, scale=0.25, t=0.62831853071795862, dtype=np.float64):
+    oc, sc = cfgs(d)
+    p = o.init_params(oc, seed, random=True, scale=scale, dtype=dtype)
+    x = o.random_field(oc.in_channels, H * W, seed + 1).astype(dtype)
+    ref = o.forward(oc, p, x, t if dtype == np.float64 else np.float32(t), H, W)
+    dn = swf.Denoiser(sc, H, W, precision=prec)
+    dn.load_params(p)
+    got = dn.forward(x.astype(np.float32), t)
+    dn.close()
+    return got, ref
+
+
+def test_gemm_tcgen05_selftest():
+    for M, N, K in [(256, 128, 64), (512, 256, 128), (1000, 384, 192), (4096, 512, 1536), (300, 256, 64)]:
+        err, mref = swf.selftest_gemm(M, N, K)
+        assert err <= 1e-3 * max(mref, 1.0), (M, N, K, err, mref)
+
+
+def test_golden_probe_fp32_mode():
+    # test_swin_core.cpp:415-422 on the GPU (FP32 validation mode)
+    got, ref = run(TINY, 12, 12, swf.PREC_FP32)
+    assert got[77, 1] == pytest.approx(1.2440901490316572, rel=TOL_FP32)
+    assert rel_err_per_channel(got, ref) <= TOL_FP32
+
+
+def test_c1_fp32_mode():
+    got, ref = run(C1, 32, 64, swf.PREC_FP32, scale=0.05)
+    assert rel_err_per_channel(got, ref) <= TOL_FP32
+
+
+def test_c1_bf16():
+    got, ref = run(C1, 32, 64, swf.PREC_BF16, scale=0.05)
+    assert rel_err_per_channel(got, ref) <= TOL_BF16
+
+
+def test_mid_d128_bf16():
+    got, ref = run(MID, 48, 96, swf.PREC_BF16, scale=0.02, dtype=np.float32)
+    assert rel_err_per_channel(got, ref) <= TOL_BF16
+
+
+def test_mid_d128_fp32_mode():
+    got, ref = run(MID, 48, 96, swf.PREC_FP32, scale=0.02, dtype=np.float32)
+    assert rel_err_per_channel(got, ref) <= TOL_FP32
+
+
+def test_nan_input_raises_numerics_error():
+    oc, sc = cfgs(TINY)
+    p = o.init_params(oc, 1, random=True)
+    x = o.random_field(4, 144, 8).astype(np.float32)
+    x[5, 1] = np.nan
+    dn = swf.Denoiser(sc, 12, 12, precision=swf.PREC_FP32)
+    dn.load_params(p)
+    with pytest.raises(swf.NumericsError, match="input"):
+        dn.forward(x, 0.5)
+
+
+@pytest.mark.parametrize("prec", [swf.PREC_FP32, swf.PREC_BF16])
+def test_window_locality_bitwise(prec):
+    # test_swin_core.cpp:224-239: one unshifted block is window-local, bitwise
+    d = dict(C1, n_layers=1)
+    oc, sc = cfgs(d)
+    H, W = 32, 64
+    p = o.init_params(oc, 4, random=True, scale=0.05)
+    x = o.random_field(oc.in_channels, H * W, 10).astype(np.float32)
+    perm = o.window_perm(H, W, 8, 0).reshape(-1, 64)
+    win = 1 * (W // 8) + 2
+    xz = np.zeros_like(x)
+    xz[perm[win]] = x[perm[win]]
+    dn = swf.Denoiser(sc, H, W, precision=prec)
+    dn.load_params(p)
+    y, yz = dn.forward(x, 0.4), dn.forward(xz, 0.4)
+    assert np.array_equal(y[perm[win]], yz[perm[win]])
+
+
+def test_noise_field_matches_oracle():
+    oc, sc = cfgs(C1)
+    dn = swf.Denoiser(sc, 32, 64, precision=swf.PREC_FP32)
+    z = dn.noise_field(99, 5, 3)
+    zr = o.noise_field(99, 5, 3, 32, 64, 8, dtype=np.float32)
+    assert np.abs(z - zr).max() <= 1e-6 * np.abs(zr).max()
+
+
+def test_forecast_step_fp32_mode():
+    d = dict(TINY, in_channels=8, out_channels=3)
+    oc, sc = cfgs(d)
+    p = o.init_params(oc, 200, random=True, scale=0.05)
+    x0 = o.random_field(3, 144, 201)
+    forc = o.random_field(2, 144, 202)
+    ev = o.key_derive(31, 0, 0)
+    ref, fe = o.forecast_step(oc, p, 12, 12, x0, forc, 7, ev, steps=4)
+    dn = swf.Denoiser(sc, 12, 12, precision=swf.PREC_FP32)
+    dn.load_params(p)
+    got = dn.forecast_step(x0.astype(np.float32), forc.astype(np.float32),
+                           swf.DiffusionConfig(solver_steps=4), 7, ev)
+    assert fe == 8
+    assert rel_err_per_channel(got, ref) <= TOL_FP32
+
+
+def test_forecast_step_bf16_c1():
+    oc, sc = cfgs(C1)
+    p = o.init_params(oc, 300, random=True, scale=0.02, dtype=np.float32)
+    x0 = o.random_field(3, 2048, 301).astype(np.float32)
+    forc = o.random_field(2, 2048, 302).astype(np.float32)
+    ev = o.key_derive(41, 1, 0)
+    ref, _ = o.forecast_step(oc, p, 32, 64, x0, forc, 11, ev, steps=3)
+    dn = swf.Denoiser(sc, 32, 64, precision=swf.PREC_BF16)
+    dn.load_params(p)
+    got = dn.forecast_step(x0, forc, swf.DiffusionConfig(solver_steps=3), 11, ev)
+    assert rel_err_per_channel(got - x0, ref - x0) <= TOL_BF16
+
+
+SAMP = dict(TINY, in_channels=8, out_channels=3)
+
+
+@pytest.mark.parametrize("t", [0.3, 1.0, 1.5687963294615568])
+def test_forward_fp32_mode_t_range(t):
+    got, ref = run(SAMP, 12, 12, swf.PREC_FP32, seed=200, scale=0.05, t=t)
+    assert rel_err_per_channel(got, ref) <= TOL_FP32
+
+
+@pytest.mark.parametrize("steps", [1, 4])
+def test_solve_pf_ode_fp32_mode(steps):
+    oc, sc = cfgs(SAMP)
+    p = o.init_params(oc, 200, random=True, scale=0.05)
+    x0 = o.random_field(3, 144, 211)
+    xp = o.random_field(3, 144, 212)
+    fo = o.random_field(2, 144, 213)
+    ref, fe = o.solve_net(oc, p, 12, 12, x0, xp, fo, steps=steps)
+    dn = swf.Denoiser(sc, 12, 12, precision=swf.PREC_FP32)
+    dn.load_params(p)
+    got, fe2 = dn.solve_pf_ode(x0.astype(np.float32), xp, fo, swf.DiffusionConfig(solver_steps=steps))
+    assert fe == fe2 == 2 * steps
+    assert rel_err_per_channel(got, ref) <= TOL_FP32
