@@ -559,20 +559,12 @@ EpiParams base_ep(swf_ctx* c) {
 }
 
 void time_vectors(swf_ctx* c, double t) {
-    // time_features (model.hpp:229-241): arguments in double, values cast to float
-    const int td = c->m.td, nf = td / 2;
-    const float tf = static_cast<float>(t);
-    for (int k = 0; k < nf; ++k) {
-        const double om = std::pow(10000.0, -double(k) / nf);
-        const double arg = double(tf) * 636.6197723675814 * om;
-        c->h_feat[2 * k] = static_cast<float>(std::sin(arg));
-        c->h_feat[2 * k + 1] = static_cast<float>(std::cos(arg));
-    }
-    if (td % 2 == 1) c->h_feat[td - 1] = 1.f;
-    SWF_CUDA(cudaMemcpyAsync(c->feat, c->h_feat, sizeof(float) * td, cudaMemcpyHostToDevice, c->st));
-    time_embed(c->feat, c->w_time_t, c->b_time, td, c->emb, c->st);
-    ada_vectors(c->emb, c->w_ada_t, c->b_ada, c->m.nb, 6 * c->m.h, td, c->six, c->st);
-    c->launches += 2;
+    // time_features (model.hpp:229-241) evaluates the arguments in double from T t
+    const double tt = double(static_cast<float>(t));
+    time_features(tt, c->m.td, c->feat, c->st);
+    time_embed(c->feat, c->w_time_t, c->b_time, c->m.td, c->emb, c->st);
+    ada_vectors(c->emb, c->w_ada_t, c->b_ada, c->m.nb, 6 * c->m.h, c->m.td, c->six, c->st);
+    c->launches += 3;
 }
 
 void peer_barrier(swf_ctx* c);

@@ -20,6 +20,20 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// ---------------------------------------------------------------- time features (model.hpp:229-241)
+// f[2k] = sin(t * 2000/pi * 10000^(-k/(td/2))), f[2k+1] = cos(...), in double, cast to float. t is
+// a kernel argument, so back-to-back evaluations at different t never share a staging buffer.
+__global__ void k_time_features(double t, int td, float* __restrict__ feat) {
+    const int nf = td / 2;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nf; k += gridDim.x * blockDim.x) {
+        const double om = pow(10000.0, -double(k) / nf);
+        const double arg = t * 636.6197723675814 * om;
+        feat[2 * k] = static_cast<float>(sin(arg));
+        feat[2 * k + 1] = static_cast<float>(cos(arg));
+    }
+    if ((td & 1) && blockIdx.x == 0 && threadIdx.x == 0) feat[td - 1] = 1.f;
+}
+
 // ---------------------------------------------------------------- time embedding (model.hpp:261-269)
 // emb[o] = silu(sum_k Wt[o][k] feat[k] + b[o]); one warp per output row.
 __global__ void k_time_embed(const float* __restrict__ feat, const float* __restrict__ wt,
@@ -240,6 +254,11 @@ __global__ void k_check_finite(const float* __restrict__ x, i64 n, int* flags, i
 }
 
 }  // namespace
+
+void time_features(double t, int td, float* feat, cudaStream_t st) {
+    k_time_features<<<(td / 2 + 255) / 256 + 1, 256, 0, st>>>(t, td, feat);
+    SWF_LAUNCH_CHECK();
+}
 
 void time_embed(const float* feat, const float* w_time_t, const float* b_time, int td, float* emb, cudaStream_t st) {
     k_time_embed<<<(td + 7) / 8, 256, 0, st>>>(feat, w_time_t, b_time, td, emb);

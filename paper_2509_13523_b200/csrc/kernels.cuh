@@ -88,6 +88,7 @@ void attention_f32(const AttnParams& p, cudaStream_t st);
 void attention_bf16(const AttnParams& p, cudaStream_t st);
 
 // ------------------------------------------------------------------ elementwise
+void time_features(double t, int td, float* feat, cudaStream_t st);
 void time_embed(const float* feat, const float* w_time_t, const float* b_time, int td, float* emb,
                 cudaStream_t st);
 void ada_vectors(const float* emb, const float* w_ada_t, const float* b_ada, int nb, int six_h, int td, float* six,
