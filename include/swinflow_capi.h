@@ -75,13 +75,22 @@ int swf_create(const swf_model_cfg* cfg, int grid_h, int grid_w, int device, int
 void swf_destroy(swf_ctx* ctx);
 
 /* Window-parallel topology (topology.hpp:74-132): this context is rank `rank` of a wp_a x wp_b
- * window-parallel grid (sp must be 1 in this build). peer_handles: wp_a*wp_b cudaIpcMemHandle_t
- * blobs (64 B each) of every rank's residual buffers, from swf_ipc_handles(); may be NULL when
- * world == 1. Must be called before swf_load_params. */
+ * window-parallel grid (sp must be 1 in this build); each rank owns whole windows of both the
+ * unshifted and the shifted layout. Must be called before swf_load_params / swf_init_params. */
 int swf_set_topology(swf_ctx* ctx, int wp_a, int wp_b, int sp, int rank, int ownership);
-/* Export this rank's residual-buffer IPC handles (2 x 64 bytes) / import all ranks' handles. */
-int swf_ipc_handles(swf_ctx* ctx, void* out128);
-int swf_connect_peers(swf_ctx* ctx, const void* all_handles /* world x 128 bytes */);
+/* Export this rank's IPC handles (residual buffers x2 + barrier flags: 3 x 64 bytes) / map all
+ * ranks' handles (world x 192 bytes, rank order). After connecting, the down-projection epilogue
+ * stores owner-changed tokens straight into the peer's residual buffer over NVLink (the
+ * shifted-layer regroup of send_boundary, simulator.hpp:781-824) and a release/acquire flag
+ * barrier over the same mapping orders block boundaries. */
+int swf_ipc_handles(swf_ctx* ctx, void* out192);
+int swf_connect_peers(swf_ctx* ctx, const void* all_handles);
+/* Host-only planning (no GPU): owner rank of every window (row-major window id) and the tokens
+ * each rank sends each other rank at a shift_from -> shift_to block boundary (sent[src*world+dst]),
+ * i.e. shift_transfer_plan (topology.hpp:149-188) aggregated per rank pair. */
+int swf_plan_owners(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, int ownership, int* owner);
+int swf_plan_exchange(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, int ownership, int shift_from,
+                      int shift_to, long long* sent);
 
 /* Parameters in canonical parameter_arrays order (model.hpp:140-168), each array Eigen
  * column-major, element type dtype. Replaces Parameters<T> / load_params. */

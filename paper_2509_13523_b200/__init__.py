@@ -108,6 +108,8 @@ def lib():
         L.swf_set_topology.argtypes = [vp, i, i, i, i, i]
         L.swf_ipc_handles.argtypes = [vp, vp]
         L.swf_connect_peers.argtypes = [vp, vp]
+        L.swf_plan_owners.argtypes = [i, i, i, i, i, i, vp]
+        L.swf_plan_exchange.argtypes = [i, i, i, i, i, i, i, i, vp]
         L.swf_load_params.argtypes = [vp, vp, i, i]
         L.swf_load_params_flat.argtypes = [vp, vp, ll, i]
         L.swf_init_params.argtypes = [vp, u64, i, d]
@@ -176,6 +178,22 @@ class Denoiser:
         if topology is not None:
             wp_a, wp_b, sp, rank, own = topology
             _check(lib().swf_set_topology(self._c, wp_a, wp_b, sp, rank, own))
+
+    def connect_peers(self, all_handles: bytes):
+        buf = C.create_string_buffer(all_handles, len(all_handles))
+        _check(lib().swf_connect_peers(self._c, buf))
+
+    def ipc_handles(self) -> bytes:
+        buf = C.create_string_buffer(192)
+        _check(lib().swf_ipc_handles(self._c, buf))
+        return buf.raw
+
+    def connect_peers_torch(self, dist):
+        """Exchange IPC handles with torch.distributed (any backend) and map every peer."""
+        mine = self.ipc_handles()
+        allh = [None] * dist.get_world_size()
+        dist.all_gather_object(allh, mine)
+        self.connect_peers(b"".join(allh))
 
     def close(self):
         if self._c:
@@ -279,6 +297,21 @@ class Denoiser:
         out = np.zeros((self.H * self.W, channels), np.float32)
         _check(lib().swf_noise_field(self._c, run_seed, event, channels, sigma_d, _p(out)))
         return out
+
+
+def plan_owners(H: int, W: int, w: int, wp_a: int, wp_b: int, ownership: int = OWN_CONTIGUOUS) -> np.ndarray:
+    own = np.zeros((H // w) * (W // w), np.int32)
+    _check(lib().swf_plan_owners(H, W, w, wp_a, wp_b, ownership, _p(own)))
+    return own
+
+
+def plan_exchange(H: int, W: int, w: int, wp_a: int, wp_b: int, ownership: int = OWN_CONTIGUOUS,
+                  shift_from: int = 0, shift_to: int | None = None) -> np.ndarray:
+    world = wp_a * wp_b
+    sent = np.zeros((world, world), np.int64)
+    _check(lib().swf_plan_exchange(H, W, w, wp_a, wp_b, ownership, shift_from, w // 2 if shift_to is None else shift_to,
+                                   _p(sent)))
+    return sent
 
 
 def exported_symbols() -> list[str]:

@@ -47,6 +47,7 @@ struct Dims {
 
 struct Peer {
     float* x[2];
+    int* flags;
 };
 
 }  // namespace swf
@@ -86,8 +87,11 @@ struct swf_ctx {
     float *in_pix = nullptr, *out_pix = nullptr;
     float** d_xdst[2] = {nullptr, nullptr};
     std::vector<Peer> peer;
+    int* bar_flags = nullptr;        // this rank's barrier slots (IPC-exported), one per peer
+    int** d_flag_table = nullptr;    // device table: flag array of every rank (peer-mapped)
+    int bar_epoch = 0;
     // TMA maps (BF16 path)
-    TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec;
+    TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec, tm_q, tm_k, tm_vt;
     std::vector<TmaMap> tm_qkv, tm_out, tm_gu, tm_down;
     long long launches = 0;
     // sampler workspace (allocated lazily)
@@ -176,6 +180,7 @@ void validate_model(const swf_model_cfg& c, int H, int W, int prec) {
         require(c.hidden_dim % 128 == 0 && c.ffn_dim % 128 == 0,
                 "BF16 path: hidden_dim and ffn_dim must be multiples of 128 (use SWF_PREC_FP32 otherwise)");
         require(d == 32 || d == 64 || d == 128, "BF16 path: head_dim must be 32, 64 or 128");
+        require(c.window_px % 4 == 0, "BF16 path: window_px must be a multiple of 4 (16-byte TMA row pitch of V^T)");
     }
 }
 
@@ -258,15 +263,16 @@ void build_layouts(swf_ctx* c) {
 void build_rope(swf_ctx* c) {
     const Dims& m = c->m;
     const int q4 = m.d / 4;
-    auto table = [&](int npos) {
+    auto table = [&](int npos) {  // [pair j][position] (cos, sin)
         std::vector<float> t(size_t(npos) * q4 * 2);
-        for (int pos = 0; pos < npos; ++pos)
-            for (int j = 0; j < q4; ++j) {
-                const double om = std::pow(10000.0, -double(j) / q4);
+        for (int j = 0; j < q4; ++j) {
+            const double om = std::pow(10000.0, -double(j) / q4);
+            for (int pos = 0; pos < npos; ++pos) {
                 const float a = static_cast<float>(pos * om);
-                t[(size_t(pos) * q4 + j) * 2] = std::cos(a);
-                t[(size_t(pos) * q4 + j) * 2 + 1] = std::sin(a);
+                t[(size_t(j) * npos + pos) * 2] = std::cos(a);
+                t[(size_t(j) * npos + pos) * 2 + 1] = std::sin(a);
             }
+        }
         return t;
     };
     const auto tr = table(c->H + m.w), tc = table(c->W + m.w);
@@ -317,9 +323,12 @@ void allocate(swf_ctx* c) {
         c->w_down.push_back(talloc(c, size_t(m.np_down) * m.fp));
     }
     // destination tables for the fused down-projection store (own buffer unless peers connect)
-    c->peer.assign(c->world, Peer{{nullptr, nullptr}});
+    c->bar_flags = dalloc<int>(c, 64);
+    c->d_flag_table = dalloc<int*>(c, 8);
+    c->peer.assign(c->world, Peer{{nullptr, nullptr}, nullptr});
     c->peer[c->rank].x[0] = c->xbuf[0];
     c->peer[c->rank].x[1] = c->xbuf[1];
+    c->peer[c->rank].flags = c->bar_flags;
     for (int par = 0; par < 2; ++par) {
         c->d_xdst[par] = dalloc<float*>(c, 8);
         std::vector<float*> t(8, nullptr);
@@ -331,6 +340,16 @@ void allocate(swf_ctx* c) {
         make_tma_bf16(&c->tm_xm, c->xm, M, m.hp, 128);
         make_tma_bf16(&c->tm_s, c->sbuf, M, m.fp, 128);
         make_tma_bf16(&c->tm_enc, c->w_enc, m.np_enc, m.cinp, m.bn_enc / 2);
+        {
+            // attention operands: q / k planes [rows][d] (box d<=64 x 128 rows), V^T [rows][s] (64 x d)
+            const int sw = m.d >= 64 ? 128 : 2 * m.d;
+            const i64 rows_qk = M * m.heads;  // (window, head, token) rows of d elements
+            const char* qb = static_cast<const char*>(c->qkv);
+            make_tma_bf16_2d(&c->tm_q, qb, rows_qk, m.d, sw / 2, 128, sw);
+            make_tma_bf16_2d(&c->tm_k, qb + size_t(M) * m.h * 2, rows_qk, m.d, sw / 2, 128, sw);
+            make_tma_bf16_2d(&c->tm_vt, qb + size_t(2) * M * m.h * 2, i64(c->lay[0].nloc) * m.heads * m.d,
+                             i64(m.w) * m.w, 64, m.d, 128);
+        }
         make_tma_bf16(&c->tm_dec, c->w_dec, m.np_dec, m.hp, m.bn_dec / 2);
         c->tm_qkv.resize(m.nb);
         c->tm_out.resize(m.nb);
@@ -551,6 +570,8 @@ EpiParams base_ep(swf_ctx* c) {
     ep.heads = c->m.heads;
     ep.rope_row = reinterpret_cast<const float2*>(c->rope_row);
     ep.rope_col = reinterpret_cast<const float2*>(c->rope_col);
+    ep.rope_nrow = c->H + c->m.w;
+    ep.rope_ncol = c->W + c->m.w;
     ep.cur = c->lay[0];
     ep.nxt = c->lay[0];
     ep.my_rank = c->rank;
@@ -605,6 +626,8 @@ template <class T>
 void forward_core(swf_ctx* c, double t, float out_scale) {
     const Dims& m = c->m;
     const i64 M = c->M;
+    // no rank may store into a peer's residual buffer while that peer still reads it
+    if (c->world > 1) peer_barrier(c);
     time_vectors(c, t);
     EpiParams ep = base_ep(c);
     // encode (swin.hpp:341-342)
@@ -652,6 +675,9 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         ap.w = m.w;
         ap.lay = c->lay[par];
         ap.scale = 1.0f / std::sqrt(float(m.d));
+        ap.tmq = &c->tm_q;
+        ap.tmk = &c->tm_k;
+        ap.tmv = &c->tm_vt;
         {
             ProfScope ps(c, K_ATTN);
             if constexpr (sizeof(T) == 4)
@@ -741,7 +767,8 @@ void check_flags(swf_ctx* c) {
     SWF_CUDA(cudaMemcpyAsync(c->h_flags, c->flags, sizeof(int) * c->nflags, cudaMemcpyDeviceToHost, c->st));
     SWF_CUDA(cudaStreamSynchronize(c->st));
     const int nb = c->m.nb;
-    for (int s = 0; s < c->nflags; ++s) {
+    if (c->h_flags[c->nflags - 1]) throw CudaError("peer barrier timed out (a window-parallel rank stopped)");
+    for (int s = 0; s < c->nflags - 1; ++s) {
         if (!c->h_flags[s]) continue;
         if (s == 0) throw NumericsError("non-finite activation entering input");
         if (s <= nb) throw NumericsError("non-finite activation entering block " + std::to_string(s - 1));
@@ -750,9 +777,40 @@ void check_flags(swf_ctx* c) {
     }
 }
 
+// Cross-GPU barrier over NVLink-mapped flags (one launch per GPU; ranks are separate GPUs, so the
+// waiting blocks never share an SM with the blocks they wait for). Each rank release-stores the
+// epoch into its slot of every peer's flag array, then acquire-polls its own slots. Stream order
+// places it after the down-projection whose epilogue stored rows into peer residual buffers.
+__global__ void k_peer_barrier(int* const* flags, int rank, int world, int epoch, int* err) {
+    const int t = threadIdx.x;
+    if (t < world) {
+        __threadfence_system();
+        int* remote = flags[t] + rank;
+        asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(remote), "r"(epoch) : "memory");
+        const int* mine = flags[rank] + t;
+        unsigned long long t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (true) {
+            int v;
+            asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+            if (v >= epoch) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 30000000000ull) {  // 30 s: a peer died -> report instead of hanging
+                atomicOr(err, 1);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
 void peer_barrier(swf_ctx* c) {
-    (void)c;
-    throw ConfigError("multi-rank barrier not connected (call swf_connect_peers)");
+    if (!c->peers) throw ConfigError("multi-rank topology: call swf_connect_peers before running");
+    ++c->bar_epoch;
+    k_peer_barrier<<<1, 32, 0, c->st>>>(c->d_flag_table, c->rank, c->world, c->bar_epoch,
+                                        c->flags + (c->nflags - 1));
+    SWF_LAUNCH_CHECK();
+    c->launches++;
 }
 
 // ------------------------------------------------------------------ sampler
@@ -1326,23 +1384,82 @@ int swf_noise_field(swf_ctx* c, uint64_t run_seed, uint64_t event, int channels,
     })
 }
 
-int swf_ipc_handles(swf_ctx* c, void* out128) {
+int swf_ipc_handles(swf_ctx* c, void* out) {
     SWF_API_TRY({
-        require(c && out128, "null argument");
+        require(c && out, "null argument");
         SWF_CUDA(cudaSetDevice(c->dev));
         allocate(c);
-        cudaIpcMemHandle_t h[2];
+        cudaIpcMemHandle_t h[3];
         SWF_CUDA(cudaIpcGetMemHandle(&h[0], c->xbuf[0]));
         SWF_CUDA(cudaIpcGetMemHandle(&h[1], c->xbuf[1]));
-        std::memcpy(out128, h, 128);
+        SWF_CUDA(cudaIpcGetMemHandle(&h[2], c->bar_flags));
+        std::memcpy(out, h, sizeof h);
     })
 }
 
 int swf_connect_peers(swf_ctx* c, const void* all) {
     SWF_API_TRY({
         require(c && all, "null argument");
-        (void)all;
-        throw ConfigError("swf_connect_peers: window-parallel peer exchange not built yet");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        allocate(c);
+        const size_t hs = 3 * sizeof(cudaIpcMemHandle_t);
+        for (int r = 0; r < c->world; ++r) {
+            if (r == c->rank) continue;
+            const cudaIpcMemHandle_t* h =
+                reinterpret_cast<const cudaIpcMemHandle_t*>(static_cast<const char*>(all) + r * hs);
+            void* p[3];
+            for (int k = 0; k < 3; ++k) SWF_CUDA(cudaIpcOpenMemHandle(&p[k], h[k], cudaIpcMemLazyEnablePeerAccess));
+            c->peer[r].x[0] = static_cast<float*>(p[0]);
+            c->peer[r].x[1] = static_cast<float*>(p[1]);
+            c->peer[r].flags = static_cast<int*>(p[2]);
+        }
+        for (int par = 0; par < 2; ++par) {
+            std::vector<float*> t(8, nullptr);
+            for (int r = 0; r < c->world; ++r) t[r] = c->peer[r].x[par];
+            SWF_CUDA(cudaMemcpy(c->d_xdst[par], t.data(), sizeof(float*) * 8, cudaMemcpyHostToDevice));
+        }
+        std::vector<int*> ft(8, nullptr);
+        for (int r = 0; r < c->world; ++r) ft[r] = c->peer[r].flags;
+        SWF_CUDA(cudaMemcpy(c->d_flag_table, ft.data(), sizeof(int*) * 8, cudaMemcpyHostToDevice));
+        c->peers = true;
+        SWF_CUDA(cudaDeviceSynchronize());
+    })
+}
+
+// ---------------------------------------------------------------- host-only planning (no GPU)
+// Window owner of every window under the given ownership rule (topology.hpp:107-109 for
+// round-robin), rank = a * wp_b + b.
+int swf_plan_owners(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, int ownership, int* owner) {
+    SWF_API_TRY({
+        require(owner && window_px > 0 && grid_h % window_px == 0 && grid_w % window_px == 0, "plan: bad grid");
+        const int ny = grid_h / window_px, nx = grid_w / window_px;
+        require(wp_a >= 1 && wp_b >= 1 && ny % wp_a == 0 && nx % wp_b == 0, "plan: WP grid does not divide windows");
+        for (int wy = 0; wy < ny; ++wy)
+            for (int wx = 0; wx < nx; ++wx) {
+                const int oa = ownership == SWF_OWN_ROUND_ROBIN ? wy % wp_a : wy / (ny / wp_a);
+                const int ob = ownership == SWF_OWN_ROUND_ROBIN ? wx % wp_b : wx / (nx / wp_b);
+                owner[wy * nx + wx] = oa * wp_b + ob;
+            }
+    })
+}
+
+// Tokens each rank sends to another rank at a block boundary shift_from -> shift_to (the
+// owner-changed tokens of shift_transfer_plan, topology.hpp:149-188): sent[src * world + dst].
+int swf_plan_exchange(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, int ownership, int shift_from,
+                      int shift_to, long long* sent) {
+    SWF_API_TRY({
+        const int ny = grid_h / window_px, nx = grid_w / window_px, world = wp_a * wp_b;
+        std::vector<int> own(size_t(ny) * nx);
+        const int rc = swf_plan_owners(grid_h, grid_w, window_px, wp_a, wp_b, ownership, own.data());
+        if (rc) return rc;
+        for (int i = 0; i < world * world; ++i) sent[i] = 0;
+        const Lay from = make_lay(grid_h, grid_w, window_px, shift_from), to = make_lay(grid_h, grid_w, window_px, shift_to);
+        const i64 N = i64(grid_h) * grid_w;
+        for (i64 p = 0; p < N; ++p) {
+            const int s = own[from.pix_to_win(p) / (window_px * window_px)];
+            const int d = own[to.pix_to_win(p) / (window_px * window_px)];
+            if (s != d) sent[s * world + d]++;
+        }
     })
 }
 

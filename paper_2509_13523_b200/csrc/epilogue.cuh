@@ -15,9 +15,11 @@ __device__ __forceinline__ void st_val<__nv_bfloat16>(__nv_bfloat16* p, float v)
 
 // RoPE (rope.hpp:34-44) on the pair (v0, v1) of column pair j of a head vector at window token
 // position (prow, pcol): pairs j < d/4 rotate with the row coordinate, the rest with the column.
+// Tables are [pair][position] (cos, sin), so the 32 lanes of a warp -- 32 consecutive tokens --
+// read one broadcast row entry and 32 contiguous column entries.
 __device__ __forceinline__ void rope_pair(const EpiParams& ep, int prow, int pcol, int j, float& v0, float& v1) {
     const int q4 = ep.d >> 2;
-    const float2 cs = j < q4 ? ep.rope_row[prow * q4 + j] : ep.rope_col[pcol * q4 + (j - q4)];
+    const float2 cs = j < q4 ? ep.rope_row[j * ep.rope_nrow + prow] : ep.rope_col[(j - q4) * ep.rope_ncol + pcol];
     const float x = v0, y = v1;
     v0 = cs.x * x - cs.y * y;
     v1 = cs.y * x + cs.x * y;

@@ -1,88 +1,67 @@
-// k_attn.cu -- BF16 windowed attention, flash-style: per (window, head, 128-query tile) CTA,
-// softmax(Q K^T / sqrt(d) + seam mask) V with an online max/sum (exp2, warp-shuffle row
-// reductions), K/V tiles double-buffered through shared memory with cp.async.
-// Restates head_attention_fwd (swin.hpp:161-188) without materialising the s x s logits; the
-// latitude-seam mask (window.hpp:107-122) becomes per-query KV-range limits, since the two seam
-// groups are the contiguous token ranges [0, (w-shift)*w) and [(w-shift)*w, w*w).
+// k_attn.cu -- BF16 windowed attention on the 5th-generation tensor cores (sm_100a).
+//
+// One CTA per (window, head, 128-query tile). Restates head_attention_fwd (swin.hpp:161-188)
+// without materialising the s x s logits:
+//   * S = Q K^T : tcgen05.mma (A = Q, B = K, both K-major SW128 smem tiles loaded by TMA),
+//     FP32 accumulator in TMEM, double-buffered so QK^T of tile j+1 overlaps softmax of tile j;
+//   * softmax: one thread per query row (TMEM lane), base-2 online max/sum, lazy O rescaling
+//     (only when the running max grows by > 2^8), P packed to BF16 and written back to TMEM;
+//   * O += P V : tcgen05.mma with the A operand (P) read from TMEM and B = V^T (K-major, written
+//     transposed by the QKV GEMM epilogue), FP32 O accumulator in TMEM;
+//   * the latitude-seam mask (window.hpp:107-122) is a per-query-tile KV range: the two seam
+//     groups are the contiguous token ranges [0, (w-shift)*w) and [(w-shift)*w, w*w).
+// Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4-w7 softmax + epilogue.
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace swf {
 
 namespace {
 
-constexpr int BQ = 128;  // queries per CTA (8 warps x 16 rows)
-constexpr int BKV = 64;  // keys per tile
-constexpr int kWarps = 8;
+using namespace tc;
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
-                                         uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
+constexpr int BQ = 128;   // queries per CTA (= UMMA M, = TMEM lanes)
+constexpr int BKV = 128;  // keys per tile
+constexpr int kThreads = 256;
+constexpr int kSoftWarp0 = 4;
+constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
 
 template <int D>
-struct Smem {
-    static constexpr int LD = D + 8;  // padded row (bf16) -> conflict-free ldmatrix
-    static constexpr int kQ = BQ * LD;
-    static constexpr int kKV = BKV * LD;
-    static constexpr int kBytes = (kQ + 4 * kKV) * 2;
+struct ACfg {
+    static constexpr int kSw = D >= 64 ? 128 : 2 * D;    // swizzle bytes of Q/K rows (d contiguous)
+    static constexpr int kColsPerBox = kSw / 2;           // d elements per TMA box row
+    static constexpr int kBoxes = D / kColsPerBox;        // boxes along d
+    static constexpr int kQBytes = BQ * D * 2;
+    static constexpr int kKBytes = BKV * D * 2;
+    static constexpr int kVBytes = D * BKV * 2;           // V^T tile: D rows x 128 keys (two SW128 boxes)
+    static constexpr int kStage = kKBytes + kVBytes;
+    static constexpr int kSmem = kQBytes + 2 * kStage + 1024 + 256;
+    static constexpr uint32_t kIdescS = idesc_bf16(BQ, BKV);
+    static constexpr uint32_t kIdescO = idesc_bf16(BQ, D);
+    static constexpr uint32_t kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256, 256+D)
 };
 
 template <int D>
-__device__ __forceinline__ void load_tile(__nv_bfloat16* dst, const __nv_bfloat16* src, int row0, int nrows_total,
-                                          int rows) {
-    constexpr int LD = Smem<D>::LD;
-    constexpr int CH = D / 8;  // 16-byte chunks per row
-    for (int c = threadIdx.x; c < rows * CH; c += kWarps * 32) {
-        const int r = c / CH, k = c - (c / CH) * CH;
-        const int gr = row0 + r;
-        const bool ok = gr < nrows_total;
-        const __nv_bfloat16* s = src + i64(ok ? gr : 0) * D + k * 8;
-        cp_async16(smem_addr(dst + r * LD + k * 8), s, ok ? 16 : 0);
-    }
-}
-
-template <int D>
-__global__ void __launch_bounds__(kWarps * 32, 1) k_attn_bf16(AttnParams p) {
-    using S = Smem<D>;
-    constexpr int LD = S::LD;
-    extern __shared__ __align__(128) uint8_t smraw[];
-    __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smraw);
-    __nv_bfloat16* sK = sQ + S::kQ;          // [2][BKV][LD]
-    __nv_bfloat16* sV = sK + 2 * S::kKV;     // [2][BKV][LD]
+__global__ void __launch_bounds__(kThreads, 1)
+    k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+              const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+    using C = ACfg<D>;
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = sm;
+    uint8_t* sKV = sm + C::kQBytes;  // [2][K tile | V^T tile]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::kQBytes + 2 * C::kStage);
+    const uint32_t q_full = smem_u32(&bars[0]);
+    const uint32_t kv_full0 = smem_u32(&bars[1]), kv_empty0 = smem_u32(&bars[3]);
+    const uint32_t s_full0 = smem_u32(&bars[5]), s_free0 = smem_u32(&bars[7]);
+    const uint32_t p_full0 = smem_u32(&bars[9]), o_done = smem_u32(&bars[11]);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[12]);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = p.s;
     const int q0 = blockIdx.x * BQ;
     const int head = blockIdx.y, lw = blockIdx.z;
-    const i64 base = (i64(lw) * p.heads + head) * s;
-    const __nv_bfloat16* Q = reinterpret_cast<const __nv_bfloat16*>(p.q) + base * D;
-    const __nv_bfloat16* K = reinterpret_cast<const __nv_bfloat16*>(p.k) + base * D;
-    const __nv_bfloat16* V = reinterpret_cast<const __nv_bfloat16*>(p.v) + base * D;
+    const int plane = lw * p.heads + head;
 
     // seam groups (window.hpp:58-65): only the last window row of a shifted layout is masked
     const int gw = p.lay.loc2glob[lw];
@@ -92,164 +71,210 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_attn_bf16(AttnParams p) {
     int kv_lo = 0, kv_hi = s;
     bool elementwise = false;
     if (masked) {
-        if (qlast < split) {
+        if (qlast < split)
             kv_hi = split;
-        } else if (q0 >= split) {
+        else if (q0 >= split)
             kv_lo = split;
-        } else {
+        else
             elementwise = true;
-        }
     }
     const int t_lo = kv_lo / BKV, t_hi = (kv_hi + BKV - 1) / BKV;
+    const int ntiles = t_hi - t_lo;
 
-    load_tile<D>(sQ, Q, q0, s, BQ);
-    load_tile<D>(sK, K, t_lo * BKV, s, BKV);
-    load_tile<D>(sV, V, t_lo * BKV, s, BKV);
-    cp_commit();
-
-    const int g = lane >> 2, tq = lane & 3;
-    const int r0 = q0 + warp * 16 + g;  // this thread's rows r0 and r0 + 8
-    const int grp0 = r0 < split ? 0 : 1, grp1 = (r0 + 8) < split ? 0 : 1;
-    const float sl2 = p.scale * 1.4426950408889634f;
-
-    uint32_t qf[D / 16][4];
-    float o[D / 8][4];
-#pragma unroll
-    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-
-    for (int t = t_lo; t < t_hi; ++t) {
-        const int buf = (t - t_lo) & 1;
-        if (t + 1 < t_hi) {
-            load_tile<D>(sK + (buf ^ 1) * S::kKV, K, (t + 1) * BKV, s, BKV);
-            load_tile<D>(sV + (buf ^ 1) * S::kKV, V, (t + 1) * BKV, s, BKV);
+    if (warp == 1 && lane == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(kv_full0 + 8 * i, 1);
+            mbar_init(kv_empty0 + 8 * i, 1);
+            mbar_init(s_full0 + 8 * i, 1);
+            mbar_init(s_free0 + 8 * i, 1);
+            mbar_init(p_full0 + 8 * i, 4);
         }
-        cp_commit();
-        cp_wait<1>();
-        __syncthreads();
-        if (t == t_lo) {
-#pragma unroll
-            for (int kc = 0; kc < D / 16; ++kc) {
-                const int row = warp * 16 + (lane & 15);
-                const int col = kc * 16 + (lane >> 4) * 8;
-                ldsm_x4(smem_addr(sQ + row * LD + col), qf[kc][0], qf[kc][1], qf[kc][2], qf[kc][3]);
-            }
-        }
-        const __nv_bfloat16* kt = sK + buf * S::kKV;
-        const __nv_bfloat16* vt = sV + buf * S::kKV;
-        // S = Q K^T : 16 x 64 per warp
-        float sc[BKV / 8][4];
-#pragma unroll
-        for (int nt = 0; nt < BKV / 8; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-#pragma unroll
-        for (int kc = 0; kc < D / 16; ++kc) {
-#pragma unroll
-            for (int np = 0; np < BKV / 16; ++np) {
-                // two n8 tiles (keys np*16 .. +16) x k16: ldmatrix x4 over K rows
-                uint32_t b0, b1, b2, b3;
-                const int krow = np * 16 + (lane & 7) + ((lane >> 4) << 3);
-                const int kcol = kc * 16 + ((lane >> 3) & 1) * 8;
-                ldsm_x4(smem_addr(kt + krow * LD + kcol), b0, b1, b2, b3);
-                mma16816(sc[2 * np], qf[kc][0], qf[kc][1], qf[kc][2], qf[kc][3], b0, b1);
-                mma16816(sc[2 * np + 1], qf[kc][0], qf[kc][1], qf[kc][2], qf[kc][3], b2, b3);
-            }
-        }
-        // scale, mask (ragged tail + seam), online softmax in base 2
-        const int kb = t * BKV;
-        float mx0 = m0, mx1 = m1;
-#pragma unroll
-        for (int nt = 0; nt < BKV / 8; ++nt) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int key = kb + nt * 8 + 2 * tq + (e & 1);
-                float v = sc[nt][e] * sl2;
-                bool keep = key < kv_hi && key >= kv_lo;
-                if (elementwise) keep = keep && ((key < split ? 0 : 1) == ((e < 2) ? grp0 : grp1));
-                v = keep ? v : -INFINITY;
-                sc[nt][e] = v;
-                if (e < 2)
-                    mx0 = fmaxf(mx0, v);
-                else
-                    mx1 = fmaxf(mx1, v);
-            }
-        }
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-        const float b0s = mx0 == -INFINITY ? 0.f : mx0;
-        const float b1s = mx1 == -INFINITY ? 0.f : mx1;
-        const float c0 = exp2f(m0 - b0s), c1 = exp2f(m1 - b1s);
-        m0 = mx0;
-        m1 = mx1;
-        l0 *= c0;
-        l1 *= c1;
-#pragma unroll
-        for (int i = 0; i < D / 8; ++i) {
-            o[i][0] *= c0;
-            o[i][1] *= c0;
-            o[i][2] *= c1;
-            o[i][3] *= c1;
-        }
-        uint32_t pf[BKV / 16][4];
-#pragma unroll
-        for (int nt = 0; nt < BKV / 8; ++nt) {
-            const float p0 = exp2f(sc[nt][0] - b0s), p1 = exp2f(sc[nt][1] - b0s);
-            const float p2 = exp2f(sc[nt][2] - b1s), p3 = exp2f(sc[nt][3] - b1s);
-            l0 += p0 + p1;
-            l1 += p2 + p3;
-            pf[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16x2(p0, p1);
-            pf[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16x2(p2, p3);
-        }
-        // O += P V : A = P (16 x 64), B = V (64 x D) via ldmatrix.trans
-#pragma unroll
-        for (int kc = 0; kc < BKV / 16; ++kc) {
-#pragma unroll
-            for (int np = 0; np < D / 16; ++np) {
-                uint32_t b0, b1, b2, b3;
-                const int vrow = kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-                const int vcol = np * 16 + (lane >> 4) * 8;
-                ldsm_x4_t(smem_addr(vt + vrow * LD + vcol), b0, b1, b2, b3);
-                mma16816(o[2 * np], pf[kc][0], pf[kc][1], pf[kc][2], pf[kc][3], b0, b1);
-                mma16816(o[2 * np + 1], pf[kc][0], pf[kc][1], pf[kc][2], pf[kc][3], b2, b3);
-            }
-        }
-        __syncthreads();
+        mbar_init(o_done, 1);
+        fence_barrier_init();
     }
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-    const float i0 = 1.f / l0, i1 = 1.f / l1;
-    __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(p.o);
+    if (warp == 2) tmem_alloc(smem_u32(tmem_slot), C::kTmemCols);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+            mbar_expect_tx(q_full, C::kQBytes);
+            for (int b = 0; b < C::kBoxes; ++b)
+                tma_load_2d(smem_u32(sQ + b * BQ * C::kSw), &tmQ, q_full, b * C::kColsPerBox, plane * s + q0);
+            for (int j = 0; j < ntiles; ++j) {
+                const int st = j & 1;
+                const int k0 = (t_lo + j) * BKV;
+                mbar_wait(kv_empty0 + 8 * st, ((j >> 1) & 1) ^ 1);
+                const uint32_t bar = kv_full0 + 8 * st;
+                mbar_expect_tx(bar, C::kStage);
+                uint8_t* sK = sKV + st * C::kStage;
+                uint8_t* sV = sK + C::kKBytes;
+                for (int b = 0; b < C::kBoxes; ++b)
+                    tma_load_2d(smem_u32(sK + b * BKV * C::kSw), &tmK, bar, b * C::kColsPerBox, plane * s + k0);
+                for (int b = 0; b < 2; ++b)  // V^T: D rows x 64 keys per box
+                    tma_load_2d(smem_u32(sV + b * D * 128), &tmV, bar, k0 + b * 64, plane * D);
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer
+        if (lane == 0) {
+            mbar_wait(q_full, 0);
+            auto issue_pv = [&](int i) {
+                const int b = i & 1;
+                mbar_wait(p_full0 + 8 * b, (i >> 1) & 1);
+                fence_after();
+                const uint8_t* sV = sKV + b * C::kStage + C::kKBytes;
 #pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt) {
-        const int col = head * D + nt * 8 + 2 * tq;
-        if (r0 < s) *reinterpret_cast<uint32_t*>(O + (i64(lw) * s + r0) * p.ldo + col) = pack_bf16x2(o[nt][0] * i0, o[nt][1] * i0);
-        if (r0 + 8 < s)
-            *reinterpret_cast<uint32_t*>(O + (i64(lw) * s + r0 + 8) * p.ldo + col) = pack_bf16x2(o[nt][2] * i1, o[nt][3] * i1);
+                for (int kk = 0; kk < BKV / 16; ++kk) {
+                    const uint32_t bA = tmem + uint32_t(b * 128 + kk * 8);  // P: bf16 pairs in S buffer cols
+                    const uint64_t bB = desc_kmajor(smem_u32(sV + (kk >> 2) * D * 128 + (kk & 3) * 32), 128);
+                    mma_ts(tmem + 256, bA, bB, C::kIdescO, (i > 0 || kk > 0) ? 1u : 0u);
+                }
+                commit(o_done);
+                commit(kv_empty0 + 8 * b);
+                commit(s_free0 + 8 * b);
+            };
+            for (int j = 0; j < ntiles; ++j) {
+                const int b = j & 1;
+                mbar_wait(kv_full0 + 8 * b, (j >> 1) & 1);
+                if (j >= 2) mbar_wait(s_free0 + 8 * b, ((j >> 1) - 1) & 1);
+                fence_after();
+                const uint8_t* sK = sKV + b * C::kStage;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const int box = (kk * 32) / C::kSw, off = (kk * 32) % C::kSw;
+                    const uint64_t a = desc_kmajor(smem_u32(sQ + box * BQ * C::kSw + off), C::kSw);
+                    const uint64_t bb = desc_kmajor(smem_u32(sK + box * BKV * C::kSw + off), C::kSw);
+                    mma_ss(tmem + uint32_t(b * 128), a, bb, C::kIdescS, kk > 0 ? 1u : 0u);
+                }
+                commit(s_full0 + 8 * b);
+                if (j >= 1) issue_pv(j - 1);
+            }
+            issue_pv(ntiles - 1);
+        }
+    } else if (warp >= kSoftWarp0) {
+        // ===== softmax (one thread per query row) + epilogue
+        const int r = (warp - kSoftWarp0) * 32 + lane;  // row in tile == TMEM lane
+        const int q = q0 + r;
+        const uint32_t lane_off = uint32_t((warp - kSoftWarp0) * 32) << 16;
+        const int gq = q < split ? 0 : 1;
+        const float sl2 = p.scale * 1.4426950408889634f;
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < ntiles; ++j) {
+            const int b = j & 1;
+            mbar_wait(s_full0 + 8 * b, (j >> 1) & 1);
+            fence_after();
+            uint32_t sr[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ld32(tmem + lane_off + uint32_t(b * 128 + c * 32), sr + 32 * c);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) wait_ld_dep(sr + 32 * c);
+            const int kb = (t_lo + j) * BKV;
+            float mx = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 128; ++i) {
+                const int key = kb + i;
+                bool keep = key < kv_hi && key >= kv_lo;
+                if (elementwise) keep = keep && ((key < split ? 0 : 1) == gq);
+                const float z = keep ? __uint_as_float(sr[i]) * sl2 : -INFINITY;
+                sr[i] = __float_as_uint(z);
+                mx = fmaxf(mx, z);
+            }
+            if (mx > m + kRescale || (m == -INFINITY && mx != -INFINITY)) {
+                if (m != -INFINITY && j > 0) {
+                    // O *= 2^(m - mx): PV of the previous tile must have landed in TMEM
+                    mbar_wait(o_done, (j - 1) & 1);
+                    fence_after();
+                    const float f = ex2(m - mx);
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t o[32];
+                        ld32(tmem + lane_off + uint32_t(256 + c * 32), o);
+                        wait_ld_dep(o);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+                        st32(tmem + lane_off + uint32_t(256 + c * 32), o);
+                    }
+                    wait_st();
+                    l *= f;
+                }
+                m = mx;
+            }
+            const float base = m == -INFINITY ? 0.f : m;
+            uint32_t pk[64];
+            float ls = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                const float p0 = ex2(__uint_as_float(sr[2 * i]) - base);
+                const float p1 = ex2(__uint_as_float(sr[2 * i + 1]) - base);
+                ls += p0 + p1;
+                pk[i] = pack_bf16x2(p0, p1);
+            }
+            l += ls;
+            st32(tmem + lane_off + uint32_t(b * 128), pk);
+            st32(tmem + lane_off + uint32_t(b * 128 + 32), pk + 32);
+            wait_st();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full0 + 8 * b);
+        }
+        // epilogue: O / l -> bf16, heads concatenated in token rows
+        mbar_wait(o_done, (ntiles - 1) & 1);
+        fence_after();
+        const float inv = 1.f / l;
+        __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(p.o) + (i64(lw) * s + q) * p.ldo + head * D;
+        for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            ld32(tmem + lane_off + uint32_t(256 + c * 32), o);
+            wait_ld_dep(o);
+            if (q < s) {
+                uint4* d4 = reinterpret_cast<uint4*>(O + c * 32);
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    d4[v] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * v]) * inv, __uint_as_float(o[8 * v + 1]) * inv),
+                                       pack_bf16x2(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv),
+                                       pack_bf16x2(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv),
+                                       pack_bf16x2(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv));
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        tmem_free(tmem, C::kTmemCols);
     }
 }
 
 template <int D>
-void launch_attn(const AttnParams& p, cudaStream_t st) {
+void launch(const AttnParams& p, cudaStream_t st) {
+    using C = ACfg<D>;
     static bool configured = false;
     if (!configured) {
-        SWF_CUDA(cudaFuncSetAttribute(k_attn_bf16<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<D>::kBytes));
+        SWF_CUDA(cudaFuncSetAttribute(k_attn_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         configured = true;
     }
     dim3 grid(unsigned((p.s + BQ - 1) / BQ), unsigned(p.heads), unsigned(p.nloc));
-    k_attn_bf16<D><<<grid, kWarps * 32, Smem<D>::kBytes, st>>>(p);
+    k_attn_tc<D><<<grid, kThreads, C::kSmem, st>>>(*reinterpret_cast<const CUtensorMap*>(p.tmq),
+                                                  *reinterpret_cast<const CUtensorMap*>(p.tmk),
+                                                  *reinterpret_cast<const CUtensorMap*>(p.tmv), p);
     SWF_LAUNCH_CHECK();
 }
 
 }  // namespace
 
 void attention_bf16(const AttnParams& p, cudaStream_t st) {
+    if (!p.tmq || !p.tmk || !p.tmv) throw CudaError("attention_bf16: TMA descriptors missing");
     switch (p.d) {
-        case 32: launch_attn<32>(p, st); break;
-        case 64: launch_attn<64>(p, st); break;
-        case 128: launch_attn<128>(p, st); break;
+        case 32: launch<32>(p, st); break;
+        case 64: launch<64>(p, st); break;
+        case 128: launch<128>(p, st); break;
         default: throw CudaError("attention_bf16: head_dim must be 32, 64 or 128");
     }
 }

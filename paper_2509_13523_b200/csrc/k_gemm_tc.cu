@@ -12,6 +12,7 @@
 
 #include "../../include/swinflow_capi.h"
 #include "epilogue.cuh"
+#include "tc_ptx.cuh"
 
 namespace swf {
 
@@ -105,15 +106,8 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    tc::ld32(taddr, r);
+    tc::wait_ld_dep(r);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
@@ -168,6 +162,15 @@ __device__ __forceinline__ void epi32(const EpiParams& ep, i64 m, int n0, float*
             const int pcol = wx * w + ep.cur.g.shift + tok % w;
 #pragma unroll
             for (int j = 0; j < 32; j += 2) rope_pair(ep, prow, pcol, (dd + j) >> 1, v[j], v[j + 1]);
+        }
+        if (which == 2) {
+            // V is stored transposed ([window][head][d][token]) so the attention's P.V MMA reads a
+            // K-major operand; the 32 lanes of a warp hold consecutive tokens -> 64 B per store.
+            __nv_bfloat16* vt = reinterpret_cast<__nv_bfloat16*>(ep.out) + 2 * ep.plane +
+                                ((i64(lw) * ep.heads + head) * ep.d + dd) * s + tok;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) vt[i64(j) * s] = __float2bfloat16_rn(v[j]);
+            return;
         }
         __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ep.out) + which * ep.plane +
                              ((i64(lw) * ep.heads + head) * s + tok) * ep.d + dd;
@@ -420,6 +423,21 @@ void make_tma_bf16(TmaMap* m, const void* base, i64 rows, i64 kcols, int box_row
                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
+void make_tma_bf16_2d(TmaMap* m, const void* base, i64 rows, i64 inner, int box_inner, int box_rows, int swizzle) {
+    if ((inner * 2) % 16 != 0) throw CudaError("make_tma_bf16_2d: row pitch must be a multiple of 16 bytes");
+    cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(inner) * 2};
+    cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw = swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                  : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r = encode_fn()(reinterpret_cast<CUtensorMap*>(m), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (2d) failed: " + std::to_string(int(r)));
 }
 
 void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int BN, int mode, const EpiParams& ep,

@@ -51,8 +51,9 @@ struct EpiParams {
     int ld_out;      // SWIGLU: row stride of s; DECODE: cout
     int h, d, heads;
     int G;           // SWIGLU interleave granularity
-    const float2* rope_row;  // [(H+w)][d/4] (cos, sin)
-    const float2* rope_col;  // [(W+w)][d/4]
+    const float2* rope_row;  // [d/4][H+w] (cos, sin)
+    const float2* rope_col;  // [d/4][W+w]
+    int rope_nrow, rope_ncol;
     LayMap cur, nxt;
     float out_scale;
 };
@@ -67,6 +68,9 @@ struct alignas(64) TmaMap {
     uint64_t bytes[16];
 };
 void make_tma_bf16(TmaMap* m, const void* base, i64 rows, i64 kcols, int box_rows);
+// General 2D bf16 map: inner extent `inner` (elements), `rows` rows, box {box_inner, box_rows},
+// swizzle in bytes (64 or 128).
+void make_tma_bf16_2d(TmaMap* m, const void* base, i64 rows, i64 inner, int box_inner, int box_rows, int swizzle);
 
 // tcgen05/TMEM/TMA BF16 GEMM (2-CTA pairs, persistent, warp-specialised): C[M][Npad] = A . B^T,
 // A = [M][K] (box 128 rows), B = [Npad][K] (box BN/2 rows), BN in {128, 256}, K % 64 == 0.
@@ -76,13 +80,16 @@ void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int 
 // ------------------------------------------------------------------ attention
 struct AttnParams {
     const void* q;  // [nloc][heads][s][d]
-    const void* k;
-    const void* v;
+    const void* k;  // [nloc][heads][s][d]
+    const void* v;  // FP32 path: [nloc][heads][s][d]; BF16 path: V^T [nloc][heads][d][s]
     void* o;        // [nloc*s][ldo] head-concatenated
     int ldo;
     int nloc, heads, s, d, w;
     LayMap lay;     // masked windows: shifted layout, last window row
     float scale;    // 1/sqrt(d)
+    const TmaMap* tmq;  // BF16 path: TMA maps of the q / k planes ([rows][d]) and of V^T ([rows][s])
+    const TmaMap* tmk;
+    const TmaMap* tmv;
 };
 void attention_f32(const AttnParams& p, cudaStream_t st);
 void attention_bf16(const AttnParams& p, cudaStream_t st);

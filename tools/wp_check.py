@@ -1,0 +1,64 @@
+"""Window-parallel correctness on N GPUs (launch with torchrun): the WP forward must equal the
+single-GPU forward BITWISE (ownership only permutes independent rows/windows; the GEMM K-loop
+order does not depend on M), and both must match the oracle at the BF16 tolerance."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2509_13523_b200 as swf  # noqa: E402
+from oracle import pyoracle as o  # noqa: E402
+
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+local = int(os.environ.get("LOCAL_RANK", rank))
+torch.cuda.set_device(local)
+dist.init_process_group("gloo")
+wp = {2: (1, 2), 4: (2, 2), 8: (2, 4)}[world]
+own = int(os.environ.get("SWF_OWN", swf.OWN_CONTIGUOUS))
+ok = True
+for name, d, H, W in [
+    ("C1", dict(hidden_dim=128, n_heads=4, ffn_dim=256, n_layers=2, window_px=8, in_channels=8, out_channels=3,
+                time_dim=128), 32, 64),
+    ("MID", dict(hidden_dim=256, n_heads=2, ffn_dim=512, n_layers=3, window_px=12, in_channels=16, out_channels=6,
+                 time_dim=256), 48, 96),
+]:
+    oc, sc = o.ModelConfig(**d), swf.ModelConfig(**d)
+    p = o.init_params(oc, 7, random=True, scale=0.03, dtype=np.float32)
+    x = o.random_field(oc.in_channels, H * W, 8).astype(np.float32)
+    dn = swf.Denoiser(sc, H, W, device=local, precision=swf.PREC_BF16, topology=(wp[0], wp[1], 1, rank, own))
+    dn.load_params(p)
+    dn.connect_peers_torch(dist)
+    y = dn.forward(x, 0.9)
+    for _ in range(3):  # repeated calls exercise the start-of-forward barrier
+        y2 = dn.forward(x, 0.9)
+        ok &= np.array_equal(y, y2)
+    owned = np.zeros(H * W, np.int64)
+    swf.lib().swf_owned_pixels(dn._c, owned.ctypes.data_as(swf.C.c_void_p))
+    n_loc = dn.local_tokens()
+    parts = [None] * world
+    dist.all_gather_object(parts, (owned[:n_loc], y[owned[:n_loc]]))
+    if rank == 0:
+        y_wp = np.zeros_like(y)
+        cover = np.zeros(H * W, np.int64)
+        for pix, vals in parts:
+            y_wp[pix] = vals
+            cover[pix] += 1
+        single = swf.Denoiser(sc, H, W, device=local, precision=swf.PREC_BF16)
+        single.load_params(p)
+        y1 = single.forward(x, 0.9)
+        ref = o.forward(oc, p, x, np.float32(0.9), H, W)
+        scale = np.maximum(np.abs(ref).max(axis=0), 1e-30)
+        err = float((np.abs(y_wp - ref).max(axis=0) / scale).max())
+        bitwise = np.array_equal(y_wp, y1)
+        print(f"{name}: world={world} wp={wp} own={own} cover_ok={bool((cover == 1).all())} "
+              f"bitwise_vs_1gpu={bitwise} err_vs_oracle={err:.3e}", flush=True)
+        ok &= bool((cover == 1).all()) and bitwise and err <= 2e-2
+    dn.close()
+dist.barrier()
+if rank == 0:
+    print("WP_CHECK", "PASS" if ok else "FAIL", flush=True)
+dist.destroy_process_group()
+sys.exit(0 if ok else 1)
