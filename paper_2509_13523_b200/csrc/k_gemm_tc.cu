@@ -30,7 +30,8 @@ struct Cfg {
     static constexpr int kStage = kStageA + kStageB;
     static constexpr int kStages = (BN == 256) ? 6 : 8;
     static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
-    static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kStageFloats = 4 * 32 * 33;  // epilogue transpose buffers (4 warps x 32x33)
+    static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/ + kStageFloats * 4;
     static constexpr uint32_t kIdesc = (1u << 4)                 // D = F32
                                        | (1u << 7) | (1u << 10)  // A, B = BF16
                                        | (uint32_t(BN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
@@ -200,6 +201,54 @@ __device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0,
     }
 }
 
+// Grouped rasterisation: bands of kGroupM m-blocks are swept n-block by n-block, so the concurrent
+// clusters share a few A row-blocks and a few B column-blocks (both L2-resident).
+constexpr int kGroupM = 16;
+__device__ __forceinline__ void tile_coords(i64 t, int n_tiles, i64 m_tiles, int& m_blk, int& n_blk) {
+    const i64 per_group = i64(kGroupM) * n_tiles;
+    const i64 g = t / per_group;
+    const i64 r = t - g * per_group;
+    const i64 gm = min(i64(kGroupM), m_tiles - g * kGroupM);
+    n_blk = int(r / gm);
+    m_blk = int(g * kGroupM + r % gm);
+}
+
+// fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)
+// is transposed through shared memory so each global access is one contiguous 128-byte row segment.
+template <int MODE>
+__device__ __forceinline__ void epi32_coalesced(const EpiParams& ep, i64 row, int n0, const float* v, float* stg,
+                                                float* drow, int lane) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+    __syncwarp();
+    const i64 row0 = row - lane;
+    const int n = n0 + lane;
+    const bool col_ok = n < ep.N;
+    const int h = ep.h;
+    const i64 mrem = ep.M - row0;  // rows of this 32-row group that exist
+    if constexpr (MODE == EPI_ENCODE) {
+        const float b = col_ok ? ep.bias[n] : 0.f;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr)
+            if (rr < mrem && col_ok) ep.x[(row0 + rr) * h + n] = stg[rr * 33 + lane] + b;
+    } else {
+        // all 32 row reads in flight before any dependent store (latency hiding with 4 warps)
+        float xv[32];
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) xv[rr] = (rr < mrem && col_ok) ? ep.x[(row0 + rr) * h + n] : 0.f;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+            float* dst;
+            if constexpr (MODE == EPI_DOWN)
+                dst = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(drow), rr)) + n;
+            else
+                dst = ep.x + (row0 + rr) * h + n;
+            if (rr < mrem && col_ok) *dst = xv[rr] + stg[rr * 33 + lane];
+        }
+    }
+    __syncwarp();
+}
+
 // ---------------------------------------------------------------- the kernel
 template <int BN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -255,7 +304,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (i64 t = cluster_id; t < total; t += n_clusters) {
-                const int m_blk = int(t / n_tiles), n_blk = int(t % n_tiles);
+                int m_blk, n_blk;
+                tile_coords(t, n_tiles, m_tiles, m_blk, n_blk);
                 const int row_a = m_blk * 2 * BM + int(crank) * BM;
                 const int row_b = n_blk * BN + int(crank) * (BN / 2);
                 for (int kb = 0; kb < num_k; ++kb) {
@@ -310,8 +360,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = map_to_rank(smem_u32(&tempty_bar[0]), 0);
+        float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256) + q * 32 * 33;
         for (i64 t = cluster_id; t < total; t += n_clusters) {
-            const int m_blk = int(t / n_tiles), n_blk = int(t % n_tiles);
+            int m_blk, n_blk;
+            tile_coords(t, n_tiles, m_tiles, m_blk, n_blk);
             mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
             tc_fence_after();
             const i64 row = i64(m_blk) * 2 * BM + crank * BM + q * 32 + lane;
@@ -324,6 +376,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tmem_ld32(tbase + ch * 32, g);
                     tmem_ld32(tbase + BN / 2 + ch * 32, u);
                     epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u);
+                }
+            } else if constexpr (MODE == EPI_ENCODE || MODE == EPI_RESID || MODE == EPI_DOWN) {
+                float* drow = nullptr;
+                if constexpr (MODE == EPI_DOWN) {
+                    // destination row in the next block's layout, possibly on a peer GPU (NVLink)
+                    if (row < ep.M) {
+                        int rank;
+                        const i64 li = ep.nxt.pix_to_loc(ep.cur.loc_to_pix(row), &rank);
+                        drow = ep.xdst[rank] + li * ep.h;
+                    }
+                }
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 32; ++ch) {
+                    float v[32];
+                    tmem_ld32(tbase + ch * 32, v);
+                    epi32_coalesced<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, drow, lane);
                 }
             } else {
 #pragma unroll 1
