@@ -140,6 +140,9 @@ long long swf_kernel_launches(swf_ctx* ctx);
  * 5 gate/up GEMM, 6 down GEMM, 7 decode GEMM, 8 other. swf_profile resets the counters. */
 int swf_profile(swf_ctx* ctx, int enable);
 int swf_profile_read(swf_ctx* ctx, double* ms, long long* launches, int n_classes);
+/* Replay one kernel class (1..6 above) reps times back-to-back on the resident buffers of the
+ * last forward for block blk; *ms = mean device time per launch (kernel isolation at steady clocks). */
+int swf_bench_kernel(swf_ctx* ctx, int kernel_class, int block, int reps, double* ms);
 /* Noise field (diffusion.hpp:91-108) for (run_seed, event) into a host C x N buffer (fp32). */
 int swf_noise_field(swf_ctx* ctx, uint64_t run_seed, uint64_t event, int channels, double sigma_d, float* out);
 /* Run one bf16 GEMM self-test of the tcgen05 kernel: C = A.B^T on device, returns max |err|

@@ -128,6 +128,7 @@ def lib():
         L.swf_owned_pixels.argtypes = [vp, vp]
         L.swf_kernel_launches.argtypes = [vp]
         L.swf_kernel_launches.restype = ll
+        L.swf_bench_kernel.argtypes = [vp, i, i, i, C.POINTER(d)]
         L.swf_profile.argtypes = [vp, i]
         L.swf_profile_read.argtypes = [vp, vp, vp, i]
         L.swf_noise_field.argtypes = [vp, u64, u64, i, d, vp]
@@ -251,6 +252,11 @@ class Denoiser:
         cnt = (C.c_longlong * n)()
         _check(lib().swf_profile_read(self._c, ms, cnt, n))
         return {k: (ms[i], cnt[i]) for i, k in enumerate(self.KERNEL_CLASSES)}
+
+    def bench_kernel(self, name: str, block: int = 1, reps: int = 10) -> float:
+        ms = C.c_double()
+        _check(lib().swf_bench_kernel(self._c, self.KERNEL_CLASSES.index(name), block, reps, C.byref(ms)))
+        return ms.value
 
     def kernel_launches(self) -> int:
         return lib().swf_kernel_launches(self._c)

@@ -1330,6 +1330,95 @@ int swf_owned_pixels(swf_ctx* c, long long* pixels) {
 
 long long swf_kernel_launches(swf_ctx* c) { return c ? c->launches : -1; }
 
+// Replay one kernel class `reps` times back-to-back on the resident buffers of the last forward
+// (block `blk`), timed with CUDA events on the context stream: isolates a kernel at steady clocks.
+// Classes as in swf_profile_read. Returns the mean ms per launch.
+int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
+    SWF_API_TRY({
+        require(c && ms && reps > 0, "bad argument");
+        require(c->loaded && c->prec == SWF_PREC_BF16, "bench_kernel: BF16 context with parameters required");
+        const Dims& m = c->m;
+        require(blk >= 0 && blk < m.nb, "bench_kernel: block out of range");
+        const i64 M = c->M;
+        const int par = blk & 1;
+        EpiParams ep = base_ep(c);
+        const float* six = c->six + size_t(blk) * 6 * m.h;
+        __nv_bfloat16* xm = static_cast<__nv_bfloat16*>(c->xm);
+        auto once = [&]() {
+            EpiParams e = ep;
+            switch (kclass) {
+                case K_RMS:
+                    rms_modulate<__nv_bfloat16>(c->xbuf[0], M, m.h, m.hp, c->g_attn, six, six + m.h, six + 2 * m.h,
+                                                xm, nullptr, 0, c->st);
+                    break;
+                case K_QKV:
+                    e.cur = c->lay[par];
+                    e.out = c->qkv;
+                    e.plane = M * m.h;
+                    e.N = 3 * m.h;
+                    gemm_bf16_tc(c->tm_xm, c->tm_qkv[blk], M, m.np_qkv, m.hp, m.bn_qkv, EPI_QKV, e, c->st);
+                    break;
+                case K_ATTN: {
+                    AttnParams ap;
+                    ap.q = c->qkv;
+                    ap.k = static_cast<const char*>(c->qkv) + size_t(M) * m.h * 2;
+                    ap.v = static_cast<const char*>(c->qkv) + size_t(2) * M * m.h * 2;
+                    ap.o = c->sbuf;  // scratch: keep xm intact
+                    ap.ldo = m.hp;
+                    ap.nloc = c->lay[par].nloc;
+                    ap.heads = m.heads;
+                    ap.s = m.w * m.w;
+                    ap.d = m.d;
+                    ap.w = m.w;
+                    ap.lay = c->lay[par];
+                    ap.scale = 1.0f / std::sqrt(float(m.d));
+                    ap.tmq = &c->tm_q;
+                    ap.tmk = &c->tm_k;
+                    ap.tmv = &c->tm_vt;
+                    attention_bf16(ap, c->st);
+                    break;
+                }
+                case K_OUT:
+                    e.x = c->xbuf[1];
+                    e.N = m.h;
+                    gemm_bf16_tc(c->tm_xm, c->tm_out[blk], M, m.np_out, m.hp, m.bn_out, EPI_RESID, e, c->st);
+                    break;
+                case K_GATEUP:
+                    e.out = c->sbuf;
+                    e.ld_out = m.fp;
+                    e.N = m.f;
+                    e.G = m.G;
+                    gemm_bf16_tc(c->tm_xm, c->tm_gu[blk], M, m.np_gu, m.hp, m.bn_gu, EPI_SWIGLU, e, c->st);
+                    break;
+                case K_DOWN:
+                    e.x = c->xbuf[0];
+                    e.N = m.h;
+                    e.cur = c->lay[par];
+                    e.nxt = c->lay[par ^ 1];
+                    e.xdst = c->d_xdst[1];
+                    gemm_bf16_tc(c->tm_s, c->tm_down[blk], M, m.np_down, m.fp, m.bn_down, EPI_DOWN, e, c->st);
+                    break;
+                default:
+                    throw ConfigError("bench_kernel: unsupported kernel class");
+            }
+        };
+        SWF_CUDA(cudaSetDevice(c->dev));
+        once();
+        cudaEvent_t a, b;
+        SWF_CUDA(cudaEventCreate(&a));
+        SWF_CUDA(cudaEventCreate(&b));
+        SWF_CUDA(cudaEventRecord(a, c->st));
+        for (int i = 0; i < reps; ++i) once();
+        SWF_CUDA(cudaEventRecord(b, c->st));
+        SWF_CUDA(cudaEventSynchronize(b));
+        float t = 0.f;
+        SWF_CUDA(cudaEventElapsedTime(&t, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *ms = double(t) / reps;
+    })
+}
+
 int swf_profile(swf_ctx* c, int enable) {
     SWF_API_TRY({
         require(c, "null context");

@@ -11,11 +11,12 @@
 //     P is packed to BF16 and written back into the S_h columns of TMEM;
 //   * O_h += P_h V : tcgen05.mma with A = P_h read from TMEM and B = V^T (K-major, written
 //     transposed by the QKV GEMM epilogue); O_h accumulates in TMEM; K/V tiles are shared by both
-//     query tiles (2-stage TMA ring);
+//     query tiles (3-stage K ring freed after QK^T, 2-stage V^T ring freed after PV);
 //   * the latitude-seam mask (window.hpp:107-122) is a per-row key range: the two seam groups are
 //     the contiguous token ranges [0, (w-shift)*w) and [(w-shift)*w, w*w); fully-outside key tiles
 //     are skipped and only boundary tiles pay per-element masking.
-// Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4-w7 softmax(q-tile 0),
+// Warp roles: w0 TMA producer (Q, K ring), w3 TMA producer (V^T ring), w1 MMA issuer, w2 TMEM allocator,
+// w4-w7 softmax(q-tile 0),
 // w8-w11 softmax(q-tile 1). TMEM: S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D).
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
@@ -39,14 +40,14 @@ struct ACfg {
     static constexpr int kQBytes = BQ * D * 2;          // one query tile
     static constexpr int kKBytes = BKV * D * 2;
     static constexpr int kVBytes = D * BKV * 2;         // V^T tile: D rows x 128 keys (two SW128 boxes)
-    static constexpr int kStage = kKBytes + kVBytes;
-    static constexpr int kSmem = 2 * kQBytes + 2 * kStage + 1024 + 256;
+    static constexpr int kNK = 3, kNV = 2;  // K ring (freed after QK^T) deeper than the V ring
+    static constexpr int kSmem = 2 * kQBytes + kNK * kKBytes + kNV * kVBytes + 1024 + 256;
     static constexpr uint32_t kIdescS = idesc_bf16(BQ, BKV);
     static constexpr uint32_t kIdescO = idesc_bf16(BQ, D);
 };
 
 // barrier slots (u64 each)
-enum : int { B_Q = 0, B_KVF = 1, B_KVE = 3, B_SF = 5, B_PF = 7, B_OD = 9, B_NUM = 11 };
+enum : int { B_Q = 0, B_KF = 1, B_KE = 4, B_VF = 7, B_VE = 9, B_SF = 11, B_PF = 13, B_OD = 15, B_NUM = 17 };
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -55,9 +56,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     using C = ACfg<D>;
     extern __shared__ __align__(1024) uint8_t smraw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = sm;                     // [2][BQ x D]
-    uint8_t* sKV = sm + 2 * C::kQBytes;   // [2 stages][K tile | V^T tile]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + 2 * C::kStage);
+    uint8_t* sQ = sm;                                // [2][BQ x D]
+    uint8_t* sK = sm + 2 * C::kQBytes;               // [kNK][BKV x D]
+    uint8_t* sV = sK + C::kNK * C::kKBytes;          // [kNV][D x BKV] (V^T)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::kNV * C::kVBytes);
     auto bar = [&](int slot) { return smem_u32(&bars[slot]); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[B_NUM]);
 
@@ -80,9 +82,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 1 && lane == 0) {
         mbar_init(bar(B_Q), 1);
+        for (int i = 0; i < C::kNK; ++i) {
+            mbar_init(bar(B_KF + i), 1);
+            mbar_init(bar(B_KE + i), 1);
+        }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(bar(B_KVF + i), 1);
-            mbar_init(bar(B_KVE + i), 1);
+            mbar_init(bar(B_VF + i), 1);
+            mbar_init(bar(B_VE + i), 1);
             mbar_init(bar(B_SF + i), 1);
             mbar_init(bar(B_PF + i), 4);
             mbar_init(bar(B_OD + i), 1);
@@ -99,41 +105,48 @@ __global__ void __launch_bounds__(kThreads, 1)
     // softmax warpgroups hold a 128-column S row each (64K-register file: 128*40 + 256*232)
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp == 0) {
-        // ===== TMA producer: both query tiles, then the K / V^T ring
+        // ===== TMA producer 1: both query tiles, then the K ring
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
             mbar_expect_tx(bar(B_Q), nq * C::kQBytes);
             for (int h = 0; h < nq; ++h)
                 for (int b = 0; b < C::kBoxes; ++b)
                     tma_load_2d(smem_u32(sQ + h * C::kQBytes + b * BQ * C::kSw), &tmQ, bar(B_Q),
                                 b * C::kColsPerBox, plane * s + q0 + h * BQ);
             for (int j = 0; j < ntiles; ++j) {
-                const int st = j & 1;
-                const int k0 = (t_lo + j) * BKV;
-                mbar_wait(bar(B_KVE + st), ((j >> 1) & 1) ^ 1);
-                mbar_expect_tx(bar(B_KVF + st), C::kStage);
-                uint8_t* sK = sKV + st * C::kStage;
-                uint8_t* sV = sK + C::kKBytes;
+                const int st = j % C::kNK;
+                mbar_wait(bar(B_KE + st), ((j / C::kNK) & 1) ^ 1);
+                mbar_expect_tx(bar(B_KF + st), C::kKBytes);
                 for (int b = 0; b < C::kBoxes; ++b)
-                    tma_load_2d(smem_u32(sK + b * BKV * C::kSw), &tmK, bar(B_KVF + st), b * C::kColsPerBox,
-                                plane * s + k0);
-                for (int b = 0; b < 2; ++b)  // V^T: D rows x 64 keys per box
-                    tma_load_2d(smem_u32(sV + b * D * 128), &tmV, bar(B_KVF + st), k0 + b * 64, plane * D);
+                    tma_load_2d(smem_u32(sK + st * C::kKBytes + b * BKV * C::kSw), &tmK, bar(B_KF + st),
+                                b * C::kColsPerBox, plane * s + (t_lo + j) * BKV);
+            }
+        }
+    } else if (warp == 3) {
+        // ===== TMA producer 2: the V^T ring (D rows x 64 keys per box)
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+            for (int j = 0; j < ntiles; ++j) {
+                const int st = j & 1;
+                mbar_wait(bar(B_VE + st), ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(bar(B_VF + st), C::kVBytes);
+                for (int b = 0; b < 2; ++b)
+                    tma_load_2d(smem_u32(sV + st * C::kVBytes + b * D * 128), &tmV, bar(B_VF + st),
+                                (t_lo + j) * BKV + b * 64, plane * D);
             }
         }
     } else if (warp == 1) {
         // ===== MMA issuer
         if (lane == 0) {
             auto issue_s = [&](int h, int j) {  // S_h = Q_h K_j^T
-                const uint8_t* sK = sKV + (j & 1) * C::kStage;
+                const uint8_t* kt = sK + (j % C::kNK) * C::kKBytes;
                 const uint8_t* qh = sQ + h * C::kQBytes;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const int box = (kk * 32) / C::kSw, off = (kk * 32) % C::kSw;
                     const uint64_t a = desc_kmajor(smem_u32(qh + box * BQ * C::kSw + off), C::kSw);
-                    const uint64_t b = desc_kmajor(smem_u32(sK + box * BKV * C::kSw + off), C::kSw);
+                    const uint64_t b = desc_kmajor(smem_u32(kt + box * BKV * C::kSw + off), C::kSw);
                     mma_ss(tmem + uint32_t(h * 128), a, b, C::kIdescS, kk > 0 ? 1u : 0u);
                 }
                 commit(bar(B_SF + h));
@@ -141,35 +154,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             auto issue_pv = [&](int h, int j) {  // O_h += P_h V_j
                 mbar_wait(bar(B_PF + h), j & 1);
                 fence_after();
-                const uint8_t* sV = sKV + (j & 1) * C::kStage + C::kKBytes;
+                const uint8_t* vt = sV + (j & 1) * C::kVBytes;
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk) {
-                    const uint64_t b = desc_kmajor(smem_u32(sV + (kk >> 2) * D * 128 + (kk & 3) * 32), 128);
+                    const uint64_t b = desc_kmajor(smem_u32(vt + (kk >> 2) * D * 128 + (kk & 3) * 32), 128);
                     mma_ts(tmem + uint32_t(256 + h * 128), tmem + uint32_t(h * 128 + kk * 8), b, C::kIdescO,
                            (j > 0 || kk > 0) ? 1u : 0u);
                 }
                 commit(bar(B_OD + h));
             };
+            auto wait_k = [&](int j) {
+                mbar_wait(bar(B_KF + j % C::kNK), (j / C::kNK) & 1);
+                fence_after();
+            };
             mbar_wait(bar(B_Q), 0);
-            mbar_wait(bar(B_KVF + 0), 0);
-            fence_after();
+            wait_k(0);
             issue_s(0, 0);
             if (nq == 2) issue_s(1, 0);
+            commit(bar(B_KE + 0));  // K_0 consumed once both S MMAs complete
             for (int j = 0; j < ntiles; ++j) {
                 const bool more = j + 1 < ntiles;
+                mbar_wait(bar(B_VF + (j & 1)), (j >> 1) & 1);
+                fence_after();
                 // P_0 V_j, then S_0 of the next key tile (in-order tensor pipe: S_0 overwrites P_0 after
                 // the P V that reads it)
                 issue_pv(0, j);
                 if (more) {
-                    mbar_wait(bar(B_KVF + ((j + 1) & 1)), ((j + 1) >> 1) & 1);
-                    fence_after();
+                    wait_k(j + 1);
                     issue_s(0, j + 1);
                 }
                 if (nq == 2) {
                     issue_pv(1, j);
                     if (more) issue_s(1, j + 1);
                 }
-                commit(bar(B_KVE + (j & 1)));  // K_j / V_j consumed
+                commit(bar(B_VE + (j & 1)));  // V_j consumed
+                if (more) commit(bar(B_KE + (j + 1) % C::kNK));
             }
         }
     } else if (warp >= 4) {

@@ -377,7 +377,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tmem_ld32(tbase + BN / 2 + ch * 32, u);
                     epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u);
                 }
-            } else if constexpr (MODE == EPI_ENCODE || MODE == EPI_RESID || MODE == EPI_DOWN) {
+            } else if constexpr (MODE == EPI_DOWN) {
                 float* drow = nullptr;
                 if constexpr (MODE == EPI_DOWN) {
                     // destination row in the next block's layout, possibly on a peer GPU (NVLink)
