@@ -1,0 +1,31 @@
+"""Window-parallel forward on >= 2 GPUs (torchrun, one process per GPU): output must equal the
+single-GPU forward bitwise for both the contiguous and the reference round-robin ownership, and
+match the oracle at the BF16 tolerance. Skipped when fewer than 2 GPUs are visible."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("own", [0, 1])
+def test_wp_bitwise_equals_single_gpu(own):
+    n = 4 if _ngpus() >= 4 else 2
+    env = dict(os.environ, SWF_OWN=str(own))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(29600 + own),
+                        os.path.join(ROOT, "tools", "wp_check.py")], capture_output=True, text=True, timeout=600,
+                       env=env, cwd=ROOT)
+    assert "WP_CHECK PASS" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
