@@ -253,8 +253,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
-                        const float p0 = ex2(fmaf(__uint_as_float(sr[32 * c + 2 * i]), sl2, nb));
-                        const float p1 = ex2(fmaf(__uint_as_float(sr[32 * c + 2 * i + 1]), sl2, nb));
+                        // 1 in 4 exponentials on the FMA pipe, the rest on MUFU (balances the two)
+                        const float z0 = fmaf(__uint_as_float(sr[32 * c + 2 * i]), sl2, nb);
+                        const float z1 = fmaf(__uint_as_float(sr[32 * c + 2 * i + 1]), sl2, nb);
+                        const float p0 = ex2(z0);
+                        const float p1 = (i & 1) ? ex2_poly(z1) : ex2(z1);
                         ls4[i & 3] += p0 + p1;
                         pk[i] = pack_bf16x2(p0, p1);
                     }
