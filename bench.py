@@ -201,8 +201,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     cfg = swf.ModelConfig(**CFG)
-    wp = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}[world]
-    topo = (wp[0], wp[1], 1, rank, swf.OWN_CONTIGUOUS) if world > 1 else None
+    sp = args.sp
+    wp = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}[world // sp]
+    topo = (wp[0], wp[1], sp, rank, swf.OWN_CONTIGUOUS) if world > 1 else None
     dn = swf.Denoiser(cfg, H, W, device=local_rank, precision=swf.PREC_BF16, topology=topo)
     if world > 1:
         dn.connect_peers_torch(dist)
@@ -301,7 +302,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "AERIS-1.3B-shaped denoiser step (BASELINE.json configs[1])", "grid": [H, W],
                        "model": "swin-dit-1.3B (h=1536, 12 heads, ffn 9216, 20 blocks, w=60, C_in=144, C_out=70)",
-                       "parallelism": f"wp{wp[0]}x{wp[1]}", "params": swf.param_count(cfg),
+                       "parallelism": f"wp{wp[0]}x{wp[1]}" + (f"_sp{sp}" if sp > 1 else ""),
+                       "params": swf.param_count(cfg),
                        "weights": "init_parameters(seed=2024) + 0.02/sqrt(td) N(0,1) on ada/decode",
                        "t": T_STEP, "l2": "inputs + per-step traffic (~50 GB) far larger than the 126 MB L2"},
             "tflops_per_gpu": tflops_gpu,
@@ -332,6 +334,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sp", type=int, default=1, help="sequence-parallel degree (window rows split into SP bands)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -75,20 +75,24 @@ int swf_create(const swf_model_cfg* cfg, int grid_h, int grid_w, int device, int
 void swf_destroy(swf_ctx* ctx);
 
 /* Window-parallel topology (topology.hpp:74-132): this context is rank `rank` of a wp_a x wp_b
- * window-parallel grid (sp must be 1 in this build); each rank owns whole windows of both the
- * unshifted and the shifted layout. Must be called before swf_load_params / swf_init_params. */
+ * window-parallel grid times sp sequence-parallel bands (rank = wp_rank * sp + band). Each WP
+ * rank owns whole windows of both the unshifted and the shifted layout; with sp > 1 its windows'
+ * rows are split into SP bands by global row phase (window.hpp:67-79), heads into sp groups
+ * (heads % sp == 0 and window_px % sp == 0, topology.hpp:95-102). Must precede parameter loading. */
 int swf_set_topology(swf_ctx* ctx, int wp_a, int wp_b, int sp, int rank, int ownership);
-/* Export this rank's IPC handles (residual buffers x2 + barrier flags: 3 x 64 bytes) / map all
- * ranks' handles (world x 192 bytes, rank order). After connecting, the down-projection epilogue
+/* Export this rank's IPC handles (residual buffers x2, barrier flags, attention planes, attention
+ * output: 5 x 64 bytes) / map all ranks' handles (world x 320 bytes, rank order). After connecting, the down-projection epilogue
  * stores owner-changed tokens straight into the peer's residual buffer over NVLink (the
  * shifted-layer regroup of send_boundary, simulator.hpp:781-824) and a release/acquire flag
  * barrier over the same mapping orders block boundaries. */
-int swf_ipc_handles(swf_ctx* ctx, void* out192);
+int swf_ipc_handles(swf_ctx* ctx, void* out320);
 int swf_connect_peers(swf_ctx* ctx, const void* all_handles);
 /* Host-only planning (no GPU): owner rank of every window (row-major window id) and the tokens
  * each rank sends each other rank at a shift_from -> shift_to block boundary (sent[src*world+dst]),
  * i.e. shift_transfer_plan (topology.hpp:149-188) aggregated per rank pair. */
 int swf_plan_owners(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, int ownership, int* owner);
+int swf_plan_tokens(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, int sp, int ownership, int rank,
+                    long long* pixels); /* pixel of every local token of `rank`, layout 0, device order */
 int swf_plan_exchange(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, int ownership, int shift_from,
                       int shift_to, long long* sent);
 
@@ -97,6 +101,12 @@ int swf_plan_exchange(int grid_h, int grid_w, int window_px, int wp_a, int wp_b,
 int swf_load_params(swf_ctx* ctx, const void* const* arrays, int n_arrays, int dtype);
 int swf_load_params_flat(swf_ctx* ctx, const void* flat, long long count, int dtype);
 long long swf_param_count(const swf_model_cfg* cfg); /* parameter_count_formula (model.hpp:118-129) */
+/* load_params(base, p) (checkpoint.hpp:84-89 / load_named_arrays :50-80): `base`.manifest (dtype
+ * line, then `name RxC offset fnv1a64` per array in canonical order) + `base`.bin, strict name /
+ * shape / dtype / checksum checks (rc 3 on any mismatch), streamed into the device repack. */
+int swf_load_checkpoint(swf_ctx* ctx, const char* base);
+/* The same checks on the host only (no GPU needed). */
+int swf_verify_checkpoint(const swf_model_cfg* cfg, const char* base);
 /* init_parameters (model.hpp:185-209) generated on the device with the reference counter RNG:
  * mode 0 = init_parameters(seed); 1 = init_parameters_random(seed, scale) (model.hpp:213-223);
  * 2 = init_parameters(seed) + scale*N(0,1) added only to the arrays it leaves at zero except the

@@ -336,6 +336,28 @@ def solve_net(cfg: ModelConfig, params, H, W, x_init, x_prev_std, forc_std, sigm
     return out, fe.value
 
 
+def fnv1a64(data: bytes, h: int = 0xcbf29ce484222325) -> int:
+    """src/chunked_file.cpp:33-41"""
+    for b in data:
+        h ^= b
+        h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def save_named_arrays(base: str, cfg: ModelConfig, flat: np.ndarray):
+    """save_params / save_named_arrays (checkpoint.hpp:29-47, 78-81): `dtype f32|f64` line, then
+    `name RxC offset fnv1a64` per canonical array; the .bin holds the arrays back to back."""
+    dt = "f64" if flat.dtype == np.float64 else "f32"
+    off = 0
+    with open(base + ".bin", "wb") as fb, open(base + ".manifest", "w") as fm:
+        fm.write(f"dtype {dt}\n")
+        for (name, r, c), a in zip(param_shapes(cfg), split_params(cfg, flat)):
+            raw = np.ascontiguousarray(a).tobytes()
+            fm.write(f"{name} {r}x{c} {off} {fnv1a64(raw)}\n")
+            fb.write(raw)
+            off += len(raw)
+
+
 def window_owner(wy, wx, a, b):
     oa, ob = C.c_int(), C.c_int()
     lib().orc_window_owner(wy, wx, a, b, C.byref(oa), C.byref(ob))

@@ -15,7 +15,7 @@ from dataclasses import dataclass, astuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libswinflow_b200.so")
+LIB_PATH = os.environ.get("SWF_LIB") or os.path.join(_HERE, "_build", "libswinflow_b200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "swinflow_capi.h")
 
 OK, ERR_NUMERICS, ERR_CONFIG, ERR_IO, ERR_CUDA = 0, 1, 2, 3, 4
@@ -39,6 +39,10 @@ class NumericsError(SwfError):
 
 
 class CudaError(SwfError):
+    pass
+
+
+class IoError(SwfError):
     pass
 
 
@@ -110,9 +114,12 @@ def lib():
         L.swf_connect_peers.argtypes = [vp, vp]
         L.swf_plan_owners.argtypes = [i, i, i, i, i, i, vp]
         L.swf_plan_exchange.argtypes = [i, i, i, i, i, i, i, i, vp]
+        L.swf_plan_tokens.argtypes = [i, i, i, i, i, i, i, i, vp]
         L.swf_load_params.argtypes = [vp, vp, i, i]
         L.swf_load_params_flat.argtypes = [vp, vp, ll, i]
         L.swf_init_params.argtypes = [vp, u64, i, d]
+        L.swf_load_checkpoint.argtypes = [vp, C.c_char_p]
+        L.swf_verify_checkpoint.argtypes = [vp, C.c_char_p]
         L.swf_param_count.argtypes = [vp]
         L.swf_param_count.restype = ll
         L.swf_forward.argtypes = [vp, vp, d, vp, i]
@@ -141,7 +148,8 @@ def _check(rc: int):
     if rc == OK:
         return
     msg = lib().swf_last_error().decode()
-    cls = {ERR_NUMERICS: NumericsError, ERR_CONFIG: ConfigError, ERR_CUDA: CudaError}.get(rc, SwfError)
+    cls = {ERR_NUMERICS: NumericsError, ERR_CONFIG: ConfigError, ERR_IO: IoError, ERR_CUDA: CudaError}.get(rc,
+                                                                                                SwfError)
     raise cls(rc, msg)
 
 
@@ -185,7 +193,7 @@ class Denoiser:
         _check(lib().swf_connect_peers(self._c, buf))
 
     def ipc_handles(self) -> bytes:
-        buf = C.create_string_buffer(192)
+        buf = C.create_string_buffer(320)
         _check(lib().swf_ipc_handles(self._c, buf))
         return buf.raw
 
@@ -211,6 +219,10 @@ class Denoiser:
     def load_params(self, flat: np.ndarray):
         flat = np.ascontiguousarray(flat)
         _check(lib().swf_load_params_flat(self._c, _p(flat), flat.size, _dt(flat)))
+
+    def load_checkpoint(self, base: str):
+        """load_params(base, p) of the reference (checkpoint.hpp:84-89): .bin + .manifest."""
+        _check(lib().swf_load_checkpoint(self._c, base.encode()))
 
     def init_params(self, seed: int, mode: int = 0, scale: float = 0.25):
         """init_parameters (mode 0) / init_parameters_random (mode 1) / bench weights (mode 2),
@@ -305,10 +317,24 @@ class Denoiser:
         return out
 
 
+def verify_checkpoint(cfg: ModelConfig, base: str):
+    """Host-only strict manifest + fnv1a64 check of a reference checkpoint (no GPU)."""
+    _check(lib().swf_verify_checkpoint(C.byref(_Cfg(*astuple(cfg))), base.encode()))
+
+
 def plan_owners(H: int, W: int, w: int, wp_a: int, wp_b: int, ownership: int = OWN_CONTIGUOUS) -> np.ndarray:
     own = np.zeros((H // w) * (W // w), np.int32)
     _check(lib().swf_plan_owners(H, W, w, wp_a, wp_b, ownership, _p(own)))
     return own
+
+
+def plan_tokens(H: int, W: int, w: int, wp_a: int, wp_b: int, sp: int, rank: int,
+                ownership: int = OWN_CONTIGUOUS) -> np.ndarray:
+    """Pixel of every local token of `rank` (unshifted layout, device order), no GPU."""
+    n = H * W // (wp_a * wp_b * sp)
+    pix = np.zeros(n, np.int64)
+    _check(lib().swf_plan_tokens(H, W, w, wp_a, wp_b, sp, ownership, rank, _p(pix)))
+    return pix
 
 
 def plan_exchange(H: int, W: int, w: int, wp_a: int, wp_b: int, ownership: int = OWN_CONTIGUOUS,

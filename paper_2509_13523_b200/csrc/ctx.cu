@@ -14,6 +14,8 @@
 #include <cuda.h>
 
 #include <cmath>
+#include <fstream>
+#include <sstream>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -30,6 +32,9 @@ struct ConfigError : std::runtime_error {
 };
 struct NumericsError : std::runtime_error {
     explicit NumericsError(const std::string& m) : std::runtime_error(m) {}
+};
+struct IoError : std::runtime_error {  // common.hpp:33-40 (IoError / IntegrityError)
+    explicit IoError(const std::string& m) : std::runtime_error(m) {}
 };
 static void require(bool c, const std::string& m) {
     if (!c) throw ConfigError(m);
@@ -48,6 +53,8 @@ struct Dims {
 struct Peer {
     float* x[2];
     int* flags;
+    void* qkv;  // attention planes (sequence parallelism: QKV epilogue stores)
+    void* xm;   // attention output rows (sequence parallelism: attention epilogue stores)
 };
 
 }  // namespace swf
@@ -64,6 +71,7 @@ struct swf_ctx {
     cudaStream_t st = nullptr;
     // topology
     int wp_a = 1, wp_b = 1, sp = 1, rank = 0, world = 1, own = SWF_OWN_CONTIGUOUS;
+    int wp_rank = 0, band = 0;  // rank = wp_rank * sp + band
     i64 M = 0;  // local tokens
     std::vector<int> l2g[2];
     int* d_l2g[2] = {nullptr, nullptr};
@@ -89,6 +97,8 @@ struct swf_ctx {
     std::vector<Peer> peer;
     int* bar_flags = nullptr;        // this rank's barrier slots (IPC-exported), one per peer
     int** d_flag_table = nullptr;    // device table: flag array of every rank (peer-mapped)
+    void** d_qkv_dst = nullptr;      // device table: attention planes of every rank
+    void** d_o_dst = nullptr;        // device table: attention-output (xm) buffer of every rank
     int bar_epoch = 0;
     // TMA maps (BF16 path)
     TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec, tm_q, tm_k, tm_vt;
@@ -221,11 +231,11 @@ void build_layouts(swf_ctx* c) {
                                    std::to_string(c->wp_a));
     require(nx % c->wp_b == 0, "topology: window cols " + std::to_string(nx) + " not divisible by WP grid B=" +
                                    std::to_string(c->wp_b));
-    const int ra = c->rank / c->wp_b, rb = c->rank % c->wp_b;
+    const int nwp = c->wp_a * c->wp_b;
     std::vector<int> g2rl(nwin);
     for (int par = 0; par < 2; ++par) {
         c->l2g[par].clear();
-        std::vector<int> cnt(c->world, 0);
+        std::vector<int> cnt(nwp, 0);
         for (int wy = 0; wy < ny; ++wy)
             for (int wx = 0; wx < nx; ++wx) {
                 int oa, ob;
@@ -236,13 +246,11 @@ void build_layouts(swf_ctx* c) {
                     oa = wy / (ny / c->wp_a);
                     ob = wx / (nx / c->wp_b);
                 }
-                const int r = oa * c->wp_b + ob;
+                const int r = oa * c->wp_b + ob;  // WP rank (shared by its SP ranks)
                 const int gw = wy * nx + wx;
                 g2rl[gw] = (r << 16) | cnt[r]++;
-                if (r == c->rank) c->l2g[par].push_back(gw);
+                if (r == c->wp_rank) c->l2g[par].push_back(gw);
             }
-        (void)ra;
-        (void)rb;
         if (!c->d_l2g[par]) {
             c->d_l2g[par] = dalloc<int>(c, nwin);
             c->d_g2rl[par] = dalloc<int>(c, nwin);
@@ -252,10 +260,12 @@ void build_layouts(swf_ctx* c) {
         LayMap& L = c->lay[par];
         L.g = make_lay(c->H, c->W, m.w, par == 0 ? 0 : m.w / 2);
         L.nloc = int(c->l2g[par].size());
+        L.sp = c->sp;
+        L.band = c->band;
         L.loc2glob = c->d_l2g[par];
         L.glob2rl = c->d_g2rl[par];
     }
-    c->M = i64(c->lay[0].nloc) * m.w * m.w;
+    c->M = i64(c->lay[0].nloc) * c->lay[0].s_loc();
 }
 
 // RoPE cos/sin tables: angle = T(pos * omega_j) in double then cast (rope.hpp:19-31), trig in
@@ -325,10 +335,21 @@ void allocate(swf_ctx* c) {
     // destination tables for the fused down-projection store (own buffer unless peers connect)
     c->bar_flags = dalloc<int>(c, 64);
     c->d_flag_table = dalloc<int*>(c, 8);
-    c->peer.assign(c->world, Peer{{nullptr, nullptr}, nullptr});
+    c->peer.assign(c->world, Peer{{nullptr, nullptr}, nullptr, nullptr, nullptr});
     c->peer[c->rank].x[0] = c->xbuf[0];
     c->peer[c->rank].x[1] = c->xbuf[1];
     c->peer[c->rank].flags = c->bar_flags;
+    c->peer[c->rank].qkv = c->qkv;
+    c->peer[c->rank].xm = c->xm;
+    c->d_qkv_dst = dalloc<void*>(c, 8);
+    c->d_o_dst = dalloc<void*>(c, 8);
+    {
+        std::vector<void*> t(8, nullptr), o(8, nullptr);
+        t[c->rank] = c->qkv;
+        o[c->rank] = c->xm;
+        SWF_CUDA(cudaMemcpy(c->d_qkv_dst, t.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+        SWF_CUDA(cudaMemcpy(c->d_o_dst, o.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+    }
     for (int par = 0; par < 2; ++par) {
         c->d_xdst[par] = dalloc<float*>(c, 8);
         std::vector<float*> t(8, nullptr);
@@ -343,11 +364,12 @@ void allocate(swf_ctx* c) {
         {
             // attention operands: q / k planes [rows][d] (box d<=64 x 128 rows), V^T [rows][s] (64 x d)
             const int sw = m.d >= 64 ? 128 : 2 * m.d;
-            const i64 rows_qk = M * m.heads;  // (window, head, token) rows of d elements
+            const int hl = m.heads / c->sp;  // heads of this rank's group
+            const i64 rows_qk = i64(c->lay[0].nloc) * hl * m.w * m.w;  // (window, head, token) rows of d
             const char* qb = static_cast<const char*>(c->qkv);
             make_tma_bf16_2d(&c->tm_q, qb, rows_qk, m.d, sw / 2, 128, sw);
             make_tma_bf16_2d(&c->tm_k, qb + size_t(M) * m.h * 2, rows_qk, m.d, sw / 2, 128, sw);
-            make_tma_bf16_2d(&c->tm_vt, qb + size_t(2) * M * m.h * 2, i64(c->lay[0].nloc) * m.heads * m.d,
+            make_tma_bf16_2d(&c->tm_vt, qb + size_t(2) * M * m.h * 2, i64(c->lay[0].nloc) * hl * m.d,
                              i64(m.w) * m.w, 64, m.d, 128);
         }
         make_tma_bf16(&c->tm_dec, c->w_dec, m.np_dec, m.hp, m.bn_dec / 2);
@@ -457,6 +479,101 @@ void load_params(swf_ctx* c, const void* const* arrays, int n_arrays, int dtype)
         SWF_CUDA(cudaMemcpyAsync(stage, f32, n * sizeof(float), cudaMemcpyHostToDevice, c->st));
         return stage;
     });
+    SWF_CUDA(cudaFree(stage));
+}
+
+// ------------------------------------------------------------------ checkpoints (checkpoint.hpp:29-89)
+u64 fnv1a64(const void* data, size_t n, u64 h = 0xcbf29ce484222325ULL) {  // src/chunked_file.cpp:33-41
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+std::vector<std::string> param_names(const Dims& m) {  // parameter_arrays names (model.hpp:140-168)
+    std::vector<std::string> v{"encode.w", "encode.b"};
+    for (int b = 0; b < m.nb; ++b)
+        for (const char* n : {"qkv.w", "out.w", "rms_attn.g", "rms_ffn.g", "gate.w", "up.w", "down.w", "ada.w", "ada.b"})
+            v.push_back("block" + std::to_string(b) + "." + n);
+    for (const char* n : {"time.w", "time.b", "decode.g", "decode.w", "decode.b"}) v.push_back(n);
+    return v;
+}
+
+struct CkptEntry {
+    u64 offset, sum;
+    size_t n;
+};
+
+// Strict manifest check (load_named_arrays): dtype line, then per array `name RxC offset fnv1a64`
+// in canonical order with matching element counts.
+std::vector<CkptEntry> read_manifest(const std::string& base, const Dims& m, int* dtype) {
+    std::ifstream man(base + ".manifest");
+    if (!man) throw IoError("cannot open manifest: " + base + ".manifest");
+    std::string tag, dt;
+    man >> tag >> dt;
+    if (tag != "dtype" || (dt != "f32" && dt != "f64"))
+        throw IoError("checkpoint dtype mismatch in " + base + " (found `" + dt + "`)");
+    *dtype = dt == "f64" ? SWF_F64 : SWF_F32;
+    const auto names = param_names(m);
+    const auto shapes = param_shapes(m);
+    std::vector<CkptEntry> out;
+    for (size_t i = 0; i < names.size(); ++i) {
+        std::string name, shape;
+        u64 off = 0, sum = 0;
+        if (!(man >> name >> shape >> off >> sum))
+            throw IoError("manifest truncated at array `" + names[i] + "` in " + base);
+        const auto xp = shape.find('x');
+        if (xp == std::string::npos) throw IoError("bad shape `" + shape + "` in " + base);
+        const long long rows = std::stoll(shape.substr(0, xp)), cols = std::stoll(shape.substr(xp + 1));
+        const i64 n = shapes[i].first * shapes[i].second;
+        if (name != names[i] || rows * cols != n)
+            throw IoError("checkpoint layout mismatch: expected `" + names[i] + "` (" + std::to_string(n) +
+                          " elements), manifest has `" + name + "` " + shape);
+        out.push_back({off, sum, size_t(n)});
+    }
+    return out;
+}
+
+void load_checkpoint(swf_ctx* c, const std::string& base) {
+    allocate(c);
+    const Dims& m = c->m;
+    int dtype = SWF_F32;
+    const auto ent = read_manifest(base, m, &dtype);
+    std::ifstream bin(base + ".bin", std::ios::binary);
+    if (!bin) throw IoError("cannot open checkpoint: " + base + ".bin");
+    const size_t es = dtype == SWF_F64 ? 8 : 4;
+    float* stage = nullptr;
+    SWF_CUDA(cudaMalloc(&stage, max_array(m) * sizeof(float)));
+    std::vector<char> raw;
+    std::vector<float> f32;
+    try {
+        load_params_from(c, [&](int ai, size_t n) -> float* {
+            SWF_CUDA(cudaStreamSynchronize(c->st));
+            const CkptEntry& e = ent[ai];
+            raw.resize(n * es);
+            bin.seekg(std::streamoff(e.offset));
+            bin.read(raw.data(), std::streamsize(raw.size()));
+            if (!bin) throw IoError("checkpoint truncated at `" + param_names(m)[ai] + "` in " + base);
+            if (fnv1a64(raw.data(), raw.size()) != e.sum)
+                throw IoError("IntegrityError: checksum mismatch for `" + param_names(m)[ai] + "` in " + base);
+            const float* src = reinterpret_cast<const float*>(raw.data());
+            if (dtype == SWF_F64) {
+                f32.resize(n);
+                const double* d = reinterpret_cast<const double*>(raw.data());
+                for (size_t i = 0; i < n; ++i) f32[i] = static_cast<float>(d[i]);
+                src = f32.data();
+            }
+            SWF_CUDA(cudaMemcpyAsync(stage, src, n * 4, cudaMemcpyHostToDevice, c->st));
+            SWF_CUDA(cudaStreamSynchronize(c->st));
+            return stage;
+        });
+    } catch (...) {
+        cudaFree(stage);
+        c->loaded = false;
+        throw;
+    }
     SWF_CUDA(cudaFree(stage));
 }
 
@@ -576,6 +693,9 @@ EpiParams base_ep(swf_ctx* c) {
     ep.nxt = c->lay[0];
     ep.my_rank = c->rank;
     ep.out_scale = 1.f;
+    ep.qkv_dst = c->d_qkv_dst;
+    ep.heads_loc = c->m.heads / c->sp;
+    ep.wp_rank = c->wp_rank;
     return ep;
 }
 
@@ -655,13 +775,14 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         EpiParams e = ep;
         e.cur = c->lay[par];
         e.out = c->qkv;
-        e.plane = M * m.h;
+        e.plane = i64(c->lay[par].nloc) * (m.heads / c->sp) * m.w * m.w * m.d;  // one q/k/v plane of a rank
         e.N = 3 * m.h;
         {
             ProfScope ps(c, K_QKV);
             Gemm<T>::run(c, xm, &c->tm_xm, c->w_qkv[b], tmap_at(c->tm_qkv, b), M, m.np_qkv, m.hp,
                      m.bn_qkv, EPI_QKV, e);
         }
+        if (c->sp > 1) peer_barrier(c);  // every head group's planes complete before attention
         AttnParams ap;
         ap.q = c->qkv;
         ap.k = static_cast<const char*>(c->qkv) + size_t(M) * m.h * esize(c);
@@ -669,7 +790,10 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         ap.o = xm;
         ap.ldo = m.hp;
         ap.nloc = c->lay[par].nloc;
-        ap.heads = m.heads;
+        ap.heads = m.heads / c->sp;
+        ap.head0 = c->band * (m.heads / c->sp);
+        ap.wp_rank = c->wp_rank;
+        ap.o_dst = c->d_o_dst;
         ap.s = m.w * m.w;
         ap.d = m.d;
         ap.w = m.w;
@@ -685,6 +809,7 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
             else
                 attention_bf16(ap, c->st);
         }
+        if (c->sp > 1) peer_barrier(c);  // all O rows of this rank's tokens landed
         e = ep;
         e.x = x;
         e.N = m.h;
@@ -1037,6 +1162,8 @@ int fail(const std::exception& e, int rc) {
         return fail(e, SWF_ERR_NUMERICS);                           \
     } catch (const swf::ConfigError& e) {                           \
         return fail(e, SWF_ERR_CONFIG);                             \
+    } catch (const swf::IoError& e) {                               \
+        return fail(e, SWF_ERR_IO);                                 \
     } catch (const swf::CudaError& e) {                             \
         return fail(e, SWF_ERR_CUDA);                               \
     } catch (const std::exception& e) {                             \
@@ -1100,15 +1227,22 @@ int swf_set_topology(swf_ctx* c, int wp_a, int wp_b, int sp, int rank, int owner
         require(c, "null context");
         require(!c->allocated, "swf_set_topology must precede swf_load_params");
         require(wp_a >= 1 && wp_b >= 1 && sp >= 1, "topology: all degrees must be >= 1");
-        require(sp == 1, "topology: sequence parallelism (SP > 1) is not built in this round");
-        require(wp_a * wp_b <= 8, "topology: at most 8 window-parallel ranks per box");
-        require(rank >= 0 && rank < wp_a * wp_b, "topology: rank out of range");
+        require(wp_a * wp_b * sp <= 8, "topology: at most 8 ranks per box");
+        require(rank >= 0 && rank < wp_a * wp_b * sp, "topology: rank out of range");
         require(ownership == SWF_OWN_CONTIGUOUS || ownership == SWF_OWN_ROUND_ROBIN, "topology: bad ownership");
+        // build_topology constraints (topology.hpp:95-102)
+        require(c->m.w % sp == 0, "topology: SP=" + std::to_string(sp) + " does not divide window side " +
+                                      std::to_string(c->m.w) + " (row-band slicing)");
+        require(c->m.heads % sp == 0, "topology: SP=" + std::to_string(sp) + " does not divide head count " +
+                                          std::to_string(c->m.heads));
+        require(sp == 1 || c->prec == SWF_PREC_BF16, "topology: sequence parallelism runs on the BF16 path");
         c->wp_a = wp_a;
         c->wp_b = wp_b;
         c->sp = sp;
         c->rank = rank;
-        c->world = wp_a * wp_b;
+        c->world = wp_a * wp_b * sp;
+        c->wp_rank = rank / sp;
+        c->band = rank % sp;
         c->own = ownership;
     })
 }
@@ -1147,6 +1281,38 @@ int swf_load_params_flat(swf_ctx* c, const void* flat, long long count, int dtyp
         }
         SWF_CUDA(cudaSetDevice(c->dev));
         load_params(c, ptrs.data(), int(ptrs.size()), dtype);
+    })
+}
+
+int swf_load_checkpoint(swf_ctx* c, const char* base) {
+    SWF_API_TRY({
+        require(c && base, "null argument");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        load_checkpoint(c, base);
+    })
+}
+
+// Host-only verification of a checkpoint against a model config (no GPU): manifest layout and
+// every array's fnv1a64 checksum.
+int swf_verify_checkpoint(const swf_model_cfg* cfg, const char* base) {
+    SWF_API_TRY({
+        require(cfg && base, "null argument");
+        const Dims m = make_dims(*cfg, SWF_PREC_FP32);
+        int dtype = SWF_F32;
+        const auto ent = read_manifest(base, m, &dtype);
+        std::ifstream bin(std::string(base) + ".bin", std::ios::binary);
+        if (!bin) throw IoError(std::string("cannot open checkpoint: ") + base + ".bin");
+        const size_t es = dtype == SWF_F64 ? 8 : 4;
+        std::vector<char> raw;
+        const auto names = param_names(m);
+        for (size_t i = 0; i < ent.size(); ++i) {
+            raw.resize(ent[i].n * es);
+            bin.seekg(std::streamoff(ent[i].offset));
+            bin.read(raw.data(), std::streamsize(raw.size()));
+            if (!bin) throw IoError("checkpoint truncated at `" + names[i] + "`");
+            if (fnv1a64(raw.data(), raw.size()) != ent[i].sum)
+                throw IoError("IntegrityError: checksum mismatch for `" + names[i] + "`");
+        }
     })
 }
 
@@ -1321,10 +1487,13 @@ long long swf_local_tokens(swf_ctx* c) {
 int swf_owned_pixels(swf_ctx* c, long long* pixels) {
     SWF_API_TRY({
         require(c && pixels, "null argument");
-        const int s = c->m.w * c->m.w;
+        const LayMap& L = c->lay[0];
+        const int w = c->m.w, R = w / c->sp;
         i64 i = 0;
         for (int gw : c->l2g[0])
-            for (int tok = 0; tok < s; ++tok) pixels[i++] = c->lay[0].g.win_to_pix(i64(gw) * s + tok);
+            for (int k = 0; k < R; ++k)
+                for (int cc = 0; cc < w; ++cc)
+                    pixels[i++] = L.g.win_to_pix(i64(gw) * w * w + i64(L.band_row(c->band, k)) * w + cc);
     })
 }
 
@@ -1354,7 +1523,7 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
                 case K_QKV:
                     e.cur = c->lay[par];
                     e.out = c->qkv;
-                    e.plane = M * m.h;
+                    e.plane = i64(c->lay[par].nloc) * (m.heads / c->sp) * m.w * m.w * m.d;
                     e.N = 3 * m.h;
                     gemm_bf16_tc(c->tm_xm, c->tm_qkv[blk], M, m.np_qkv, m.hp, m.bn_qkv, EPI_QKV, e, c->st);
                     break;
@@ -1366,7 +1535,18 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
                     ap.o = c->sbuf;  // scratch: keep xm intact
                     ap.ldo = m.hp;
                     ap.nloc = c->lay[par].nloc;
-                    ap.heads = m.heads;
+                    ap.heads = m.heads / c->sp;
+                    ap.head0 = c->band * (m.heads / c->sp);
+                    ap.wp_rank = c->wp_rank;
+                    {
+                        static void** scratch_tab = nullptr;  // o_dst table pointing at sbuf (scratch)
+                        if (!scratch_tab) {
+                            scratch_tab = dalloc<void*>(c, 8);
+                            std::vector<void*> t(8, c->sbuf);
+                            SWF_CUDA(cudaMemcpy(scratch_tab, t.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+                        }
+                        ap.o_dst = scratch_tab;
+                    }
                     ap.s = m.w * m.w;
                     ap.d = m.d;
                     ap.w = m.w;
@@ -1478,10 +1658,12 @@ int swf_ipc_handles(swf_ctx* c, void* out) {
         require(c && out, "null argument");
         SWF_CUDA(cudaSetDevice(c->dev));
         allocate(c);
-        cudaIpcMemHandle_t h[3];
+        cudaIpcMemHandle_t h[5];
         SWF_CUDA(cudaIpcGetMemHandle(&h[0], c->xbuf[0]));
         SWF_CUDA(cudaIpcGetMemHandle(&h[1], c->xbuf[1]));
         SWF_CUDA(cudaIpcGetMemHandle(&h[2], c->bar_flags));
+        SWF_CUDA(cudaIpcGetMemHandle(&h[3], c->qkv));
+        SWF_CUDA(cudaIpcGetMemHandle(&h[4], c->xm));
         std::memcpy(out, h, sizeof h);
     })
 }
@@ -1491,16 +1673,18 @@ int swf_connect_peers(swf_ctx* c, const void* all) {
         require(c && all, "null argument");
         SWF_CUDA(cudaSetDevice(c->dev));
         allocate(c);
-        const size_t hs = 3 * sizeof(cudaIpcMemHandle_t);
+        const size_t hs = 5 * sizeof(cudaIpcMemHandle_t);
         for (int r = 0; r < c->world; ++r) {
             if (r == c->rank) continue;
             const cudaIpcMemHandle_t* h =
                 reinterpret_cast<const cudaIpcMemHandle_t*>(static_cast<const char*>(all) + r * hs);
-            void* p[3];
-            for (int k = 0; k < 3; ++k) SWF_CUDA(cudaIpcOpenMemHandle(&p[k], h[k], cudaIpcMemLazyEnablePeerAccess));
+            void* p[5];
+            for (int k = 0; k < 5; ++k) SWF_CUDA(cudaIpcOpenMemHandle(&p[k], h[k], cudaIpcMemLazyEnablePeerAccess));
             c->peer[r].x[0] = static_cast<float*>(p[0]);
             c->peer[r].x[1] = static_cast<float*>(p[1]);
             c->peer[r].flags = static_cast<int*>(p[2]);
+            c->peer[r].qkv = p[3];
+            c->peer[r].xm = p[4];
         }
         for (int par = 0; par < 2; ++par) {
             std::vector<float*> t(8, nullptr);
@@ -1508,8 +1692,15 @@ int swf_connect_peers(swf_ctx* c, const void* all) {
             SWF_CUDA(cudaMemcpy(c->d_xdst[par], t.data(), sizeof(float*) * 8, cudaMemcpyHostToDevice));
         }
         std::vector<int*> ft(8, nullptr);
-        for (int r = 0; r < c->world; ++r) ft[r] = c->peer[r].flags;
+        std::vector<void*> qt(8, nullptr), ot(8, nullptr);
+        for (int r = 0; r < c->world; ++r) {
+            ft[r] = c->peer[r].flags;
+            qt[r] = c->peer[r].qkv;
+            ot[r] = c->peer[r].xm;
+        }
         SWF_CUDA(cudaMemcpy(c->d_flag_table, ft.data(), sizeof(int*) * 8, cudaMemcpyHostToDevice));
+        SWF_CUDA(cudaMemcpy(c->d_qkv_dst, qt.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+        SWF_CUDA(cudaMemcpy(c->d_o_dst, ot.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
         c->peers = true;
         SWF_CUDA(cudaDeviceSynchronize());
     })
@@ -1529,6 +1720,32 @@ int swf_plan_owners(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, i
                 const int ob = ownership == SWF_OWN_ROUND_ROBIN ? wx % wp_b : wx / (nx / wp_b);
                 owner[wy * nx + wx] = oa * wp_b + ob;
             }
+    })
+}
+
+// Local token order of a rank (no GPU): pixel of every local token of layout 0, as the device uses
+// it (owned windows, SP band rows in ascending r, columns).
+int swf_plan_tokens(int grid_h, int grid_w, int window_px, int wp_a, int wp_b, int sp, int ownership, int rank,
+                    long long* pixels) {
+    SWF_API_TRY({
+        require(pixels && sp >= 1 && window_px % sp == 0, "plan: bad SP degree");
+        const int ny = grid_h / window_px, nx = grid_w / window_px;
+        std::vector<int> own(size_t(ny) * nx);
+        const int rc = swf_plan_owners(grid_h, grid_w, window_px, wp_a, wp_b, ownership, own.data());
+        if (rc) return rc;
+        LayMap L;
+        L.g = make_lay(grid_h, grid_w, window_px, 0);
+        L.sp = sp;
+        L.band = rank % sp;
+        const int R = window_px / sp;
+        i64 i = 0;
+        for (int gw = 0; gw < ny * nx; ++gw) {
+            if (own[gw] != rank / sp) continue;
+            for (int k = 0; k < R; ++k)
+                for (int cc = 0; cc < window_px; ++cc)
+                    pixels[i++] = L.g.win_to_pix(i64(gw) * window_px * window_px +
+                                                 i64(L.band_row(L.band, k)) * window_px + cc);
+        }
     })
 }
 

@@ -54,9 +54,8 @@ __device__ __forceinline__ void epi_apply(const EpiParams& ep, i64 m, int n0, fl
             if (n0 + j < ep.N) o[n0 + j] = (v[j] + ep.bias[n0 + j]) * ep.out_scale;
     } else if constexpr (MODE == EPI_QKV) {
         const int s = ep.cur.g.w * ep.cur.g.w;
-        const int lw = int(m / s);
-        const int tok = int(m - i64(lw) * s);
-        const int gw = ep.cur.loc2glob[lw];
+        int gw, tok, lw;
+        ep.cur.loc_to_wtok(m, gw, tok, lw);
         const int wy = gw / ep.cur.g.nx, wx = gw - (gw / ep.cur.g.nx) * ep.cur.g.nx;
         const int w = ep.cur.g.w;
         const int prow = wy * w + ep.cur.g.shift + tok / w;  // unwrapped rope position (window.hpp:54-56)

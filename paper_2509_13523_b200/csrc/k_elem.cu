@@ -207,11 +207,10 @@ __device__ __forceinline__ double d_gaussian(u64 key, u64 ctr) {
 }
 
 __global__ void k_noise(u64 zfk, int C, LayMap lay, double sd, float* __restrict__ z, i64 M) {
-    const int s = lay.g.w * lay.g.w;
     for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < M; i += i64(gridDim.x) * blockDim.x) {
-        const int lw = int(i / s);
-        const int tok = int(i - i64(lw) * s);
-        const u64 key = d_kd(d_kd(zfk, u64(lay.loc2glob[lw])), u64(tok));
+        int gw, tok, lw;
+        lay.loc_to_wtok(i, gw, tok, lw);
+        const u64 key = d_kd(d_kd(zfk, u64(gw)), u64(tok));  // z_cell_key(window, token)
         for (int c = 0; c < C; ++c) z[i * C + c] = float(sd * d_gaussian(key, u64(c)));
     }
 }
@@ -327,7 +326,7 @@ template void assemble_state<__nv_bfloat16>(const float*, const float*, i64, int
                                             cudaStream_t);
 
 void noise_field(u64 zfk, int C, const LayMap& lay0, double sigma_d, float* z, cudaStream_t st) {
-    const i64 M = i64(lay0.nloc) * lay0.g.w * lay0.g.w;
+    const i64 M = i64(lay0.nloc) * lay0.s_loc();
     k_noise<<<grid_for(M), kThreads, 0, st>>>(zfk, C, lay0, sigma_d, z, M);
     SWF_LAUNCH_CHECK();
 }

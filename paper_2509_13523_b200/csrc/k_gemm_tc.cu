@@ -147,34 +147,35 @@ __device__ __forceinline__ void epi32(const EpiParams& ep, i64 m, int n0, float*
             xd[j] = make_float4(o.x + v[4 * j], o.y + v[4 * j + 1], o.z + v[4 * j + 2], o.w + v[4 * j + 3]);
         }
     } else if constexpr (MODE == EPI_QKV) {
-        // d >= 32 so the 32 columns lie inside one head of one of q/k/v
+        // d >= 32 so the 32 columns lie inside one head of one of q/k/v. The head's planes live on
+        // the rank of its head group (Ulysses sequence parallelism, simulator.hpp:464-507): the
+        // store goes straight to that rank over NVLink (own buffer when sp == 1).
         const int s = ep.cur.g.w * ep.cur.g.w;
-        const int lw = int(m / s);
-        const int tok = int(m - i64(lw) * s);
+        int gw, tok, lw;
+        ep.cur.loc_to_wtok(m, gw, tok, lw);
         const int which = n0 / h;
         const int e = n0 - which * h;
         const int head = e / ep.d;
         const int dd = e - head * ep.d;
+        const int hg = head / ep.heads_loc, hl = head - hg * ep.heads_loc;
+        __nv_bfloat16* base =
+            reinterpret_cast<__nv_bfloat16*>(ep.qkv_dst[ep.wp_rank * ep.cur.sp + hg]) + which * ep.plane;
         if (which < 2) {
-            const int gw = ep.cur.loc2glob[lw];
             const int w = ep.cur.g.w;
             const int wy = gw / ep.cur.g.nx, wx = gw - wy * ep.cur.g.nx;
             const int prow = wy * w + ep.cur.g.shift + tok / w;
             const int pcol = wx * w + ep.cur.g.shift + tok % w;
 #pragma unroll
             for (int j = 0; j < 32; j += 2) rope_pair(ep, prow, pcol, (dd + j) >> 1, v[j], v[j + 1]);
-        }
-        if (which == 2) {
+        } else {
             // V is stored transposed ([window][head][d][token]) so the attention's P.V MMA reads a
             // K-major operand; the 32 lanes of a warp hold consecutive tokens -> 64 B per store.
-            __nv_bfloat16* vt = reinterpret_cast<__nv_bfloat16*>(ep.out) + 2 * ep.plane +
-                                ((i64(lw) * ep.heads + head) * ep.d + dd) * s + tok;
+            __nv_bfloat16* vt = base + ((i64(lw) * ep.heads_loc + hl) * ep.d + dd) * s + tok;
 #pragma unroll
             for (int j = 0; j < 32; ++j) vt[i64(j) * s] = __float2bfloat16_rn(v[j]);
             return;
         }
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ep.out) + which * ep.plane +
-                             ((i64(lw) * ep.heads + head) * s + tok) * ep.d + dd;
+        __nv_bfloat16* dst = base + ((i64(lw) * ep.heads_loc + hl) * s + tok) * ep.d + dd;
         uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
         for (int j = 0; j < 4; ++j)

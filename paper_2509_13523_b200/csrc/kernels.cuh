@@ -5,18 +5,65 @@
 
 namespace swf {
 
-// Which tokens a rank owns under one layout (whole windows, SWiPe-style). loc2glob[lw] is the
-// global window id of local window lw; glob2rl[gw] = (owner_rank << 16) | local_window.
+// Which tokens a rank owns under one layout (SWiPe WP x SP). Whole windows go to a WP rank; with
+// sequence parallelism the window's rows are split into SP bands keyed by the global row phase
+// ((shift + r) mod w) / (w / sp) (window.hpp:67-79, shift-invariant), so rank = wp * sp + band.
+// Local token order: owned window (loc2glob order), then the band's rows in ascending r (the
+// reference band_rows order), then column. With sp == 1 this is the canonical window order.
+// glob2rl[gw] = (wp_rank << 16) | local_window.
 struct LayMap {
     Lay g;
-    int nloc;              // local windows
-    const int* loc2glob;   // device [nloc]
-    const int* glob2rl;    // device [n_windows]
+    int nloc;             // local windows
+    int sp, band;         // sequence-parallel degree, this rank's band
+    const int* loc2glob;  // device [nloc]
+    const int* glob2rl;   // device [n_windows]
+    __host__ __device__ int s_loc() const { return g.w * g.w / sp; }
+    // first rolled-frame row of a band and whether the band's row range wraps past r = w - 1
+    __host__ __device__ void band_geom(int b, int& st, int& e, bool& wrap) const {
+        const int R = g.w / sp;
+        st = b * R - g.shift;
+        if (st < 0) st += g.w;
+        wrap = st + R > g.w;
+        e = wrap ? st + R - g.w : 0;
+    }
+    // k-th row (ascending r) of band b
+    __host__ __device__ int band_row(int b, int k) const {
+        int st, e;
+        bool wrap;
+        band_geom(b, st, e, wrap);
+        return wrap ? (k < e ? k : st + (k - e)) : st + k;
+    }
+    __host__ __device__ int band_of_row(int r) const {
+        int ph = g.shift + r;
+        if (ph >= g.w) ph -= g.w;
+        return ph / (g.w / sp);
+    }
+    __host__ __device__ int row_index_in_band(int b, int r) const {
+        int st, e;
+        bool wrap;
+        band_geom(b, st, e, wrap);
+        return wrap ? (r < e ? r : e + (r - st)) : r - st;
+    }
+    // local token -> (global window, canonical in-window token r*w+c)
+    __device__ __forceinline__ void loc_to_wtok(i64 i, int& gw, int& tok, int& lw) const {
+        const int sl = s_loc();
+        lw = int(i / sl);
+        const int t = int(i - i64(lw) * sl);
+        const int k = t / g.w, c = t - (t / g.w) * g.w;
+        gw = loc2glob[lw];
+        tok = band_row(band, k) * g.w + c;
+    }
     __device__ __forceinline__ i64 loc_to_pix(i64 i) const {
-        const int s = g.w * g.w;
-        const int lw = int(i / s);
-        const int tok = int(i - i64(lw) * s);
-        return g.win_to_pix(i64(loc2glob[lw]) * s + tok);
+        int gw, tok, lw;
+        loc_to_wtok(i, gw, tok, lw);
+        return g.win_to_pix(i64(gw) * (g.w * g.w) + tok);
+    }
+    // (local window of the WP group, canonical token) -> (owner rank in WP*SP, its local index)
+    __device__ __forceinline__ i64 wtok_to_loc(int wp_rank, int lw, int tok, int* rank) const {
+        const int r = tok / g.w, c = tok - (tok / g.w) * g.w;
+        const int b = band_of_row(r);
+        *rank = wp_rank * sp + b;
+        return i64(lw) * s_loc() + i64(row_index_in_band(b, r)) * g.w + c;
     }
     // pixel -> (owner rank, local token index) under this layout
     __device__ __forceinline__ i64 pix_to_loc(i64 p, int* rank) const {
@@ -24,8 +71,7 @@ struct LayMap {
         const int s = g.w * g.w;
         const int gw = int(gi / s);
         const int rl = glob2rl[gw];
-        *rank = rl >> 16;
-        return i64(rl & 0xffff) * s + (gi - i64(gw) * s);
+        return wtok_to_loc(rl >> 16, rl & 0xffff, int(gi - i64(gw) * s), rank);
     }
 };
 
@@ -56,6 +102,11 @@ struct EpiParams {
     int rope_nrow, rope_ncol;
     LayMap cur, nxt;
     float out_scale;
+    // sequence parallelism: QKV planes of every rank of this WP group (peer-mapped), heads per
+    // rank, this rank's WP index
+    void* const* qkv_dst;
+    int heads_loc;
+    int wp_rank;
 };
 
 // C[M][N] = A[M][K] . B[N][K]^T (both K-major), fp32 SIMT -- the FP32 validation mode GEMM.
@@ -82,9 +133,12 @@ struct AttnParams {
     const void* q;  // [nloc][heads][s][d]
     const void* k;  // [nloc][heads][s][d]
     const void* v;  // FP32 path: [nloc][heads][s][d]; BF16 path: V^T [nloc][heads][d][s]
-    void* o;        // [nloc*s][ldo] head-concatenated
+    void* o;        // [nloc*s][ldo] head-concatenated (FP32 path, sp == 1)
+    void* const* o_dst;  // BF16 path: attention-output buffer of every rank (peer-mapped; own when sp == 1)
     int ldo;
     int nloc, heads, s, d, w;
+    int head0;      // first global head of this rank's head group (sequence parallelism)
+    int wp_rank;
     LayMap lay;     // masked windows: shifted layout, last window row
     float scale;    // 1/sqrt(d)
     const TmaMap* tmq;  // BF16 path: TMA maps of the q / k planes ([rows][d]) and of V^T ([rows][s])

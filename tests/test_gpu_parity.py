@@ -161,3 +161,30 @@ def test_solve_pf_ode_fp32_mode(steps):
     got, fe2 = dn.solve_pf_ode(x0.astype(np.float32), xp, fo, swf.DiffusionConfig(solver_steps=steps))
     assert fe == fe2 == 2 * steps
     assert rel_err_per_channel(got, ref) <= TOL_FP32
+
+
+def test_load_checkpoint_equals_load_params(tmp_path):
+    # load_params(base, p) (checkpoint.hpp:84-89) -> same device weights -> bitwise-equal forward
+    oc, sc = cfgs(C1)
+    p = o.init_params(oc, 12, random=True, scale=0.05)
+    base = str(tmp_path / "ck")
+    o.save_named_arrays(base, oc, p)
+    x = o.random_field(8, 2048, 13).astype(np.float32)
+    a = swf.Denoiser(sc, 32, 64, precision=swf.PREC_BF16)
+    a.load_params(p)
+    b = swf.Denoiser(sc, 32, 64, precision=swf.PREC_BF16)
+    b.load_checkpoint(base)
+    assert np.array_equal(a.forward(x, 0.5), b.forward(x, 0.5))
+
+
+def test_device_init_matches_oracle_init():
+    # init_parameters_random generated on the device with the reference counter RNG
+    oc, sc = cfgs(C1)
+    p = o.init_params(oc, 77, random=True, scale=0.05, dtype=np.float32)
+    x = o.random_field(8, 2048, 78).astype(np.float32)
+    a = swf.Denoiser(sc, 32, 64, precision=swf.PREC_FP32)
+    a.load_params(p)
+    b = swf.Denoiser(sc, 32, 64, precision=swf.PREC_FP32)
+    b.init_params(77, mode=1, scale=0.05)
+    ya, yb = a.forward(x, 0.5), b.forward(x, 0.5)
+    assert rel_err_per_channel(yb, ya) <= 1e-5

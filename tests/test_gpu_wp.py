@@ -20,12 +20,12 @@ def _ngpus():
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("own", [0, 1])
-def test_wp_bitwise_equals_single_gpu(own):
+@pytest.mark.parametrize("own,sp", [(0, 1), (1, 1), (0, 2)])
+def test_wp_bitwise_equals_single_gpu(own, sp):
     n = 4 if _ngpus() >= 4 else 2
-    env = dict(os.environ, SWF_OWN=str(own))
+    env = dict(os.environ, SWF_OWN=str(own), SWF_SP=str(sp))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-                        "--master-addr", "127.0.0.1", "--master-port", str(29600 + own),
+                        "--master-addr", "127.0.0.1", "--master-port", str(29600 + own + 10 * sp),
                         os.path.join(ROOT, "tools", "wp_check.py")], capture_output=True, text=True, timeout=600,
                        env=env, cwd=ROOT)
     assert "WP_CHECK PASS" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]

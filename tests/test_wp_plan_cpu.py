@@ -53,3 +53,29 @@ def test_exchange_is_symmetric_inverse():
     a = swf.plan_exchange(720, 1440, 60, 2, 2, swf.OWN_CONTIGUOUS, 0, 30)
     b = swf.plan_exchange(720, 1440, 60, 2, 2, swf.OWN_CONTIGUOUS, 30, 0)
     assert np.array_equal(a, b.T)
+
+
+@pytest.mark.parametrize("wp,sp", [((1, 1), 2), ((1, 2), 2), ((1, 1), 4), ((1, 2), 4), ((2, 2), 2)])
+def test_sp_token_partition_and_bands(wp, sp):
+    # SP bands by global row phase (window.hpp:67-79): every pixel owned exactly once; a rank's
+    # tokens all sit in its band under the reference band_of_row, for both shifts (shift-invariant)
+    H, W, w = 48, 96, 12
+    world = wp[0] * wp[1] * sp
+    allp = []
+    for r in range(world):
+        pix = swf.plan_tokens(H, W, w, *wp, sp, r)
+        allp.append(pix)
+        band = r % sp
+        ys = pix // W
+        # row phase y mod w decides the band, independent of the layout shift
+        for shift in (0, 6):
+            rr = (ys - shift) % H % w
+            assert all(o.band_of_row(H, W, w, shift, int(x), sp) == band for x in np.unique(rr))
+    allp = np.concatenate(allp)
+    assert np.array_equal(np.sort(allp), np.arange(H * W))
+
+
+def test_sp1_order_is_canonical_window_order():
+    H, W, w = 48, 96, 12
+    pix = swf.plan_tokens(H, W, w, 1, 1, 1, 0)
+    assert np.array_equal(pix, o.window_perm(H, W, w, 0))

@@ -16,7 +16,8 @@ rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 local = int(os.environ.get("LOCAL_RANK", rank))
 torch.cuda.set_device(local)
 dist.init_process_group("gloo")
-wp = {2: (1, 2), 4: (2, 2), 8: (2, 4)}[world]
+sp = int(os.environ.get("SWF_SP", 1))
+wp = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}[world // sp]
 own = int(os.environ.get("SWF_OWN", swf.OWN_CONTIGUOUS))
 ok = True
 for name, d, H, W in [
@@ -24,11 +25,15 @@ for name, d, H, W in [
                 time_dim=128), 32, 64),
     ("MID", dict(hidden_dim=256, n_heads=2, ffn_dim=512, n_layers=3, window_px=12, in_channels=16, out_channels=6,
                  time_dim=256), 48, 96),
+    ("MID4", dict(hidden_dim=512, n_heads=4, ffn_dim=1024, n_layers=2, window_px=12, in_channels=16, out_channels=6,
+                  time_dim=256), 48, 96),
 ]:
+    if d["n_heads"] % sp or d["window_px"] % sp:
+        continue
     oc, sc = o.ModelConfig(**d), swf.ModelConfig(**d)
     p = o.init_params(oc, 7, random=True, scale=0.03, dtype=np.float32)
     x = o.random_field(oc.in_channels, H * W, 8).astype(np.float32)
-    dn = swf.Denoiser(sc, H, W, device=local, precision=swf.PREC_BF16, topology=(wp[0], wp[1], 1, rank, own))
+    dn = swf.Denoiser(sc, H, W, device=local, precision=swf.PREC_BF16, topology=(wp[0], wp[1], sp, rank, own))
     dn.load_params(p)
     dn.connect_peers_torch(dist)
     y = dn.forward(x, 0.9)
@@ -53,7 +58,7 @@ for name, d, H, W in [
         scale = np.maximum(np.abs(ref).max(axis=0), 1e-30)
         err = float((np.abs(y_wp - ref).max(axis=0) / scale).max())
         bitwise = np.array_equal(y_wp, y1)
-        print(f"{name}: world={world} wp={wp} own={own} cover_ok={bool((cover == 1).all())} "
+        print(f"{name}: world={world} wp={wp} sp={sp} own={own} cover_ok={bool((cover == 1).all())} "
               f"bitwise_vs_1gpu={bitwise} err_vs_oracle={err:.3e}", flush=True)
         ok &= bool((cover == 1).all()) and bitwise and err <= 2e-2
     dn.close()
