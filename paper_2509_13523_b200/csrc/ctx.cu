@@ -1214,9 +1214,13 @@ void swf_destroy(swf_ctx* c) {
     for (void* p : c->allocs) cudaFree(p);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->h_feat) cudaFreeHost(c->h_feat);
-    for (const auto& pr : c->peer)
-        for (int k = 0; k < 2; ++k)
-            if (pr.x[k] && pr.x[k] != c->xbuf[k]) cudaIpcCloseMemHandle(pr.x[k]);
+    for (int r = 0; r < int(c->peer.size()); ++r) {  // unmap every IPC-opened peer buffer
+        if (r == c->rank) continue;
+        const Peer& pr = c->peer[r];
+        for (void* p : {static_cast<void*>(pr.x[0]), static_cast<void*>(pr.x[1]), static_cast<void*>(pr.flags),
+                        pr.qkv, pr.xm})
+            if (p) cudaIpcCloseMemHandle(p);
+    }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     cudaStreamDestroy(c->st);
     delete c;
