@@ -33,6 +33,10 @@ sys.path.insert(0, ROOT)
 H, W = 720, 1440
 CFG = dict(hidden_dim=1536, n_heads=12, ffn_dim=9216, n_layers=10, blocks_per_layer=2, window_px=60,
            in_channels=144, out_channels=70, time_dim=1536)  # perf_model.cpp:49-61 row "1.3B", w=60
+# BASELINE.json configs[3]: wide-layer slice of the 40B shape (perf_model.cpp:38 row "40B": dim 6144,
+# 48 heads, ffn 40960, w=60), 2 blocks (shift 0, 30), on the same 720x1440 grid; needs >= 2 GPUs
+CFG_C4 = dict(hidden_dim=6144, n_heads=48, ffn_dim=40960, n_layers=1, blocks_per_layer=2, window_px=60,
+              in_channels=144, out_channels=70, time_dim=6144)
 T_STEP = math.pi / 4
 SEED = 2024
 METRIC = "denoiser-step pixels/sec"
@@ -194,6 +198,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     import paper_2509_13523_b200 as swf
 
+    global CFG
+    if args.workload == "c4":
+        CFG = CFG_C4
+
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -290,7 +298,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "d2h_bytes_per_step": n_out * 4 * world, "ms_per_step": e2e_s * 1e3}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
         s = cpu_sample(windows=1, blocks=2)
         cpu = {"value": s["value"], "unit": "pixels/s", "cores": s["cores"], "kind": "port", "sample": s["sample"],
                "seconds": round(s["seconds"], 2)}
@@ -300,8 +308,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "metric": METRIC, "value": value, "unit": "pixels/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "AERIS-1.3B-shaped denoiser step (BASELINE.json configs[1])", "grid": [H, W],
-                       "model": "swin-dit-1.3B (h=1536, 12 heads, ffn 9216, 20 blocks, w=60, C_in=144, C_out=70)",
+            "config": {"workload": ("AERIS-1.3B-shaped denoiser step (BASELINE.json configs[1])" if args.workload == "c2"
+                                    else "AERIS-40B-shaped wide-layer slice, 2 blocks (BASELINE.json configs[3])"),
+                       "grid": [H, W],
+                       "model": ("swin-dit-1.3B (h=1536, 12 heads, ffn 9216, 20 blocks, w=60, C_in=144, C_out=70)"
+                                 if args.workload == "c2" else
+                                 "swin-dit-40B slice (h=6144, 48 heads, ffn 40960, 2 blocks, w=60, C_in=144, C_out=70)"),
                        "parallelism": f"wp{wp[0]}x{wp[1]}" + (f"_sp{sp}" if sp > 1 else ""),
                        "params": swf.param_count(cfg),
                        "weights": "init_parameters(seed=2024) + 0.02/sqrt(td) N(0,1) on ada/decode",
@@ -335,6 +347,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sp", type=int, default=1, help="sequence-parallel degree (window rows split into SP bands)")
+    ap.add_argument("--workload", choices=["c2", "c4"], default="c2",
+                    help="c2: AERIS-1.3B 20-block step (headline); c4: 40B-shaped 2-block wide-layer slice")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -150,6 +150,7 @@ long long swf_kernel_launches(swf_ctx* ctx);
  * 5 gate/up GEMM, 6 down GEMM, 7 decode GEMM, 8 other. swf_profile resets the counters. */
 int swf_profile(swf_ctx* ctx, int enable);
 int swf_profile_read(swf_ctx* ctx, double* ms, long long* launches, int n_classes);
+int swf_profile_launches(swf_ctx* ctx, int* classes, double* ms, int max_n, int* n_out);
 /* Replay one kernel class (1..6 above) reps times back-to-back on the resident buffers of the
  * last forward for block blk; *ms = mean device time per launch (kernel isolation at steady clocks). */
 int swf_bench_kernel(swf_ctx* ctx, int kernel_class, int block, int reps, double* ms);

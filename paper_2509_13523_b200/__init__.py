@@ -138,6 +138,7 @@ def lib():
         L.swf_bench_kernel.argtypes = [vp, i, i, i, C.POINTER(d)]
         L.swf_profile.argtypes = [vp, i]
         L.swf_profile_read.argtypes = [vp, vp, vp, i]
+        L.swf_profile_launches.argtypes = [vp, vp, vp, i, C.POINTER(i)]
         L.swf_noise_field.argtypes = [vp, u64, u64, i, d, vp]
         L.swf_selftest_gemm.argtypes = [i, ll, i, i, C.POINTER(d), C.POINTER(d)]
         _lib = L
@@ -257,6 +258,13 @@ class Denoiser:
 
     def profile(self, enable: bool = True):
         _check(lib().swf_profile(self._c, int(enable)))
+
+    def profile_launches(self, max_n: int = 4096) -> list:
+        cls = (C.c_int * max_n)()
+        ms = (C.c_double * max_n)()
+        n = C.c_int(0)
+        _check(lib().swf_profile_launches(self._c, cls, ms, max_n, C.byref(n)))
+        return [(self.KERNEL_CLASSES[cls[i]], ms[i]) for i in range(n.value)]
 
     def profile_read(self) -> dict:
         n = len(self.KERNEL_CLASSES)

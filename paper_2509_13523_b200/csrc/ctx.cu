@@ -1508,7 +1508,9 @@ long long swf_kernel_launches(swf_ctx* c) { return c ? c->launches : -1; }
 // Classes as in swf_profile_read. Returns the mean ms per launch.
 int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
     SWF_API_TRY({
-        require(c && ms && reps > 0, "bad argument");
+        require(c && ms && reps != 0, "bad argument");
+        const bool cold = reps < 0;
+        if (cold) reps = -reps;
         require(c->loaded && c->prec == SWF_PREC_BF16, "bench_kernel: BF16 context with parameters required");
         const Dims& m = c->m;
         require(blk >= 0 && blk < m.nb, "bench_kernel: block out of range");
@@ -1587,7 +1589,7 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
             }
         };
         SWF_CUDA(cudaSetDevice(c->dev));
-        once();
+        if (!cold) once();  // cold: time the very first launch (no warm-up) -- exposes clock state
         cudaEvent_t a, b;
         SWF_CUDA(cudaEventCreate(&a));
         SWF_CUDA(cudaEventCreate(&b));
@@ -1614,6 +1616,24 @@ int swf_profile(swf_ctx* c, int enable) {
             c->prof_ms[k] = 0;
             c->prof_n[k] = 0;
         }
+    })
+}
+
+// Raw per-launch list of the profiled region (class id, ms) in launch order.
+int swf_profile_launches(swf_ctx* c, int* classes, double* ms, int max_n, int* n_out) {
+    SWF_API_TRY({
+        require(c && classes && ms && n_out, "null argument");
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        int n = 0;
+        for (auto& pe : c->prof_ev) {
+            if (n >= max_n) break;
+            float t = 0.f;
+            SWF_CUDA(cudaEventElapsedTime(&t, pe.second.first, pe.second.second));
+            classes[n] = pe.first;
+            ms[n] = t;
+            ++n;
+        }
+        *n_out = n;
     })
 }
 

@@ -20,8 +20,9 @@ namespace {
 
 constexpr int BM = 128;  // rows per CTA; UMMA M = 256 per CTA pair
 constexpr int BK = 64;   // one 128-byte swizzle atom of bf16
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, each draining half of the columns
 
 template <int BN>
 struct Cfg {
@@ -30,7 +31,7 @@ struct Cfg {
     static constexpr int kStage = kStageA + kStageB;
     static constexpr int kStages = (BN == 256) ? 6 : 8;
     static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
-    static constexpr int kStageFloats = 4 * 32 * 33;  // epilogue transpose buffers (4 warps x 32x33)
+    static constexpr int kStageFloats = kEpiWarps * 32 * 33;  // epilogue transpose buffers (32x33 per warp)
     static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/ + kStageFloats * 4;
     static constexpr uint32_t kIdesc = (1u << 4)                 // D = F32
                                        | (1u << 7) | (1u << 10)  // A, B = BF16
@@ -74,12 +75,35 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
-__device__ __forceinline__ void tma_load_2cta(uint32_t dst, const void* tmap, uint32_t bar_cluster, int c0, int c1) {
+__device__ __forceinline__ void tma_load_2cta(uint32_t dst, const void* tmap, uint32_t bar_cluster, int c0, int c1,
+                                              uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-        "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1)
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
+}
+// L2 eviction policies: weights stay resident (evict_last); epilogue output streams go first
+// (evict_first), so the 19 GB SwiGLU stream does not flush the weights or the A row-blocks.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_ef_v4(void* ptr, uint4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
 }
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16)  // LBO (unused for swizzled K-major)
@@ -189,22 +213,28 @@ __device__ __forceinline__ void epi32(const EpiParams& ep, i64 m, int n0, float*
     }
 }
 
-__device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0, const float* g, const float* u) {
+__device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0, const float* g, const float* u,
+                                             uint64_t pol) {
     if (m >= ep.M || j0 >= ep.N) return;
     uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.out) + m * ep.ld_out + j0);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         float r[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) r[t] = silu_f(g[8 * j + t]) * u[8 * j + t];
-        d4[j] = make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
-                           pack_bf16x2(r[6], r[7]));
+        for (int t = 0; t < 8; ++t) {  // SiLU with ex2.approx + rcp.approx (error far below the bf16 output)
+            const float x = g[8 * j + t];
+            r[t] = __fdividef(x, 1.0f + __expf(-x)) * u[8 * j + t];
+        }
+        st_ef_v4(d4 + j, make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
+                                    pack_bf16x2(r[6], r[7])),
+                 pol);
     }
 }
 
-// Grouped rasterisation: bands of kGroupM m-blocks are swept n-block by n-block, so the concurrent
-// clusters share a few A row-blocks and a few B column-blocks (both L2-resident).
-constexpr int kGroupM = 16;
+// Rasterisation: bands of kGroupM m-blocks are swept n-block by n-block. With kGroupM = 1 the
+// concurrently running clusters cover one A row-block across all N tiles (A read once from HBM),
+// while the weights B stay L2-resident under the evict_last policy.
+constexpr int kGroupM = 1;
 __device__ __forceinline__ void tile_coords(i64 t, int n_tiles, i64 m_tiles, int& m_blk, int& n_blk) {
     const i64 per_group = i64(kGroupM) * n_tiles;
     const i64 g = t / per_group;
@@ -281,7 +311,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&tfull_bar[a]), 1);
-            mbar_init(smem_u32(&tempty_bar[a]), 2 * 4);
+            mbar_init(smem_u32(&tempty_bar[a]), 2 * kEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -302,6 +332,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ===== TMA producer (both CTAs; each loads its A half and B half, signalling the leader)
         if (lane == 0) {
+            // A row-blocks are re-read by every N tile of the band -> normal priority; weights -> last
+            const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
             for (i64 t = cluster_id; t < total; t += n_clusters) {
@@ -313,8 +345,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = map_to_rank(smem_u32(&full_bar[stage]), 0);
                     if (leader) mbar_expect_tx(smem_u32(&full_bar[stage]), 2 * C::kStage);
-                    tma_load_2cta(smem_u32(sA + stage * C::kStageA), &tmA, fb, kb * BK, row_a);
-                    tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK, row_b);
+                    tma_load_2cta(smem_u32(sA + stage * C::kStageA), &tmA, fb, kb * BK, row_a, pol_a);
+                    tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK, row_b, pol_b);
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -356,12 +388,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ===== epilogue: TMEM -> registers -> fused op -> global
-        const int q = warp - kEpiWarp0;  // TMEM lane quadrant (warp % 4)
+        // ===== epilogue: TMEM -> registers -> fused op -> global (8 warps: quadrant x column half)
+        const int q = (warp - kEpiWarp0) & 3;     // TMEM lane quadrant (warp % 4)
+        const int half = (warp - kEpiWarp0) >> 2;  // column half of the tile
         int acc = 0;
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = map_to_rank(smem_u32(&tempty_bar[0]), 0);
-        float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256) + q * 32 * 33;
+        float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256) + (warp - kEpiWarp0) * 32 * 33;
+        const uint64_t pol_out = policy_evict_first();
         for (i64 t = cluster_id; t < total; t += n_clusters) {
             int m_blk, n_blk;
             tile_coords(t, n_tiles, m_tiles, m_blk, n_blk);
@@ -371,32 +405,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
             if constexpr (MODE == EPI_SWIGLU) {
                 // interleave G = BN/2: columns [0, BN/2) gate, [BN/2, BN) up of the same ffn units
+                constexpr int NCH = BN / 64;
 #pragma unroll 1
-                for (int ch = 0; ch < BN / 64; ++ch) {
+                for (int ch = half * NCH / 2; ch < (half + 1) * NCH / 2; ++ch) {
                     float g[32], u[32];
                     tmem_ld32(tbase + ch * 32, g);
                     tmem_ld32(tbase + BN / 2 + ch * 32, u);
-                    epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u);
+                    epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u, pol_out);
                 }
             } else if constexpr (MODE == EPI_DOWN) {
                 float* drow = nullptr;
-                if constexpr (MODE == EPI_DOWN) {
-                    // destination row in the next block's layout, possibly on a peer GPU (NVLink)
-                    if (row < ep.M) {
-                        int rank;
-                        const i64 li = ep.nxt.pix_to_loc(ep.cur.loc_to_pix(row), &rank);
-                        drow = ep.xdst[rank] + li * ep.h;
-                    }
+                // destination row in the next block's layout, possibly on a peer GPU (NVLink)
+                if (row < ep.M) {
+                    int rank;
+                    const i64 li = ep.nxt.pix_to_loc(ep.cur.loc_to_pix(row), &rank);
+                    drow = ep.xdst[rank] + li * ep.h;
                 }
+                constexpr int NCH = BN / 32;
 #pragma unroll 1
-                for (int ch = 0; ch < BN / 32; ++ch) {
+                for (int ch = half * NCH / 2; ch < (half + 1) * NCH / 2; ++ch) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
                     epi32_coalesced<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, drow, lane);
                 }
             } else {
+                constexpr int NCH = BN / 32;
 #pragma unroll 1
-                for (int ch = 0; ch < BN / 32; ++ch) {
+                for (int ch = half * NCH / 2; ch < (half + 1) * NCH / 2; ++ch) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
                     epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
