@@ -102,6 +102,7 @@ struct swf_ctx {
     int bar_epoch = 0;
     // TMA maps (BF16 path)
     TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec, tm_q, tm_k, tm_vt;
+    TmaMap tm_so;  // sbuf viewed as [M][hp] (attention output of the kernel benchmark)
     std::vector<TmaMap> tm_qkv, tm_out, tm_gu, tm_down;
     long long launches = 0;
     // sampler workspace (allocated lazily)
@@ -360,6 +361,7 @@ void allocate(swf_ctx* c) {
         make_tma_bf16(&c->tm_ain, c->a_in, M, m.cinp, 128);
         make_tma_bf16(&c->tm_xm, c->xm, M, m.hp, 128);
         make_tma_bf16(&c->tm_s, c->sbuf, M, m.fp, 128);
+        make_tma_bf16(&c->tm_so, c->sbuf, M, m.hp, 128);
         make_tma_bf16(&c->tm_enc, c->w_enc, m.np_enc, m.cinp, m.bn_enc / 2);
         {
             // attention operands: q / k planes [rows][d] (box d<=64 x 128 rows), V^T [rows][s] (64 x d)
@@ -368,9 +370,10 @@ void allocate(swf_ctx* c) {
             const i64 rows_qk = i64(c->lay[0].nloc) * hl * m.w * m.w;  // (window, head, token) rows of d
             const char* qb = static_cast<const char*>(c->qkv);
             make_tma_bf16_2d(&c->tm_q, qb, rows_qk, m.d, sw / 2, 128, sw);
-            make_tma_bf16_2d(&c->tm_k, qb + size_t(M) * m.h * 2, rows_qk, m.d, sw / 2, 128, sw);
+            // K and V^T tiles are fetched half per CTA of a 2-CTA cluster and multicast (k_attn.cu)
+            make_tma_bf16_2d(&c->tm_k, qb + size_t(M) * m.h * 2, rows_qk, m.d, sw / 2, 64, sw);
             make_tma_bf16_2d(&c->tm_vt, qb + size_t(2) * M * m.h * 2, i64(c->lay[0].nloc) * hl * m.d,
-                             i64(m.w) * m.w, 64, m.d, 128);
+                             i64(m.w) * m.w, 64, m.d / 2, 128);
         }
         make_tma_bf16(&c->tm_dec, c->w_dec, m.np_dec, m.hp, m.bn_dec / 2);
         c->tm_qkv.resize(m.nb);
@@ -802,6 +805,7 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         ap.tmq = &c->tm_q;
         ap.tmk = &c->tm_k;
         ap.tmv = &c->tm_vt;
+        ap.tmo = c->sp == 1 ? &c->tm_xm : nullptr;  // SP: rows go to the band owners row by row
         {
             ProfScope ps(c, K_ATTN);
             if constexpr (sizeof(T) == 4)
@@ -1561,6 +1565,7 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
                     ap.tmq = &c->tm_q;
                     ap.tmk = &c->tm_k;
                     ap.tmv = &c->tm_vt;
+                    ap.tmo = c->sp == 1 ? &c->tm_so : nullptr;
                     attention_bf16(ap, c->st);
                     break;
                 }

@@ -1,22 +1,37 @@
 // k_attn.cu -- BF16 windowed attention on the 5th-generation tensor cores (sm_100a).
 //
-// Persistent CTAs; a work item is one 128-query tile of one (window, head). Restates
-// head_attention_fwd (swin.hpp:161-188) without materialising the s x s logits:
-//   * S = Q K^T : tcgen05.mma (M=128, N=128 keys, K=d), A = Q and B = K, K-major SW128 shared-
-//     memory tiles loaded by TMA; FP32 S in TMEM, double-buffered (S0 / S1) so the QK^T of key
-//     tile j+1 runs while the softmax warps work on tile j;
-//   * softmax: one thread per query row (TMEM lane), base-2 online max/sum with lazy O rescaling
-//     (only when the running max grows by > 2^8), packed f32x2 arithmetic for the exponent
-//     arguments and the row sum, 3/8 of the exponentials on the FMA pipe (degree-3 polynomial)
-//     and 5/8 on MUFU; P is packed to BF16 and written back into its S buffer's columns;
-//   * O += P V : tcgen05.mma with A = P read from TMEM and B = V^T (K-major, written transposed by
-//     the QKV GEMM epilogue); O accumulates in TMEM;
+// Persistent 2-CTA clusters running the pair-wide tensor-core MMA (tcgen05.mma.cta_group::2): a
+// work item is a pair of 128-query tiles of one (window, head), one tile per CTA, and every MMA
+// covers both (M = 256). Each CTA holds its own query tile and HALF of every K / V^T tile (the MMA's
+// B operand is split by N across the pair), so a key tile costs each SM 32 KB of TMA fill and half
+// the B-operand shared-memory reads. Restates head_attention_fwd (swin.hpp:161-188) without
+// materialising the s x s logits:
+//   * S = Q K^T : M=256 (2 x 128 queries), N=128 keys, K=d; A = Q and B = K, K-major SW128 tiles
+//     loaded by TMA; FP32 S in each CTA's TMEM, triple-buffered (S0 / S1 / S2): the QK^T issuer runs
+//     up to three key tiles ahead of the P V issuer (over the flattened sequence of work items), so
+//     the softmax warps find the next S ready when they finish a tile;
+//   * softmax (per CTA): 8 warps, each TMEM lane (query row) is shared by two threads that take 64
+//     keys each (the row maximum is exchanged through shared memory); base-2 online max/sum with lazy
+//     O rescaling (only when the running max grows by > 2^8), packed f32x2 arithmetic, 3/8 of the
+//     exponentials on the FMA pipe (degree-3 polynomial) and 5/8 on MUFU; P is packed to BF16 into
+//     the first 32 columns of each thread's 64-column S slice;
+//   * O += P V : M=256, N=d, A = P read from TMEM, B = V^T (K-major, written transposed by the QKV
+//     GEMM epilogue); O accumulates in TMEM. S(j+3) is issued only after P(j) V completed;
+//   * epilogue: O / l in BF16 is staged in the finished item's Q buffer (SW128) and written by TMA
+//     tensor stores (whole tiles, sp == 1); partial tiles and sequence-parallel rows (scattered to
+//     the band owners) are stored row by row;
 //   * the latitude-seam mask (window.hpp:107-122) is a per-row key range: the two seam groups are
 //     the contiguous token ranges [0, (w-shift)*w) and [(w-shift)*w, w*w); fully-outside key tiles
 //     are skipped and only boundary tiles pay per-element masking.
-// Warp roles: w0 TMA producer (Q double buffer, 3-stage K ring), w3 TMA producer (2-stage V^T
-// ring), w1 MMA issuer, w2 TMEM allocator, w4-w7 softmax + epilogue.
-// TMEM: S0 [0,128) S1 [128,256) O [256,256+D).
+// Two leader-CTA warps issue the pair's MMAs (QK^T and P V), each one key tile per asm block with a
+// single elect.sync: a tcgen05.mma instruction costs ~45 cycles to issue, so one issuer serialising
+// 16 MMAs and its barrier waits per key tile cannot keep the tensor pipe busy. TMA loads of both CTAs and the P-ready / O-free
+// arrivals of both CTAs' softmax warps complete on the leader's barriers; MMA commits multicast to
+// both CTAs.
+// Warp roles (per CTA): w0 TMA (Q double buffer, K-half ring), w3 TMA (V^T-half ring), w1 QK^T
+// issuer (leader), w2 TMEM allocator + P V issuer (leader), w4-w7 softmax keys [0,64), w8-w11 keys
+// [64,128).
+// TMEM (per CTA): S0 [0,128) S1 [128,256) S2 [256,384) O [384,384+D).
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 
@@ -26,9 +41,31 @@ namespace {
 
 using namespace tc;
 
-constexpr int BQ = 128;   // queries per work item (= UMMA M, = TMEM lanes)
+#ifdef SWF_ATTN_TRACE
+// development build only (make EXTRA=-DSWF_ATTN_TRACE): clock64 stamps of CTA 0's pipeline events,
+// written to $SWF_ATTN_TRACE_OUT after each launch. Per key tile g: 0 S ready, 1 row max exchanged,
+// 2 P stores issued, 3 P stored, 4 P seen by the MMA issuer, 5 P V issued; per item n: 6 MMA saw
+// Q, 7 MMA saw O free, 8 epilogue start, 9 epilogue end; MMA warp per tile: 10 S issue entry,
+// 11 K landed, 12 S issued, 13 P V entry, 14 P seen.
+constexpr int kTrN = 1024;
+__device__ unsigned long long g_trace[2][16][kTrN];  // [CTA 0 / 1 of the first cluster]
+__device__ unsigned long long g_trace_w[2][16][kTrN];  // per softmax warp: [cta][warp-4 (S ready) / 8+warp-4 (P done)]
+#define SWF_TR(row, idx)                                                                 \
+    do {                                                                                 \
+        if (blockIdx.x < 2 && (idx) < kTrN) g_trace[blockIdx.x][row][idx] = clock64(); \
+    } while (0)
+#else
+#define SWF_TR(row, idx) \
+    do {                 \
+    } while (0)
+#endif
+
+constexpr int BQ = 128;   // queries per CTA tile (= UMMA M, = TMEM lanes)
 constexpr int BKV = 128;  // keys per tile
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
+constexpr int kNS = 3;       // S buffers in TMEM
+constexpr uint32_t kBackoffNs = 40;  // poll back-off of the control warps' barrier waits
+constexpr uint32_t kTO = 384;  // TMEM column of O
 constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
 
 template <int D>
@@ -36,37 +73,41 @@ struct ACfg {
     static constexpr int kSw = D >= 64 ? 128 : 2 * D;  // swizzle bytes of Q/K rows (d contiguous)
     static constexpr int kColsPerBox = kSw / 2;         // d elements per TMA box row
     static constexpr int kBoxes = D / kColsPerBox;      // boxes along d
-    static constexpr int kQBytes = BQ * D * 2;
-    static constexpr int kKBytes = BKV * D * 2;
-    static constexpr int kVBytes = D * BKV * 2;         // V^T tile: D rows x 128 keys (two SW128 boxes)
-    static constexpr int kNK = 3, kNV = 2;
-    static constexpr int kSmem = 2 * kQBytes + kNK * kKBytes + kNV * kVBytes + 1024 + 256;
-    static constexpr uint32_t kIdescS = idesc_bf16(BQ, BKV);
-    static constexpr uint32_t kIdescO = idesc_bf16(BQ, D);
+    static constexpr int kQBytes = BQ * D * 2;          // this CTA's query tile
+    static constexpr int kKHalf = (BKV / 2) * D * 2;    // this CTA's 64 keys of a K tile
+    static constexpr int kVHalf = (D / 2) * BKV * 2;    // this CTA's d/2 rows of a V^T tile
+    static constexpr int kNK = 4, kNV = 4;
+    static constexpr int kRedBytes = 2 * BQ * 4;        // row-max / row-sum exchange between key halves
+    static constexpr int kSmem = 2 * kQBytes + kNK * kKHalf + kNV * kVHalf + kRedBytes + 256 + 1024;
+    static constexpr int kOC = D / 2;                   // O columns per key half (epilogue / rescale)
+    static constexpr uint32_t kIdescS = idesc_bf16(2 * BQ, BKV);
+    static constexpr uint32_t kIdescO = idesc_bf16(2 * BQ, D);
 };
 
 // barrier slots (u64 each)
 enum : int {
-    B_QF = 0, B_QE = 2, B_KF = 4, B_KE = 7, B_VF = 10, B_VE = 12, B_SF = 14, B_SE = 16, B_PF = 18, B_OD = 20,
-    B_OF = 21, B_NUM = 22
+    B_QF = 0, B_QE = 2, B_KF = 4, B_KE = 8, B_VF = 12, B_VE = 16, B_SF = 20, B_PF = 23, B_PVD = 26, B_OD = 29,
+    B_OF = 30, B_NUM = 31
 };
 
-// Work item -> (q tile, head, local window); items of one (window, head) are consecutive so the
-// concurrently running CTAs share K / V^T tiles through L2.
+// Work item -> (pair of q tiles, head, local window); the two CTAs of a cluster take the two q tiles
+// of a pair (crank 0 / 1). Items of one (window, head) are consecutive so concurrently running
+// clusters also share K / V^T tiles through L2.
 struct Item {
-    int q0, head, lw;
+    int q0, qp0, head, lw;  // q0: this CTA's tile; qp0: first row of the pair
 };
-__device__ __forceinline__ Item item_of(int it, int nqt, int heads) {
+__device__ __forceinline__ Item item_of(int it, int npairs, int heads, int crank) {
     Item r;
-    const int qt = it % nqt;
-    const int hw = it / nqt;
-    r.q0 = qt * BQ;
+    const int qp = it % npairs;
+    const int hw = it / npairs;
+    r.qp0 = qp * 2 * BQ;
+    r.q0 = r.qp0 + crank * BQ;
     r.head = hw % heads;
     r.lw = hw / heads;
     return r;
 }
 
-// key range of a work item (seam groups)
+// key range of a work item (seam groups), the union over the pair so both CTAs walk the same tiles
 struct Range {
     int split, t_lo, ntiles;
     bool masked;
@@ -77,12 +118,223 @@ __device__ __forceinline__ Range range_of(const AttnParams& p, const Item& it) {
     const int gw = p.lay.loc2glob[it.lw];
     r.masked = p.lay.g.shift > 0 && (gw / p.lay.g.nx) == p.lay.g.ny - 1;
     r.split = r.masked ? (p.w - p.lay.g.shift) * p.w : s;
-    const int qlast = min(it.q0 + BQ, s) - 1;
-    const int kv_lo = (r.masked && it.q0 >= r.split) ? r.split : 0;
+    const int qlast = min(it.qp0 + 2 * BQ, s) - 1;
+    const int kv_lo = (r.masked && it.qp0 >= r.split) ? r.split : 0;
     const int kv_hi = (r.masked && qlast < r.split) ? r.split : s;
     r.t_lo = kv_lo / BKV;
     r.ntiles = (kv_hi + BKV - 1) / BKV - r.t_lo;
     return r;
+}
+
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// arrive on a (possibly remote) barrier of the cluster; CTA-scope release: the data handed over lives
+// in TMEM (ordered by tcgen05.wait + tcgen05.fence::before_thread_sync), and a cluster-scope release
+// would cost a GPU-wide MEMBAR per arrival
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+// TMA 2D tile load into this CTA's shared memory, completing on the leader CTA's mbarrier
+__device__ __forceinline__ void tma_load_2cta(uint32_t dst, const void* tmap, uint32_t bar_cluster, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+// mbarrier wait for the control warps: poll with a short nanosleep back-off, so a waiting producer /
+// MMA warp leaves the issue slots of its SM sub-partition to the softmax warp pair that shares it
+__device__ __forceinline__ void mbar_sleep_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    for (;;) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(kBackoffNs);
+    }
+}
+// named barrier of the two warps sharing a TMEM lane quadrant (one per key half)
+__device__ __forceinline__ void pair_sync(int quadrant) {
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quadrant) : "memory");
+}
+
+// TMA tensor store of a 2D box from shared memory (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap), "r"(src),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+// all 256 softmax threads
+__device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 5, 256;" ::: "memory"); }
+
+// commit of the pair's MMAs arriving on this CTA's barrier
+__device__ __forceinline__ void commit2(uint32_t bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+        "}\n" ::"r"(bar)
+        : "memory");
+}
+// commit of the pair's MMAs arriving on the barrier at the same offset in both CTAs
+__device__ __forceinline__ void commit2_mc(uint32_t bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        ".reg .b16 m;\n"
+        "mov.b16 m, 3;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+        "}\n" ::"r"(bar)
+        : "memory");
+}
+
+// Tile-level pair-wide MMA issue: ONE asm block per tile with one elect.sync, descriptor start
+// addresses advanced by immediates inside the block. Issuing MMA by MMA costs a register-to-uniform
+// broadcast chain per instruction (~50 cycles each), which starves the tensor pipe at N = 128.
+template <int OA1, int OB1>
+__device__ __forceinline__ void mma2_ss_x2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, pf, pt;\n"
+        ".reg .b64 a, b;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 pf, %3, %3;\n"
+        "setp.eq.b32 pt, %3, %3;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, pf;\n"
+        "add.s64 a, %1, %4;\n"
+        "add.s64 b, %2, %5;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "}\n"
+        ::"r"(d), "l"(a), "l"(b), "r"(idesc), "n"(OA1), "n"(OB1));
+}
+template <int OA1, int OA2, int OA3, int OB1, int OB2, int OB3>
+__device__ __forceinline__ void mma2_ss_x4(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, pf, pt;\n"
+        ".reg .b64 a, b;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 pf, %3, %3;\n"
+        "setp.eq.b32 pt, %3, %3;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, pf;\n"
+        "add.s64 a, %1, %4;\n"
+        "add.s64 b, %2, %7;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, %5;\n"
+        "add.s64 b, %2, %8;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, %6;\n"
+        "add.s64 b, %2, %9;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "}\n"
+        ::"r"(d), "l"(a), "l"(b), "r"(idesc), "n"(OA1), "n"(OA2), "n"(OA3), "n"(OB1), "n"(OB2), "n"(OB3));
+}
+template <int OA1, int OA2, int OA3, int OA4, int OA5, int OA6, int OA7, int OB1, int OB2, int OB3, int OB4, int OB5, int OB6, int OB7>
+__device__ __forceinline__ void mma2_ss_x8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, pf, pt;\n"
+        ".reg .b64 a, b;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 pf, %3, %3;\n"
+        "setp.eq.b32 pt, %3, %3;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, pf;\n"
+        "add.s64 a, %1, %4;\n"
+        "add.s64 b, %2, %11;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, %5;\n"
+        "add.s64 b, %2, %12;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, %6;\n"
+        "add.s64 b, %2, %13;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, %7;\n"
+        "add.s64 b, %2, %14;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, %8;\n"
+        "add.s64 b, %2, %15;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, %9;\n"
+        "add.s64 b, %2, %16;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, %10;\n"
+        "add.s64 b, %2, %17;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, pt;\n"
+        "}\n"
+        ::"r"(d), "l"(a), "l"(b), "r"(idesc), "n"(OA1), "n"(OA2), "n"(OA3), "n"(OA4), "n"(OA5), "n"(OA6), "n"(OA7), "n"(OB1), "n"(OB2), "n"(OB3), "n"(OB4), "n"(OB5), "n"(OB6), "n"(OB7));
+}
+// 8 pair-wide TS MMAs of one P V tile: A = P at TMEM columns a + TA_k, B start address + OB_k
+template <int TA1, int TA2, int TA3, int TA4, int TA5, int TA6, int TA7, int OB1, int OB2, int OB3, int OB4, int OB5, int OB6, int OB7>
+__device__ __forceinline__ void mma2_ts_x8(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, p0, pt;\n"
+        ".reg .b64 b;\n"
+        ".reg .b32 a;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p0, %4, 0;\n"
+        "setp.eq.b32 pt, %3, %3;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p0;\n"
+        "add.u32 a, %1, %5;\n"
+        "add.s64 b, %2, %12;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.u32 a, %1, %6;\n"
+        "add.s64 b, %2, %13;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.u32 a, %1, %7;\n"
+        "add.s64 b, %2, %14;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.u32 a, %1, %8;\n"
+        "add.s64 b, %2, %15;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.u32 a, %1, %9;\n"
+        "add.s64 b, %2, %16;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.u32 a, %1, %10;\n"
+        "add.s64 b, %2, %17;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.u32 a, %1, %11;\n"
+        "add.s64 b, %2, %18;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "}\n"
+        ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc0), "n"(TA1), "n"(TA2), "n"(TA3), "n"(TA4), "n"(TA5), "n"(TA6), "n"(TA7), "n"(OB1), "n"(OB2), "n"(OB3), "n"(OB4), "n"(OB5), "n"(OB6), "n"(OB7));
+}
+// all QK^T MMAs of one key tile (D/16 k-steps): A = Q rows (BQ x kSw boxes), B = this CTA's 64 keys
+template <int D>
+__device__ __forceinline__ void issue_s_tile(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    if constexpr (D == 128)
+        mma2_ss_x8<2, 4, 6, 1024, 1026, 1028, 1030, 2, 4, 6, 512, 514, 516, 518>(d, a, b, idesc);
+    else if constexpr (D == 64)
+        mma2_ss_x4<2, 4, 6, 2, 4, 6>(d, a, b, idesc);
+    else
+        mma2_ss_x2<2, 2>(d, a, b, idesc);
+}
+// all P V MMAs of one key tile: P of keys [64h, 64h+64) at S columns [64h, 64h+32); V^T half in
+// two 64-key SW128 boxes of D/2 rows
+template <int D>
+__device__ __forceinline__ void issue_pv_tile(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    constexpr int BX = (D / 2) * 128 / 16;  // 16-byte units per V^T box
+    mma2_ts_x8<8, 16, 24, 64, 72, 80, 88, 2, 4, 6, BX, BX + 2, BX + 4, BX + 6>(d, a, b, idesc, acc0);
 }
 
 __device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
@@ -118,47 +370,117 @@ __device__ __forceinline__ unsigned long long ex2_poly2(unsigned long long z) {
     return (unsigned long long)lo | ((unsigned long long)hi << 32);
 }
 
+// this thread's OC = D/2 O columns (TMEM address t): scale in place / read out
+template <int OC>
+__device__ __forceinline__ void o_scale(uint32_t t, float f) {
+    if constexpr (OC == 16) {
+        uint32_t o[16];
+        ld16(t, o);
+        wait_ld_dep16(o);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+        st16(t, o);
+    } else {
+#pragma unroll 1
+        for (int c = 0; c < OC / 32; ++c) {
+            uint32_t o[32];
+            ld32(t + uint32_t(c * 32), o);
+            wait_ld_dep(o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+            st32(t + uint32_t(c * 32), o);
+        }
+    }
+    wait_st();
+}
+__device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const uint32_t* o, float inv) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+        d4[v] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * v]) * inv, __uint_as_float(o[8 * v + 1]) * inv),
+                           pack_bf16x2(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv),
+                           pack_bf16x2(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv),
+                           pack_bf16x2(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv));
+}
+template <int OC>
+__device__ __forceinline__ void o_store(uint32_t t, __nv_bfloat16* dst, float inv, bool valid) {
+    if constexpr (OC == 16) {
+        uint32_t o[16];
+        ld16(t, o);
+        wait_ld_dep16(o);
+        if (valid) store_bf16x16(dst, o, inv);
+    } else {
+#pragma unroll 1
+        for (int c = 0; c < OC / 32; ++c) {
+            uint32_t o[32];
+            ld32(t + uint32_t(c * 32), o);
+            wait_ld_dep(o);
+            if (valid) {
+                store_bf16x16(dst + c * 32, o, inv);
+                store_bf16x16(dst + c * 32 + 16, o + 16, inv);
+            }
+        }
+    }
+}
+
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-              const __grid_constant__ CUtensorMap tmV, AttnParams p, int n_items) {
+              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, AttnParams p,
+              int n_items) {
     using C = ACfg<D>;
     extern __shared__ __align__(1024) uint8_t smraw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = sm;                        // [2][BQ x D]
-    uint8_t* sK = sm + 2 * C::kQBytes;       // [kNK][BKV x D]
-    uint8_t* sV = sK + C::kNK * C::kKBytes;  // [kNV][D x BKV] (V^T)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::kNV * C::kVBytes);
+    uint8_t* sK = sm + 2 * C::kQBytes;       // [kNK][BKV/2 x D]: keys [64 crank, 64 crank + 64)
+    uint8_t* sV = sK + C::kNK * C::kKHalf;   // [kNV][D/2 x BKV]: V^T rows [D/2 crank, D/2 crank + D/2)
+    float* red = reinterpret_cast<float*>(sV + C::kNV * C::kVHalf);  // [2 key halves][BQ rows]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::kNV * C::kVHalf + C::kRedBytes);
     auto bar = [&](int slot) { return smem_u32(&bars[slot]); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[B_NUM]);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = p.s;
-    const int nqt = (s + BQ - 1) / BQ;
+    const int npairs = (s + 2 * BQ - 1) / (2 * BQ);
+    const int crank = int(cta_rank());
+    const bool lead = crank == 0;
+    auto lbar = [&](int slot) { return map_to_rank(bar(slot), 0); };  // the leader CTA's barrier
+    const int cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
 
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(bar(B_QF + i), 1);
-            mbar_init(bar(B_QE + i), 1);
-            mbar_init(bar(B_VF + i), 1);
-            mbar_init(bar(B_VE + i), 1);
+            mbar_init(bar(B_QE + i), 1);  // released by the epilogue (its TMA store reads the buffer)
+        }
+        for (int i = 0; i < kNS; ++i) {
             mbar_init(bar(B_SF + i), 1);
-            mbar_init(bar(B_SE + i), 1);
-            mbar_init(bar(B_PF + i), 4);
+            mbar_init(bar(B_PF + i), 16);  // leader's: the softmax warps of both CTAs
+            mbar_init(bar(B_PVD + i), 1);   // leader's: P V of this buffer complete
         }
         for (int i = 0; i < C::kNK; ++i) {
             mbar_init(bar(B_KF + i), 1);
             mbar_init(bar(B_KE + i), 1);
         }
+        for (int i = 0; i < C::kNV; ++i) {
+            mbar_init(bar(B_VF + i), 1);
+            mbar_init(bar(B_VE + i), 1);
+        }
         mbar_init(bar(B_OD), 1);
-        mbar_init(bar(B_OF), 4);
+        mbar_init(bar(B_OF), 16);  // leader's: the epilogue warps of both CTAs
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
     fence_before();
-    __syncthreads();
+    cluster_sync_all();  // barrier inits visible to the peer's TMA completions / commits / arrivals
     fence_after();
     const uint32_t tmem = *tmem_slot;
+
+    // register rebalancing within the 168 x 384 launch allocation: the control warpgroup drops to 72,
+    // the softmax warpgroups rise to 216 (128 x (168 - 72) >= 256 x (216 - 168), else the increase blocks)
+    if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
 
     if (warp == 0) {
         // ===== TMA producer 1: Q (double-buffered across work items) and the K ring
@@ -166,23 +488,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
             int g = 0, n = 0;
-            for (int itx = blockIdx.x; itx < n_items; itx += gridDim.x, ++n) {
-                const Item it = item_of(itx, nqt, p.heads);
+            for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
+                const Item it = item_of(itx, npairs, p.heads, crank);
                 const Range rg = range_of(p, it);
                 const int plane = it.lw * p.heads + it.head;
                 const int qb = n & 1;
-                mbar_wait(bar(B_QE + qb), ((n >> 1) & 1) ^ 1);
-                mbar_expect_tx(bar(B_QF + qb), C::kQBytes);
+                mbar_sleep_wait(bar(B_QE + qb), ((n >> 1) & 1) ^ 1);
+                if (lead) mbar_expect_tx(bar(B_QF + qb), 2 * C::kQBytes);  // both query tiles
                 for (int b = 0; b < C::kBoxes; ++b)
-                    tma_load_2d(smem_u32(sQ + qb * C::kQBytes + b * BQ * C::kSw), &tmQ, bar(B_QF + qb),
-                                b * C::kColsPerBox, plane * s + it.q0);
+                    tma_load_2cta(smem_u32(sQ + qb * C::kQBytes + b * BQ * C::kSw), &tmQ, lbar(B_QF + qb),
+                                  b * C::kColsPerBox, plane * s + it.q0);
                 for (int j = 0; j < rg.ntiles; ++j, ++g) {
                     const int st = g % C::kNK;
-                    mbar_wait(bar(B_KE + st), ((g / C::kNK) & 1) ^ 1);
-                    mbar_expect_tx(bar(B_KF + st), C::kKBytes);
+                    mbar_sleep_wait(bar(B_KE + st), ((g / C::kNK) & 1) ^ 1);
+                    if (lead) mbar_expect_tx(bar(B_KF + st), 2 * C::kKHalf);  // both key halves
                     for (int b = 0; b < C::kBoxes; ++b)
-                        tma_load_2d(smem_u32(sK + st * C::kKBytes + b * BKV * C::kSw), &tmK, bar(B_KF + st),
-                                    b * C::kColsPerBox, plane * s + (rg.t_lo + j) * BKV);
+                        tma_load_2cta(smem_u32(sK + st * C::kKHalf + b * (BKV / 2) * C::kSw), &tmK, lbar(B_KF + st),
+                                      b * C::kColsPerBox, plane * s + (rg.t_lo + j) * BKV + crank * (BKV / 2));
                 }
             }
         }
@@ -191,124 +513,154 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
             int g = 0;
-            for (int itx = blockIdx.x; itx < n_items; itx += gridDim.x) {
-                const Item it = item_of(itx, nqt, p.heads);
+            for (int itx = cluster_id; itx < n_items; itx += n_clusters) {
+                const Item it = item_of(itx, npairs, p.heads, crank);
                 const Range rg = range_of(p, it);
                 const int plane = it.lw * p.heads + it.head;
                 for (int j = 0; j < rg.ntiles; ++j, ++g) {
-                    const int st = g & 1;
-                    mbar_wait(bar(B_VE + st), ((g >> 1) & 1) ^ 1);
-                    mbar_expect_tx(bar(B_VF + st), C::kVBytes);
+                    const int st = g % C::kNV;
+                    mbar_sleep_wait(bar(B_VE + st), ((g / C::kNV) & 1) ^ 1);
+                    if (lead) mbar_expect_tx(bar(B_VF + st), 2 * C::kVHalf);  // both d halves
+                    // this CTA's d rows [D/2 crank, D/2 crank + D/2), keys in two 64-key boxes
                     for (int b = 0; b < 2; ++b)
-                        tma_load_2d(smem_u32(sV + st * C::kVBytes + b * D * 128), &tmV, bar(B_VF + st),
-                                    (rg.t_lo + j) * BKV + b * 64, plane * D);
+                        tma_load_2cta(smem_u32(sV + st * C::kVHalf + b * (D / 2) * 128), &tmV, lbar(B_VF + st),
+                                      (rg.t_lo + j) * BKV + b * 64, plane * D + crank * (D / 2));
                 }
             }
         }
-    } else if (warp == 1) {
-        // ===== MMA issuer: S(g) is issued before PV(g-1), so QK^T of the next key tile overlaps the
-        // softmax of the current one; tensor-pipe order guarantees PV(g-2) read P before S(g) lands
-        // in the same buffer (s_free is committed after that PV).
-        if (lane == 0) {
-            int g = 0, n = 0;
-            auto issue_pv = [&](int gg, bool first) {
-                const int b = gg & 1;
-                mbar_wait(bar(B_PF + b), (gg >> 1) & 1);
-                mbar_wait(bar(B_VF + b), (gg >> 1) & 1);
+    } else if (warp == 1 && lead) {
+        // ===== QK^T issuer for the pair (leader CTA; whole warp, converged; one elected lane issues),
+        // running over the flattened (item, key tile) sequence up to three tiles ahead of P V
+        // a CTA holding all 512 columns owns TMEM from address 0 (checked)
+        if (tmem != 0) __trap();
+        const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK);
+        int g = 0, n = 0;
+        for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
+            const Range rg = range_of(p, item_of(itx, npairs, p.heads, crank));
+            const int qb = n & 1;
+            mbar_sleep_wait(bar(B_QF + qb), (n >> 1) & 1);
+            if (lane == 0) SWF_TR(6, n);
+            for (int j = 0; j < rg.ntiles; ++j, ++g) {
+                const int st = g % C::kNK, b = g % kNS;
+                if (lane == 0) SWF_TR(10, g);
+                mbar_sleep_wait(bar(B_KF + st), (g / C::kNK) & 1);
+                // S buffer b last held P(g-3): its P V must have completed
+                mbar_sleep_wait(bar(B_PVD + b), ((g / kNS) & 1) ^ 1);
+                if (lane == 0) SWF_TR(11, g);
                 fence_after();
-                const uint8_t* vt = sV + b * C::kVBytes;
-#pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk) {
-                    const uint64_t bd = desc_kmajor(smem_u32(vt + (kk >> 2) * D * 128 + (kk & 3) * 32), 128);
-                    mma_ts(tmem + 256u, tmem + uint32_t(b * 128 + kk * 8), bd, C::kIdescO,
-                           (!first || kk > 0) ? 1u : 0u);
+                const uint64_t a0 = desc_kmajor(sQa + uint32_t(qb * C::kQBytes), C::kSw);
+                const uint64_t b0 = desc_kmajor(sKa + uint32_t(st * C::kKHalf), C::kSw);
+                issue_s_tile<D>(uint32_t(b * 128), a0, b0, C::kIdescS);
+                commit2_mc(bar(B_SF + b));
+                commit2_mc(bar(B_KE + st));  // K halves consumed in both CTAs
+                if (lane == 0) SWF_TR(12, g);
+#ifdef SWF_ATTN_SWAIT  // development only: measure the QK^T completion latency
+                mbar_wait(bar(B_SF + b), (g / kNS) & 1);
+                if (lane == 0) SWF_TR(15, g);
+#endif
+            }
+        }
+    } else if (warp == 2 && lead) {
+        // ===== P V issuer for the pair (leader CTA), in key-tile order
+        const uint32_t sVa = smem_u32(sV);
+        int g = 0, n = 0;
+        for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
+            const Range rg = range_of(p, item_of(itx, npairs, p.heads, crank));
+            for (int j = 0; j < rg.ntiles; ++j, ++g) {
+                const int b = g % kNS, vs = g % C::kNV;
+                if (j == 0 && n >= 1) {
+                    mbar_sleep_wait(bar(B_OF), (n - 1) & 1);  // O of the previous item read out
+                    if (lane == 0) SWF_TR(7, n);
                 }
-                commit(bar(B_OD));
-                commit(bar(B_VE + b));
-                commit(bar(B_SE + b));
-            };
-            for (int itx = blockIdx.x; itx < n_items; itx += gridDim.x, ++n) {
-                const Item it = item_of(itx, nqt, p.heads);
-                const Range rg = range_of(p, it);
-                const int qb = n & 1;
-                mbar_wait(bar(B_QF + qb), (n >> 1) & 1);
-                for (int j = 0; j < rg.ntiles; ++j, ++g) {
-                    const int b = g & 1, st = g % C::kNK;
-                    mbar_wait(bar(B_KF + st), (g / C::kNK) & 1);
-                    if (g >= 2) mbar_wait(bar(B_SE + b), ((g >> 1) + 1) & 1);
-                    fence_after();
-                    const uint8_t* kt = sK + st * C::kKBytes;
-                    const uint8_t* qt = sQ + qb * C::kQBytes;
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const int box = (kk * 32) / C::kSw, off = (kk * 32) % C::kSw;
-                        const uint64_t a = desc_kmajor(smem_u32(qt + box * BQ * C::kSw + off), C::kSw);
-                        const uint64_t bd = desc_kmajor(smem_u32(kt + box * BKV * C::kSw + off), C::kSw);
-                        mma_ss(tmem + uint32_t(b * 128), a, bd, C::kIdescS, kk > 0 ? 1u : 0u);
-                    }
-                    commit(bar(B_SF + b));
-                    commit(bar(B_KE + st));
-                    if (j + 1 == rg.ntiles) commit(bar(B_QE + qb));  // Q of this item no longer read
-                    if (j >= 1) {
-                        if (j == 1 && n >= 1) mbar_wait(bar(B_OF), (n - 1) & 1);  // O of the last item read out
-                        issue_pv(g - 1, j == 1);
-                    }
-                }
-                if (rg.ntiles == 1 && n >= 1) mbar_wait(bar(B_OF), (n - 1) & 1);
-                issue_pv(g - 1, rg.ntiles == 1);
+                if (lane == 0) SWF_TR(13, g);
+                mbar_sleep_wait(bar(B_PF + b), (g / kNS) & 1);
+                if (lane == 0) SWF_TR(14, g);
+                mbar_sleep_wait(bar(B_VF + vs), (g / C::kNV) & 1);
+                fence_after();
+                if (lane == 0) SWF_TR(4, g);
+                const uint64_t b0 = desc_kmajor(sVa + uint32_t(vs * C::kVHalf), 128);
+                issue_pv_tile<D>(kTO, uint32_t(b * 128), b0, C::kIdescO, j == 0 ? 0u : 1u);
+                commit2_mc(bar(B_OD));
+                commit2_mc(bar(B_VE + vs));  // V^T halves consumed in both CTAs
+                commit2(bar(B_PVD + b));     // S buffer b free for S(g+3)
+                if (lane == 0) SWF_TR(5, g);
             }
         }
     } else if (warp >= 4) {
-        // ===== softmax (one thread per query row) + epilogue
-        const int wq = warp - 4;  // TMEM lane quadrant (warp % 4)
+        // ===== softmax (two threads per query row, 64 keys each) + epilogue
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+        const int hk = (warp - 4) >> 2;  // key half of every tile
+        const int wq = warp & 3;         // TMEM lane quadrant
         const int r = wq * 32 + lane;
         const uint32_t lane_off = uint32_t(wq * 32) << 16;
-        const uint32_t tO = tmem + lane_off + 256u;
+        const uint32_t tO = lane_off + kTO + uint32_t(hk * C::kOC);
         const float sl2 = p.scale * 1.4426950408889634f;
-        int g = 0;
-        for (int itx = blockIdx.x; itx < n_items; itx += gridDim.x) {
-            const Item it = item_of(itx, nqt, p.heads);
+        const bool tr = threadIdx.x == 128;
+        const bool leader = threadIdx.x == 128;  // issues the O TMA stores, releases Q buffers
+        int qe_pending = -1;                     // Q buffer whose TMA-store read is still in flight
+        auto release_q = [&]() {
+            if (qe_pending >= 0) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(bar(B_QE + qe_pending));
+                qe_pending = -1;
+            }
+        };
+        int g = 0, n = 0;
+        for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
+            const Item it = item_of(itx, npairs, p.heads, crank);
             const Range rg = range_of(p, it);
             const int q = it.q0 + r;
             const int rlo = (rg.masked && q >= rg.split) ? rg.split : 0;
             const int rhi = (rg.masked && q < rg.split) ? rg.split : s;
+            // destination row (token owner's SP band; this rank when sp == 1), resolved early
+            int orank = 0;
+            const i64 oloc = q < s ? p.lay.wtok_to_loc(p.wp_rank, it.lw, q, &orank) : 0;
             float m = -INFINITY, l = 0.f;
             for (int j = 0; j < rg.ntiles; ++j, ++g) {
-                const int b = g & 1;
-                const uint32_t tS = tmem + lane_off + uint32_t(b * 128);
-                mbar_wait(bar(B_SF + b), (g >> 1) & 1);
+                const int b = g % kNS;
+                const uint32_t tS = lane_off + uint32_t(b * 128 + hk * 64);
+                mbar_wait(bar(B_SF + b), (g / kNS) & 1);
                 fence_after();
-                uint32_t sr[128];
+                if (tr) SWF_TR(0, g);
+#ifdef SWF_ATTN_TRACE
+                if (lane == 0 && blockIdx.x < 2 && g < kTrN) g_trace_w[blockIdx.x][warp - 4][g] = clock64();
+#endif
+#ifdef SWF_ATTN_NOSOFTMAX  // development only: pipeline rate without the softmax
+                if (tr) SWF_TR(3, g);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(lbar(B_PF + b));
+                if (leader) release_q();
+                l = 1.f;
+                continue;
+#endif
+                uint32_t sa[64];
+                ld32(tS, sa);
+                ld32(tS + 32u, sa + 32);
+                wait_ld_dep(sa);
+                wait_ld_dep(sa + 32);
+                const int kb = (rg.t_lo + j) * BKV + hk * 64;
+                if (kb < rlo || kb + 64 > rhi) {  // boundary tile: mask keys outside [rlo, rhi)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) ld32(tS + uint32_t(c * 32), sr + 32 * c);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) wait_ld_dep(sr + 32 * c);
-                const int kb = (rg.t_lo + j) * BKV;
-                if (kb < rlo || kb + BKV > rhi) {  // boundary tile: mask keys outside [rlo, rhi)
-#pragma unroll
-                    for (int i = 0; i < 128; ++i)
-                        if (kb + i < rlo || kb + i >= rhi) sr[i] = __float_as_uint(-INFINITY);
+                    for (int i = 0; i < 64; ++i)
+                        if (kb + i < rlo || kb + i >= rhi) sa[i] = __float_as_uint(-INFINITY);
                 }
                 float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int i = 0; i < 128; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[i]));
-                const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+                for (int i = 0; i < 64; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sa[i]));
+                const float pm = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+                red[hk * BQ + r] = pm;
+                pair_sync(wq);
+                const float mx = fmaxf(pm, red[(1 - hk) * BQ + r]) * sl2;
+                pair_sync(wq);  // both halves read before the next exchange overwrites
+                if (tr) SWF_TR(1, g);
+                // both halves take the same rescale decision (same mx, same m)
                 if (mx > m + kRescale || (m == -INFINITY && mx != -INFINITY)) {
                     if (m != -INFINITY) {
-                        // O *= 2^(m - mx): the PV of the previous key tile must have landed
+                        // O *= 2^(m - mx): P(g-1) V must have landed
                         mbar_wait(bar(B_OD), (g - 1) & 1);
                         fence_after();
                         const float f = ex2(m - mx);
-#pragma unroll 1
-                        for (int c = 0; c < D / 32; ++c) {
-                            uint32_t o[32];
-                            ld32(tO + uint32_t(c * 32), o);
-                            wait_ld_dep(o);
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-                            st32(tO + uint32_t(c * 32), o);
-                        }
-                        wait_st();
+                        o_scale<C::kOC>(tO, f);
                         l *= f;
                     }
                     m = mx;
@@ -317,12 +669,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const unsigned long long sl2x2 = f2_pack(sl2, sl2), nbx2 = f2_pack(nb, nb);
                 unsigned long long ls2 = 0ull, ls2b = 0ull;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {  // 32 keys -> 16 packed bf16x2 columns per store
+                for (int c = 0; c < 2; ++c) {  // 32 keys -> 16 packed bf16x2 columns per store
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const unsigned long long sv =
-                            (unsigned long long)sr[32 * c + 2 * i] | ((unsigned long long)sr[32 * c + 2 * i + 1] << 32);
+                            (unsigned long long)sa[32 * c + 2 * i] | ((unsigned long long)sa[32 * c + 2 * i + 1] << 32);
                         const unsigned long long z = ffma2(sv, sl2x2, nbx2);
                         unsigned long long pv;
                         if ((i & 7) < 3)  // 3/8 of the exponentials on the FMA pipe
@@ -337,48 +689,79 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     st16(tS + uint32_t(16 * c), pk);
                 }
+                if (tr) SWF_TR(2, g);
                 const unsigned long long lsum = fadd2(ls2, ls2b);
                 l += lo_f(lsum) + hi_f(lsum);
                 wait_st();
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar(B_PF + b));
+                if (tr) SWF_TR(3, g);
+#ifdef SWF_ATTN_TRACE
+                if (lane == 0 && blockIdx.x < 2 && g < kTrN) g_trace_w[blockIdx.x][8 + warp - 4][g] = clock64();
+#endif
+                if (lane == 0) mbar_arrive_cluster(lbar(B_PF + b));
+                if (leader) release_q();  // the previous item's O store has long finished reading
             }
-            // epilogue: O / l -> bf16 rows to the token owner (its SP band; this rank when sp == 1),
-            // head columns of the global head index (swin.hpp:319-320 concat)
-            mbar_wait(bar(B_OD), (g - 1) & 1);
+            // epilogue: O / l -> bf16 (swin.hpp:319-320 head concat); l is the sum of both halves
+            mbar_wait(bar(B_OD), (g - 1) & 1);  // every MMA of this item (incl. its QK^T) complete
             fence_after();
-            const float inv = 1.f / l;
-            int orank = 0;
-            const i64 oloc = q < s ? p.lay.wtok_to_loc(p.wp_rank, it.lw, q, &orank) : 0;
-            __nv_bfloat16* O =
-                reinterpret_cast<__nv_bfloat16*>(p.o_dst[orank]) + oloc * p.ldo + (p.head0 + it.head) * D;
+            if (tr) SWF_TR(8, n);
+            red[hk * BQ + r] = l;
+            pair_sync(wq);
+            const float inv = 1.f / (l + red[(1 - hk) * BQ + r]);
+            pair_sync(wq);
+            const int qb = n & 1;
+            if (D >= 64 && p.tmo != nullptr && it.q0 + BQ <= s) {  // (p.tmo: host flag; the map is tmO)
+                // whole tile, own rows lw*s + q0 ..: stage in this item's Q buffer (SW128, the TMA
+                // box layout) and store with TMA
+                uint8_t* stg = sQ + qb * C::kQBytes;
 #pragma unroll 1
-            for (int c = 0; c < D / 32; ++c) {
-                uint32_t o[32];
-                ld32(tO + uint32_t(c * 32), o);
-                wait_ld_dep(o);
-                if (q < s) {
-                    uint4* d4 = reinterpret_cast<uint4*>(O + c * 32);
+                for (int c = 0; c < C::kOC / 32; ++c) {
+                    uint32_t o[32];
+                    ld32(tO + uint32_t(c * 32), o);
+                    wait_ld_dep(o);
 #pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        d4[v] = make_uint4(
+                    for (int v = 0; v < 4; ++v) {
+                        const int col = hk * C::kOC + c * 32 + v * 8;  // first of 8 bf16 = one 16-byte chunk
+                        const int ch = (col & 63) >> 3;
+                        uint4* dst = reinterpret_cast<uint4*>(stg + (col >> 6) * (BQ * 128) + r * 128 +
+                                                              ((ch ^ (r & 7)) << 4));
+                        *dst = make_uint4(
                             pack_bf16x2(__uint_as_float(o[8 * v]) * inv, __uint_as_float(o[8 * v + 1]) * inv),
                             pack_bf16x2(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv),
                             pack_bf16x2(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv),
                             pack_bf16x2(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv));
+                    }
                 }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                fence_before();
+                softmax_sync();
+                if (leader) {
+                    // this thread holds row 0 of the tile: its destination row starts the box
+                    for (int bx = 0; bx < D / 64; ++bx)
+                        tma_store_2d(&tmO, smem_u32(stg + bx * (BQ * 128)), (p.head0 + it.head) * D + bx * 64,
+                                     int(oloc));
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    qe_pending = qb;
+                }
+            } else {
+                __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(p.o_dst[orank]) + oloc * p.ldo +
+                                   (p.head0 + it.head) * D + hk * C::kOC;
+                o_store<C::kOC>(tO, O, inv, q < s);
+                fence_before();
+                if (leader) mbar_arrive(bar(B_QE + qb));
             }
-            fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar(B_OF));  // O may be overwritten by the next item's first PV
+            if (tr) SWF_TR(9, n);
+            if (lane == 0) mbar_arrive_cluster(lbar(B_OF));  // O may be overwritten by the next item's first PV
         }
+        if (leader && qe_pending >= 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     fence_before();
-    __syncthreads();
+    cluster_sync_all();  // the peer may still arrive on / commit to this CTA until here
     if (warp == 2) {
         fence_after();
-        tmem_free(tmem, 512);
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
 }
 
@@ -390,13 +773,27 @@ void launch(const AttnParams& p, cudaStream_t st) {
         SWF_CUDA(cudaFuncSetAttribute(k_attn_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         configured = true;
     }
-    const int nqt = (p.s + BQ - 1) / BQ;
-    const int n_items = nqt * p.heads * p.nloc;
-    const int grid = std::min(n_items, 148);
+    const int npairs = (p.s + 2 * BQ - 1) / (2 * BQ);
+    const int n_items = npairs * p.heads * p.nloc;
+    const int grid = 2 * std::min(n_items, 74);  // 2-CTA clusters, one CTA per SM
     k_attn_tc<D><<<grid, kThreads, C::kSmem, st>>>(*reinterpret_cast<const CUtensorMap*>(p.tmq),
                                                   *reinterpret_cast<const CUtensorMap*>(p.tmk),
-                                                  *reinterpret_cast<const CUtensorMap*>(p.tmv), p, n_items);
+                                                  *reinterpret_cast<const CUtensorMap*>(p.tmv),
+                                                  *reinterpret_cast<const CUtensorMap*>(p.tmo ? p.tmo : p.tmv), p, n_items);
     SWF_LAUNCH_CHECK();
+#ifdef SWF_ATTN_TRACE
+    if (const char* path = getenv("SWF_ATTN_TRACE_OUT")) {
+        static unsigned long long h[2][16][kTrN];
+        SWF_CUDA(cudaStreamSynchronize(st));
+        SWF_CUDA(cudaMemcpyFromSymbol(h, g_trace, sizeof(h)));
+        if (FILE* f = fopen(path, "wb")) {
+            fwrite(h, sizeof(h), 1, f);
+            SWF_CUDA(cudaMemcpyFromSymbol(h, g_trace_w, sizeof(h)));
+            fwrite(h, sizeof(h), 1, f);
+            fclose(f);
+        }
+    }
+#endif
 }
 
 }  // namespace

@@ -72,8 +72,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// arrive on a (possibly remote) barrier of the cluster; CTA-scope release: the data handed over lives
+// in TMEM (ordered by tcgen05.wait + tcgen05.fence::before_thread_sync), and a cluster-scope release
+// would cost a GPU-wide MEMBAR per arrival
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma_load_2cta(uint32_t dst, const void* tmap, uint32_t bar_cluster, int c0, int c1,
                                               uint64_t policy) {

@@ -144,6 +144,8 @@ struct AttnParams {
     const TmaMap* tmq;  // BF16 path: TMA maps of the q / k planes ([rows][d]) and of V^T ([rows][s])
     const TmaMap* tmk;
     const TmaMap* tmv;
+    const TmaMap* tmo;  // BF16 path, sp == 1: map of the own output buffer (box 64 x 128, SW128) for TMA
+                        // stores of whole query tiles; nullptr = per-row stores
 };
 void attention_f32(const AttnParams& p, cudaStream_t st);
 void attention_bf16(const AttnParams& p, cudaStream_t st);
