@@ -134,6 +134,34 @@ int swf_solve_pf_ode(swf_ctx* ctx, const void* x_init, const void* x_prev_std, c
 int swf_forecast_step(swf_ctx* ctx, const void* x_prev_phys, const void* forcing_phys,
                       const swf_standardizers* stds, const swf_diffusion_cfg* dc, uint64_t run_seed,
                       uint64_t noise_event, void* out, int dtype);
+/* Per-rank input loading (f4; ChunkedReader::read_window_slice, chunked_file.cpp:156-188): forecast_step
+ * with x_prev and forcings read from chunked containers (format of write_chunked, chunked_file.cpp:44-99).
+ * Each rank reads only the chunks covering its own windows (its SP band rows), with parallel readers,
+ * checksum-verified, straight into pinned staging in its local token order. swf_prefetch_chunked starts
+ * that read on a background thread (two slots), so the next step's fields load while the current step
+ * computes; a forecast call with the same paths consumes the prefetched slot. rc 3 on a checksum /
+ * format error, rc 2 on a grid or channel mismatch. */
+int swf_prefetch_chunked(swf_ctx* ctx, const char* state_path, const char* forcing_path);
+int swf_forecast_step_chunked(swf_ctx* ctx, const char* state_path, const char* forcing_path,
+                              const swf_standardizers* stds, const swf_diffusion_cfg* dc, uint64_t run_seed,
+                              uint64_t noise_event, void* out, int dtype);
+long long swf_last_chunk_reads(swf_ctx* ctx); /* chunks read by the last chunked forecast */
+
+/* The chunked container itself (host only; chunked_file.hpp). Fields are C x (H*W) column-major
+ * ([pixel][channel]), as FieldTensor<float>::values. read fills an h x w rect as [h*w][C].
+ * A rect outside the grid is rc 2 (the reference's std::out_of_range), a checksum mismatch rc 3
+ * (IntegrityError). */
+typedef struct swf_chunked swf_chunked;
+int swf_chunked_write(const char* path, const float* field, int channels, int height, int width, int chunk_h,
+                      int chunk_w);
+int swf_chunked_open(const char* path, swf_chunked** out);
+void swf_chunked_close(swf_chunked* r);
+int swf_chunked_info(swf_chunked* r, int* channels, int* height, int* width, int* chunk_h, int* chunk_w);
+int swf_chunked_read(swf_chunked* r, int y0, int x0, int h, int w, float* out);
+int swf_chunked_cover(swf_chunked* r, int y0, int x0, int h, int w, long long* n_chunks);
+long long swf_chunked_reads(swf_chunked* r);
+void swf_chunked_reset_reads(swf_chunked* r);
+
 /* rollout_ensemble (diffusion.hpp:323-339): members x steps, out is members*steps fields
  * (member-major), forcings is steps fields. */
 int swf_rollout_ensemble(swf_ctx* ctx, const void* x_init_phys, const void* forcings_phys, int n_members,

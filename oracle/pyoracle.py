@@ -358,6 +358,68 @@ def save_named_arrays(base: str, cfg: ModelConfig, flat: np.ndarray):
             off += len(raw)
 
 
+# ---- chunked field container (chunked_file.hpp:5-13, src/chunked_file.cpp:44-188), numpy restatement
+CHUNK_MAGIC = b"SWCHNK01"
+
+
+def write_chunked_np(path: str, field: np.ndarray, H: int, W: int, ch: int, cw: int):
+    """write_chunked (chunked_file.cpp:44-99): field [H*W][C] float32; header of u64s, offset and
+    fnv1a64 tables, then each clipped chunk as (c, y, x) row-major."""
+    C_ = field.shape[1]
+    f = field.reshape(H, W, C_).astype(np.float32)
+    ny, nx = -(-H // ch), -(-W // cw)
+    chunks = []
+    for cy in range(ny):
+        for cx in range(nx):
+            tile = f[cy * ch:min(H, cy * ch + ch), cx * cw:min(W, cx * cw + cw), :]
+            chunks.append(np.ascontiguousarray(tile.transpose(2, 0, 1)).tobytes())
+    pos = 8 + 6 * 8 + 2 * 8 * len(chunks)
+    offs = []
+    for b in chunks:
+        offs.append(pos)
+        pos += len(b)
+    with open(path, "wb") as fo:
+        fo.write(CHUNK_MAGIC)
+        fo.write(np.array([1, C_, H, W, ch, cw], "<u8").tobytes())
+        fo.write(np.array(offs, "<u8").tobytes())
+        fo.write(np.array([fnv1a64(b) for b in chunks], "<u8").tobytes())
+        for b in chunks:
+            fo.write(b)
+
+
+def read_chunked_np(path: str, y0: int, x0: int, h: int, w: int):
+    """ChunkedReader::read_window_slice (chunked_file.cpp:156-188) -> ([h*w][C] float32, chunks read).
+    Raises IndexError for a rect outside the grid (std::out_of_range) and ValueError on a checksum
+    mismatch (IntegrityError)."""
+    raw = open(path, "rb").read()
+    if raw[:8] != CHUNK_MAGIC:
+        raise ValueError("bad container magic")
+    ver, C_, H, W, ch, cw = (int(v) for v in np.frombuffer(raw[8:56], "<u8"))
+    if ver != 1:
+        raise ValueError("unsupported container version")
+    ny, nx = -(-H // ch), -(-W // cw)
+    n = ny * nx
+    offs = np.frombuffer(raw[56:56 + 8 * n], "<u8")
+    sums = np.frombuffer(raw[56 + 8 * n:56 + 16 * n], "<u8")
+    if h <= 0 or w <= 0 or y0 < 0 or x0 < 0 or y0 + h > H or x0 + w > W:
+        raise IndexError("window rect outside grid")
+    out = np.zeros((h, w, C_), np.float32)
+    reads = 0
+    for cy in range(y0 // ch, (y0 + h - 1) // ch + 1):
+        for cx in range(x0 // cw, (x0 + w - 1) // cw + 1):
+            idx = cy * nx + cx
+            hh, ww = min(ch, H - cy * ch), min(cw, W - cx * cw)
+            b = raw[int(offs[idx]):int(offs[idx]) + 4 * C_ * hh * ww]
+            if fnv1a64(b) != int(sums[idx]):
+                raise ValueError(f"checksum mismatch in chunk {idx}")
+            reads += 1
+            tile = np.frombuffer(b, np.float32).reshape(C_, hh, ww).transpose(1, 2, 0)
+            ys, ye = max(y0, cy * ch), min(y0 + h, cy * ch + hh)
+            xs, xe = max(x0, cx * cw), min(x0 + w, cx * cw + ww)
+            out[ys - y0:ye - y0, xs - x0:xe - x0] = tile[ys - cy * ch:ye - cy * ch, xs - cx * cw:xe - cx * cw]
+    return out.reshape(h * w, C_), reads
+
+
 def window_owner(wy, wx, a, b):
     oa, ob = C.c_int(), C.c_int()
     lib().orc_window_owner(wy, wx, a, b, C.byref(oa), C.byref(ob))

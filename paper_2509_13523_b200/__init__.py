@@ -141,6 +141,21 @@ def lib():
         L.swf_profile_launches.argtypes = [vp, vp, vp, i, C.POINTER(i)]
         L.swf_noise_field.argtypes = [vp, u64, u64, i, d, vp]
         L.swf_selftest_gemm.argtypes = [i, ll, i, i, C.POINTER(d), C.POINTER(d)]
+        L.swf_prefetch_chunked.argtypes = [vp, C.c_char_p, C.c_char_p]
+        L.swf_forecast_step_chunked.argtypes = [vp, C.c_char_p, C.c_char_p, vp, vp, u64, u64, vp, i]
+        L.swf_last_chunk_reads.argtypes = [vp]
+        L.swf_last_chunk_reads.restype = ll
+        L.swf_chunked_write.argtypes = [C.c_char_p, vp, i, i, i, i, i]
+        L.swf_chunked_open.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.swf_chunked_close.argtypes = [vp]
+        L.swf_chunked_close.restype = None
+        L.swf_chunked_info.argtypes = [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(i)]
+        L.swf_chunked_read.argtypes = [vp, i, i, i, i, vp]
+        L.swf_chunked_cover.argtypes = [vp, i, i, i, i, C.POINTER(ll)]
+        L.swf_chunked_reads.argtypes = [vp]
+        L.swf_chunked_reads.restype = ll
+        L.swf_chunked_reset_reads.argtypes = [vp]
+        L.swf_chunked_reset_reads.restype = None
         _lib = L
     return _lib
 
@@ -319,10 +334,76 @@ class Denoiser:
                                           run_seed, rollout_id, _p(out), _dt(x)))
         return out
 
+    # ---- per-rank input loading from chunked containers (chunked_file.cpp:156-188)
+    def prefetch_chunked(self, state_path: str, forcing_path: str | None = None):
+        _check(lib().swf_prefetch_chunked(self._c, state_path.encode(), None if forcing_path is None
+                                          else forcing_path.encode()))
+
+    def forecast_step_chunked(self, state_path: str, forcing_path: str | None, dc: DiffusionConfig, run_seed: int,
+                              event: int, stds=None, dtype=np.float32):
+        st, keep = self._stds(stds, np.dtype(dtype))
+        out = np.zeros((self.H * self.W, self.cfg.out_channels), dtype)
+        _check(lib().swf_forecast_step_chunked(self._c, state_path.encode(),
+                                               None if forcing_path is None else forcing_path.encode(),
+                                               None if st is None else C.byref(st), C.byref(_DCfg(*astuple(dc))),
+                                               run_seed, event, _p(out), 1 if np.dtype(dtype) == np.float64 else 0))
+        return out
+
+    def last_chunk_reads(self) -> int:
+        return lib().swf_last_chunk_reads(self._c)
+
     def noise_field(self, run_seed: int, event: int, channels: int, sigma_d: float = 1.0) -> np.ndarray:
         out = np.zeros((self.H * self.W, channels), np.float32)
         _check(lib().swf_noise_field(self._c, run_seed, event, channels, sigma_d, _p(out)))
         return out
+
+
+def write_chunked(path: str, field: np.ndarray, height: int, width: int, chunk_h: int, chunk_w: int):
+    """write_chunked (chunked_file.cpp:44-99): field is [H*W][C] float32 (FieldTensor values)."""
+    f = np.ascontiguousarray(field, np.float32)
+    _check(lib().swf_chunked_write(path.encode(), _p(f), f.shape[1], height, width, chunk_h, chunk_w))
+
+
+class ChunkedReader:
+    """ChunkedReader (chunked_file.hpp:36-75) over the C-ABI: read_window_slice returns [h*w][C]."""
+
+    def __init__(self, path: str):
+        h = C.c_void_p()
+        _check(lib().swf_chunked_open(path.encode(), C.byref(h)))
+        self._h = h
+        v = [C.c_int() for _ in range(5)]
+        _check(lib().swf_chunked_info(self._h, *[C.byref(x) for x in v]))
+        self.channels, self.height, self.width, self.chunk_h, self.chunk_w = [x.value for x in v]
+
+    def read_window_slice(self, y0: int, x0: int, h: int, w: int) -> np.ndarray:
+        out = np.zeros((max(h, 0) * max(w, 0), self.channels), np.float32)
+        _check(lib().swf_chunked_read(self._h, y0, x0, h, w, _p(out)))
+        return out
+
+    def read_full(self) -> np.ndarray:
+        return self.read_window_slice(0, 0, self.height, self.width)
+
+    def chunk_cover(self, y0: int, x0: int, h: int, w: int) -> int:
+        n = C.c_longlong()
+        _check(lib().swf_chunked_cover(self._h, y0, x0, h, w, C.byref(n)))
+        return n.value
+
+    def chunk_reads(self) -> int:
+        return lib().swf_chunked_reads(self._h)
+
+    def reset_chunk_reads(self):
+        lib().swf_chunked_reset_reads(self._h)
+
+    def close(self):
+        if self._h:
+            lib().swf_chunked_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def verify_checkpoint(cfg: ModelConfig, base: str):

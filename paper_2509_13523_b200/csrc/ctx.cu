@@ -18,8 +18,10 @@
 #include <sstream>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/swinflow_capi.h"
@@ -36,6 +38,9 @@ struct NumericsError : std::runtime_error {
 struct IoError : std::runtime_error {  // common.hpp:33-40 (IoError / IntegrityError)
     explicit IoError(const std::string& m) : std::runtime_error(m) {}
 };
+}  // namespace swf
+#include "chunked.hpp"
+namespace swf {
 static void require(bool c, const std::string& m) {
     if (!c) throw ConfigError(m);
 }
@@ -110,6 +115,18 @@ struct swf_ctx {
     float *s_cond = nullptr, *s_stats = nullptr;
     std::vector<void*> allocs;
     int nflags = 0;
+    // chunked-container input staging (pinned, local token order), two prefetch slots
+    struct Staged {
+        std::string state_path, forcing_path;
+        float *state = nullptr, *forcing = nullptr;  // pinned [M][C_out], [M][C_f]
+        unsigned long long reads = 0;
+        std::thread th;
+        std::exception_ptr err;
+        bool pending = false;
+        long long seq = 0;
+    } staged[2];
+    long long staged_seq = 0;
+    unsigned long long last_chunk_reads = 0;
     // per-kernel-class CUDA-event timing (bench roofline): class id -> accumulated ms / launches
     bool prof = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
@@ -1104,6 +1121,127 @@ void h2d_local(swf_ctx* c, const void* src, int C, int dtype, float* dst_loc) {
     SWF_CUDA(cudaStreamSynchronize(c->st));
 }
 
+// Per-rank input loading from chunked containers (ChunkedReader::read_window_slice,
+// chunked_file.cpp:156-188; the reference CLI reads whole fields, swinflow_main.cpp:128-157): the
+// rank's owned windows of the unshifted layout (its SP band rows) are merged into pixel rects -- runs
+// of adjacent windows in a window row, stacked over window rows when sp == 1 -- read by parallel
+// readers (one file handle each) and gathered into the local token order [M][C]. Returns the number
+// of chunks read (each chunk's checksum verified).
+unsigned long long read_local_chunked(const swf_ctx* c, const std::string& path, int C, float* dst) {
+    const int w = c->m.w, R = w / c->sp, nx = c->W / w;
+    const std::vector<int>& l2g = c->l2g[0];
+    std::vector<int> g2l(size_t(c->H / w) * nx, -1);
+    for (size_t i = 0; i < l2g.size(); ++i) g2l[l2g[i]] = int(i);
+    struct Run {
+        int wy0, wx0, nwy, nwx;
+    };
+    std::vector<Run> runs;
+    for (int gw : l2g) {
+        const int wy = gw / nx, wx = gw % nx;
+        if (!runs.empty() && runs.back().wy0 == wy && runs.back().wx0 + runs.back().nwx == wx) {
+            ++runs.back().nwx;
+            continue;
+        }
+        runs.push_back({wy, wx, 1, 1});
+    }
+    if (c->sp == 1) {
+        std::vector<Run> st;
+        for (const Run& r : runs) {
+            if (!st.empty() && st.back().wx0 == r.wx0 && st.back().nwx == r.nwx && st.back().wy0 + st.back().nwy == r.wy0) {
+                ++st.back().nwy;
+                continue;
+            }
+            st.push_back(r);
+        }
+        runs.swap(st);
+    }
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int T = std::max(1, std::min<int>(int(runs.size()), int(std::min(16u, hw))));
+    std::vector<unsigned long long> reads(T, 0);
+    std::vector<std::exception_ptr> errs(T);
+    auto work = [&](int t) {
+        try {
+            chunked::Reader rd(path);
+            require(rd.height() == c->H && rd.width() == c->W,
+                    "chunked input " + path + ": grid " + std::to_string(rd.height()) + "x" +
+                        std::to_string(rd.width()) + " != model grid " + std::to_string(c->H) + "x" +
+                        std::to_string(c->W));
+            require(rd.channels() == C, "chunked input " + path + ": " + std::to_string(rd.channels()) +
+                                            " channels, expected " + std::to_string(C));
+            std::vector<float> buf;
+            for (size_t j = t; j < runs.size(); j += T) {
+                const Run& u = runs[j];
+                const chunked::Rect rc{u.wy0 * w + c->band * R, u.wx0 * w, u.nwy * R, u.nwx * w};
+                buf.resize(size_t(rc.h) * rc.w * C);
+                rd.read(rc, buf.data());
+                for (int a = 0; a < u.nwy; ++a)
+                    for (int b = 0; b < u.nwx; ++b) {
+                        const int lw = g2l[(u.wy0 + a) * nx + u.wx0 + b];
+                        for (int k = 0; k < R; ++k)
+                            std::memcpy(dst + (size_t(lw) * R * w + size_t(k) * w) * C,
+                                        buf.data() + (size_t(a * R + k) * rc.w + size_t(b) * w) * C,
+                                        size_t(w) * C * sizeof(float));
+                    }
+            }
+            reads[t] = rd.chunk_reads();
+        } catch (...) {
+            errs[t] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> ths;
+    for (int t = 1; t < T; ++t) ths.emplace_back(work, t);
+    work(0);
+    for (auto& th : ths) th.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    unsigned long long n = 0;
+    for (auto v : reads) n += v;
+    return n;
+}
+
+// chunked staging slots: pinned local-order buffers filled by a (background) reader thread
+void stage_alloc(swf_ctx* c, swf_ctx::Staged& s) {
+    const int cf = std::max(c->m.cin - 2 * c->m.cout, 1);
+    if (!s.state) SWF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.state), size_t(c->M) * c->m.cout * 4, 0));
+    if (!s.forcing) SWF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.forcing), size_t(c->M) * cf * 4, 0));
+}
+void stage_fill(swf_ctx* c, swf_ctx::Staged& s) {
+    const int cf = c->m.cin - 2 * c->m.cout;
+    s.reads = read_local_chunked(c, s.state_path, c->m.cout, s.state);
+    if (cf > 0) s.reads += read_local_chunked(c, s.forcing_path, cf, s.forcing);
+}
+void stage_join(swf_ctx::Staged& s) {
+    if (s.th.joinable()) s.th.join();
+}
+// start (background) loading of (state, forcing) into a free slot; returns the slot
+int stage_start(swf_ctx* c, const std::string& state, const std::string& forcing, bool background) {
+    int slot = 0;
+    if (c->staged[0].pending && !c->staged[1].pending)
+        slot = 1;
+    else if (c->staged[0].pending && c->staged[1].pending)
+        slot = c->staged[0].seq <= c->staged[1].seq ? 0 : 1;  // drop the older prefetch
+    swf_ctx::Staged& s = c->staged[slot];
+    stage_join(s);
+    stage_alloc(c, s);
+    s.state_path = state;
+    s.forcing_path = forcing;
+    s.err = nullptr;
+    s.pending = true;
+    s.seq = ++c->staged_seq;
+    if (background) {
+        s.th = std::thread([c, &s] {
+            try {
+                stage_fill(c, s);
+            } catch (...) {
+                s.err = std::current_exception();
+            }
+        });
+    } else {
+        stage_fill(c, s);
+    }
+    return slot;
+}
+
 void upload_stats(swf_ctx* c, const swf_standardizers* s, int dtype) {
     const Dims& m = c->m;
     const int cp = m.cout, cf = std::max(m.cin - 2 * m.cout, 0);
@@ -1216,6 +1354,11 @@ void swf_destroy(swf_ctx* c) {
     cudaSetDevice(c->dev);
     cudaStreamSynchronize(c->st);
     for (void* p : c->allocs) cudaFree(p);
+    for (auto& sl : c->staged) {
+        if (sl.th.joinable()) sl.th.join();
+        if (sl.state) cudaFreeHost(sl.state);
+        if (sl.forcing) cudaFreeHost(sl.forcing);
+    }
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->h_feat) cudaFreeHost(c->h_feat);
     for (int r = 0; r < int(c->peer.size()); ++r) {  // unmap every IPC-opened peer buffer
@@ -1431,6 +1574,113 @@ int swf_forecast_step(swf_ctx* c, const void* x_prev_phys, const void* forcing_p
                 }
         }
     })
+}
+
+int swf_prefetch_chunked(swf_ctx* c, const char* state_path, const char* forcing_path) {
+    SWF_API_TRY({
+        require(c && state_path, "null argument");
+        require(c->allocated, "prefetch: load parameters first (the topology fixes the local windows)");
+        const int cf = c->m.cin - 2 * c->m.cout;
+        require(cf <= 0 || forcing_path, "prefetch: forcing container required");
+        stage_start(c, state_path, forcing_path ? forcing_path : "", true);
+    })
+}
+
+int swf_forecast_step_chunked(swf_ctx* c, const char* state_path, const char* forcing_path,
+                              const swf_standardizers* stds, const swf_diffusion_cfg* dc, uint64_t run_seed,
+                              uint64_t noise_event, void* out, int dtype) {
+    SWF_API_TRY({
+        require(c && state_path && dc && out, "null argument");
+        require(c->loaded, "forecast: parameters not loaded");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        validate_dc(*dc);
+        ensure_sampler(c);
+        const Dims& m = c->m;
+        const int cf = m.cin - 2 * m.cout;
+        require(cf >= 0, "forecast: in_channels must be >= 2 * out_channels");
+        require(cf == 0 || forcing_path, "forecast: forcing container required");
+        const std::string sp_ = state_path, fp_ = forcing_path ? forcing_path : "";
+        int slot = -1;
+        for (int i = 0; i < 2; ++i)
+            if (c->staged[i].pending && c->staged[i].state_path == sp_ && c->staged[i].forcing_path == fp_) slot = i;
+        if (slot < 0) slot = stage_start(c, sp_, fp_, false);
+        swf_ctx::Staged& s = c->staged[slot];
+        stage_join(s);
+        s.pending = false;
+        if (s.err) std::rethrow_exception(s.err);
+        c->last_chunk_reads = s.reads;
+        reset_flags(c);
+        upload_stats(c, stds, dtype);
+        SWF_CUDA(cudaMemcpyAsync(c->s_base, s.state, size_t(c->M) * m.cout * 4, cudaMemcpyHostToDevice, c->st));
+        float* forc = nullptr;
+        if (cf > 0) {
+            forc = dalloc<float>(c, size_t(c->M) * cf);
+            SWF_CUDA(cudaMemcpyAsync(forc, s.forcing, size_t(c->M) * cf * 4, cudaMemcpyHostToDevice, c->st));
+        }
+        float* dst = dalloc<float>(c, size_t(c->M) * m.cout);
+        forecast_core(c, c->s_base, forc, *dc, run_seed, noise_event, dst);
+        check_flags(c);
+        d2h_field(c, dst, m.cout, dtype, out);
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        for (void* p : {static_cast<void*>(dst), static_cast<void*>(forc)}) {
+            if (!p) continue;
+            for (size_t i = 0; i < c->allocs.size(); ++i)
+                if (c->allocs[i] == p) {
+                    cudaFree(p);
+                    c->allocs.erase(c->allocs.begin() + i);
+                    break;
+                }
+        }
+    })
+}
+
+long long swf_last_chunk_reads(swf_ctx* c) { return c ? (long long)c->last_chunk_reads : -1; }
+
+// ---- the container itself (host only; chunked_file.hpp / src/chunked_file.cpp)
+struct swf_chunked {
+    explicit swf_chunked(const std::string& p) : r(p) {}
+    swf::chunked::Reader r;
+};
+
+int swf_chunked_write(const char* path, const float* field, int channels, int height, int width, int chunk_h,
+                      int chunk_w) {
+    SWF_API_TRY({
+        require(path && field, "null argument");
+        swf::chunked::write(path, field, channels, height, width, chunk_h, chunk_w);
+    })
+}
+int swf_chunked_open(const char* path, swf_chunked** out) {
+    SWF_API_TRY({
+        require(path && out, "null argument");
+        *out = new swf_chunked(path);
+    })
+}
+void swf_chunked_close(swf_chunked* r) { delete r; }
+int swf_chunked_info(swf_chunked* r, int* channels, int* height, int* width, int* chunk_h, int* chunk_w) {
+    SWF_API_TRY({
+        require(r, "null reader");
+        if (channels) *channels = r->r.channels();
+        if (height) *height = r->r.height();
+        if (width) *width = r->r.width();
+        if (chunk_h) *chunk_h = r->r.chunk_h();
+        if (chunk_w) *chunk_w = r->r.chunk_w();
+    })
+}
+int swf_chunked_read(swf_chunked* r, int y0, int x0, int h, int w, float* out) {
+    SWF_API_TRY({
+        require(r && out, "null argument");
+        r->r.read({y0, x0, h, w}, out);
+    })
+}
+int swf_chunked_cover(swf_chunked* r, int y0, int x0, int h, int w, long long* n) {
+    SWF_API_TRY({
+        require(r && n, "null argument");
+        *n = (long long)r->r.cover({y0, x0, h, w});
+    })
+}
+long long swf_chunked_reads(swf_chunked* r) { return r ? (long long)r->r.chunk_reads() : -1; }
+void swf_chunked_reset_reads(swf_chunked* r) {
+    if (r) r->r.reset_chunk_reads();
 }
 
 int swf_rollout_ensemble(swf_ctx* c, const void* x_init_phys, const void* forcings_phys, int n_members, int n_steps,

@@ -490,6 +490,11 @@ void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiP
     const i64 total = m_tiles * n_tiles;
     int sms = 148;
     int clusters = int(std::min<i64>(total, sms / 2));
+    // Rounds of the static schedule (tile t on cluster t mod clusters) cover whole M blocks when the
+    // cluster count is a multiple of the N-tile count: the clusters sharing an A row block then stream
+    // it in lock step and it is fetched from DRAM once, instead of straddling two rounds.
+    static const bool align = getenv("SWF_GEMM_NOALIGN") == nullptr;
+    if (align && n_tiles <= clusters && total > clusters) clusters = (clusters / n_tiles) * n_tiles;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * clusters));
     cfg.blockDim = dim3(kThreads);

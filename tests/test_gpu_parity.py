@@ -188,3 +188,29 @@ def test_device_init_matches_oracle_init():
     b.init_params(77, mode=1, scale=0.05)
     ya, yb = a.forward(x, 0.5), b.forward(x, 0.5)
     assert rel_err_per_channel(yb, ya) <= 1e-5
+
+
+def test_forecast_step_chunked_matches_host_inputs(tmp_path):
+    """f4: x_prev / forcings read from chunked containers (each rank only its windows' chunks, straight
+    into the local token order) give the bit-identical forecast of the host-array path; a prefetched
+    slot is consumed by the matching call."""
+    oc, sc = cfgs(C1)
+    p = o.init_params(oc, 300, random=True, scale=0.02, dtype=np.float32)
+    x0 = o.random_field(3, 2048, 301).astype(np.float32)
+    forc = o.random_field(2, 2048, 302).astype(np.float32)
+    ev = o.key_derive(41, 1, 0)
+    sp, fp = str(tmp_path / "state.chk"), str(tmp_path / "forcing.chk")
+    swf.write_chunked(sp, x0, 32, 64, 12, 20)  # chunks not aligned with the 8 x 8 windows
+    swf.write_chunked(fp, forc, 32, 64, 12, 20)
+    dn = swf.Denoiser(sc, 32, 64, precision=swf.PREC_BF16)
+    dn.load_params(p)
+    dc = swf.DiffusionConfig(solver_steps=3)
+    want = dn.forecast_step(x0, forc, dc, 11, ev)
+    got = dn.forecast_step_chunked(sp, fp, dc, 11, ev)
+    assert np.array_equal(got, want)
+    assert dn.last_chunk_reads() == 2 * 3 * 4  # full cover of both containers on one rank
+    dn.prefetch_chunked(sp, fp)
+    got2 = dn.forecast_step_chunked(sp, fp, dc, 11, ev)
+    assert np.array_equal(got2, want)
+    with pytest.raises(swf.ConfigError):  # channel mismatch
+        dn.forecast_step_chunked(fp, fp, dc, 11, ev)

@@ -29,10 +29,21 @@ except swf.NumericsError as e:  # development builds that skip work (e.g. SWF_AT
 M = dn.local_tokens()
 cf = bench.class_flops(bench.CFG, M)
 res = {}
+try:  # board energy counter (mJ): under the 1 kW cap, energy per launch decides the clock
+    import pynvml
+    pynvml.nvmlInit()
+    _h = pynvml.nvmlDeviceGetHandleByIndex(0)
+    energy_mj = lambda: pynvml.nvmlDeviceGetTotalEnergyConsumption(_h)  # noqa: E731
+except Exception:
+    energy_mj = None
 for k in classes:
+    e0 = energy_mj() if energy_mj else None
     with bench.ClockSampler(0) as clk:
         ms = dn.bench_kernel(k, block=1, reps=reps)
+    e1 = energy_mj() if energy_mj else None
     res[k] = {"ms": ms, "tflops": cf[k] / (ms / 1e3) / 1e12 if k in cf else None, "clocks": clk.summary()}
+    if e0 is not None:
+        res[k]["J_per_launch"] = (e1 - e0) / 1e3 / reps  # includes the untimed warm-up launch share
     if k == "rms_adaln":
         res[k]["GBps"] = M * bench.CFG["hidden_dim"] * 6 / (ms / 1e3) / 1e9
     print(k, json.dumps(res[k]), flush=True)

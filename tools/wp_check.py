@@ -36,6 +36,29 @@ for name, d, H, W in [
     dn = swf.Denoiser(sc, H, W, device=local, precision=swf.PREC_BF16, topology=(wp[0], wp[1], sp, rank, own))
     dn.load_params(p)
     dn.connect_peers_torch(dist)
+    if name == "C1":  # f4: per-rank chunked input loading == host-array inputs, partial reads
+        import tempfile
+        tmp = os.path.join(tempfile.gettempdir(), f"swf_wp_chunked_{os.getpid() if world == 1 else 'job'}")
+        if rank == 0:
+            os.makedirs(tmp, exist_ok=True)
+            x0 = o.random_field(3, H * W, 301).astype(np.float32)
+            fo = o.random_field(2, H * W, 302).astype(np.float32)
+            swf.write_chunked(os.path.join(tmp, "s.chk"), x0, H, W, 4, 16)
+            swf.write_chunked(os.path.join(tmp, "f.chk"), fo, H, W, 4, 16)
+        dist.barrier()
+        rs, rf = swf.ChunkedReader(os.path.join(tmp, "s.chk")), swf.ChunkedReader(os.path.join(tmp, "f.chk"))
+        x0, fo = rs.read_full(), rf.read_full()
+        dc = swf.DiffusionConfig(solver_steps=2)
+        ev = o.key_derive(41, 1, 0)
+        a = dn.forecast_step(x0, fo, dc, 11, ev)
+        b = dn.forecast_step_chunked(os.path.join(tmp, "s.chk"), os.path.join(tmp, "f.chk"), dc, 11, ev)
+        full = 2 * rs.chunk_cover(0, 0, H, W)
+        reads = dn.last_chunk_reads()
+        same = bool(np.array_equal(a, b))
+        partial = reads == full // world  # 4 x 16 chunks tile every rank's rows / columns exactly
+        print(f"rank {rank}: chunked forecast bitwise={same} chunk_reads={reads}/{full}", flush=True)
+        ok &= same and partial
+        dist.barrier()
     y = dn.forward(x, 0.9)
     for _ in range(3):  # repeated calls exercise the start-of-forward barrier
         y2 = dn.forward(x, 0.9)
