@@ -325,7 +325,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "flops_per_step": step_flops,
             "roofline": {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_sus"],
                          "peak_kind": f"{peaks['src']} sustained bf16 (kernel timed inside a long step)",
-                         "unit": "TFLOP/s", "frac": achieved / peaks["bf16_sus"], "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / peaks["bf16_sus"], "traffic": ncu_traffic(dom),
+                         "traffic_unit": "DRAM bytes per launch (ncu --set full capture, profiles/)",
                          "flops_per_launch": cf[dom], "ms_per_launch": dom_ms},
             "kernel_shares": shares, "kernels": per_class,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
@@ -336,6 +337,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     dn.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def ncu_traffic(kernel_class: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel class from the committed
+    ncu --set full capture (profiles/ncu_traffic_bytes.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic_bytes.json")) as f:
+            return json.load(f)["dram_bytes_per_launch"].get(kernel_class)
+    except Exception:
+        return None
 
 
 def main():
