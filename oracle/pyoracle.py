@@ -99,6 +99,10 @@ def lib():
         L.orc_block_window_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_float, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_int, C.c_void_p, C.c_void_p]
         L.orc_time_embed_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
+        L.orc_backward_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_int,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_backward_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_int, C.c_int,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_noise_field_f64.argtypes = [u64, u64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p]
         L.orc_noise_field_f32.argtypes = [u64, u64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p]
         L.orc_solve_gaussian.argtypes = [C.c_double] * 6 + [C.c_int, C.c_double, u64, C.c_void_p, C.c_int64,
@@ -200,6 +204,19 @@ def forward(cfg: ModelConfig, params: np.ndarray, inp: np.ndarray, t: float, H: 
     else:
         _check(lib().orc_forward_f32(C.byref(c), _p(params), _p(inp), t, H, W, _p(out)))
     return out
+
+
+def backward(cfg: ModelConfig, params: np.ndarray, inp: np.ndarray, t: float, H: int, W: int,
+             dout: np.ndarray):
+    """backward (swin.hpp:419-467): (parameter gradients in canonical flat order, input gradient)."""
+    inp = np.ascontiguousarray(inp, params.dtype)
+    dout = np.ascontiguousarray(dout, params.dtype)
+    g = np.empty_like(params)
+    din = np.empty((H * W, cfg.in_channels), params.dtype)
+    c = _c(cfg)
+    fn = lib().orc_backward_f64 if params.dtype == np.float64 else lib().orc_backward_f32
+    _check(fn(C.byref(c), _p(params), _p(inp), t, H, W, _p(dout), _p(g), _p(din)))
+    return g, din
 
 
 def hidden(cfg: ModelConfig, params: np.ndarray, inp: np.ndarray, t: float, H: int, W: int,

@@ -469,6 +469,352 @@ static void forward(const Params<T>& p, const T* input, T t, int H, int W, T* ou
     linear<T>(p.tail(3), p.tail(4), c.out_channels, h, nrm.data(), N, out);
 }
 
+// ---------------------------------------------------------------- backward (swin.hpp:370-467)
+// Gradient buffers mirror the flat canonical parameter vector (accumulated, +=).
+template <class T>
+struct Grads {
+    std::vector<T*> arr;
+    T* blk(int b, int k) const { return arr[kHead + b * kPerBlock + k]; }
+};
+template <class T>
+static Grads<T> gview(const Cfg& c, T* flat) {
+    Grads<T> g;
+    i64 off = 0;
+    for (const auto& a : param_arrays(c)) {
+        g.arr.push_back(flat + off);
+        off += a.rows * a.cols;
+    }
+    return g;
+}
+template <class T>
+static T silu_grad(T x) {  // model.hpp:248-252
+    const T s = T(1) / (T(1) + std::exp(-x));
+    return s * (T(1) + x * (T(1) - s));
+}
+// linear_cols_t (swin.hpp:57-62): Y[n][in] = W^T X[n][out], W col-major out x in
+template <class T>
+static void linear_t(const T* Wm, int out, int in, const T* X, i64 n, T* Y) {
+#pragma omp parallel for schedule(static)
+    for (i64 j = 0; j < n; ++j)
+        for (int k = 0; k < in; ++k) {
+            T acc = T(0);
+            const T* wc = Wm + i64(k) * out;
+            for (int o = 0; o < out; ++o) acc += wc[o] * X[j * out + o];
+            Y[j * in + k] = acc;
+        }
+}
+// accum_outer (swin.hpp:64-68): G(out x in, col-major) += sum_j dY[j][out] X[j][in]^T, row_off
+// selects a row block of a taller matrix with ld rows.
+template <class T>
+static void accum_outer(T* G, int ld, int row_off, int out, int in, const T* dY, int ldy, const T* X, int ldx, i64 n) {
+#pragma omp parallel for schedule(static)
+    for (int k = 0; k < in; ++k)
+        for (int o = 0; o < out; ++o) {
+            T acc = T(0);
+            for (i64 j = 0; j < n; ++j) acc += dY[j * ldy + o] * X[j * ldx + k];
+            G[i64(k) * ld + row_off + o] += acc;
+        }
+}
+// prenorm_modulate_bwd (swin.hpp:86-107)
+template <class T>
+static void prenorm_modulate_bwd(const T* X, i64 n, int h, const T* g, const T* a, const T* b, const T* gate,
+                                 const T* dXM, T* dX, T* dg, T* da, T* db, T* dgate) {
+    for (i64 j = 0; j < n; ++j) {
+        const T* x = X + j * h;
+        T ss = T(0);
+        for (int i = 0; i < h; ++i) ss += x[i] * x[i];
+        const T r = std::sqrt(ss / T(h) + T(1e-8));
+        std::vector<T> du(h);
+        T xdotdu = T(0);
+        for (int i = 0; i < h; ++i) {
+            const T u = x[i] / r, dxm = dXM[j * h + i], gu = g[i] * u;
+            da[i] += dxm * gate[i] * gu;
+            db[i] += dxm * gate[i];
+            dgate[i] += dxm * (gu * (T(1) + a[i]) + b[i]);
+            const T dgu = dxm * gate[i] * (T(1) + a[i]);
+            dg[i] += dgu * u;
+            du[i] = dgu * g[i];
+            xdotdu += x[i] * du[i];
+        }
+        for (int i = 0; i < h; ++i) dX[j * h + i] += du[i] / r - x[i] * (xdotdu / (T(h) * r * r * r));
+    }
+}
+// prenorm_plain_bwd (swin.hpp:125-136)
+template <class T>
+static void prenorm_plain_bwd(const T* X, i64 n, int h, const T* g, const T* dN, T* dX, T* dg) {
+    for (i64 j = 0; j < n; ++j) {
+        const T* x = X + j * h;
+        T ss = T(0);
+        for (int i = 0; i < h; ++i) ss += x[i] * x[i];
+        const T r = std::sqrt(ss / T(h) + T(1e-8));
+        T xdotdu = T(0);
+        std::vector<T> du(h);
+        for (int i = 0; i < h; ++i) {
+            dg[i] += dN[j * h + i] * (x[i] / r);
+            du[i] = dN[j * h + i] * g[i];
+            xdotdu += x[i] * du[i];
+        }
+        for (int i = 0; i < h; ++i) dX[j * h + i] += du[i] / r - x[i] * (xdotdu / (T(h) * r * r * r));
+    }
+}
+
+// block_window_backward (swin.hpp:370-417) with head_attention_bwd (:189-226) and swiglu_bwd
+// (:236-252). The window's forward internals are recomputed from its block input (no cache of the
+// s x s probabilities is kept across windows). xin, dX: [s][h]; returns dxin; d6 accumulates
+// [da1, db1, dg1, da2, db2, dg2].
+template <class T>
+static void block_window_backward(const Params<T>& p, const Grads<T>& G, int blk, const std::vector<T>& six,
+                                  const Layout& lay, int wy, int wx, const T* xin, const T* dX, T* dxin, T* d6) {
+    const Cfg& c = p.cfg;
+    const int h = c.hidden_dim, d = c.hd(), f = c.ffn_dim, heads = c.n_heads, w = lay.w, s = lay.s();
+    const T *a1 = &six[0], *b1 = &six[h], *g1 = &six[2 * h], *a2 = &six[3 * h], *b2 = &six[4 * h],
+            *g2 = &six[5 * h];
+    std::vector<T> ang(size_t(s) * (d / 2));
+    for (int r = 0; r < w; ++r)
+        for (int cc = 0; cc < w; ++cc)
+            rope_angles<T>(d, wy * w + lay.shift + r, wx * w + lay.shift + cc, &ang[size_t(r * w + cc) * (d / 2)]);
+    const bool masked = lay.seam(wy);
+    const T scale = T(1) / std::sqrt(T(d));
+    // ---- forward recompute
+    std::vector<T> xm(size_t(s) * h), qkv(size_t(s) * 3 * h), concat(size_t(s) * h), tmp(size_t(s) * h);
+    prenorm_modulate<T>(xin, s, h, p.blk(blk, 2), a1, b1, g1, xm.data());
+    linear<T>(p.blk(blk, 0), nullptr, 3 * h, h, xm.data(), s, qkv.data());
+    std::vector<std::vector<T>> Q(heads), K(heads), V(heads), P(heads);
+    for (int hd = 0; hd < heads; ++hd) {
+        std::vector<T>&q = Q[hd], &k = K[hd], &v = V[hd], &pr = P[hd];
+        q.resize(size_t(s) * d);
+        k.resize(size_t(s) * d);
+        v.resize(size_t(s) * d);
+        pr.resize(size_t(s) * s);
+        for (int j = 0; j < s; ++j) {
+            for (int e = 0; e < d; ++e) {
+                q[size_t(j) * d + e] = qkv[size_t(j) * 3 * h + hd * d + e];
+                k[size_t(j) * d + e] = qkv[size_t(j) * 3 * h + h + hd * d + e];
+                v[size_t(j) * d + e] = qkv[size_t(j) * 3 * h + 2 * h + hd * d + e];
+            }
+            for (int pp = 0; pp < d / 2; ++pp) {
+                const T an = ang[size_t(j) * (d / 2) + pp];
+                const T cs = std::cos(an), sn = std::sin(an);
+                for (T* z : {&q[size_t(j) * d + 2 * pp], &k[size_t(j) * d + 2 * pp]}) {
+                    const T x0 = z[0], y0 = z[1];
+                    z[0] = cs * x0 - sn * y0;
+                    z[1] = sn * x0 + cs * y0;
+                }
+            }
+        }
+        const T ninf = -std::numeric_limits<T>::infinity();
+        for (int i = 0; i < s; ++i) {
+            const int gq = masked ? lay.seam_group(i / w) : 0;
+            T m = ninf;
+            T* row = &pr[size_t(i) * s];
+            for (int j = 0; j < s; ++j) {
+                T acc = T(0);
+                for (int e = 0; e < d; ++e) acc += q[size_t(i) * d + e] * k[size_t(j) * d + e];
+                T l = acc * scale;
+                if (masked && lay.seam_group(j / w) != gq) l = l + ninf;
+                row[j] = l;
+                if (l > m) m = l;
+            }
+            T sum = T(0);
+            for (int j = 0; j < s; ++j) {
+                row[j] = std::exp(row[j] - m);
+                sum += row[j];
+            }
+            for (int j = 0; j < s; ++j) row[j] = row[j] / sum;
+            T* o = &concat[size_t(i) * h + hd * d];
+            for (int e = 0; e < d; ++e) o[e] = T(0);
+            for (int j = 0; j < s; ++j)
+                for (int e = 0; e < d; ++e) o[e] += v[size_t(j) * d + e] * row[j];
+        }
+    }
+    std::vector<T> xmid(size_t(s) * h);
+    linear<T>(p.blk(blk, 1), nullptr, h, h, concat.data(), s, tmp.data());
+    for (size_t i = 0; i < size_t(s) * h; ++i) xmid[i] = xin[i] + tmp[i];
+    std::vector<T> x2m(size_t(s) * h), gp(size_t(s) * f), up(size_t(s) * f), act(size_t(s) * f);
+    prenorm_modulate<T>(xmid.data(), s, h, p.blk(blk, 3), a2, b2, g2, x2m.data());
+    linear<T>(p.blk(blk, 4), nullptr, f, h, x2m.data(), s, gp.data());
+    linear<T>(p.blk(blk, 5), nullptr, f, h, x2m.data(), s, up.data());
+    for (size_t i = 0; i < size_t(s) * f; ++i) act[i] = silu(gp[i]) * up[i];
+    // ---- feed-forward branch backward (swiglu_bwd + prenorm_modulate_bwd)
+    std::vector<T> dxmid(dX, dX + size_t(s) * h);
+    accum_outer<T>(G.blk(blk, 6), h, 0, h, f, dX, h, act.data(), f, s);
+    std::vector<T> dS(size_t(s) * f), dG(size_t(s) * f), dU(size_t(s) * f);
+    linear_t<T>(p.blk(blk, 6), h, f, dX, s, dS.data());
+    for (size_t i = 0; i < size_t(s) * f; ++i) {
+        dG[i] = dS[i] * up[i] * silu_grad(gp[i]);
+        dU[i] = dS[i] * silu(gp[i]);
+    }
+    accum_outer<T>(G.blk(blk, 4), f, 0, f, h, dG.data(), f, x2m.data(), h, s);
+    accum_outer<T>(G.blk(blk, 5), f, 0, f, h, dU.data(), f, x2m.data(), h, s);
+    std::vector<T> dx2m(size_t(s) * h), t2(size_t(s) * h);
+    linear_t<T>(p.blk(blk, 4), f, h, dG.data(), s, dx2m.data());
+    linear_t<T>(p.blk(blk, 5), f, h, dU.data(), s, t2.data());
+    for (size_t i = 0; i < size_t(s) * h; ++i) dx2m[i] += t2[i];
+    prenorm_modulate_bwd<T>(xmid.data(), s, h, p.blk(blk, 3), a2, b2, g2, dx2m.data(), dxmid.data(), G.blk(blk, 3),
+                            d6 + 3 * h, d6 + 4 * h, d6 + 5 * h);
+    // ---- attention branch backward
+    for (size_t i = 0; i < size_t(s) * h; ++i) dxin[i] = dxmid[i];
+    accum_outer<T>(G.blk(blk, 1), h, 0, h, h, dxmid.data(), h, concat.data(), h, s);
+    std::vector<T> dOc(size_t(s) * h), dXm(size_t(s) * h, T(0));
+    linear_t<T>(p.blk(blk, 1), h, h, dxmid.data(), s, dOc.data());
+    std::vector<T> dqkv(size_t(s) * 3 * h, T(0));  // [s][3h] like qkv
+    for (int hd = 0; hd < heads; ++hd) {
+        const std::vector<T>&q = Q[hd], &k = K[hd], &v = V[hd], &pr = P[hd];
+        std::vector<T> dV(size_t(s) * d, T(0)), dQ(size_t(s) * d, T(0)), dK(size_t(s) * d, T(0)), dA(size_t(s) * s);
+        for (int i = 0; i < s; ++i) {  // dP(i,j) = dO_i . v_j ; dA = P .* (dP - rowdot)
+            const T* dOi = &dOc[size_t(i) * h + hd * d];
+            T dot = T(0);
+            for (int j = 0; j < s; ++j) {
+                T acc = T(0);
+                for (int e = 0; e < d; ++e) acc += dOi[e] * v[size_t(j) * d + e];
+                dA[size_t(i) * s + j] = acc;
+                dot += acc * pr[size_t(i) * s + j];
+            }
+            for (int j = 0; j < s; ++j) dA[size_t(i) * s + j] = pr[size_t(i) * s + j] * (dA[size_t(i) * s + j] - dot);
+            for (int j = 0; j < s; ++j)  // dV_j += dO_i P(i,j)
+                for (int e = 0; e < d; ++e) dV[size_t(j) * d + e] += dOi[e] * pr[size_t(i) * s + j];
+        }
+        for (int i = 0; i < s; ++i)
+            for (int j = 0; j < s; ++j) {
+                const T a = dA[size_t(i) * s + j];
+                for (int e = 0; e < d; ++e) {
+                    dQ[size_t(i) * d + e] += k[size_t(j) * d + e] * a;
+                    dK[size_t(j) * d + e] += q[size_t(i) * d + e] * a;
+                }
+            }
+        for (int j = 0; j < s; ++j) {
+            for (int e = 0; e < d; ++e) {
+                dQ[size_t(j) * d + e] *= scale;
+                dK[size_t(j) * d + e] *= scale;
+            }
+            for (int pp = 0; pp < d / 2; ++pp) {  // rope_rotate(..., inverse=true)
+                const T an = -ang[size_t(j) * (d / 2) + pp];
+                const T cs = std::cos(an), sn = std::sin(an);
+                for (T* z : {&dQ[size_t(j) * d + 2 * pp], &dK[size_t(j) * d + 2 * pp]}) {
+                    const T x0 = z[0], y0 = z[1];
+                    z[0] = cs * x0 - sn * y0;
+                    z[1] = sn * x0 + cs * y0;
+                }
+            }
+            for (int e = 0; e < d; ++e) {
+                dqkv[size_t(j) * 3 * h + hd * d + e] = dQ[size_t(j) * d + e];
+                dqkv[size_t(j) * 3 * h + h + hd * d + e] = dK[size_t(j) * d + e];
+                dqkv[size_t(j) * 3 * h + 2 * h + hd * d + e] = dV[size_t(j) * d + e];
+            }
+        }
+    }
+    accum_outer<T>(G.blk(blk, 0), 3 * h, 0, 3 * h, h, dqkv.data(), 3 * h, xm.data(), h, s);
+    linear_t<T>(p.blk(blk, 0), 3 * h, h, dqkv.data(), s, dXm.data());
+    prenorm_modulate_bwd<T>(xin, s, h, p.blk(blk, 2), a1, b1, g1, dXm.data(), dxin, G.blk(blk, 2), d6, d6 + h,
+                            d6 + 2 * h);
+}
+
+// backward (swin.hpp:419-467) of the full forward for output gradient dout [N][C_out]: parameter
+// gradients in canonical flat order (overwritten) and the input gradient [N][C_in].
+template <class T>
+static void backward(const Params<T>& p, const T* input, T t, int H, int W, const T* dout, T* gflat, T* din) {
+    const Cfg& c = p.cfg;
+    c.validate_grid(H, W);
+    const i64 N = i64(H) * W;
+    const int h = c.hidden_dim, td = c.td(), nb = c.nb();
+    i64 total = 0;
+    for (const auto& a : param_arrays(c)) total += a.rows * a.cols;
+    std::memset(gflat, 0, sizeof(T) * total);
+    const Grads<T> G = gview<T>(c, gflat);
+    // forward, keeping every block's input (pixel order)
+    const std::vector<T> emb = time_embed(p, t);
+    std::vector<std::vector<T>> xb(nb + 1, std::vector<T>(size_t(N) * h));
+    linear<T>(p.enc_w(), p.enc_b(), h, c.in_channels, input, N, xb[0].data());
+    for (int blk = 0; blk < nb; ++blk) {
+        const Layout lay{H, W, c.window_px, shift_for_block(blk, c.window_px)};
+        const std::vector<T> six = ada_six(p, blk, emb);
+        const int s = lay.s();
+        std::vector<T> xin(size_t(s) * h), xo(size_t(s) * h);
+        xb[blk + 1] = xb[blk];
+        for (int wy = 0; wy < lay.ny(); ++wy)
+            for (int wx = 0; wx < lay.nx(); ++wx) {
+                for (int tk = 0; tk < s; ++tk)
+                    std::memcpy(&xin[size_t(tk) * h], &xb[blk][size_t(lay.pixel_of(wy, wx, tk / lay.w, tk % lay.w)) * h],
+                                sizeof(T) * h);
+                block_window<T>(p, blk, six, lay, wy, wx, xin.data(), xo.data());
+                for (int tk = 0; tk < s; ++tk)
+                    std::memcpy(&xb[blk + 1][size_t(lay.pixel_of(wy, wx, tk / lay.w, tk % lay.w)) * h],
+                                &xo[size_t(tk) * h], sizeof(T) * h);
+            }
+    }
+    const std::vector<T>& xf = xb[nb];
+    // decode head
+    std::vector<T> n3(size_t(N) * h), dn3(size_t(N) * h), dx(size_t(N) * h, T(0));
+    prenorm_plain<T>(xf.data(), N, h, p.tail(2), n3.data());
+    T* gdw = G.arr[kHead + nb * kPerBlock + 3];
+    T* gdb = G.arr[kHead + nb * kPerBlock + 4];
+    accum_outer<T>(gdw, c.out_channels, 0, c.out_channels, h, dout, c.out_channels, n3.data(), h, N);
+    for (i64 j = 0; j < N; ++j)
+        for (int o = 0; o < c.out_channels; ++o) gdb[o] += dout[j * c.out_channels + o];
+    linear_t<T>(p.tail(3), c.out_channels, h, dout, N, dn3.data());
+    prenorm_plain_bwd<T>(xf.data(), N, h, p.tail(2), dn3.data(), dx.data(), G.arr[kHead + nb * kPerBlock + 2]);
+    // blocks in reverse
+    std::vector<T> d_embed(td, T(0));
+    for (int blk = nb - 1; blk >= 0; --blk) {
+        const Layout lay{H, W, c.window_px, shift_for_block(blk, c.window_px)};
+        const std::vector<T> six = ada_six(p, blk, emb);
+        const int s = lay.s();
+        std::vector<T> d6(6 * h, T(0)), dxn(size_t(N) * h, T(0)), xin(size_t(s) * h), dwin(size_t(s) * h),
+            dwin_in(size_t(s) * h);
+        for (int wy = 0; wy < lay.ny(); ++wy)
+            for (int wx = 0; wx < lay.nx(); ++wx) {
+                for (int tk = 0; tk < s; ++tk) {
+                    const i64 pix = lay.pixel_of(wy, wx, tk / lay.w, tk % lay.w);
+                    std::memcpy(&xin[size_t(tk) * h], &xb[blk][size_t(pix) * h], sizeof(T) * h);
+                    std::memcpy(&dwin[size_t(tk) * h], &dx[size_t(pix) * h], sizeof(T) * h);
+                }
+                block_window_backward<T>(p, G, blk, six, lay, wy, wx, xin.data(), dwin.data(), dwin_in.data(),
+                                         d6.data());
+                for (int tk = 0; tk < s; ++tk)
+                    std::memcpy(&dxn[size_t(lay.pixel_of(wy, wx, tk / lay.w, tk % lay.w)) * h],
+                                &dwin_in[size_t(tk) * h], sizeof(T) * h);
+            }
+        dx.swap(dxn);
+        // ada: six = b_ada + W_ada embed (W_ada 6h x td col-major)
+        T* gwa = G.blk(blk, 7);
+        T* gba = G.blk(blk, 8);
+        const T* Wa = p.blk(blk, 7);
+        for (int k = 0; k < td; ++k)
+            for (int o = 0; o < 6 * h; ++o) {
+                gwa[i64(k) * 6 * h + o] += d6[o] * emb[k];
+                d_embed[k] += Wa[i64(k) * 6 * h + o] * d6[o];
+            }
+        for (int o = 0; o < 6 * h; ++o) gba[o] += d6[o];
+    }
+    // encode
+    accum_outer<T>(G.arr[0], h, 0, h, c.in_channels, dx.data(), h, input, c.in_channels, N);
+    for (i64 j = 0; j < N; ++j)
+        for (int o = 0; o < h; ++o) G.arr[1][o] += dx[j * h + o];
+    if (din) linear_t<T>(p.enc_w(), h, c.in_channels, dx.data(), N, din);
+    // shared time projection: embed = silu(lin), lin = W_time feat + b_time
+    std::vector<T> feat(td), lin(td);
+    const int nf = td / 2;
+    for (int k = 0; k < nf; ++k) {
+        const double om = std::pow(10000.0, -double(k) / nf);
+        const double arg = double(t) * 636.6197723675814 * om;
+        feat[2 * k] = static_cast<T>(std::sin(arg));
+        feat[2 * k + 1] = static_cast<T>(std::cos(arg));
+    }
+    if (td % 2 == 1) feat[td - 1] = T(1);
+    for (int o = 0; o < td; ++o) {
+        T acc = T(0);
+        for (int k = 0; k < td; ++k) acc += p.tail(0)[i64(k) * td + o] * feat[k];
+        lin[o] = acc + p.tail(1)[o];
+    }
+    T* gwt = G.arr[kHead + nb * kPerBlock + 0];
+    T* gbt = G.arr[kHead + nb * kPerBlock + 1];
+    for (int o = 0; o < td; ++o) {
+        const T dl = d_embed[o] * silu_grad(lin[o]);
+        for (int k = 0; k < td; ++k) gwt[i64(k) * td + o] += dl * feat[k];
+        gbt[o] += dl;
+    }
+}
+
 // ---------------------------------------------------------------- posenc.hpp:16-37
 template <class T>
 static void posenc(int H, int W, int C, T* enc) {
@@ -747,6 +1093,17 @@ int orc_block_window_f32(const orc_cfg* c, const float* params, float t, int H, 
         const Layout lay{H, W, cf.window_px, shift_for_block(blk, cf.window_px)};
         block_window<float>(p, blk, six, lay, wy, wx, xin, xout);
     })
+}
+
+// backward (swin.hpp:419-467): parameter gradients (canonical flat order) and input gradient for
+// an output gradient dout [N][C_out] at the given input / t.
+int orc_backward_f64(const orc_cfg* c, const double* params, const double* input, double t, int H, int W,
+                     const double* dout, double* grads, double* din) {
+    ORC_TRY(backward<double>(view<double>(to_cfg(c), params), input, t, H, W, dout, grads, din))
+}
+int orc_backward_f32(const orc_cfg* c, const float* params, const float* input, float t, int H, int W,
+                     const float* dout, float* grads, float* din) {
+    ORC_TRY(backward<float>(view<float>(to_cfg(c), params), input, t, H, W, dout, grads, din))
 }
 
 // Time embedding (td) and all blocks' ada vectors ([nb][6h]).
