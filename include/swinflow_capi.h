@@ -120,6 +120,13 @@ int swf_forward(swf_ctx* ctx, const void* input, double t, void* output, int dty
 /* Same, on device pointers (fp32, [N][C]) on the context stream, without synchronising;
  * numerics flags are checked by swf_sync(). */
 int swf_forward_device(swf_ctx* ctx, const float* d_input, double t, float* d_output);
+/* backward(p, fc, d_output) (swin.hpp:419-467) of forward(p, input, t) (f3, FP32 validation mode,
+ * one rank): parameter gradients in the canonical parameter_arrays order and column-major layout
+ * (model.hpp:140-168; swf_param_count elements) and, if d_input is not NULL, the input gradient
+ * (C_in x N). The forward is re-run with its block inputs saved; each block's internals are
+ * recomputed from them in the backward (no s x s probabilities are stored). */
+int swf_backward(swf_ctx* ctx, const void* input, double t, const void* d_output, void* grads, void* d_input,
+                 int dtype);
 int swf_sync(swf_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) for callers that enqueue their own copies. */
 void* swf_stream(swf_ctx* ctx);

@@ -141,6 +141,7 @@ def lib():
         L.swf_profile_launches.argtypes = [vp, vp, vp, i, C.POINTER(i)]
         L.swf_noise_field.argtypes = [vp, u64, u64, i, d, vp]
         L.swf_selftest_gemm.argtypes = [i, ll, i, i, C.POINTER(d), C.POINTER(d)]
+        L.swf_backward.argtypes = [vp, vp, d, vp, vp, vp, i]
         L.swf_prefetch_chunked.argtypes = [vp, C.c_char_p, C.c_char_p]
         L.swf_forecast_step_chunked.argtypes = [vp, C.c_char_p, C.c_char_p, vp, vp, u64, u64, vp, i]
         L.swf_last_chunk_reads.argtypes = [vp]
@@ -333,6 +334,18 @@ class Denoiser:
                                           None if st is None else C.byref(st), C.byref(_DCfg(*astuple(dc))),
                                           run_seed, rollout_id, _p(out), _dt(x)))
         return out
+
+    # ---- backward (swin.hpp:419-467), FP32 validation mode
+    def backward(self, inp, t: float, d_output, want_input_grad: bool = True):
+        """Parameter gradients (canonical flat order, column-major arrays) and input gradient of
+        sum(d_output * forward(inp, t))."""
+        inp = np.ascontiguousarray(inp)
+        dt = inp.dtype
+        dout = np.ascontiguousarray(d_output, dt)
+        g = np.zeros(param_count(self.cfg), dt)
+        din = np.zeros_like(inp) if want_input_grad else None
+        _check(lib().swf_backward(self._c, _p(inp), t, _p(dout), _p(g), _p(din), _dt(inp)))
+        return g, din
 
     # ---- per-rank input loading from chunked containers (chunked_file.cpp:156-188)
     def prefetch_chunked(self, state_path: str, forcing_path: str | None = None):

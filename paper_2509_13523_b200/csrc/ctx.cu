@@ -127,6 +127,17 @@ struct swf_ctx {
     } staged[2];
     long long staged_seq = 0;
     unsigned long long last_chunk_reads = 0;
+    // backward (FP32 validation mode): canonical fp32 parameters in the reference layout, the saved
+    // block inputs of the last forward, and work buffers (allocated on first use)
+    float* pflat = nullptr;
+    std::vector<size_t> poff;
+    bool save_x = false;
+    float* xsave = nullptr;
+    struct Bwd {
+        float *dx[2], *dtmp, *xmid, *dxm, *xm1, *obuf, *x2m, *dO, *gu, *act, *dS, *dG, *dU, *dqkv, *dplanes, *stats,
+            *rms, *d6, *demb, *zero, *gflat, *din;
+    } bw = {};
+    bool bw_alloc = false;
     // per-kernel-class CUDA-event timing (bench roofline): class id -> accumulated ms / launches
     bool prof = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
@@ -439,7 +450,23 @@ void load_params_from(swf_ctx* c, Next&& next) {
     allocate(c);
     const Dims& m = c->m;
     int ai = 0;
-    auto up = [&](size_t n) -> float* { return next(ai++, n); };
+    if (c->prec == SWF_PREC_FP32 && !c->pflat) {  // the backward reads the reference-layout weights
+        size_t tot = 0;
+        c->poff.clear();
+        for (const auto& sh : param_shapes(m)) {
+            c->poff.push_back(tot);
+            tot += size_t(sh.first * sh.second);
+        }
+        c->poff.push_back(tot);
+        c->pflat = dalloc<float>(c, tot);
+    }
+    auto up = [&](size_t n) -> float* {
+        float* src = next(ai, n);
+        if (c->pflat)
+            SWF_CUDA(cudaMemcpyAsync(c->pflat + c->poff[ai], src, n * 4, cudaMemcpyDeviceToDevice, c->st));
+        ++ai;
+        return src;
+    };
     auto copy_vec = [&](float* dst, size_t n) {
         float* s = up(n);
         SWF_CUDA(cudaMemcpyAsync(dst, s, n * 4, cudaMemcpyDeviceToDevice, c->st));
@@ -786,6 +813,9 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         const int npar = (b + 1 < m.nb) ? ((b + 1) & 1) : 0;
         const float* six = c->six + size_t(b) * 6 * m.h;
         float* x = c->xbuf[cur];
+        if (c->save_x)
+            SWF_CUDA(cudaMemcpyAsync(c->xsave + size_t(b) * M * m.h, x, size_t(M) * m.h * 4, cudaMemcpyDeviceToDevice,
+                                     c->st));
         // attention branch: prenorm_modulate -> heads -> out projection (swin.hpp:313-322)
         {
             ProfScope ps(c, K_RMS);
@@ -870,6 +900,9 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         if (c->world > 1) peer_barrier(c);
         cur ^= 1;
     }
+    if (c->save_x)
+        SWF_CUDA(cudaMemcpyAsync(c->xsave + size_t(m.nb) * M * m.h, c->xbuf[cur], size_t(M) * m.h * 4,
+                                 cudaMemcpyDeviceToDevice, c->st));
     // decode (swin.hpp:362-366)
     {
             ProfScope ps(c, K_RMS);
@@ -893,6 +926,149 @@ void forward_any(swf_ctx* c, double t, float out_scale) {
         forward_core<__nv_bfloat16>(c, t, out_scale);
     else
         forward_core<float>(c, t, out_scale);
+}
+
+// ------------------------------------------------------------------ backward (swin.hpp:370-467)
+// FP32 validation mode, one rank. The forward saves every block's input (its layout's local order);
+// the backward recomputes each block's internals from it (no s x s probabilities are stored),
+// then runs the reference backward in reverse block order with k_bwd.cu kernels. Weight gradients
+// come out in the reference's canonical order and column-major layout.
+void ensure_bwd(swf_ctx* c) {
+    if (c->bw_alloc) return;
+    const Dims& m = c->m;
+    const i64 M = c->M;
+    auto& b = c->bw;
+    c->xsave = dalloc<float>(c, size_t(m.nb + 1) * M * m.h);
+    b.dx[0] = dalloc<float>(c, size_t(M) * m.h);
+    b.dx[1] = dalloc<float>(c, size_t(M) * m.h);
+    b.dtmp = dalloc<float>(c, size_t(M) * m.h);
+    b.xmid = dalloc<float>(c, size_t(M) * m.h);
+    b.dxm = dalloc<float>(c, size_t(M) * m.h);
+    b.xm1 = dalloc<float>(c, size_t(M) * m.hp);
+    b.obuf = dalloc<float>(c, size_t(M) * m.hp);
+    b.x2m = dalloc<float>(c, size_t(M) * m.hp);
+    b.dO = dalloc<float>(c, size_t(M) * m.hp);
+    b.gu = dalloc<float>(c, size_t(M) * m.np_gu);
+    b.act = dalloc<float>(c, size_t(M) * m.f);
+    b.dS = dalloc<float>(c, size_t(M) * m.f);
+    b.dG = dalloc<float>(c, size_t(M) * m.f);
+    b.dU = dalloc<float>(c, size_t(M) * m.f);
+    b.dqkv = dalloc<float>(c, size_t(M) * 3 * m.h);
+    b.dplanes = dalloc<float>(c, size_t(3) * M * m.h);
+    b.stats = dalloc<float>(c, size_t(3) * M * m.heads);
+    b.rms = dalloc<float>(c, size_t(M));
+    b.d6 = dalloc<float>(c, size_t(6) * m.h);
+    b.demb = dalloc<float>(c, size_t(m.td));
+    b.zero = dalloc<float>(c, size_t(m.np_gu) + m.np_dec + 64);
+    b.gflat = dalloc<float>(c, c->poff.back());
+    b.din = dalloc<float>(c, size_t(M) * m.cin);
+    c->bw_alloc = true;
+}
+
+void backward_core(swf_ctx* c, const float* dout) {
+    const Dims& m = c->m;
+    const i64 M = c->M;
+    const int h = m.h, hp = m.hp, f = m.f, td = m.td, nb = m.nb;
+    auto& bw = c->bw;
+    cudaStream_t st = c->st;
+    float* G = bw.gflat;
+    const float* P = c->pflat;
+    auto pa = [&](int ai) { return P + c->poff[ai]; };
+    auto ga = [&](int ai) { return G + c->poff[ai]; };
+    const int kHead = 2, kPer = 9, tail = kHead + nb * kPer;
+    SWF_CUDA(cudaMemsetAsync(G, 0, c->poff.back() * 4, st));
+    SWF_CUDA(cudaMemsetAsync(bw.demb, 0, size_t(td) * 4, st));
+    // decode head (swin.hpp:430-436): n3 = prenorm_plain(x_final); dW_dec, db_dec, dN3, prenorm_plain_bwd
+    const float* xf = c->xsave + size_t(nb) * M * h;
+    rms_modulate<float>(xf, M, h, hp, c->g_dec, nullptr, nullptr, nullptr, bw.xm1, nullptr, 0, st);
+    gemm_strided_f32(h, m.cout, int(M), bw.xm1, 1, hp, dout, m.cout, 1, ga(tail + 3), m.cout, 1.f, st);
+    colsum_f32(dout, m.cout, M, m.cout, ga(tail + 4), st);
+    gemm_strided_f32(int(M), h, m.cout, dout, m.cout, 1, pa(tail + 3), 1, m.cout, bw.dtmp, h, 0.f, st);
+    SWF_CUDA(cudaMemsetAsync(bw.dx[0], 0, size_t(M) * h * 4, st));
+    norm_bwd(xf, h, bw.dtmp, h, M, h, c->g_dec, nullptr, nullptr, nullptr, bw.dx[0], h, bw.rms, ga(tail + 2), nullptr,
+             nullptr, nullptr, st);
+    int cur = 0;  // bw.dx[cur]: gradient of the current block's output, in that output's layout
+    EpiParams ep = base_ep(c);
+    for (int b = nb - 1; b >= 0; --b) {
+        const int par = b & 1, npar = (b + 1 < nb) ? ((b + 1) & 1) : 0;
+        const int base = kHead + b * kPer;
+        const float* xb = c->xsave + size_t(b) * M * h;
+        const float* six = c->six + size_t(b) * 6 * h;
+        // ---- recompute the block's internals (block_window_forward, swin.hpp:306-325)
+        rms_modulate<float>(xb, M, h, hp, c->g_attn + size_t(b) * h, six, six + h, six + 2 * h, bw.xm1, nullptr, 0, st);
+        EpiParams e = ep;
+        e.cur = c->lay[par];
+        e.out = c->qkv;
+        e.plane = i64(c->lay[par].nloc) * m.heads * m.w * m.w * m.d;
+        e.N = 3 * h;
+        gemm_f32(bw.xm1, static_cast<const float*>(c->w_qkv[b]), M, m.np_qkv, hp, EPI_QKV, e, st);
+        const float* q = static_cast<const float*>(c->qkv);
+        const float* kk = q + size_t(M) * h;
+        const float* v = q + size_t(2) * M * h;
+        AttnParams ap;
+        std::memset(&ap, 0, sizeof ap);
+        ap.q = q;
+        ap.k = kk;
+        ap.v = v;
+        ap.o = bw.obuf;
+        ap.ldo = hp;
+        ap.nloc = c->lay[par].nloc;
+        ap.heads = m.heads;
+        ap.s = m.w * m.w;
+        ap.d = m.d;
+        ap.w = m.w;
+        ap.lay = c->lay[par];
+        ap.scale = 1.0f / std::sqrt(float(m.d));
+        attention_f32(ap, st);
+        SWF_CUDA(cudaMemcpyAsync(bw.xmid, xb, size_t(M) * h * 4, cudaMemcpyDeviceToDevice, st));
+        e = ep;
+        e.x = bw.xmid;
+        e.N = h;
+        gemm_f32(bw.obuf, static_cast<const float*>(c->w_out[b]), M, m.np_out, hp, EPI_RESID, e, st);
+        rms_modulate<float>(bw.xmid, M, h, hp, c->g_ffn + size_t(b) * h, six + 3 * h, six + 4 * h, six + 5 * h, bw.x2m,
+                            nullptr, 0, st);
+        e = ep;
+        e.out = bw.gu;
+        e.ld_out = m.np_gu;
+        e.N = m.np_gu;
+        e.bias = bw.zero;
+        gemm_f32(bw.x2m, static_cast<const float*>(c->w_gu[b]), M, m.np_gu, hp, EPI_DECODE, e, st);
+        // ---- backward (block_window_backward, swin.hpp:370-417)
+        float* dXp = bw.dtmp;  // output gradient in this block's layout
+        relayout_rows(bw.dx[cur], c->lay[npar], c->lay[par], M, h, dXp, st);
+        // feed-forward branch: swiglu_bwd (:236-252)
+        gemm_strided_f32(int(M), f, h, dXp, h, 1, pa(base + 6), 1, h, bw.dS, f, 0.f, st);
+        swiglu_bwd(bw.gu, m.np_gu, bw.dS, f, M, f, m.G, bw.act, bw.dG, bw.dU, st);
+        gemm_strided_f32(f, h, int(M), bw.act, 1, f, dXp, h, 1, ga(base + 6), h, 1.f, st);     // dW_down
+        gemm_strided_f32(h, f, int(M), bw.x2m, 1, hp, bw.dG, f, 1, ga(base + 4), f, 1.f, st);  // dW_gate
+        gemm_strided_f32(h, f, int(M), bw.x2m, 1, hp, bw.dU, f, 1, ga(base + 5), f, 1.f, st);  // dW_up
+        gemm_strided_f32(int(M), h, f, bw.dG, f, 1, pa(base + 4), 1, f, bw.dxm, h, 0.f, st);
+        gemm_strided_f32(int(M), h, f, bw.dU, f, 1, pa(base + 5), 1, f, bw.dxm, h, 1.f, st);
+        SWF_CUDA(cudaMemsetAsync(bw.d6, 0, size_t(6) * h * 4, st));
+        float* dxmid = bw.dx[cur ^ 1];
+        SWF_CUDA(cudaMemcpyAsync(dxmid, dXp, size_t(M) * h * 4, cudaMemcpyDeviceToDevice, st));
+        norm_bwd(bw.xmid, h, bw.dxm, h, M, h, c->g_ffn + size_t(b) * h, six + 3 * h, six + 4 * h, six + 5 * h, dxmid,
+                 h, bw.rms, ga(base + 3), bw.d6 + 3 * h, bw.d6 + 4 * h, bw.d6 + 5 * h, st);
+        // attention branch: out projection, head_attention_bwd (:189-226), prenorm_modulate_bwd
+        gemm_strided_f32(h, h, int(M), bw.obuf, 1, hp, dxmid, h, 1, ga(base + 1), h, 1.f, st);  // dW_out
+        gemm_strided_f32(int(M), h, h, dxmid, h, 1, pa(base + 1), 1, h, bw.dO, hp, 0.f, st);
+        float* dq = bw.dplanes;
+        attention_bwd_f32(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h, bw.stats,
+                          c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, st);
+        gemm_strided_f32(h, 3 * h, int(M), bw.xm1, 1, hp, bw.dqkv, 3 * h, 1, ga(base + 0), 3 * h, 1.f, st);  // dW_qkv
+        gemm_strided_f32(int(M), h, 3 * h, bw.dqkv, 3 * h, 1, pa(base + 0), 1, 3 * h, bw.dxm, h, 0.f, st);
+        // dx_in = dx_mid + prenorm_modulate_bwd(...) -- accumulated in place in dxmid
+        norm_bwd(xb, h, bw.dxm, h, M, h, c->g_attn + size_t(b) * h, six, six + h, six + 2 * h, dxmid, h, bw.rms,
+                 ga(base + 2), bw.d6, bw.d6 + h, bw.d6 + 2 * h, st);
+        ada_bwd(bw.d6, c->emb, pa(base + 7), 6 * h, td, ga(base + 7), ga(base + 8), bw.demb, st);
+        cur ^= 1;  // the block input's gradient, in layout par = the previous block's output layout
+    }
+    // encode (swin.hpp:458-461) and the shared time projection (:463-466)
+    const float* dx = bw.dx[cur];
+    gemm_strided_f32(m.cin, h, int(M), static_cast<const float*>(c->a_in), 1, m.cinp, dx, h, 1, ga(0), h, 1.f, st);
+    colsum_f32(dx, h, M, h, ga(1), st);
+    gemm_strided_f32(int(M), m.cin, h, dx, h, 1, pa(0), 1, h, bw.din, m.cin, 0.f, st);
+    time_bwd(bw.demb, c->feat, pa(tail + 0), pa(tail + 1), td, ga(tail + 0), ga(tail + 1), st);
 }
 
 void gather_input_any(swf_ctx* c, const float* in_pix) {
@@ -1487,6 +1663,48 @@ int swf_forward(swf_ctx* c, const void* input, double t, void* output, int dtype
         forward_any(c, t, 1.f);
         check_flags(c);
         d2h_field(c, c->out_loc, c->m.cout, dtype, output);
+    })
+}
+
+int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, void* grads, void* d_input,
+                 int dtype) {
+    SWF_API_TRY({
+        require(c && input && d_output && grads, "null argument");
+        require(c->loaded, "backward: parameters not loaded");
+        require(c->prec == SWF_PREC_FP32, "backward: available in the FP32 validation mode (SWF_PREC_FP32)");
+        require(c->world == 1, "backward: single rank");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        ensure_bwd(c);
+        reset_flags(c);
+        h2d_field(c, input, c->m.cin, dtype, c->in_pix);
+        gather_input_any(c, c->in_pix);
+        c->save_x = true;
+        forward_any(c, t, 1.f);
+        c->save_x = false;
+        check_flags(c);
+        h2d_local(c, d_output, c->m.cout, dtype, c->bw.dtmp);  // [M][C_out] in layout-0 order
+        SWF_CUDA(cudaMemcpyAsync(c->bw.dS, c->bw.dtmp, size_t(c->M) * c->m.cout * 4, cudaMemcpyDeviceToDevice, c->st));
+        backward_core(c, c->bw.dS);
+        const size_t n = c->poff.back();
+        std::vector<float> g(n);
+        SWF_CUDA(cudaMemcpyAsync(g.data(), c->bw.gflat, n * 4, cudaMemcpyDeviceToHost, c->st));
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        if (dtype == SWF_F64)
+            for (size_t i = 0; i < n; ++i) static_cast<double*>(grads)[i] = g[i];
+        else
+            std::memcpy(grads, g.data(), n * 4);
+        if (d_input) {  // local layout-0 rows -> pixel order (in_pix holds N x C_in)
+            const size_t ni = size_t(c->N) * c->m.cin;
+            SWF_CUDA(cudaMemsetAsync(c->in_pix, 0, ni * 4, c->st));
+            scatter_rows(c->bw.din, c->lay[0], c->m.cin, c->M, c->in_pix, c->st);
+            std::vector<float> di(ni);
+            SWF_CUDA(cudaMemcpyAsync(di.data(), c->in_pix, ni * 4, cudaMemcpyDeviceToHost, c->st));
+            SWF_CUDA(cudaStreamSynchronize(c->st));
+            if (dtype == SWF_F64)
+                for (size_t i = 0; i < ni; ++i) static_cast<double*>(d_input)[i] = di[i];
+            else
+                std::memcpy(d_input, di.data(), ni * 4);
+        }
     })
 }
 

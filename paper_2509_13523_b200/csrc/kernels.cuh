@@ -150,6 +150,26 @@ struct AttnParams {
 void attention_f32(const AttnParams& p, cudaStream_t st);
 void attention_bf16(const AttnParams& p, cudaStream_t st);
 
+// ------------------------------------------------------------------ backward (k_bwd.cu, FP32 mode)
+// C[i][j] = beta C[i][j] + sum_k A[i*sai + k*sak] B[k*sbk + j*sbj]
+void gemm_strided_f32(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj,
+                      float* C, i64 ldc, float beta, cudaStream_t st);
+// prenorm_modulate_bwd / prenorm_plain_bwd (a, b, gate null): dX += ..., per-channel grads +=
+void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h, const float* g, const float* a,
+              const float* b, const float* gate, float* dX, int lddx, float* rms, float* dg, float* da, float* db,
+              float* dgate, cudaStream_t st);
+void colsum_f32(const float* X, int ldx, i64 M, int n, float* out, cudaStream_t st);
+void swiglu_bwd(const float* gu, int ldgu, const float* dS, int ldds, i64 M, int f, int G, float* act, float* dG,
+                float* dU, cudaStream_t st);
+void relayout_rows(const float* src, const LayMap& A, const LayMap& B, i64 M, int h, float* dst, cudaStream_t st);
+void attention_bwd_f32(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,
+                       float* dq, float* dk, float* dv, float* stats, int nloc, int heads, int s, int d, int w,
+                       const LayMap& lay, const EpiParams& ep, float* dqkv, cudaStream_t st);
+void ada_bwd(const float* d6, const float* emb, const float* Wa, int n6, int td, float* gWa, float* gba, float* demb,
+             cudaStream_t st);
+void time_bwd(const float* demb, const float* feat, const float* Wt, const float* bt, int td, float* gWt, float* gbt,
+              cudaStream_t st);
+
 // ------------------------------------------------------------------ elementwise
 void time_features(double t, int td, float* feat, cudaStream_t st);
 void time_embed(const float* feat, const float* w_time_t, const float* b_time, int td, float* emb,

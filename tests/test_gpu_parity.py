@@ -214,3 +214,41 @@ def test_forecast_step_chunked_matches_host_inputs(tmp_path):
     assert np.array_equal(got2, want)
     with pytest.raises(swf.ConfigError):  # channel mismatch
         dn.forecast_step_chunked(fp, fp, dc, 11, ev)
+
+
+# Gradients sum FP32 products over every token of the grid; the oracle's own float32 restatement
+# differs from its float64 one by up to ~5e-4 of an array's max |grad| at MID (tools/bwd_probe.py),
+# so the device backward is held to 1e-3 of the f64 oracle (2e-3 for the input gradient) and 5e-4 of
+# the f32 oracle (a different FP32 summation order).
+TOL_GRAD_F64 = 1e-3
+TOL_GRAD_F32 = 5e-4
+
+
+@pytest.mark.parametrize("cfg,H,W", [(TINY, 12, 12), (C1, 32, 64), (MID, 24, 48)])
+def test_backward_fp32_matches_oracle(cfg, H, W):
+    """f3: the device backward (FP32 validation mode) against the oracle backward, which is pinned
+    by central finite differences (tests/test_oracle_backward.py); repeated calls are bitwise equal."""
+    oc, sc = cfgs(cfg)
+    p = o.init_params(oc, 77, random=True, scale=0.1, dtype=np.float64)
+    x = o.random_field(oc.in_channels, H * W, 78)
+    R = o.random_field(oc.out_channels, H * W, 79)
+    gref, dref = o.backward(oc, p, x, 0.8, H, W, R)
+    g32, d32 = o.backward(oc, p.astype(np.float32), x.astype(np.float32), np.float32(0.8), H, W,
+                          R.astype(np.float32))
+    dn = swf.Denoiser(sc, H, W, precision=swf.PREC_FP32)
+    dn.load_params(p.astype(np.float32))
+    g, din = dn.backward(x.astype(np.float32), 0.8, R.astype(np.float32))
+    g2, _ = dn.backward(x.astype(np.float32), 0.8, R.astype(np.float32))
+    assert np.array_equal(g, g2)
+    off = 0
+    for name, r, c in o.param_shapes(oc):
+        a, b, f = g[off:off + r * c], gref[off:off + r * c], g32[off:off + r * c]
+        off += r * c
+        scale = max(float(np.abs(b).max()), 1e-30)
+        assert float(np.abs(a - b).max()) / scale <= TOL_GRAD_F64, name
+        assert float(np.abs(a - f).max()) / scale <= TOL_GRAD_F32, name
+    # input gradient, per channel: the f32 restatement's own deviation from f64 is the same size
+    scale = np.maximum(np.abs(dref).max(axis=0), 1e-30)
+    assert float((np.abs(din - d32).max(axis=0) / scale).max()) <= TOL_GRAD_F32
+    assert float((np.abs(d32 - dref).max(axis=0) / scale).max()) <= 2 * TOL_GRAD_F64
+    assert float((np.abs(din - dref).max(axis=0) / scale).max()) <= 2 * TOL_GRAD_F64
