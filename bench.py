@@ -349,6 +349,81 @@ def ncu_traffic(kernel_class: str):
         return None
 
 
+def run_c5(args, rank: int, world: int, local_rank: int):
+    """BASELINE.json configs[4]: ensemble generation, members x (2 x solver_steps) TrigFlow sampler
+    evaluations x 1 autoregressive step on the C2 model, replicas only (members split across ranks;
+    each rank holds the whole grid). "20 TrigFlow sampler steps" is read as 10 DPM-Solver++ 2S
+    steps = 20 network evaluations (test_trigflow.cpp:239-245). One rollout_ensemble call per
+    rank (device-resident solver, window-keyed noise) with host buffers in and out; value = member
+    evaluations x pixels / max-over-ranks wall time."""
+    import torch
+    import paper_2509_13523_b200 as swf
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    if args.members % world:
+        raise SystemExit(f"--members {args.members} must divide over {world} ranks")
+    per = args.members // world
+    cfg = swf.ModelConfig(**CFG)
+    dn = swf.Denoiser(cfg, H, W, device=local_rank, precision=swf.PREC_BF16)
+    dn.init_params(SEED, mode=2, scale=0.02 / math.sqrt(CFG["time_dim"]))
+    cp, cf = CFG["out_channels"], CFG["in_channels"] - 2 * CFG["out_channels"]
+    rng = np.random.default_rng(SEED + 7)
+    x0 = rng.standard_normal((H * W, cp), dtype=np.float32)
+    forc = [rng.standard_normal((H * W, cf), dtype=np.float32)]
+    dc = swf.DiffusionConfig(solver_steps=args.solver_steps)
+    evals = 2 * args.solver_steps
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    x_in = synthetic_input(dn, CFG)
+    d_in = torch.from_numpy(x_in).to(f"cuda:{local_rank}")
+    d_out = torch.empty(H * W * cp, dtype=torch.float32, device=f"cuda:{local_rank}")
+    for _ in range(max(args.warmup, 1)):  # warm the forward path (kernels, clocks)
+        dn.forward_device(d_in.data_ptr(), T_STEP, d_out.data_ptr())
+    dn.sync()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t0 = time.perf_counter()
+        out = dn.rollout_ensemble(x0, forc, per, 1, dc, SEED, 1000 + rank)
+        barrier()
+        sec = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([sec], device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    finite = bool(np.isfinite(out).all())
+    total_evals = args.members * evals
+    value = total_evals * H * W / sec
+    if rank == 0:
+        step_flops = flops_per_step(CFG, H * W)
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "pixels/s", "n_gpus": world, "steps": 1, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "ensemble generation (BASELINE.json configs[4]), replicas",
+                       "grid": [H, W], "members": args.members, "members_per_gpu": per,
+                       "sampler": f"{args.solver_steps} DPM-Solver++ 2S steps = {evals} denoiser evaluations per member",
+                       "autoregressive_steps": 1, "model": "swin-dit-1.3B (C2)", "parallelism": f"replicas x{world}",
+                       "step": "one rollout_ensemble call per rank (host buffers in/out, device-resident solver)"},
+            "tflops_per_gpu": total_evals * step_flops / sec / world / 1e12,
+            "evals_per_s": total_evals / sec,
+            "e2e": {"value": value, "unit": "pixels/s", "h2d_bytes_per_step": int(x0.nbytes + forc[0].nbytes) * world,
+                    "d2h_bytes_per_step": int(out.nbytes) * world, "ms_per_step": sec * 1e3},
+            "clocks": clk.summary(), "output_check": {"finite": finite},
+        }), flush=True)
+    dn.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -358,14 +433,19 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sp", type=int, default=1, help="sequence-parallel degree (window rows split into SP bands)")
-    ap.add_argument("--workload", choices=["c2", "c4"], default="c2",
-                    help="c2: AERIS-1.3B 20-block step (headline); c4: 40B-shaped 2-block wide-layer slice")
+    ap.add_argument("--workload", choices=["c2", "c4", "c5"], default="c2",
+                    help="c2: AERIS-1.3B 20-block step (headline); c4: 40B-shaped 2-block wide-layer slice; "
+                         "c5: ensemble generation (members x sampler evaluations, replicas)")
+    ap.add_argument("--members", type=int, default=16, help="c5: ensemble members over all ranks")
+    ap.add_argument("--solver-steps", type=int, default=10, help="c5: DPM-Solver++ 2S steps (2 evaluations each)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload == "c5":
+        run_c5(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 
