@@ -53,6 +53,7 @@ struct Dims {
     int bn_enc, bn_qkv, bn_out, bn_gu, bn_down, bn_dec;
     int np_enc, np_qkv, np_out, np_gu, np_down, np_dec;  // N dims padded
     int G;                         // gate/up interleave granularity
+    int nss;                       // fused-norm partial sums per row (BF16): 2 per N tile of h
 };
 
 struct Peer {
@@ -108,6 +109,15 @@ struct swf_ctx {
     // TMA maps (BF16 path)
     TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec, tm_q, tm_k, tm_vt;
     TmaMap tm_so;  // sbuf viewed as [M][hp] (attention output of the kernel benchmark)
+    // fused RMSNorm + AdaLN (BF16): bf16 copy + row partial sums of squares of each residual buffer
+    // (inside xbuf[par] at off_xb / off_ss floats), fp32 masters of the folded weights, shift biases
+    __nv_bfloat16* xbb[2] = {nullptr, nullptr};
+    float* ssb[2] = {nullptr, nullptr};
+    float* invr = nullptr;  // [M] 1 / rms of the current normed GEMM's A rows
+    i64 off_xb = 0, off_ss = 0;
+    TmaMap tm_xb[2];
+    std::vector<float*> w_qkv_m, w_gu_m, beta_qkv, beta_gu;
+    float* w_dec_m = nullptr;
     std::vector<TmaMap> tm_qkv, tm_out, tm_gu, tm_down;
     long long launches = 0;
     // sampler workspace (allocated lazily)
@@ -192,6 +202,7 @@ Dims make_dims(const swf_model_cfg& cf, int prec) {
     m.np_out = int(roundup(m.h, m.bn_out));
     m.np_down = int(roundup(m.h, m.bn_down));
     m.np_dec = int(roundup(m.cout, 128));
+    m.nss = prec == SWF_PREC_BF16 ? 2 * (m.np_out / m.bn_out) : 0;
     if (prec == SWF_PREC_BF16) {
         m.bn_gu = (2 * m.f) % 256 == 0 ? 256 : 128;
         m.G = m.bn_gu / 2;
@@ -327,8 +338,18 @@ void allocate(swf_ctx* c) {
     build_layouts(c);
     build_rope(c);
     const i64 M = c->M;
-    c->xbuf[0] = dalloc<float>(c, size_t(M) * m.h);
-    c->xbuf[1] = dalloc<float>(c, size_t(M) * m.h);
+    if (c->prec == SWF_PREC_BF16) {  // [x fp32 M x h][x bf16 M x hp][sum-of-squares partials M x nss]
+        c->off_xb = M * m.h;
+        c->off_ss = c->off_xb + M * m.hp / 2;
+        for (int par = 0; par < 2; ++par) {
+            c->xbuf[par] = dalloc<float>(c, size_t(c->off_ss) + size_t(M) * m.nss);
+            c->xbb[par] = reinterpret_cast<__nv_bfloat16*>(c->xbuf[par] + c->off_xb);
+            c->ssb[par] = c->xbuf[par] + c->off_ss;
+        }
+    } else {
+        c->xbuf[0] = dalloc<float>(c, size_t(M) * m.h);
+        c->xbuf[1] = dalloc<float>(c, size_t(M) * m.h);
+    }
     c->xm = talloc(c, size_t(M) * m.hp);
     c->qkv = talloc(c, size_t(3) * M * m.h);
     c->sbuf = talloc(c, size_t(M) * m.fp);
@@ -361,6 +382,16 @@ void allocate(swf_ctx* c) {
         c->w_gu.push_back(talloc(c, size_t(m.np_gu) * m.hp));
         c->w_down.push_back(talloc(c, size_t(m.np_down) * m.fp));
     }
+    if (c->prec == SWF_PREC_BF16) {
+        for (int b = 0; b < m.nb; ++b) {
+            c->w_qkv_m.push_back(dalloc<float>(c, size_t(m.np_qkv) * m.hp));
+            c->w_gu_m.push_back(dalloc<float>(c, size_t(m.np_gu) * m.hp));
+            c->beta_qkv.push_back(dalloc<float>(c, size_t(m.np_qkv)));
+            c->beta_gu.push_back(dalloc<float>(c, size_t(m.np_gu)));
+        }
+        c->w_dec_m = dalloc<float>(c, size_t(m.np_dec) * m.hp);
+        c->invr = dalloc<float>(c, size_t(M));
+    }
     // destination tables for the fused down-projection store (own buffer unless peers connect)
     c->bar_flags = dalloc<int>(c, 64);
     c->d_flag_table = dalloc<int*>(c, 8);
@@ -388,6 +419,8 @@ void allocate(swf_ctx* c) {
     if (c->prec == SWF_PREC_BF16) {
         make_tma_bf16(&c->tm_ain, c->a_in, M, m.cinp, 128);
         make_tma_bf16(&c->tm_xm, c->xm, M, m.hp, 128);
+        make_tma_bf16(&c->tm_xb[0], c->xbb[0], M, m.hp, 128);
+        make_tma_bf16(&c->tm_xb[1], c->xbb[1], M, m.hp, 128);
         make_tma_bf16(&c->tm_s, c->sbuf, M, m.fp, 128);
         make_tma_bf16(&c->tm_so, c->sbuf, M, m.hp, 128);
         make_tma_bf16(&c->tm_enc, c->w_enc, m.np_enc, m.cinp, m.bn_enc / 2);
@@ -467,6 +500,7 @@ void load_params_from(swf_ctx* c, Next&& next) {
         ++ai;
         return src;
     };
+    const bool bf = c->prec == SWF_PREC_BF16;
     auto copy_vec = [&](float* dst, size_t n) {
         float* s = up(n);
         SWF_CUDA(cudaMemcpyAsync(dst, s, n * 4, cudaMemcpyDeviceToDevice, c->st));
@@ -474,12 +508,19 @@ void load_params_from(swf_ctx* c, Next&& next) {
     repack(c, up(size_t(m.h) * m.cin), m.h, m.cin, c->w_enc, m.cinp, 0, 0, false);  // encode.w (h x C_in)
     copy_vec(c->enc_b, m.h);
     for (int b = 0; b < m.nb; ++b) {
-        repack(c, up(size_t(3) * m.h * m.h), 3 * m.h, m.h, c->w_qkv[b], m.hp, 0, 0, false);
+        {
+            float* src = up(size_t(3) * m.h * m.h);
+            repack(c, src, 3 * m.h, m.h, c->w_qkv[b], m.hp, 0, 0, false);
+            if (bf) repack(c, src, 3 * m.h, m.h, c->w_qkv_m[b], m.hp, 0, 0, true);
+        }
         repack(c, up(size_t(m.h) * m.h), m.h, m.h, c->w_out[b], m.hp, 0, 0, false);
         copy_vec(c->g_attn + size_t(b) * m.h, m.h);
         copy_vec(c->g_ffn + size_t(b) * m.h, m.h);
-        repack(c, up(size_t(m.f) * m.h), m.f, m.h, c->w_gu[b], m.hp, m.G, 0, false);  // gate
-        repack(c, up(size_t(m.f) * m.h), m.f, m.h, c->w_gu[b], m.hp, m.G, 1, false);  // up
+        for (int part = 0; part < 2; ++part) {  // gate, up (interleaved per G rows)
+            float* src = up(size_t(m.f) * m.h);
+            repack(c, src, m.f, m.h, c->w_gu[b], m.hp, m.G, part, false);
+            if (bf) repack(c, src, m.f, m.h, c->w_gu_m[b], m.hp, m.G, part, true);
+        }
         repack(c, up(size_t(m.h) * m.f), m.h, m.f, c->w_down[b], m.fp, 0, 0, false);
         repack(c, up(size_t(6) * m.h * m.td), 6 * m.h, m.td, c->w_ada_t + size_t(b) * 6 * m.h * m.td, m.td, 0, 0,
                true);
@@ -488,7 +529,11 @@ void load_params_from(swf_ctx* c, Next&& next) {
     repack(c, up(size_t(m.td) * m.td), m.td, m.td, c->w_time_t, m.td, 0, 0, true);
     copy_vec(c->b_time, m.td);
     copy_vec(c->g_dec, m.h);
-    repack(c, up(size_t(m.cout) * m.h), m.cout, m.h, c->w_dec, m.hp, 0, 0, false);
+    {
+        float* src = up(size_t(m.cout) * m.h);
+        repack(c, src, m.cout, m.h, c->w_dec, m.hp, 0, 0, false);
+        if (bf) repack(c, src, m.cout, m.h, c->w_dec_m, m.hp, 0, 0, true);
+    }
     copy_vec(c->b_dec, m.cout);
     SWF_CUDA(cudaStreamSynchronize(c->st));
     c->loaded = true;
@@ -743,6 +788,10 @@ EpiParams base_ep(swf_ctx* c) {
     ep.qkv_dst = c->d_qkv_dst;
     ep.heads_loc = c->m.heads / c->sp;
     ep.wp_rank = c->wp_rank;
+    ep.hp = c->m.hp;
+    ep.nss = c->prec == SWF_PREC_BF16 ? c->m.nss : 0;  // fused norm: producers emit xb / partial sums
+    ep.off_xb = c->off_xb;
+    ep.off_ss = c->off_ss;
     return ep;
 }
 
@@ -796,6 +845,21 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
     // no rank may store into a peer's residual buffer while that peer still reads it
     if (c->world > 1) peer_barrier(c);
     time_vectors(c, t);
+    constexpr bool kFuse = sizeof(T) == 2;  // BF16: RMSNorm + AdaLN fused into the GEMMs
+    if constexpr (kFuse) {
+        // fold this t's AdaLN scale into the normed GEMMs' weights and its shift into their biases
+        const int h = m.h;
+        for (int b = 0; b < m.nb; ++b) {
+            const float* six = c->six + size_t(b) * 6 * h;
+            fold_adaln(c->w_qkv_m[b], m.np_qkv, h, m.hp, c->g_attn + size_t(b) * h, six, six + h, six + 2 * h,
+                       static_cast<__nv_bfloat16*>(c->w_qkv[b]), c->beta_qkv[b], c->st);
+            fold_adaln(c->w_gu_m[b], m.np_gu, h, m.hp, c->g_ffn + size_t(b) * h, six + 3 * h, six + 4 * h,
+                       six + 5 * h, static_cast<__nv_bfloat16*>(c->w_gu[b]), c->beta_gu[b], c->st);
+        }
+        fold_adaln(c->w_dec_m, m.np_dec, h, m.hp, c->g_dec, nullptr, nullptr, nullptr,
+                   static_cast<__nv_bfloat16*>(c->w_dec), nullptr, c->st);
+        c->launches += 2 * m.nb + 1;
+    }
     EpiParams ep = base_ep(c);
     // encode (swin.hpp:341-342)
     ep.x = c->xbuf[0];
@@ -817,7 +881,7 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
             SWF_CUDA(cudaMemcpyAsync(c->xsave + size_t(b) * M * m.h, x, size_t(M) * m.h * 4, cudaMemcpyDeviceToDevice,
                                      c->st));
         // attention branch: prenorm_modulate -> heads -> out projection (swin.hpp:313-322)
-        {
+        if constexpr (!kFuse) {
             ProfScope ps(c, K_RMS);
             rms_modulate<T>(x, M, m.h, m.hp, c->g_attn + size_t(b) * m.h, six, six + m.h, six + 2 * m.h, xm, c->flags,
                         1 + b, c->st);
@@ -827,10 +891,16 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         e.out = c->qkv;
         e.plane = i64(c->lay[par].nloc) * (m.heads / c->sp) * m.w * m.w * m.d;  // one q/k/v plane of a rank
         e.N = 3 * m.h;
+        if constexpr (kFuse) {  // A = bf16 copy of x; norm from the producer's partial sums
+            inv_rms(c->ssb[cur], M, m.nss, m.h, c->invr, c->flags, 1 + b, c->st);
+            e.inv_r = c->invr;
+            e.beta = c->beta_qkv[b];
+            c->launches++;
+        }
         {
             ProfScope ps(c, K_QKV);
-            Gemm<T>::run(c, xm, &c->tm_xm, c->w_qkv[b], tmap_at(c->tm_qkv, b), M, m.np_qkv, m.hp,
-                     m.bn_qkv, EPI_QKV, e);
+            Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_qkv[b], tmap_at(c->tm_qkv, b), M, m.np_qkv,
+                         m.hp, m.bn_qkv, EPI_QKV, e);
         }
         if (c->sp > 1) peer_barrier(c);  // every head group's planes complete before attention
         AttnParams ap;
@@ -870,7 +940,7 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
                      m.bn_out, EPI_RESID, e);
         }
         // feed-forward branch (swin.hpp:323-324)
-        {
+        if constexpr (!kFuse) {
             ProfScope ps(c, K_RMS);
             rms_modulate<T>(x, M, m.h, m.hp, c->g_ffn + size_t(b) * m.h, six + 3 * m.h, six + 4 * m.h, six + 5 * m.h, xm,
                         nullptr, 0, c->st);
@@ -880,10 +950,16 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         e.ld_out = m.fp;
         e.N = m.f;
         e.G = m.G;
+        if constexpr (kFuse) {
+            inv_rms(c->ssb[cur], M, m.nss, m.h, c->invr, nullptr, 0, c->st);
+            e.inv_r = c->invr;
+            e.beta = c->beta_gu[b];
+            c->launches++;
+        }
         {
             ProfScope ps(c, K_GATEUP);
-            Gemm<T>::run(c, xm, &c->tm_xm, c->w_gu[b], tmap_at(c->tm_gu, b), M, m.np_gu, m.hp,
-                     m.bn_gu, EPI_SWIGLU, e);
+            Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_gu[b], tmap_at(c->tm_gu, b), M, m.np_gu,
+                         m.hp, m.bn_gu, EPI_SWIGLU, e);
         }
         e = ep;
         e.x = x;
@@ -904,7 +980,7 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         SWF_CUDA(cudaMemcpyAsync(c->xsave + size_t(m.nb) * M * m.h, c->xbuf[cur], size_t(M) * m.h * 4,
                                  cudaMemcpyDeviceToDevice, c->st));
     // decode (swin.hpp:362-366)
-    {
+    if constexpr (!kFuse) {
             ProfScope ps(c, K_RMS);
             rms_modulate<T>(c->xbuf[cur], M, m.h, m.hp, c->g_dec, nullptr, nullptr, nullptr, xm, c->flags, 1 + m.nb, c->st);
         }
@@ -914,9 +990,15 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
     e.N = m.cout;
     e.bias = c->b_dec;
     e.out_scale = out_scale;
+    if constexpr (kFuse) {
+        inv_rms(c->ssb[cur], M, m.nss, m.h, c->invr, c->flags, 1 + m.nb, c->st);
+        e.inv_r = c->invr;
+        c->launches++;
+    }
     {
             ProfScope ps(c, K_DECODE);
-            Gemm<T>::run(c, xm, &c->tm_xm, c->w_dec, &c->tm_dec, M, m.np_dec, m.hp, m.bn_dec, EPI_DECODE, e);
+            Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_dec, &c->tm_dec, M, m.np_dec, m.hp, m.bn_dec,
+                         EPI_DECODE, e);
         }
     c->launches += 2;
 }
@@ -2003,7 +2085,9 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
                     e.out = c->qkv;
                     e.plane = i64(c->lay[par].nloc) * (m.heads / c->sp) * m.w * m.w * m.d;
                     e.N = 3 * m.h;
-                    gemm_bf16_tc(c->tm_xm, c->tm_qkv[blk], M, m.np_qkv, m.hp, m.bn_qkv, EPI_QKV, e, c->st);
+                    e.inv_r = c->invr;  // fused norm, as in the forward (last reduced rows)
+                    e.beta = c->beta_qkv[blk];
+                    gemm_bf16_tc(c->tm_xb[par], c->tm_qkv[blk], M, m.np_qkv, m.hp, m.bn_qkv, EPI_QKV, e, c->st);
                     break;
                 case K_ATTN: {
                     AttnParams ap;
@@ -2047,7 +2131,9 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
                     e.ld_out = m.fp;
                     e.N = m.f;
                     e.G = m.G;
-                    gemm_bf16_tc(c->tm_xm, c->tm_gu[blk], M, m.np_gu, m.hp, m.bn_gu, EPI_SWIGLU, e, c->st);
+                    e.inv_r = c->invr;
+                    e.beta = c->beta_gu[blk];
+                    gemm_bf16_tc(c->tm_xb[par], c->tm_gu[blk], M, m.np_gu, m.hp, m.bn_gu, EPI_SWIGLU, e, c->st);
                     break;
                 case K_DOWN:
                     e.x = c->xbuf[0];

@@ -286,6 +286,57 @@ void scatter_rows(const float* src_loc, const LayMap& lay, int C, i64 M, float* 
     SWF_LAUNCH_CHECK();
 }
 
+namespace {
+// one warp per weight row: fold the AdaLN scale into the row and dot it with the shift vector
+__global__ void k_fold_adaln(const float* __restrict__ Wm, int Np, int K, int ld, const float* __restrict__ g,
+                             const float* __restrict__ a, const float* __restrict__ b, const float* __restrict__ gate,
+                             __nv_bfloat16* __restrict__ Wf, float* __restrict__ beta) {
+    const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (n >= Np) return;
+    const float* w = Wm + i64(n) * ld;
+    __nv_bfloat16* o = Wf + i64(n) * ld;
+    float acc = 0.f;
+    for (int k = lane; k < ld; k += 32) {
+        float sk = 0.f, ck = 0.f;
+        if (k < K) {
+            const float q = gate ? gate[k] : 1.f;
+            sk = q * g[k] * (a ? 1.f + a[k] : 1.f);
+            ck = b ? q * b[k] : 0.f;
+        }
+        const float wv = w[k];
+        o[k] = __float2bfloat16_rn(wv * sk);
+        acc = fmaf(wv, ck, acc);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (beta && lane == 0) beta[n] = acc;
+}
+}  // namespace
+
+namespace {
+__global__ void k_inv_rms(const float* __restrict__ ss, i64 M, int nss, int h, float* __restrict__ inv_r,
+                          int* __restrict__ flags, int slot) {
+    const i64 m = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    float sq = 0.f;
+    for (int i = 0; i < nss; ++i) sq += ss[m * nss + i];
+    inv_r[m] = 1.f / sqrtf(sq / float(h) + 1e-8f);  // kRmsEps, swin.hpp:45
+    if (flags && !isfinite(sq)) atomicOr(flags + slot, 1);
+}
+}  // namespace
+
+void inv_rms(const float* ss, i64 M, int nss, int h, float* inv_r, int* flags, int slot, cudaStream_t st) {
+    k_inv_rms<<<unsigned((M + 255) / 256), 256, 0, st>>>(ss, M, nss, h, inv_r, flags, slot);
+    SWF_LAUNCH_CHECK();
+}
+
+void fold_adaln(const float* Wm, int Np, int K, int ld, const float* g, const float* a, const float* b,
+                const float* gate, __nv_bfloat16* Wf, float* beta, cudaStream_t st) {
+    k_fold_adaln<<<unsigned((Np + 7) / 8), 256, 0, st>>>(Wm, Np, K, ld, g, a, b, gate, Wf, beta);
+    SWF_LAUNCH_CHECK();
+}
+
 template <class T>
 void rms_modulate(const float* x, i64 M, int h, int ldo, const float* g, const float* a, const float* b,
                   const float* gate, T* out, int* flags, int slot, cudaStream_t st) {

@@ -141,28 +141,55 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 }
 
 // ---------------------------------------------------------------- vectorised epilogues (32 columns)
+// bf16 copy of 32 residual values (operand A of the next normed GEMM); returns their sum of squares
+__device__ __forceinline__ float store_xb32(const EpiParams& ep, const float* xbase, i64 m, int n0, const float* o) {
+    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(const_cast<float*>(xbase) + ep.off_xb) +
+                                        m * ep.hp + n0);
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        d[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]), pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                          pack_bf16x2(o[8 * j + 4], o[8 * j + 5]), pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+#pragma unroll
+        for (int t = 0; t < 8; ++t) ss = fmaf(o[8 * j + t], o[8 * j + t], ss);
+    }
+    return ss;
+}
+
 template <int MODE>
-__device__ __forceinline__ void epi32(const EpiParams& ep, i64 m, int n0, float* v) {
-    if (m >= ep.M || n0 >= ep.N) return;
+__device__ __forceinline__ float epi32(const EpiParams& ep, i64 m, int n0, float* v) {
+    if (m >= ep.M || n0 >= ep.N) return 0.f;
     const int h = ep.h;
     if constexpr (MODE == EPI_ENCODE) {
         float4* xr = reinterpret_cast<float4*>(ep.x + m * h + n0);
+        float o[32];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const float4 b = reinterpret_cast<const float4*>(ep.bias + n0)[j];
-            xr[j] = make_float4(v[4 * j] + b.x, v[4 * j + 1] + b.y, v[4 * j + 2] + b.z, v[4 * j + 3] + b.w);
+            o[4 * j] = v[4 * j] + b.x;
+            o[4 * j + 1] = v[4 * j + 1] + b.y;
+            o[4 * j + 2] = v[4 * j + 2] + b.z;
+            o[4 * j + 3] = v[4 * j + 3] + b.w;
+            xr[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
         }
+        return ep.nss ? store_xb32(ep, ep.x, m, n0, o) : 0.f;
     } else if constexpr (MODE == EPI_RESID) {
         float4* xr = reinterpret_cast<float4*>(ep.x + m * h + n0);
+        float o[32];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            float4 o = xr[j];
-            o.x += v[4 * j];
-            o.y += v[4 * j + 1];
-            o.z += v[4 * j + 2];
-            o.w += v[4 * j + 3];
-            xr[j] = o;
+            float4 x4 = xr[j];
+            x4.x += v[4 * j];
+            x4.y += v[4 * j + 1];
+            x4.z += v[4 * j + 2];
+            x4.w += v[4 * j + 3];
+            xr[j] = x4;
+            o[4 * j] = x4.x;
+            o[4 * j + 1] = x4.y;
+            o[4 * j + 2] = x4.z;
+            o[4 * j + 3] = x4.w;
         }
+        return ep.nss ? store_xb32(ep, ep.x, m, n0, o) : 0.f;
     } else if constexpr (MODE == EPI_DOWN) {
         int rank;
         const i64 li = ep.nxt.pix_to_loc(ep.cur.loc_to_pix(m), &rank);
@@ -200,7 +227,7 @@ __device__ __forceinline__ void epi32(const EpiParams& ep, i64 m, int n0, float*
             __nv_bfloat16* vt = base + ((i64(lw) * ep.heads_loc + hl) * ep.d + dd) * s + tok;
 #pragma unroll
             for (int j = 0; j < 32; ++j) vt[i64(j) * s] = __float2bfloat16_rn(v[j]);
-            return;
+            return 0.f;
         }
         __nv_bfloat16* dst = base + ((i64(lw) * ep.heads_loc + hl) * s + tok) * ep.d + dd;
         uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -214,6 +241,7 @@ __device__ __forceinline__ void epi32(const EpiParams& ep, i64 m, int n0, float*
         for (int j = 0; j < 32; ++j)
             if (n0 + j < ep.N) o[n0 + j] = (v[j] + ep.bias[n0 + j]) * ep.out_scale;
     }
+    return 0.f;
 }
 
 __device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0, const float* g, const float* u,
@@ -250,8 +278,8 @@ __device__ __forceinline__ void tile_coords(i64 t, int n_tiles, i64 m_tiles, int
 // fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)
 // is transposed through shared memory so each global access is one contiguous 128-byte row segment.
 template <int MODE>
-__device__ __forceinline__ void epi32_coalesced(const EpiParams& ep, i64 row, int n0, const float* v, float* stg,
-                                                float* drow, int lane) {
+__device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, int n0, const float* v, float* stg,
+                                                 float* drow, __nv_bfloat16* dbrow, int lane) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
     __syncwarp();
@@ -277,10 +305,26 @@ __device__ __forceinline__ void epi32_coalesced(const EpiParams& ep, i64 row, in
                 dst = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(drow), rr)) + n;
             else
                 dst = ep.x + (row0 + rr) * h + n;
-            if (rr < mrem && col_ok) *dst = xv[rr] + stg[rr * 33 + lane];
+            const float o = xv[rr] + stg[rr * 33 + lane];
+            if (rr < mrem && col_ok) *dst = o;
+            if (ep.nss) {
+                if constexpr (MODE == EPI_DOWN) {
+                    __nv_bfloat16* db = reinterpret_cast<__nv_bfloat16*>(
+                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dbrow), rr));
+                    if (rr < mrem && col_ok) db[n] = __float2bfloat16_rn(o);
+                }
+                stg[rr * 33 + lane] = col_ok ? o : 0.f;
+            }
         }
     }
     __syncwarp();
+    float ss = 0.f;
+    if (ep.nss) {  // this lane's row: sum of squares of the 32 new values
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ss = fmaf(stg[lane * 33 + i], stg[lane * 33 + i], ss);
+        __syncwarp();
+    }
+    return ss;
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -406,6 +450,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const i64 row = i64(m_blk) * 2 * BM + crank * BM + q * 32 + lane;
             const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+            // fused RMSNorm + AdaLN of operand A's rows (consumers): 1 / rms from the producer partials
+            float inv_r = 1.f;
+            if constexpr (MODE == EPI_QKV || MODE == EPI_SWIGLU || MODE == EPI_DECODE)
+                if (ep.inv_r && row < ep.M) inv_r = ep.inv_r[row];
+            auto normed = [&](float* v, int col) {
+                if constexpr (MODE == EPI_QKV || MODE == EPI_SWIGLU || MODE == EPI_DECODE) {
+                    if (ep.inv_r) {
+                        if (ep.beta) {
+                            const float4* b4 = reinterpret_cast<const float4*>(ep.beta + col);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const float4 bb = b4[j];
+                                v[4 * j] = fmaf(v[4 * j], inv_r, bb.x);
+                                v[4 * j + 1] = fmaf(v[4 * j + 1], inv_r, bb.y);
+                                v[4 * j + 2] = fmaf(v[4 * j + 2], inv_r, bb.z);
+                                v[4 * j + 3] = fmaf(v[4 * j + 3], inv_r, bb.w);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) v[j] *= inv_r;
+                        }
+                    }
+                }
+            };
             if constexpr (MODE == EPI_SWIGLU) {
                 // interleave G = BN/2: columns [0, BN/2) gate, [BN/2, BN) up of the same ffn units
                 constexpr int NCH = BN / 64;
@@ -414,31 +482,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     float g[32], u[32];
                     tmem_ld32(tbase + ch * 32, g);
                     tmem_ld32(tbase + BN / 2 + ch * 32, u);
+                    normed(g, n_blk * BN + ch * 32);
+                    normed(u, n_blk * BN + BN / 2 + ch * 32);
                     epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u, pol_out);
                 }
             } else if constexpr (MODE == EPI_DOWN) {
                 float* drow = nullptr;
+                __nv_bfloat16* dbrow = nullptr;
+                float* dsrow = nullptr;
                 // destination row in the next block's layout, possibly on a peer GPU (NVLink)
                 if (row < ep.M) {
                     int rank;
                     const i64 li = ep.nxt.pix_to_loc(ep.cur.loc_to_pix(row), &rank);
-                    drow = ep.xdst[rank] + li * ep.h;
+                    float* xb = ep.xdst[rank];
+                    drow = xb + li * ep.h;
+                    if (ep.nss) {
+                        dbrow = reinterpret_cast<__nv_bfloat16*>(xb + ep.off_xb) + li * ep.hp;
+                        dsrow = xb + ep.off_ss + li * ep.nss;
+                    }
                 }
                 constexpr int NCH = BN / 32;
+                float ssum = 0.f;
 #pragma unroll 1
                 for (int ch = half * NCH / 2; ch < (half + 1) * NCH / 2; ++ch) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
-                    epi32_coalesced<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, drow, lane);
+                    ssum += epi32_coalesced<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, drow, dbrow, lane);
                 }
+                if (dsrow) dsrow[2 * n_blk + half] = ssum;
             } else {
                 constexpr int NCH = BN / 32;
+                float ssum = 0.f;
 #pragma unroll 1
                 for (int ch = half * NCH / 2; ch < (half + 1) * NCH / 2; ++ch) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
-                    epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
+                    normed(v, n_blk * BN + ch * 32);
+                    ssum += epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
                 }
+                if constexpr (MODE == EPI_ENCODE || MODE == EPI_RESID)
+                    if (ep.nss && row < ep.M) ep.x[ep.off_ss + row * ep.nss + 2 * n_blk + half] = ssum;
             }
             tc_fence_before();
             __syncwarp();

@@ -107,7 +107,21 @@ struct EpiParams {
     void* const* qkv_dst;
     int heads_loc;
     int wp_rank;
+    // RMSNorm + AdaLN fused into the GEMMs (BF16 path; nss == 0 disables it). Producers (ENCODE,
+    // RESID, DOWN) also store a bf16 copy of the residual row (operand A of the next normed GEMM) at
+    // (bf16*)(xbase + off_xb) + row * hp and the partial sum of squares of their 128 columns at
+    // xbase + off_ss + row * nss + slot (slot = 2 * n_tile + half), xbase being ep.x or ep.xdst[rank].
+    // Consumers (QKV, SWIGLU, DECODE) scale the accumulator by inv_r[row] = 1 / rms(row) (reduced
+    // from the partials by inv_rms) and add beta[col] = (W (gate .* b))[col], the weights having been
+    // folded with diag(gate .* g .* (1 + a)) (swin.hpp:72-85).
+    int hp, nss;
+    i64 off_xb, off_ss;
+    const float* inv_r;
+    const float* beta;
 };
+// inv_r[m] = 1 / sqrt(sum_i ss[m][i] / h + 1e-8) over the nss partials; non-finite rows flag
+// flags[slot] (check_finite, swin.hpp:295-300)
+void inv_rms(const float* ss, i64 M, int nss, int h, float* inv_r, int* flags, int slot, cudaStream_t st);
 
 // C[M][N] = A[M][K] . B[N][K]^T (both K-major), fp32 SIMT -- the FP32 validation mode GEMM.
 void gemm_f32(const float* A, const float* B, i64 M, int N, int K, int mode, const EpiParams& ep,
@@ -185,6 +199,11 @@ void gather_rows(const float* src_pix, const LayMap& lay, int C, int ldo, i64 M,
 void scatter_rows(const float* src_loc, const LayMap& lay, int C, i64 M, float* dst_pix, cudaStream_t st);
 // RMSNorm + AdaLN modulation (prenorm_modulate, swin.hpp:72-85) or plain (prenorm_plain :111-123 when
 // a == nullptr): out[m][i] = gate*((g*x/r)*(1+a)+b); non-finite input -> flags[slot].
+// AdaLN folding for the fused norm (BF16 path): Wf[n][k] = bf16(Wm[n][k] * s[k]) and
+// beta[n] = sum_k Wm[n][k] c[k] with s = gate .* g .* (1 + a), c = gate .* b (a, b, gate may be null
+// = 0, 0, 1), Wm the fp32 master in the repacked [Np][ld] layout.
+void fold_adaln(const float* Wm, int Np, int K, int ld, const float* g, const float* a, const float* b,
+                const float* gate, __nv_bfloat16* Wf, float* beta, cudaStream_t st);
 template <class T>
 void rms_modulate(const float* x, i64 M, int h, int ldo, const float* g, const float* a, const float* b,
                   const float* gate, T* out, int* flags, int slot, cudaStream_t st);
