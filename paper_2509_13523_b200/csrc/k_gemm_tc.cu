@@ -308,11 +308,9 @@ __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, i
             const float o = xv[rr] + stg[rr * 33 + lane];
             if (rr < mrem && col_ok) *dst = o;
             if (ep.nss) {
-                if constexpr (MODE == EPI_DOWN) {
-                    __nv_bfloat16* db = reinterpret_cast<__nv_bfloat16*>(
-                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dbrow), rr));
-                    if (rr < mrem && col_ok) db[n] = __float2bfloat16_rn(o);
-                }
+                __nv_bfloat16* db = reinterpret_cast<__nv_bfloat16*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dbrow), rr));
+                if (rr < mrem && col_ok) db[n] = __float2bfloat16_rn(o);
                 stg[rr * 33 + lane] = col_ok ? o : 0.f;
             }
         }
@@ -486,15 +484,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     normed(u, n_blk * BN + BN / 2 + ch * 32);
                     epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u, pol_out);
                 }
-            } else if constexpr (MODE == EPI_DOWN) {
+            } else if constexpr (MODE == EPI_DOWN || MODE == EPI_RESID) {
                 float* drow = nullptr;
                 __nv_bfloat16* dbrow = nullptr;
                 float* dsrow = nullptr;
-                // destination row in the next block's layout, possibly on a peer GPU (NVLink)
                 if (row < ep.M) {
-                    int rank;
-                    const i64 li = ep.nxt.pix_to_loc(ep.cur.loc_to_pix(row), &rank);
-                    float* xb = ep.xdst[rank];
+                    // DOWN: destination row in the next block's layout, possibly on a peer GPU
+                    // (NVLink); RESID: in place
+                    int rank = 0;
+                    i64 li = row;
+                    float* xb = ep.x;
+                    if constexpr (MODE == EPI_DOWN) {
+                        li = ep.nxt.pix_to_loc(ep.cur.loc_to_pix(row), &rank);
+                        xb = ep.xdst[rank];
+                    }
                     drow = xb + li * ep.h;
                     if (ep.nss) {
                         dbrow = reinterpret_cast<__nv_bfloat16*>(xb + ep.off_xb) + li * ep.hp;
@@ -520,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     normed(v, n_blk * BN + ch * 32);
                     ssum += epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
                 }
-                if constexpr (MODE == EPI_ENCODE || MODE == EPI_RESID)
+                if constexpr (MODE == EPI_ENCODE)
                     if (ep.nss && row < ep.M) ep.x[ep.off_ss + row * ep.nss + 2 * n_blk + half] = ssum;
             }
             tc_fence_before();
