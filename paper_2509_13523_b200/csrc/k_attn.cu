@@ -50,7 +50,7 @@ using namespace tc;
 // 11 K landed, 12 S issued, 13 P V entry, 14 P seen.
 constexpr int kTrN = 1024;
 __device__ unsigned long long g_trace[2][16][kTrN];  // [CTA 0 / 1 of the first cluster]
-__device__ unsigned long long g_trace_w[2][16][kTrN];  // per softmax warp: [cta][warp-4 (S ready) / 8+warp-4 (P done)]
+__device__ unsigned long long g_trace_w[2][32][kTrN];  // per softmax warp: [cta][warp-4 (S ready) / 8+warp-4 (P done)]
 #define SWF_TR(row, idx)                                                                 \
     do {                                                                                 \
         if (blockIdx.x < 2 && (idx) < kTrN) g_trace[blockIdx.x][row][idx] = clock64(); \
@@ -63,7 +63,16 @@ __device__ unsigned long long g_trace_w[2][16][kTrN];  // per softmax warp: [cta
 
 constexpr int BQ = 128;   // queries per CTA tile (= UMMA M, = TMEM lanes)
 constexpr int BKV = 128;  // keys per tile
-constexpr int kThreads = 384;
+// softmax threads per query row (each takes BKV / kSplit keys of every tile); 4 control warps +
+// 4 * kSplit softmax warps. 2 is the default: with 4 (640 threads) the C2 launch is ~5% slower --
+// the softmax is bound by its sub-partition's issue / MUFU throughput, not by per-thread latency
+// (tools/gpu_attn_ab.sh).
+#ifndef SWF_ATTN_SPLIT
+#define SWF_ATTN_SPLIT 2
+#endif
+constexpr int kSplit = SWF_ATTN_SPLIT;
+constexpr int kKPT = 128 / kSplit;  // keys per thread per tile
+constexpr int kThreads = 128 + 128 * kSplit;
 constexpr int kNS = 3;       // S buffers in TMEM
 constexpr uint32_t kBackoffNs = 40;  // poll back-off of the control warps' barrier waits
 constexpr uint32_t kTO = 384;  // TMEM column of O
@@ -78,9 +87,9 @@ struct ACfg {
     static constexpr int kKHalf = (BKV / 2) * D * 2;    // this CTA's 64 keys of a K tile
     static constexpr int kVHalf = (D / 2) * BKV * 2;    // this CTA's d/2 rows of a V^T tile
     static constexpr int kNK = 4, kNV = 4;
-    static constexpr int kRedBytes = 2 * BQ * 4;        // row-max / row-sum exchange between key halves
+    static constexpr int kRedBytes = kSplit * BQ * 4;   // row-max / row-sum exchange between key splits
     static constexpr int kSmem = 2 * kQBytes + kNK * kKHalf + kNV * kVHalf + kRedBytes + 256 + 1024;
-    static constexpr int kOC = D / 2;                   // O columns per key half (epilogue / rescale)
+    static constexpr int kOC = D / kSplit;              // O columns per softmax thread (epilogue / rescale)
     static constexpr uint32_t kIdescS = idesc_bf16(2 * BQ, BKV);
     static constexpr uint32_t kIdescO = idesc_bf16(2 * BQ, D);
 };
@@ -172,9 +181,9 @@ __device__ __forceinline__ void mbar_sleep_wait(uint32_t bar, uint32_t parity) {
         __nanosleep(kBackoffNs);
     }
 }
-// named barrier of the two warps sharing a TMEM lane quadrant (one per key half)
+// named barrier of the kSplit warps sharing a TMEM lane quadrant (one per key split)
 __device__ __forceinline__ void pair_sync(int quadrant) {
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + quadrant) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + quadrant), "r"(32 * kSplit) : "memory");
 }
 
 // TMA tensor store of a 2D box from shared memory (bulk-group completion)
@@ -184,7 +193,7 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int
                  : "memory");
 }
 // all 256 softmax threads
-__device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 5, 256;" ::: "memory"); }
+__device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 5, %0;" ::"r"(128 * kSplit) : "memory"); }
 
 // commit of the pair's MMAs arriving on this CTA's barrier
 __device__ __forceinline__ void commit2(uint32_t bar) {
@@ -332,10 +341,14 @@ __device__ __forceinline__ void issue_s_tile(uint32_t d, uint64_t a, uint64_t b,
 }
 // all P V MMAs of one key tile: P of keys [64h, 64h+64) at S columns [64h, 64h+32); V^T half in
 // two 64-key SW128 boxes of D/2 rows
+// P of keys [KPT s, KPT s + KPT) sits at S columns [KPT s, KPT s + KPT/2): key block kk of 16 keys
+// starts at column KPT * (16 kk / KPT) + (16 kk % KPT) / 2
+__host__ __device__ constexpr int p_col(int kk) { return kKPT * ((16 * kk) / kKPT) + ((16 * kk) % kKPT) / 2; }
 template <int D>
 __device__ __forceinline__ void issue_pv_tile(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
     constexpr int BX = (D / 2) * 128 / 16;  // 16-byte units per V^T box
-    mma2_ts_x8<8, 16, 24, 64, 72, 80, 88, 2, 4, 6, BX, BX + 2, BX + 4, BX + 6>(d, a, b, idesc, acc0);
+    mma2_ts_x8<p_col(1), p_col(2), p_col(3), p_col(4), p_col(5), p_col(6), p_col(7), 2, 4, 6, BX, BX + 2, BX + 4,
+               BX + 6>(d, a, b, idesc, acc0);
 }
 
 __device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
@@ -374,7 +387,14 @@ __device__ __forceinline__ unsigned long long ex2_poly2(unsigned long long z) {
 // this thread's OC = D/2 O columns (TMEM address t): scale in place / read out
 template <int OC>
 __device__ __forceinline__ void o_scale(uint32_t t, float f) {
-    if constexpr (OC == 16) {
+    if constexpr (OC == 8) {
+        uint32_t o[8];
+        ld8(t, o);
+        wait_ld_dep8(o);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+        st8(t, o);
+    } else if constexpr (OC == 16) {
         uint32_t o[16];
         ld16(t, o);
         wait_ld_dep16(o);
@@ -405,7 +425,17 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const uint32_t
 }
 template <int OC>
 __device__ __forceinline__ void o_store(uint32_t t, __nv_bfloat16* dst, float inv, bool valid) {
-    if constexpr (OC == 16) {
+    if constexpr (OC == 8) {
+        uint32_t o[8];
+        ld8(t, o);
+        wait_ld_dep8(o);
+        if (valid)
+            *reinterpret_cast<uint4*>(dst) =
+                make_uint4(pack_bf16x2(__uint_as_float(o[0]) * inv, __uint_as_float(o[1]) * inv),
+                           pack_bf16x2(__uint_as_float(o[2]) * inv, __uint_as_float(o[3]) * inv),
+                           pack_bf16x2(__uint_as_float(o[4]) * inv, __uint_as_float(o[5]) * inv),
+                           pack_bf16x2(__uint_as_float(o[6]) * inv, __uint_as_float(o[7]) * inv));
+    } else if constexpr (OC == 16) {
         uint32_t o[16];
         ld16(t, o);
         wait_ld_dep16(o);
@@ -455,7 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < kNS; ++i) {
             mbar_init(bar(B_SF + i), 1);
-            mbar_init(bar(B_PF + i), 16);  // leader's: the softmax warps of both CTAs
+            mbar_init(bar(B_PF + i), 2 * 4 * kSplit);  // leader's: the softmax warps of both CTAs
             mbar_init(bar(B_PVD + i), 1);   // leader's: P V of this buffer complete
         }
         for (int i = 0; i < C::kNK; ++i) {
@@ -467,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_init(bar(B_VE + i), 1);
         }
         mbar_init(bar(B_OD), 1);
-        mbar_init(bar(B_OF), 16);  // leader's: the epilogue warps of both CTAs
+        mbar_init(bar(B_OF), 2 * 4 * kSplit);  // leader's: the epilogue warps of both CTAs
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -481,7 +511,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     // register rebalancing within the 168 x 384 launch allocation: the control warpgroup drops to 72,
     // the softmax warpgroups rise to 216 (128 x (168 - 72) >= 256 x (216 - 168), else the increase blocks)
-    if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    if constexpr (kSplit == 2)
+        if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
 
     if (warp == 0) {
         // ===== TMA producer 1: Q (double-buffered across work items) and the K ring
@@ -588,9 +619,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // ===== softmax (two threads per query row, 64 keys each) + epilogue
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
-        const int hk = (warp - 4) >> 2;  // key half of every tile
+        // ===== softmax (kSplit threads per query row, kKPT keys each) + epilogue
+        if constexpr (kSplit == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+        const int hk = (warp - 4) >> 2;  // key split of every tile
         const int wq = warp & 3;         // TMEM lane quadrant
         const int r = wq * 32 + lane;
         const uint32_t lane_off = uint32_t(wq * 32) << 16;
@@ -619,7 +650,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             float m = -INFINITY, l = 0.f;
             for (int j = 0; j < rg.ntiles; ++j, ++g) {
                 const int b = g % kNS;
-                const uint32_t tS = lane_off + uint32_t(b * 128 + hk * 64);
+                const uint32_t tS = lane_off + uint32_t(b * 128 + hk * kKPT);
                 mbar_wait(bar(B_SF + b), (g / kNS) & 1);
                 fence_after();
                 if (tr) SWF_TR(0, g);
@@ -634,25 +665,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 l = 1.f;
                 continue;
 #endif
-                uint32_t sa[64];
-                ld32(tS, sa);
-                ld32(tS + 32u, sa + 32);
-                wait_ld_dep(sa);
-                wait_ld_dep(sa + 32);
-                const int kb = (rg.t_lo + j) * BKV + hk * 64;
-                if (kb < rlo || kb + 64 > rhi) {  // boundary tile: mask keys outside [rlo, rhi)
+                uint32_t sa[kKPT];
 #pragma unroll
-                    for (int i = 0; i < 64; ++i)
+                for (int c = 0; c < kKPT / 32; ++c) ld32(tS + uint32_t(32 * c), sa + 32 * c);
+#pragma unroll
+                for (int c = 0; c < kKPT / 32; ++c) wait_ld_dep(sa + 32 * c);
+                const int kb = (rg.t_lo + j) * BKV + hk * kKPT;
+                if (kb < rlo || kb + kKPT > rhi) {  // boundary tile: mask keys outside [rlo, rhi)
+#pragma unroll
+                    for (int i = 0; i < kKPT; ++i)
                         if (kb + i < rlo || kb + i >= rhi) sa[i] = __float_as_uint(-INFINITY);
                 }
                 float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int i = 0; i < 64; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sa[i]));
+                for (int i = 0; i < kKPT; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sa[i]));
                 const float pm = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
                 red[hk * BQ + r] = pm;
                 pair_sync(wq);
-                const float mx = fmaxf(pm, red[(1 - hk) * BQ + r]) * sl2;
-                pair_sync(wq);  // both halves read before the next exchange overwrites
+                float mxr = red[r];
+#pragma unroll
+                for (int k2 = 1; k2 < kSplit; ++k2) mxr = fmaxf(mxr, red[k2 * BQ + r]);
+                const float mx = mxr * sl2;
+                pair_sync(wq);  // every split read before the next exchange overwrites
                 if (tr) SWF_TR(1, g);
                 // both halves take the same rescale decision (same mx, same m)
                 if (mx > m + kRescale || (m == -INFINITY && mx != -INFINITY)) {
@@ -670,7 +704,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const unsigned long long sl2x2 = f2_pack(sl2, sl2), nbx2 = f2_pack(nb, nb);
                 unsigned long long ls2 = 0ull, ls2b = 0ull;
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {  // 32 keys -> 16 packed bf16x2 columns per store
+                for (int c = 0; c < kKPT / 32; ++c) {  // 32 keys -> 16 packed bf16x2 columns per store
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -698,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (tr) SWF_TR(3, g);
 #ifdef SWF_ATTN_TRACE
-                if (lane == 0 && blockIdx.x < 2 && g < kTrN) g_trace_w[blockIdx.x][8 + warp - 4][g] = clock64();
+                if (lane == 0 && blockIdx.x < 2 && g < kTrN) g_trace_w[blockIdx.x][16 + warp - 4][g] = clock64();
 #endif
                 if (lane == 0) mbar_arrive_cluster(lbar(B_PF + b));
                 if (leader) release_q();  // the previous item's O store has long finished reading
@@ -709,21 +743,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (tr) SWF_TR(8, n);
             red[hk * BQ + r] = l;
             pair_sync(wq);
-            const float inv = 1.f / (l + red[(1 - hk) * BQ + r]);
+            float lt = 0.f;
+#pragma unroll
+            for (int k2 = 0; k2 < kSplit; ++k2) lt += red[k2 * BQ + r];  // fixed order: deterministic
+            const float inv = 1.f / lt;
             pair_sync(wq);
             const int qb = n & 1;
             if (D >= 64 && p.tmo != nullptr && it.q0 + BQ <= s) {  // (p.tmo: host flag; the map is tmO)
                 // whole tile, own rows lw*s + q0 ..: stage in this item's Q buffer (SW128, the TMA
                 // box layout) and store with TMA
                 uint8_t* stg = sQ + qb * C::kQBytes;
+                constexpr int CW = C::kOC < 32 ? C::kOC : 32;  // columns per TMEM load
 #pragma unroll 1
-                for (int c = 0; c < C::kOC / 32; ++c) {
+                for (int c = 0; c < C::kOC / CW; ++c) {
                     uint32_t o[32];
-                    ld32(tO + uint32_t(c * 32), o);
-                    wait_ld_dep(o);
+                    if constexpr (CW == 32) {
+                        ld32(tO + uint32_t(c * 32), o);
+                        wait_ld_dep(o);
+                    } else {
+                        ld16(tO + uint32_t(c * 16), o);
+                        wait_ld_dep16(o);
+                    }
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int col = hk * C::kOC + c * 32 + v * 8;  // first of 8 bf16 = one 16-byte chunk
+                    for (int v = 0; v < CW / 8; ++v) {
+                        const int col = hk * C::kOC + c * CW + v * 8;  // first of 8 bf16 = one 16-byte chunk
                         const int ch = (col & 63) >> 3;
                         uint4* dst = reinterpret_cast<uint4*>(stg + (col >> 6) * (BQ * 128) + r * 128 +
                                                               ((ch ^ (r & 7)) << 4));
