@@ -71,6 +71,12 @@ constexpr int BKV = 128;  // keys per tile
 #define SWF_ATTN_SPLIT 2
 #endif
 constexpr int kSplit = SWF_ATTN_SPLIT;
+#ifndef SWF_ATTN_POLY8
+#define SWF_ATTN_POLY8 2
+#endif
+// exponentials per 8 evaluated by the FMA-pipe polynomial: 0..2 of 8 measured equal within noise and
+// ~5% faster / ~25% less energy than 4 of 8 (tools/gpu_attn_poly.sh)
+constexpr int kPoly8 = SWF_ATTN_POLY8;
 constexpr int kKPT = 128 / kSplit;  // keys per thread per tile
 constexpr int kThreads = 128 + 128 * kSplit;
 constexpr int kNS = 3;       // S buffers in TMEM
@@ -712,7 +718,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             (unsigned long long)sa[32 * c + 2 * i] | ((unsigned long long)sa[32 * c + 2 * i + 1] << 32);
                         const unsigned long long z = ffma2(sv, sl2x2, nbx2);
                         unsigned long long pv;
-                        if ((i & 7) < 3)  // 3/8 of the exponentials on the FMA pipe
+                        if ((i & 7) < kPoly8)  // kPoly8/8 of the exponentials on the FMA pipe
                             pv = ex2_poly2(z);
                         else
                             pv = f2_pack(ex2(lo_f(z)), ex2(hi_f(z)));
