@@ -12,10 +12,10 @@
 //     the softmax warps find the next S ready when they finish a tile;
 //   * softmax (per CTA): 8 warps, each TMEM lane (query row) is shared by two threads that take 64
 //     keys each (the row maximum is exchanged through shared memory); base-2 online max/sum with lazy
-//     O rescaling (only when the running max grows by > 2^8), packed f32x2 arithmetic, 3/8 of the
-//     exponentials on the FMA pipe (degree-3 polynomial) and 5/8 on MUFU (sm_100 has no packed
-//     BF16x2 MUFU: ex2.approx.bf16x2 compiles to two scalar MUFU ops); P is packed to BF16 into the
-//     first 32 columns of each thread's 64-column S slice;
+//     O rescaling (only when the running max grows by > 2^8), packed f32x2 arithmetic, kPoly8/8 of
+//     the exponentials on the FMA pipe (degree-3 polynomial) and the rest on MUFU (sm_100 has no
+//     packed BF16x2 MUFU: ex2.approx.bf16x2 compiles to two scalar MUFU ops); P is packed to BF16
+//     into the first columns of each thread's S slice;
 //   * O += P V : M=256, N=d, A = P read from TMEM, B = V^T (K-major, written transposed by the QKV
 //     GEMM epilogue); O accumulates in TMEM. S(j+3) is issued only after P(j) V completed;
 //   * epilogue: O / l in BF16 is staged in the finished item's Q buffer (SW128) and written by TMA
