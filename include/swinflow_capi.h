@@ -127,6 +127,30 @@ int swf_forward_device(swf_ctx* ctx, const float* d_input, double t, float* d_ou
  * recomputed from them in the backward (no s x s probabilities are stored). */
 int swf_backward(swf_ctx* ctx, const void* input, double t, const void* d_output, void* grads, void* d_input,
                  int dtype);
+
+/* LossWeights (grid.hpp:76-96): alpha_row = per-row latitude weights (H entries, unit mean),
+ * kappa = per-variable weights (C_out entries, > 0); element type given by the call's dtype. */
+typedef struct swf_loss_weights {
+    const void *alpha_row, *kappa;
+} swf_loss_weights;
+/* diffusion_loss_sample(p, sb, w, dc, t_key, z, pos_enc, H, W) (diffusion.hpp:168-192), FP32
+ * validation mode, one rank: t from sample_noise_draw(t_key), x_t / v_t from the standardized
+ * residual target x0 (C_out x N) and noise z (C_out x N), the weighted v-prediction loss into *loss
+ * and, if grads is not NULL, the parameter gradients (canonical order, swf_param_count elements). */
+int swf_diffusion_loss_sample(swf_ctx* ctx, const void* x_prev, const void* x0, const void* forcings,
+                              const swf_loss_weights* w, const swf_diffusion_cfg* dc, uint64_t t_key, const void* z,
+                              double* loss, void* grads, int dtype);
+/* One microbatch of reference_train_step (simulator.hpp:50-86): z = noise_field(seeds, sample_id)
+ * and t_key = SeedProtocol::t_key(sample_id) (rng.hpp:72-80) for run_seed, loss into *loss, the
+ * gradient added to the device accumulator. swf_train_reset zeroes it; swf_train_grads exposes it
+ * (FP32 device pointer + element count) for an in-place all-reduce across data-parallel ranks;
+ * swf_train_read copies it out multiplied by scale. */
+int swf_train_accumulate(swf_ctx* ctx, const void* x_prev, const void* x0, const void* forcings,
+                         const swf_loss_weights* w, const swf_diffusion_cfg* dc, uint64_t run_seed,
+                         uint64_t sample_id, double* loss, int dtype);
+int swf_train_reset(swf_ctx* ctx);
+int swf_train_grads(swf_ctx* ctx, float** dev_ptr, long long* n);
+int swf_train_read(swf_ctx* ctx, double scale, void* grads, int dtype);
 int swf_sync(swf_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) for callers that enqueue their own copies. */
 void* swf_stream(swf_ctx* ctx);
@@ -184,6 +208,10 @@ long long swf_kernel_launches(swf_ctx* ctx);
  * launch while enabled. Classes: 0 encode GEMM, 1 RMS+AdaLN, 2 QKV GEMM, 3 attention, 4 out GEMM,
  * 5 gate/up GEMM, 6 down GEMM, 7 decode GEMM, 8 other. swf_profile resets the counters. */
 int swf_profile(swf_ctx* ctx, int enable);
+/* CUDA-graph replay of the sampler's 2*S evaluations (default on; not a reference interface):
+ * the first solve with a diffusion config runs eagerly, the second captures, later ones replay.
+ * Disabled while profiling or while the forward saves activations. */
+int swf_set_graphs(swf_ctx* ctx, int enable);
 int swf_profile_read(swf_ctx* ctx, double* ms, long long* launches, int n_classes);
 int swf_profile_launches(swf_ctx* ctx, int* classes, double* ms, int max_n, int* n_out);
 /* Replay one kernel class (1..6 above) reps times back-to-back on the resident buffers of the

@@ -353,6 +353,58 @@ def solve_net(cfg: ModelConfig, params, H, W, x_init, x_prev_std, forc_std, sigm
     return out, fe.value
 
 
+# ------------------------------------------------------------------ training loss (diffusion.hpp:111-192)
+def latitude_weights(H: int) -> np.ndarray:
+    """grid.hpp:17-82: cos(latitude of each row centre), scaled to unit mean."""
+    d = 180.0 / H
+    w = np.cos((90.0 - d * (np.arange(H) + 0.5)) * np.pi / 180.0)
+    return w * (H / w.sum())
+
+
+def noise_draw_from_u(u: float, sigma_d=1.0, sigma_min=0.2, sigma_max=500.0) -> float:
+    """noise_draw_from_u (diffusion.hpp:76-82): tau log-uniform in [log sigma_min, log sigma_max]."""
+    tau = (1.0 - u) * np.log(sigma_min) + u * np.log(sigma_max)
+    return float(np.arctan(np.exp(tau) / sigma_d))
+
+
+def noise_draw_t(t_key: int, sigma_d=1.0, sigma_min=0.2, sigma_max=500.0) -> float:
+    """sample_noise_draw (diffusion.hpp:84-86): u = uniform01(t_key, 0)."""
+    return noise_draw_from_u(lib().orc_uniform01(t_key, 0), sigma_d, sigma_min, sigma_max)
+
+
+def weighted_sq_loss(err, alpha_row, kappa, W):
+    """weighted_sq_loss (diffusion.hpp:111-123) and its gradient (:125-133); err is [N][C]."""
+    N = err.shape[0]
+    alpha = np.repeat(np.asarray(alpha_row, err.dtype), W)[:, None]
+    kap = np.asarray(kappa, err.dtype)[None, :]
+    if kap.shape[1] != err.shape[1]:
+        raise ValueError("loss: kappa size does not match channels")
+    loss = float((alpha * kap * err * err).sum() / N)
+    return loss, (2.0 * alpha / N) * kap * err
+
+
+def loss_sample(cfg: ModelConfig, params, H, W, x_prev, x0, forc, alpha_row, kappa, t_key, z, sigma_d=1.0,
+                sigma_min=0.2, sigma_max=500.0):
+    """diffusion_loss_sample (diffusion.hpp:168-192) over the oracle forward / backward: fields are
+    [N][C] numpy arrays; returns (loss, parameter gradients in canonical order)."""
+    dt = params.dtype
+    t = noise_draw_t(t_key, sigma_d, sigma_min, sigma_max)
+    t = dt.type(t)
+    c, s = (1.0, 0.0) if t == 0 else (np.cos(t), np.sin(t))
+    x0 = np.asarray(x0, dt)
+    z = np.asarray(z, dt)
+    xt = c * x0 + s * z
+    v = c * z - s * x0
+    inp = np.concatenate([xt / dt.type(sigma_d), np.asarray(x_prev, dt), np.asarray(forc, dt)], axis=1)
+    inp = inp + posenc(H, W, cfg.in_channels, dt)
+    f = forward(cfg, params, inp, float(t), H, W)
+    err = dt.type(sigma_d) * f - v
+    loss, gerr = weighted_sq_loss(err, alpha_row, kappa, W)
+    dout = dt.type(sigma_d) * gerr
+    g, _ = backward(cfg, params, inp, float(t), H, W, dout)
+    return loss, g
+
+
 def fnv1a64(data: bytes, h: int = 0xcbf29ce484222325) -> int:
     """src/chunked_file.cpp:33-41"""
     for b in data:

@@ -83,6 +83,10 @@ class _DCfg(C.Structure):
                 ("solver_steps", C.c_int), ("churn", C.c_double)]
 
 
+class _LW(C.Structure):
+    _fields_ = [("alpha_row", C.c_void_p), ("kappa", C.c_void_p)]
+
+
 class _Std(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("state_mean", "state_std", "resid_mean", "resid_std", "forcing_mean",
                                           "forcing_std")]
@@ -137,11 +141,17 @@ def lib():
         L.swf_kernel_launches.restype = ll
         L.swf_bench_kernel.argtypes = [vp, i, i, i, C.POINTER(d)]
         L.swf_profile.argtypes = [vp, i]
+        L.swf_set_graphs.argtypes = [vp, i]
         L.swf_profile_read.argtypes = [vp, vp, vp, i]
         L.swf_profile_launches.argtypes = [vp, vp, vp, i, C.POINTER(i)]
         L.swf_noise_field.argtypes = [vp, u64, u64, i, d, vp]
         L.swf_selftest_gemm.argtypes = [i, ll, i, i, C.POINTER(d), C.POINTER(d)]
         L.swf_backward.argtypes = [vp, vp, d, vp, vp, vp, i]
+        L.swf_diffusion_loss_sample.argtypes = [vp, vp, vp, vp, vp, vp, u64, vp, C.POINTER(d), vp, i]
+        L.swf_train_accumulate.argtypes = [vp, vp, vp, vp, vp, vp, u64, u64, C.POINTER(d), i]
+        L.swf_train_reset.argtypes = [vp]
+        L.swf_train_grads.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(ll)]
+        L.swf_train_read.argtypes = [vp, d, vp, i]
         L.swf_prefetch_chunked.argtypes = [vp, C.c_char_p, C.c_char_p]
         L.swf_forecast_step_chunked.argtypes = [vp, C.c_char_p, C.c_char_p, vp, vp, u64, u64, vp, i]
         L.swf_last_chunk_reads.argtypes = [vp]
@@ -272,6 +282,10 @@ class Denoiser:
     KERNEL_CLASSES = ("encode_gemm", "rms_adaln", "qkv_gemm", "attention", "out_gemm", "gateup_gemm",
                       "down_gemm", "decode_gemm", "other")
 
+    def set_graphs(self, enable: bool = True):
+        """CUDA-graph replay of the sampler's evaluations (default on)."""
+        _check(lib().swf_set_graphs(self._c, int(enable)))
+
     def profile(self, enable: bool = True):
         _check(lib().swf_profile(self._c, int(enable)))
 
@@ -346,6 +360,64 @@ class Denoiser:
         din = np.zeros_like(inp) if want_input_grad else None
         _check(lib().swf_backward(self._c, _p(inp), t, _p(dout), _p(g), _p(din), _dt(inp)))
         return g, din
+
+    # ---- training (diffusion.hpp:168-192, simulator.hpp:50-86; FP32 validation mode)
+    def _lw(self, w, dt):
+        a = np.ascontiguousarray(w.alpha_row, dt)
+        k = np.ascontiguousarray(w.kappa, dt)
+        if a.shape != (self.H,) or k.shape != (self.cfg.out_channels,):
+            raise ConfigError(ERR_CONFIG, "loss weights: alpha_row needs H entries and kappa C_out entries")
+        return _LW(_p(a), _p(k)), (a, k)
+
+    def _train_fields(self, x_prev, x0, forcings, dt):
+        f = [np.ascontiguousarray(v, dt) for v in (x_prev, x0)]
+        fo = None if forcings is None else np.ascontiguousarray(forcings, dt)
+        return f[0], f[1], fo
+
+    def diffusion_loss_sample(self, x_prev, x0, forcings, w, dc: DiffusionConfig, t_key: int, z,
+                              want_grads: bool = True):
+        """(loss, parameter gradients) of diffusion_loss_sample for one standardized sample."""
+        dt = np.asarray(x0).dtype if np.asarray(x0).dtype in (np.float32, np.float64) else np.float32
+        xp, x0_, fo = self._train_fields(x_prev, x0, forcings, dt)
+        zz = np.ascontiguousarray(z, dt)
+        lw, keep = self._lw(w, dt)
+        loss = C.c_double(0)
+        g = np.zeros(param_count(self.cfg), dt) if want_grads else None
+        _check(lib().swf_diffusion_loss_sample(self._c, _p(xp), _p(x0_), _p(fo), C.byref(lw),
+                                               C.byref(_DCfg(*astuple(dc))), t_key, _p(zz), C.byref(loss), _p(g),
+                                               _dt(x0_)))
+        return loss.value, g
+
+    def train_reset(self):
+        _check(lib().swf_train_reset(self._c))
+
+    def train_accumulate(self, x_prev, x0, forcings, w, dc: DiffusionConfig, run_seed: int, sample_id: int) -> float:
+        """One microbatch (noise and t from the seed protocol); gradient added on the device."""
+        dt = np.asarray(x0).dtype if np.asarray(x0).dtype in (np.float32, np.float64) else np.float32
+        xp, x0_, fo = self._train_fields(x_prev, x0, forcings, dt)
+        lw, keep = self._lw(w, dt)
+        loss = C.c_double(0)
+        _check(lib().swf_train_accumulate(self._c, _p(xp), _p(x0_), _p(fo), C.byref(lw),
+                                          C.byref(_DCfg(*astuple(dc))), run_seed, sample_id, C.byref(loss),
+                                          _dt(x0_)))
+        return loss.value
+
+    def train_grads_device(self):
+        """(device pointer, element count) of the FP32 gradient accumulator."""
+        ptr, n = C.c_void_p(), C.c_longlong()
+        _check(lib().swf_train_grads(self._c, C.byref(ptr), C.byref(n)))
+        return int(ptr.value), int(n.value)
+
+    def train_read(self, scale: float = 1.0, dtype=np.float64) -> np.ndarray:
+        g = np.zeros(param_count(self.cfg), dtype)
+        _check(lib().swf_train_read(self._c, scale, _p(g), _dt(g)))
+        return g
+
+    def train_step(self, data, first_sample: int, dp: int, gas: int, w, dc: DiffusionConfig, run_seed: int,
+                   group=None):
+        """reference_train_step with data-parallel replicas on ranks (see train.py)."""
+        from .train import train_step
+        return train_step(self, data, first_sample, dp, gas, w, dc, run_seed, group)
 
     # ---- per-rank input loading from chunked containers (chunked_file.cpp:156-188)
     def prefetch_chunked(self, state_path: str, forcing_path: str | None = None):
@@ -453,3 +525,4 @@ def exported_symbols() -> list[str]:
     import re
     src = open(HEADER).read()
     return sorted(set(re.findall(r"\b(swf_[a-z0-9_]+)\s*\(", src)))
+from .train import DataSet, LossWeights, TrainStepResult, latitude_weights  # noqa: E402,F401

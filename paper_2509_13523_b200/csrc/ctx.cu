@@ -105,7 +105,7 @@ struct swf_ctx {
     int** d_flag_table = nullptr;    // device table: flag array of every rank (peer-mapped)
     void** d_qkv_dst = nullptr;      // device table: attention planes of every rank
     void** d_o_dst = nullptr;        // device table: attention-output (xm) buffer of every rank
-    int bar_epoch = 0;
+    int* d_epoch = nullptr;          // device barrier epoch (advanced by k_peer_barrier; graph-safe)
     // TMA maps (BF16 path)
     TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec, tm_q, tm_k, tm_vt;
     TmaMap tm_so;  // sbuf viewed as [M][hp] (attention output of the kernel benchmark)
@@ -148,6 +148,13 @@ struct swf_ctx {
             *rms, *d6, *demb, *zero, *gflat, *din;
     } bw = {};
     bool bw_alloc = false;
+    // diffusion training loss (FP32 validation mode): residual target x0, noise z, velocity target v,
+    // loss weights, per-block loss partials, and the gradient accumulator of the training step
+    struct Train {
+        float *x0, *z, *v, *kappa, *alpha, *gacc;
+        double *part, *h_part;
+    } tr = {};
+    bool tr_alloc = false;
     // per-kernel-class CUDA-event timing (bench roofline): class id -> accumulated ms / launches
     bool prof = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
@@ -155,6 +162,16 @@ struct swf_ctx {
     size_t ev_used = 0;
     double prof_ms[16] = {0};
     long long prof_n[16] = {0};
+    // CUDA graph of solve_pf_ode's 2*S evaluations (+ sampler updates and churn), keyed on the
+    // diffusion config; the churn key is read from device memory so one graph serves every
+    // member / step of a rollout. First call with a new key runs eagerly, the second captures.
+    bool graphs = true;
+    cudaGraphExec_t solve_exec = nullptr;
+    swf_diffusion_cfg graph_dc = {};
+    int graph_seen = 0;  // 1: key seen once (eager), 2: captured
+    long long graph_launches = 0;
+    u64* d_churn_key = nullptr;
+    u64* h_churn_key = nullptr;  // pinned staging
 };
 
 namespace {
@@ -395,6 +412,9 @@ void allocate(swf_ctx* c) {
     // destination tables for the fused down-projection store (own buffer unless peers connect)
     c->bar_flags = dalloc<int>(c, 64);
     c->d_flag_table = dalloc<int*>(c, 8);
+    c->d_epoch = dalloc<int>(c, 1);
+    c->d_churn_key = dalloc<u64>(c, 1);
+    SWF_CUDA(cudaMallocHost(&c->h_churn_key, sizeof(u64)));
     c->peer.assign(c->world, Peer{{nullptr, nullptr}, nullptr, nullptr, nullptr});
     c->peer[c->rank].x[0] = c->xbuf[0];
     c->peer[c->rank].x[1] = c->xbuf[1];
@@ -1185,8 +1205,11 @@ void check_flags(swf_ctx* c) {
 // waiting blocks never share an SM with the blocks they wait for). Each rank release-stores the
 // epoch into its slot of every peer's flag array, then acquire-polls its own slots. Stream order
 // places it after the down-projection whose epilogue stored rows into peer residual buffers.
-__global__ void k_peer_barrier(int* const* flags, int rank, int world, int epoch, int* err) {
+__global__ void k_peer_barrier(int* const* flags, int rank, int world, int* epoch_ctr, int* err) {
+    __shared__ int epoch;
     const int t = threadIdx.x;
+    if (t == 0) epoch = *epoch_ctr + 1;  // every rank runs the same barrier sequence
+    __syncthreads();
     if (t < world) {
         __threadfence_system();
         int* remote = flags[t] + rank;
@@ -1206,13 +1229,12 @@ __global__ void k_peer_barrier(int* const* flags, int rank, int world, int epoch
         }
     }
     __syncthreads();
+    if (t == 0) *epoch_ctr = epoch;
 }
 
 void peer_barrier(swf_ctx* c) {
     if (!c->peers) throw ConfigError("multi-rank topology: call swf_connect_peers before running");
-    ++c->bar_epoch;
-    k_peer_barrier<<<1, 32, 0, c->st>>>(c->d_flag_table, c->rank, c->world, c->bar_epoch,
-                                        c->flags + (c->nflags - 1));
+    k_peer_barrier<<<1, 32, 0, c->st>>>(c->d_flag_table, c->rank, c->world, c->d_epoch, c->flags + (c->nflags - 1));
     SWF_LAUNCH_CHECK();
     c->launches++;
 }
@@ -1289,8 +1311,9 @@ static std::pair<float, float> trig_coeffs_f(float t) {  // diffusion.hpp:50-55 
 }
 
 // solve_pf_ode (diffusion.hpp:207-272) on the state c->s_x (local window order, [M][C_out]).
-void solve(swf_ctx* c, const swf_diffusion_cfg& dc, u64 churn_key, int* f_evals) {
-    validate_dc(dc);
+// Enqueues the 2*S net evaluations, sampler updates and churn rotations on c->st; every scalar is a
+// function of dc alone (the churn key is read from c->d_churn_key), so the sequence can be captured.
+void enqueue_solve(swf_ctx* c, const swf_diffusion_cfg& dc) {
     const Dims& m = c->m;
     const i64 n = c->M * m.cout;
     const int S = dc.solver_steps;
@@ -1303,7 +1326,6 @@ void solve(swf_ctx* c, const swf_diffusion_cfg& dc, u64 churn_key, int* f_evals)
     }
     double t_cur = t_of(sigma[0]), sig_cur = sigma[0];
     u64 churn_ctr = 0;
-    int fe = 0;
     for (int k = 0; k < S; ++k) {
         const double sig_next = sigma[k + 1], t_next = t_of(sig_next);
         const double sig_mid = std::sqrt(sig_cur * sig_next), t_mid = t_of(sig_mid);
@@ -1322,7 +1344,6 @@ void solve(swf_ctx* c, const swf_diffusion_cfg& dc, u64 churn_key, int* f_evals)
         const double r = sig_next / sig_cur;
         sampler_update(c->s_x, c->s_xmid, c->out_loc, n, cs2.first, cs2.second, float(b_t / b_s),
                        float(a_t * (r - 1.0)), c->s_x, c->flags, m.nb + 2 + std::min(k, 4000), c->st);
-        fe += 2;
         c->launches += 2;
         t_cur = t_next;
         sig_cur = sig_next;
@@ -1330,7 +1351,7 @@ void solve(swf_ctx* c, const swf_diffusion_cfg& dc, u64 churn_key, int* f_evals)
         if (active && k + 1 < S) {
             const double delta = dc.churn * 0.05 * (t_of(sigma[k]) - t_next);
             if (delta > 0) {
-                churn_rotate(c->s_x, c->lay[0], c->M, m.cout, churn_key, churn_ctr, sd, float(std::cos(delta)),
+                churn_rotate(c->s_x, c->lay[0], c->M, m.cout, c->d_churn_key, churn_ctr, sd, float(std::cos(delta)),
                              float(std::sin(delta)), c->st);
                 churn_ctr += u64(c->N) * m.cout;
                 t_cur += delta;
@@ -1339,7 +1360,52 @@ void solve(swf_ctx* c, const swf_diffusion_cfg& dc, u64 churn_key, int* f_evals)
             }
         }
     }
-    if (f_evals) *f_evals = fe;
+}
+
+static bool same_dc(const swf_diffusion_cfg& a, const swf_diffusion_cfg& b) {
+    return a.sigma_d == b.sigma_d && a.sigma_min == b.sigma_min && a.sigma_max == b.sigma_max &&
+           a.solver_steps == b.solver_steps && a.churn == b.churn;
+}
+
+void solve(swf_ctx* c, const swf_diffusion_cfg& dc, u64 churn_key, int* f_evals) {
+    validate_dc(dc);
+    if (f_evals) *f_evals = 2 * dc.solver_steps;
+    // stream-ordered: the previous solve's churn kernels read the key before this copy lands
+    *c->h_churn_key = churn_key;
+    SWF_CUDA(cudaMemcpyAsync(c->d_churn_key, c->h_churn_key, sizeof(u64), cudaMemcpyHostToDevice, c->st));
+    SWF_CUDA(cudaStreamSynchronize(c->st));  // pinned staging reused by the next call
+    const bool use_graph = c->graphs && !c->prof && !c->save_x;
+    if (!use_graph || !same_dc(dc, c->graph_dc) || c->graph_seen == 0) {
+        if (c->solve_exec) {
+            SWF_CUDA(cudaGraphExecDestroy(c->solve_exec));
+            c->solve_exec = nullptr;
+        }
+        c->graph_dc = dc;
+        c->graph_seen = use_graph ? 1 : 0;
+        enqueue_solve(c, dc);
+        return;
+    }
+    if (c->graph_seen == 1) {  // second call with this config: capture once
+        const long long l0 = c->launches;
+        cudaGraph_t g = nullptr;
+        SWF_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_solve(c, dc);
+        } catch (...) {
+            cudaStreamEndCapture(c->st, &g);
+            if (g) cudaGraphDestroy(g);
+            c->graph_seen = 0;
+            throw;
+        }
+        SWF_CUDA(cudaStreamEndCapture(c->st, &g));
+        SWF_CUDA(cudaGraphInstantiate(&c->solve_exec, g, 0));
+        SWF_CUDA(cudaGraphDestroy(g));
+        c->graph_launches = c->launches - l0;
+        c->launches = l0;
+        c->graph_seen = 2;
+    }
+    SWF_CUDA(cudaGraphLaunch(c->solve_exec, c->st));
+    c->launches += c->graph_launches;
 }
 
 // host-side helpers: host [N][C] (f32/f64) <-> device pixel staging
@@ -1551,6 +1617,110 @@ int fail(const std::exception& e, int rc) {
     return rc;
 }
 
+// ------------------------------------------------------------------ training loss + step
+// diffusion_loss_sample (diffusion.hpp:168-192) and the microbatch loop of reference_train_step
+// (simulator.hpp:50-86) in the FP32 validation mode on one rank; the DP all-reduce of the
+// accumulated gradient runs over NCCL on the device buffer (swf_train_grads).
+void ensure_train(swf_ctx* c) {
+    ensure_sampler(c);
+    ensure_bwd(c);
+    if (c->tr_alloc) return;
+    const Dims& m = c->m;
+    const size_t n = size_t(c->M) * m.cout;
+    auto& t = c->tr;
+    t.x0 = dalloc<float>(c, n);
+    t.z = dalloc<float>(c, n);
+    t.v = dalloc<float>(c, n);
+    t.kappa = dalloc<float>(c, size_t(m.cout));
+    t.alpha = dalloc<float>(c, size_t(c->H));
+    t.gacc = dalloc<float>(c, c->poff.back());
+    t.part = dalloc<double>(c, kTrainLossBlocks);
+    SWF_CUDA(cudaMallocHost(&t.h_part, sizeof(double) * kTrainLossBlocks));
+    c->tr_alloc = true;
+}
+
+double h_uniform01(u64 key, u64 ctr) {  // rng.hpp:28-35
+    return double(h_splitmix(key + 0x632be59bd9b4e019ULL * (ctr + 1)) >> 11) * 0x1.0p-53;
+}
+
+void set_loss_weights(swf_ctx* c, const swf_loss_weights* w, int dtype) {
+    require(w && w->alpha_row && w->kappa, "loss weights: alpha_row and kappa required");
+    const Dims& m = c->m;
+    std::vector<float> kap(m.cout), al(c->H);
+    for (int i = 0; i < m.cout; ++i) {
+        kap[i] = dtype == SWF_F64 ? float(static_cast<const double*>(w->kappa)[i]) : static_cast<const float*>(w->kappa)[i];
+        if (!(kap[i] > 0.f)) throw ConfigError("loss weights: kappa must be positive");  // grid.hpp:87
+    }
+    for (int r = 0; r < c->H; ++r)
+        al[r] = dtype == SWF_F64 ? float(static_cast<const double*>(w->alpha_row)[r])
+                                 : static_cast<const float*>(w->alpha_row)[r];
+    SWF_CUDA(cudaMemcpyAsync(c->tr.kappa, kap.data(), kap.size() * 4, cudaMemcpyHostToDevice, c->st));
+    SWF_CUDA(cudaMemcpyAsync(c->tr.alpha, al.data(), al.size() * 4, cudaMemcpyHostToDevice, c->st));
+    SWF_CUDA(cudaStreamSynchronize(c->st));
+}
+
+// One sample: x_prev in s_tmp, forcings in s_cond, x0 and z in tr (local layout-0 order). Gradient
+// into bw.gflat; returns the loss.
+double train_sample_core(swf_ctx* c, const swf_diffusion_cfg& dc, u64 t_key) {
+    validate_dc(dc);
+    const Dims& m = c->m;
+    const i64 n = c->M * m.cout;
+    const double u = h_uniform01(t_key, 0);  // sample_noise_draw (diffusion.hpp:76-86)
+    const double tau = (1.0 - u) * std::log(dc.sigma_min) + u * std::log(dc.sigma_max);
+    const float t = static_cast<float>(std::atan(std::exp(tau) / dc.sigma_d));
+    const float sd = static_cast<float>(dc.sigma_d);
+    const auto cs = trig_coeffs_f(t);
+    reset_flags(c);
+    set_conditioning(c, c->s_tmp, c->s_cond);
+    train_prep(c->tr.x0, c->tr.z, n, cs.first, cs.second, c->s_x, c->tr.v, c->st);
+    assemble_state<float>(c->s_x, c->pe_loc, c->M, m.cout, m.cin, m.cinp, sd, static_cast<float*>(c->a_in), c->st);
+    c->save_x = true;
+    forward_any(c, double(t), 1.f);
+    c->save_x = false;
+    train_loss(c->out_loc, c->tr.v, c->lay[0], c->M, m.cout, c->tr.kappa, c->tr.alpha, sd, 2.f / float(c->N),
+               c->bw.dS, c->tr.part, c->st);
+    SWF_CUDA(cudaMemcpyAsync(c->tr.h_part, c->tr.part, sizeof(double) * kTrainLossBlocks, cudaMemcpyDeviceToHost,
+                             c->st));
+    check_flags(c);  // synchronizes
+    double loss = 0.0;
+    for (int b = 0; b < kTrainLossBlocks; ++b) loss += c->tr.h_part[b];
+    backward_core(c, c->bw.dS);
+    c->launches += 4;
+    return loss / double(c->N);
+}
+
+void train_inputs(swf_ctx* c, const void* x_prev, const void* x0, const void* forcings, int dtype) {
+    const Dims& m = c->m;
+    const int cf = m.cin - 2 * m.cout;
+    require(cf >= 0, "train: in_channels must be >= 2 * out_channels");
+    h2d_local(c, x_prev, m.cout, dtype, c->s_tmp);
+    h2d_local(c, x0, m.cout, dtype, c->tr.x0);
+    if (cf > 0) {
+        require(forcings != nullptr, "train: forcings required");
+        h2d_local(c, forcings, cf, dtype, c->s_cond);
+    }
+}
+
+void train_checks(swf_ctx* c) {
+    require(c->loaded, "train: parameters not loaded");
+    require(c->prec == SWF_PREC_FP32, "train: available in the FP32 validation mode (SWF_PREC_FP32)");
+    require(c->world == 1, "train: one rank per replica (data parallel across ranks)");
+    SWF_CUDA(cudaSetDevice(c->dev));
+    ensure_train(c);
+}
+
+void grads_to_host(swf_ctx* c, const float* src, double scale, void* out, int dtype) {
+    const size_t n = c->poff.back();
+    std::vector<float> g(n);
+    SWF_CUDA(cudaMemcpyAsync(g.data(), src, n * 4, cudaMemcpyDeviceToHost, c->st));
+    SWF_CUDA(cudaStreamSynchronize(c->st));
+    if (dtype == SWF_F64)
+        for (size_t i = 0; i < n; ++i) static_cast<double*>(out)[i] = double(g[i]) * scale;
+    else
+        for (size_t i = 0; i < n; ++i) static_cast<float*>(out)[i] = float(double(g[i]) * scale);
+}
+
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1618,6 +1788,9 @@ void swf_destroy(swf_ctx* c) {
         if (sl.forcing) cudaFreeHost(sl.forcing);
     }
     if (c->h_flags) cudaFreeHost(c->h_flags);
+    if (c->h_churn_key) cudaFreeHost(c->h_churn_key);
+    if (c->tr.h_part) cudaFreeHost(c->tr.h_part);
+    if (c->solve_exec) cudaGraphExecDestroy(c->solve_exec);
     if (c->h_feat) cudaFreeHost(c->h_feat);
     for (int r = 0; r < int(c->peer.size()); ++r) {  // unmap every IPC-opened peer buffer
         if (r == c->rank) continue;
@@ -1748,6 +1921,7 @@ int swf_forward(swf_ctx* c, const void* input, double t, void* output, int dtype
     })
 }
 
+
 int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, void* grads, void* d_input,
                  int dtype) {
     SWF_API_TRY({
@@ -1787,6 +1961,65 @@ int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, 
             else
                 std::memcpy(d_input, di.data(), ni * 4);
         }
+    })
+}
+
+
+int swf_diffusion_loss_sample(swf_ctx* c, const void* x_prev, const void* x0, const void* forcings,
+                              const swf_loss_weights* w, const swf_diffusion_cfg* dc, uint64_t t_key, const void* z,
+                              double* loss, void* grads, int dtype) {
+    SWF_API_TRY({
+        require(c && x_prev && x0 && dc && z && loss, "null argument");
+        train_checks(c);
+        set_loss_weights(c, w, dtype);
+        train_inputs(c, x_prev, x0, forcings, dtype);
+        h2d_local(c, z, c->m.cout, dtype, c->tr.z);
+        *loss = train_sample_core(c, *dc, t_key);
+        if (grads) grads_to_host(c, c->bw.gflat, 1.0, grads, dtype);
+    })
+}
+
+int swf_train_accumulate(swf_ctx* c, const void* x_prev, const void* x0, const void* forcings,
+                         const swf_loss_weights* w, const swf_diffusion_cfg* dc, uint64_t run_seed,
+                         uint64_t sample_id, double* loss, int dtype) {
+    SWF_API_TRY({
+        require(c && x_prev && x0 && dc && loss, "null argument");
+        train_checks(c);
+        set_loss_weights(c, w, dtype);
+        train_inputs(c, x_prev, x0, forcings, dtype);
+        // z = noise_field(seeds, sample_id, ...) on the unshifted grid; t_key = SeedProtocol::t_key
+        noise_field(h_kd(h_kd(run_seed, 0x7au), sample_id), c->m.cout, c->lay[0], dc->sigma_d, c->tr.z, c->st);
+        c->launches++;
+        *loss = train_sample_core(c, *dc, h_kd(h_kd(run_seed, 0x74u), sample_id));
+        axpy_f32(c->bw.gflat, i64(c->poff.back()), 1.f, c->tr.gacc, c->st);
+        c->launches++;
+        SWF_CUDA(cudaStreamSynchronize(c->st));  // the accumulator is complete for an all-reduce
+    })
+}
+
+int swf_train_reset(swf_ctx* c) {
+    SWF_API_TRY({
+        require(c, "null context");
+        train_checks(c);
+        SWF_CUDA(cudaMemsetAsync(c->tr.gacc, 0, c->poff.back() * 4, c->st));
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+    })
+}
+
+int swf_train_grads(swf_ctx* c, float** dev_ptr, long long* n) {
+    SWF_API_TRY({
+        require(c && dev_ptr && n, "null argument");
+        train_checks(c);
+        *dev_ptr = c->tr.gacc;
+        *n = static_cast<long long>(c->poff.back());
+    })
+}
+
+int swf_train_read(swf_ctx* c, double scale, void* grads, int dtype) {
+    SWF_API_TRY({
+        require(c && grads, "null argument");
+        train_checks(c);
+        grads_to_host(c, c->tr.gacc, scale, grads, dtype);
     })
 }
 
@@ -2161,6 +2394,14 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
         cudaEventDestroy(a);
         cudaEventDestroy(b);
         *ms = double(t) / reps;
+    })
+}
+
+int swf_set_graphs(swf_ctx* c, int enable) {
+    SWF_API_TRY({
+        require(c, "null context");
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        c->graphs = enable != 0;
     })
 }
 

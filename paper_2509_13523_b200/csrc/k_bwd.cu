@@ -327,6 +327,50 @@ __global__ void k_time_bwd(const float* __restrict__ demb, const float* __restri
     if (k == 0) gbt[o] += dl;
 }
 
+
+// ---- diffusion training loss (diffusion.hpp:57-67, 111-133, 168-192)
+// x_t = c x0 + s z (interpolate), v = c z - s x0 (velocity_target)
+__global__ void k_train_prep(const float* __restrict__ x0, const float* __restrict__ z, i64 n, float cs, float sn,
+                             float* __restrict__ xt, float* __restrict__ v) {
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
+        const float a = x0[e], b = z[e];
+        xt[e] = cs * a + sn * b;
+        v[e] = cs * b - sn * a;
+    }
+}
+
+// err = sd f - v; loss terms alpha(row) kappa(c) err^2 summed per block in double (fixed grid, fixed
+// order: deterministic); dS = sd * 2 alpha kappa err / N (weighted_sq_loss_grad scaled by sigma_d).
+__global__ void __launch_bounds__(256) k_train_loss(const float* __restrict__ f, const float* __restrict__ v,
+                                                    LayMap lay, i64 M, int C, const float* __restrict__ kappa,
+                                                    const float* __restrict__ alpha_row, float sd, float g_scale,
+                                                    float* __restrict__ dS, double* __restrict__ part) {
+    __shared__ double red[256];
+    double acc = 0.0;
+    const i64 total = M * C;
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+        const i64 i = e / C;
+        const int ch = int(e - i * C);
+        const float alpha = alpha_row[lay.loc_to_pix(i) / lay.g.W];
+        const float err = sd * f[e] - v[e];
+        const float ak = alpha * kappa[ch];
+        acc += double(ak) * double(err) * double(err);
+        dS[e] = sd * (g_scale * ak * err);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void k_axpy(const float* __restrict__ x, i64 n, float a, float* __restrict__ y) {
+    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x)
+        y[e] += a * x[e];
+}
+
 }  // namespace
 
 void gemm_strided_f32(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj,
@@ -403,6 +447,21 @@ void ada_bwd(const float* d6, const float* emb, const float* Wa, int n6, int td,
 void time_bwd(const float* demb, const float* feat, const float* Wt, const float* bt, int td, float* gWt, float* gbt,
               cudaStream_t st) {
     k_time_bwd<<<unsigned((td * td + 255) / 256), 256, 0, st>>>(demb, feat, Wt, bt, td, gWt, gbt);
+    SWF_LAUNCH_CHECK();
+}
+
+
+void train_prep(const float* x0, const float* z, i64 n, float cs, float sn, float* xt, float* v, cudaStream_t st) {
+    k_train_prep<<<unsigned(std::min<i64>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(x0, z, n, cs, sn, xt, v);
+    SWF_LAUNCH_CHECK();
+}
+void train_loss(const float* f, const float* v, const LayMap& lay, i64 M, int C, const float* kappa,
+                const float* alpha_row, float sd, float g_scale, float* dS, double* part, cudaStream_t st) {
+    k_train_loss<<<kTrainLossBlocks, 256, 0, st>>>(f, v, lay, M, C, kappa, alpha_row, sd, g_scale, dS, part);
+    SWF_LAUNCH_CHECK();
+}
+void axpy_f32(const float* x, i64 n, float a, float* y, cudaStream_t st) {
+    k_axpy<<<unsigned(std::min<i64>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(x, n, a, y);
     SWF_LAUNCH_CHECK();
 }
 

@@ -215,9 +215,10 @@ __global__ void k_noise(u64 zfk, int C, LayMap lay, double sd, float* __restrict
     }
 }
 
-__global__ void k_churn(float* __restrict__ x, LayMap lay, i64 M, int C, u64 key, u64 ctr0, double sd, float c,
-                        float s) {
+__global__ void k_churn(float* __restrict__ x, LayMap lay, i64 M, int C, const u64* __restrict__ key_p, u64 ctr0,
+                        double sd, float c, float s) {
     const i64 total = M * C;
+    const u64 key = *key_p;
     for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
         const i64 i = e / C;
         const int ch = int(e - i * C);
@@ -382,7 +383,7 @@ void noise_field(u64 zfk, int C, const LayMap& lay0, double sigma_d, float* z, c
     SWF_LAUNCH_CHECK();
 }
 
-void churn_rotate(float* x, const LayMap& lay0, i64 M, int C, u64 key, u64 ctr0, double sigma_d, float c, float s,
+void churn_rotate(float* x, const LayMap& lay0, i64 M, int C, const u64* key, u64 ctr0, double sigma_d, float c, float s,
                   cudaStream_t st) {
     k_churn<<<grid_for(M * C), kThreads, 0, st>>>(x, lay0, M, C, key, ctr0, sigma_d, c, s);
     SWF_LAUNCH_CHECK();

@@ -181,6 +181,13 @@ void attention_bwd_f32(const float* q, const float* k, const float* v, const flo
                        const LayMap& lay, const EpiParams& ep, float* dqkv, cudaStream_t st);
 void ada_bwd(const float* d6, const float* emb, const float* Wa, int n6, int td, float* gWa, float* gba, float* demb,
              cudaStream_t st);
+// diffusion training loss (diffusion.hpp:57-67, 111-133): x_t / v targets, weighted squared error
+// with per-block double partials (kTrainLossBlocks of them) and its gradient into dS, y += a x
+constexpr int kTrainLossBlocks = 592;
+void train_prep(const float* x0, const float* z, i64 n, float cs, float sn, float* xt, float* v, cudaStream_t st);
+void train_loss(const float* f, const float* v, const LayMap& lay, i64 M, int C, const float* kappa,
+                const float* alpha_row, float sd, float g_scale, float* dS, double* part, cudaStream_t st);
+void axpy_f32(const float* x, i64 n, float a, float* y, cudaStream_t st);
 void time_bwd(const float* demb, const float* feat, const float* Wt, const float* bt, int td, float* gWt, float* gbt,
               cudaStream_t st);
 
@@ -223,7 +230,7 @@ void assemble_state(const float* x, const float* pe, i64 M, int cp, int cin, int
 // noise_field (diffusion.hpp:91-108) generated directly in local window order of the unshifted layout.
 void noise_field(u64 zfk, int C, const LayMap& lay0, double sigma_d, float* z, cudaStream_t st);
 // churn rotation (diffusion.hpp:255-268): x = c*x + s*sd*gaussian(key, ctr0 + pix*C + ch)
-void churn_rotate(float* x, const LayMap& lay0, i64 M, int C, u64 key, u64 ctr0, double sigma_d, float c, float s,
+void churn_rotate(float* x, const LayMap& lay0, i64 M, int C, const u64* key, u64 ctr0, double sigma_d, float c, float s,
                   cudaStream_t st);
 // y = (x - mean) / std  (Standardizer::apply_mat, grid.hpp:127-129)
 void standardize(const float* x, i64 M, int C, const float* mean, const float* stdv, float* y, cudaStream_t st);

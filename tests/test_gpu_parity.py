@@ -252,3 +252,79 @@ def test_backward_fp32_matches_oracle(cfg, H, W):
     assert float((np.abs(din - d32).max(axis=0) / scale).max()) <= TOL_GRAD_F32
     assert float((np.abs(d32 - dref).max(axis=0) / scale).max()) <= 2 * TOL_GRAD_F64
     assert float((np.abs(din - dref).max(axis=0) / scale).max()) <= 2 * TOL_GRAD_F64
+
+
+@pytest.mark.parametrize("prec", [swf.PREC_BF16, swf.PREC_FP32])
+def test_solver_graph_replay_bitwise(prec):
+    """CUDA-graph replay of the sampler (eager -> capture -> replay) equals eager execution bit for bit,
+    with churn active (the churn key is device-resident, so replays with new events draw new noise)."""
+    oc, sc = cfgs(C1)
+    p = o.init_params(oc, 310, random=True, scale=0.02, dtype=np.float32)
+    x0 = o.random_field(3, 2048, 311).astype(np.float32)
+    forc = o.random_field(2, 2048, 312).astype(np.float32)
+    dc = swf.DiffusionConfig(solver_steps=6, churn=0.5)
+    outs = {}
+    for graphs in (False, True):
+        dn = swf.Denoiser(sc, 32, 64, precision=prec)
+        dn.load_params(p)
+        dn.set_graphs(graphs)
+        outs[graphs] = [dn.forecast_step(x0, forc, dc, 11, o.key_derive(41, k, 0)) for k in range(4)]
+        dn.close()
+    for a, b in zip(outs[False], outs[True]):
+        assert np.array_equal(a, b)
+    assert not np.array_equal(outs[True][2], outs[True][3])  # new event -> new churn / init noise
+
+
+def test_diffusion_loss_sample_matches_oracle():
+    """f3: the device diffusion_loss_sample (FP32 validation mode) against the oracle's, which is pinned
+    by central differences (tests/test_oracle_train.py, test_trigflow.cpp:148-196 restated)."""
+    oc, sc = cfgs(SAMP)
+    H = W = 12
+    p = o.init_params(oc, 55, random=True, scale=0.1)
+    xp, x0, fo, z = (o.random_field(c, H * W, k) for c, k in ((3, 61), (3, 62), (2, 63), (3, 64)))
+    w = swf.LossWeights.make(H, [1.0, 0.6, 1.7])
+    lref, gref = o.loss_sample(oc, p, H, W, xp, x0, fo, w.alpha_row, w.kappa, 4242, z)
+    dn = swf.Denoiser(sc, H, W, precision=swf.PREC_FP32)
+    dn.load_params(p.astype(np.float32))
+    loss, g = dn.diffusion_loss_sample(xp.astype(np.float32), x0.astype(np.float32), fo.astype(np.float32), w,
+                                       swf.DiffusionConfig(), 4242, z.astype(np.float32))
+    assert abs(loss - lref) <= TOL_FP32 * abs(lref)
+    off = 0
+    for name, r, c in o.param_shapes(oc):
+        a, b = g[off:off + r * c], gref[off:off + r * c]
+        off += r * c
+        assert float(np.abs(a - b).max()) / max(float(np.abs(b).max()), 1e-30) <= TOL_GRAD_F64, name
+
+
+def test_train_step_matches_oracle():
+    """reference_train_step (dp=2, gas=2 on one rank): seed protocol (noise, t), pair cycling, scaling."""
+    oc, sc = cfgs(SAMP)
+    H = W = 12
+    p = o.init_params(oc, 56, random=True, scale=0.1)
+    data = swf.DataSet(*[[o.random_field(c, H * W, 900 + 3 * i + j) for i in range(3)]
+                         for j, c in ((0, 3), (1, 2), (2, 3))])
+    w = swf.LossWeights.make(H, [1.0, 0.6, 1.7])
+    dc = swf.DiffusionConfig()
+    dn = swf.Denoiser(sc, H, W, precision=swf.PREC_FP32)
+    dn.load_params(p.astype(np.float32))
+    res = dn.train_step(data, 5, 2, 2, w, dc, 31)
+    acc, losses = np.zeros_like(p), []
+    for sid in range(5, 9):
+        i = sid % 3
+        z = o.noise_field(31, sid, 3, H, W, 6)
+        l_, gr = o.loss_sample(oc, p, H, W, data.states[i], data.residuals[i], data.forcings[i], w.alpha_row,
+                               w.kappa, o.key_derive(31, 0x74, sid), z)
+        acc += gr
+        losses.append(l_)
+    assert np.allclose(res.mb_losses, losses, rtol=TOL_FP32, atol=0)
+    assert abs(res.loss - sum(losses) / 4) <= TOL_FP32 * abs(res.loss)
+    ref = acc / 4
+    off = 0
+    for name, r, c in o.param_shapes(oc):
+        a, b = res.grads[off:off + r * c], ref[off:off + r * c]
+        off += r * c
+        assert float(np.abs(a - b).max()) / max(float(np.abs(b).max()), 1e-30) <= TOL_GRAD_F64, name
+    again = dn.train_step(data, 5, 2, 2, w, dc, 31)
+    assert np.array_equal(again.grads, res.grads) and again.mb_losses == res.mb_losses
+    with pytest.raises(swf.ConfigError):
+        swf.Denoiser(sc, H, W, precision=swf.PREC_BF16).train_reset()

@@ -29,3 +29,14 @@ def test_wp_bitwise_equals_single_gpu(own, sp):
                         os.path.join(ROOT, "tools", "wp_check.py")], capture_output=True, text=True, timeout=600,
                        env=env, cwd=ROOT)
     assert "WP_CHECK PASS" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_dp_train_step_nccl_equals_single_rank():
+    """f3: data-parallel training step, replicas on ranks, NCCL all-reduce of the device gradients."""
+    n = 4 if _ngpus() >= 4 else 2
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29700",
+                        os.path.join(ROOT, "tools", "dp_check.py")], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT)
+    assert "DP_CHECK PASS" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
