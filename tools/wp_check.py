@@ -13,7 +13,9 @@ import paper_2509_13523_b200 as swf  # noqa: E402
 from oracle import pyoracle as o  # noqa: E402
 
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-local = int(os.environ.get("LOCAL_RANK", rank))
+# more ranks than GPUs (e.g. 8 ranks on a 4-GPU box) shares devices: a functional check of the
+# 8-way topology (peer stores and barriers between processes on one device), not a timing
+local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
 torch.cuda.set_device(local)
 dist.init_process_group("gloo")
 sp = int(os.environ.get("SWF_SP", 1))
@@ -55,10 +57,15 @@ for name, d, H, W in [
         full = 2 * rs.chunk_cover(0, 0, H, W)
         reads = dn.last_chunk_reads()
         same = bool(np.array_equal(a, b))
-        # contiguous ownership: 4 x 16 chunks tile every rank's rows / columns exactly; round-robin
-        # ownership interleaves windows inside every chunk, so each rank reads them all
-        partial = reads == (full // world if own == swf.OWN_CONTIGUOUS else full)
-        print(f"rank {rank}: chunked forecast bitwise={same} chunk_reads={reads}/{full}", flush=True)
+        # every chunk holding an owned pixel is read (state + forcing); contiguous ownership with 4 x 16
+        # chunks reads exactly those, round-robin ownership may revisit a chunk from two window runs
+        owned = np.zeros(H * W, np.int64)
+        swf.lib().swf_owned_pixels(dn._c, owned.ctypes.data_as(swf.C.c_void_p))
+        pix = owned[:dn.local_tokens()]
+        need = 2 * len(np.unique((pix // W) // 4 * (W // 16) + (pix % W) // 16))
+        partial = reads == need if own == swf.OWN_CONTIGUOUS else need <= reads <= full
+        print(f"rank {rank}: chunked forecast bitwise={same} chunk_reads={reads}/{full} (owned chunks {need})",
+              flush=True)
         ok &= same and partial
         dist.barrier()
     y = dn.forward(x, 0.9)
