@@ -211,9 +211,11 @@ class Denoiser:
         self._c = C.c_void_p()
         _check(lib().swf_create(C.byref(_Cfg(*astuple(cfg))), grid_h, grid_w, device, precision,
                                 C.byref(self._c)))
+        self.wp_world, self.wp_rank = 1, 0  # ranks sharing this model's windows (WP x SP group)
         if topology is not None:
             wp_a, wp_b, sp, rank, own = topology
             _check(lib().swf_set_topology(self._c, wp_a, wp_b, sp, rank, own))
+            self.wp_world, self.wp_rank = wp_a * wp_b * sp, rank
 
     def connect_peers(self, all_handles: bytes):
         buf = C.create_string_buffer(all_handles, len(all_handles))
@@ -224,11 +226,12 @@ class Denoiser:
         _check(lib().swf_ipc_handles(self._c, buf))
         return buf.raw
 
-    def connect_peers_torch(self, dist):
-        """Exchange IPC handles with torch.distributed (any backend) and map every peer."""
+    def connect_peers_torch(self, dist, group=None):
+        """Exchange IPC handles with torch.distributed (any backend) over the WP group (default: the
+        whole world, ranks in topology order) and map every peer."""
         mine = self.ipc_handles()
-        allh = [None] * dist.get_world_size()
-        dist.all_gather_object(allh, mine)
+        allh = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allh, mine, group=group)
         self.connect_peers(b"".join(allh))
 
     def close(self):

@@ -1078,6 +1078,9 @@ void backward_core(swf_ctx* c, const float* dout) {
     auto pa = [&](int ai) { return P + c->poff[ai]; };
     auto ga = [&](int ai) { return G + c->poff[ai]; };
     const int kHead = 2, kPer = 9, tail = kHead + nb * kPer;
+    // WP: every rank's gradients are partial sums over its tokens (all-reduced by the caller); no
+    // rank may store into a peer's landing buffer while that peer still runs its forward
+    if (c->world > 1) peer_barrier(c);
     SWF_CUDA(cudaMemsetAsync(G, 0, c->poff.back() * 4, st));
     SWF_CUDA(cudaMemsetAsync(bw.demb, 0, size_t(td) * 4, st));
     // decode head (swin.hpp:430-436): n3 = prenorm_plain(x_final); dW_dec, db_dec, dN3, prenorm_plain_bwd
@@ -1137,7 +1140,14 @@ void backward_core(swf_ctx* c, const float* dout) {
         gemm_f32(bw.x2m, static_cast<const float*>(c->w_gu[b]), M, m.np_gu, hp, EPI_DECODE, e, st);
         // ---- backward (block_window_backward, swin.hpp:370-417)
         float* dXp = bw.dtmp;  // output gradient in this block's layout
-        relayout_rows(bw.dx[cur], c->lay[npar], c->lay[par], M, h, dXp, st);
+        if (c->world > 1) {    // WP: owners change between the layouts -> peer stores, then a barrier
+            relayout_push(bw.dx[cur], c->lay[npar], c->lay[par], M, h, c->d_xdst[par], st);
+            peer_barrier(c);
+            dXp = c->xbuf[par];  // landing buffer (the forward's residual stream is free here)
+            c->launches++;
+        } else {
+            relayout_rows(bw.dx[cur], c->lay[npar], c->lay[par], M, h, dXp, st);
+        }
         // feed-forward branch: swiglu_bwd (:236-252)
         gemm_strided_f32(int(M), f, h, dXp, h, 1, pa(base + 6), 1, h, bw.dS, f, 0.f, st);
         swiglu_bwd(bw.gu, m.np_gu, bw.dS, f, M, f, m.G, bw.act, bw.dG, bw.dU, st);
@@ -1704,7 +1714,7 @@ void train_inputs(swf_ctx* c, const void* x_prev, const void* x0, const void* fo
 void train_checks(swf_ctx* c) {
     require(c->loaded, "train: parameters not loaded");
     require(c->prec == SWF_PREC_FP32, "train: available in the FP32 validation mode (SWF_PREC_FP32)");
-    require(c->world == 1, "train: one rank per replica (data parallel across ranks)");
+    require(c->sp == 1, "train: window parallelism only (SP == 1)");
     SWF_CUDA(cudaSetDevice(c->dev));
     ensure_train(c);
 }
@@ -1928,7 +1938,7 @@ int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, 
         require(c && input && d_output && grads, "null argument");
         require(c->loaded, "backward: parameters not loaded");
         require(c->prec == SWF_PREC_FP32, "backward: available in the FP32 validation mode (SWF_PREC_FP32)");
-        require(c->world == 1, "backward: single rank");
+        require(c->sp == 1, "backward: window parallelism only (SP == 1)");
         SWF_CUDA(cudaSetDevice(c->dev));
         ensure_bwd(c);
         reset_flags(c);

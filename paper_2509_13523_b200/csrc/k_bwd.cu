@@ -173,6 +173,19 @@ __global__ void k_relayout(const float* __restrict__ src, LayMap A, LayMap B, i6
     for (int e = lane; e < h; e += 32) dst[i * h + e] = src[j * h + e];
 }
 
+// window parallelism: push row i of layout A (this rank's rows) to its owner under layout B,
+// dst[rank] = that rank's landing buffer (CUDA-IPC mapped), one warp per row
+__global__ void k_relayout_push(const float* __restrict__ src, LayMap A, LayMap B, i64 M, int h,
+                                float* const* __restrict__ dst) {
+    const i64 i = i64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= M) return;
+    int rk;
+    const i64 j = B.pix_to_loc(A.loc_to_pix(i), &rk);
+    float* d = dst[rk] + j * h;
+    for (int e = lane; e < h; e += 32) d[e] = src[i * h + e];
+}
+
 // ---- attention backward (head_attention_bwd, swin.hpp:189-226), planes [nloc][heads][s][d],
 // O / dO rows [lw*s + tok][ldo] (head-concatenated), one thread per query (pass 1) or key (pass 2).
 struct AttnBwd {
@@ -401,6 +414,11 @@ void swiglu_bwd(const float* gu, int ldgu, const float* dS, int ldds, i64 M, int
 }
 void relayout_rows(const float* src, const LayMap& A, const LayMap& B, i64 M, int h, float* dst, cudaStream_t st) {
     k_relayout<<<unsigned((M + 7) / 8), 256, 0, st>>>(src, A, B, M, h, dst);
+    SWF_LAUNCH_CHECK();
+}
+void relayout_push(const float* src, const LayMap& A, const LayMap& B, i64 M, int h, float* const* dst,
+                   cudaStream_t st) {
+    k_relayout_push<<<unsigned((M + 7) / 8), 256, 0, st>>>(src, A, B, M, h, dst);
     SWF_LAUNCH_CHECK();
 }
 void attention_bwd_f32(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,

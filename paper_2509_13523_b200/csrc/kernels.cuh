@@ -175,6 +175,9 @@ void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h
 void colsum_f32(const float* X, int ldx, i64 M, int n, float* out, cudaStream_t st);
 void swiglu_bwd(const float* gu, int ldgu, const float* dS, int ldds, i64 M, int f, int G, float* act, float* dG,
                 float* dU, cudaStream_t st);
+// WP: row i of A's local order -> dst[owner rank][B-local index] (peer stores)
+void relayout_push(const float* src, const LayMap& A, const LayMap& B, i64 M, int h, float* const* dst,
+                   cudaStream_t st);
 void relayout_rows(const float* src, const LayMap& A, const LayMap& B, i64 M, int h, float* dst, cudaStream_t st);
 void attention_bwd_f32(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,
                        float* dq, float* dk, float* dv, float* stats, int nloc, int heads, int s, int d, int w,

@@ -3,10 +3,12 @@
 `train_step` restates `reference_train_step` (simulator.hpp:50-86) -- microbatches sample_id =
 first_sample + d * gas + g, pair index sample_id % n_pairs, per-sample noise and diffusion time from
 the shared-seed protocol (rng.hpp:72-80), gradients summed then scaled by 1 / (dp * gas) -- with the
-data-parallel dimension mapped onto ranks: with a `torch.distributed` group of size dp, rank d runs
-replica d's `gas` microbatches into the engine's device gradient accumulator and the replicas are
-summed by one in-place all-reduce (NCCL on the device buffer; gloo through host memory), the
-role of `grad_allreduce` (simulator.hpp:92-120). With group=None (or a group of size 1) one rank
+data-parallel dimension mapped onto ranks: with a `torch.distributed` group of size dp x wp, the
+wp consecutive ranks of replica d run its `gas` microbatches window-parallel (each rank's loss and
+gradients are partial sums over its own tokens, the engine's WP topology) into the device gradient
+accumulators, and one in-place all-reduce over the group (NCCL on the device buffer; gloo through
+host memory) sums the WP partials and the replicas at once -- the roles of the intra-instance
+gradient sum and of `grad_allreduce` (simulator.hpp:92-120, 169-202). With group=None (or a group of size 1) one rank
 runs all dp replicas in order, which is the reference's single-rank semantics.
 
 The engine is a `Denoiser` (FP32 validation mode) or anything with the same four methods:
@@ -113,10 +115,15 @@ def train_step(engine, data: DataSet, first_sample: int, dp: int, gas: int, w: L
     if dp < 1 or gas < 1:
         raise ValueError("train_step: dp and gas must be >= 1")
     dist, world, rank = _world(group)
+    wp = int(getattr(engine, "wp_world", 1))  # ranks sharing one replica's windows
     sharded = world > 1
-    if sharded and world != dp:
-        raise ValueError(f"train_step: dp={dp} must equal the data-parallel group size {world}")
-    replicas = [rank] if sharded else list(range(dp))
+    if wp > 1 and not sharded:
+        raise ValueError("train_step: a window-parallel engine needs the process group")
+    if sharded and world != dp * wp:
+        raise ValueError(f"train_step: group size {world} must equal dp={dp} x window-parallel ranks {wp}")
+    if wp > 1 and getattr(engine, "wp_rank", rank % wp) != rank % wp:
+        raise ValueError("train_step: window-parallel ranks of a replica must be consecutive group ranks")
+    replicas = [rank // wp] if sharded else list(range(dp))
     engine.train_reset()
     mb = np.zeros(dp * gas, np.float64)
     for d in replicas:
@@ -134,7 +141,7 @@ def train_step(engine, data: DataSet, first_sample: int, dp: int, gas: int, w: L
         lt = torch.from_numpy(mb)
         if dist.get_backend(group) == "nccl":
             lt = lt.cuda()
-        dist.all_reduce(lt, group=group)  # every slot is written by exactly one rank
+        dist.all_reduce(lt, group=group)  # slot d*gas+g: the partial losses of replica d's WP ranks
         mb = lt.cpu().numpy()
     scale = 1.0 / (dp * gas)
     res = TrainStepResult()

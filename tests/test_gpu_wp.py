@@ -32,11 +32,15 @@ def test_wp_bitwise_equals_single_gpu(own, sp):
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-def test_dp_train_step_nccl_equals_single_rank():
-    """f3: data-parallel training step, replicas on ranks, NCCL all-reduce of the device gradients."""
+@pytest.mark.parametrize("wp", [1, 2, 4])
+def test_sharded_train_step_equals_single_rank(wp):
+    """f3: training step with replicas on ranks (DP) and windows of a replica on ranks (WP), one NCCL
+    all-reduce of the device gradients; equals the single-GPU reference_train_step."""
     n = 4 if _ngpus() >= 4 else 2
+    if wp > n:
+        pytest.skip("needs 4 GPUs")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-                        "--master-addr", "127.0.0.1", "--master-port", "29700",
+                        "--master-addr", "127.0.0.1", "--master-port", str(29700 + wp),
                         os.path.join(ROOT, "tools", "dp_check.py")], capture_output=True, text=True, timeout=600,
-                       cwd=ROOT)
+                       env=dict(os.environ, SWF_DP_WP=str(wp)), cwd=ROOT)
     assert "DP_CHECK PASS" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]

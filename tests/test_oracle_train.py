@@ -174,3 +174,6 @@ def test_train_step_rejects_bad_arguments():
         swf.train.train_step(eng, data, 0, 1, 0, w, dc, 1)
     with pytest.raises(ValueError):
         swf.LossWeights.make(4, [1.0, 0.0])
+    eng.wp_world = 2  # a window-parallel replica cannot run without its process group
+    with pytest.raises(ValueError):
+        swf.train.train_step(eng, data, 0, 1, 1, w, dc, 1)

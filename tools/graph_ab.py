@@ -12,8 +12,8 @@ import paper_2509_13523_b200 as swf  # noqa: E402
 
 CFGS = [("C1 32x64 d128 2 blocks", dict(hidden_dim=128, n_heads=4, ffn_dim=256, n_layers=2, window_px=8,
                                         in_channels=8, out_channels=3, time_dim=128), 32, 64),
-        ("90x180 d512 8 blocks w30", dict(hidden_dim=512, n_heads=4, ffn_dim=1024, n_layers=8, window_px=30,
-                                          in_channels=8, out_channels=3, time_dim=256), 90, 180)]
+        ("72x144 d512 8 blocks w36", dict(hidden_dim=512, n_heads=4, ffn_dim=1024, n_layers=8, window_px=36,
+                                          in_channels=8, out_channels=3, time_dim=256), 72, 144)]
 for name, d, H, W in CFGS:
     sc = swf.ModelConfig(**d)
     rng = np.random.default_rng(0)
