@@ -424,6 +424,94 @@ def run_c5(args, rank: int, world: int, local_rank: int):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------- f3: training step
+def run_train(args, rank: int, world: int, local_rank: int):
+    """One data-parallel training step of the AERIS-1.3B-shaped model (C2 widths, 20 blocks) on a
+    TH x TW grid slice in the FP32 validation mode: per rank `gas` microbatches (swf_train_accumulate:
+    H2D of the sample's fields, device noise / t, forward with saved block inputs, loss, backward,
+    accumulate) and one in-place NCCL all-reduce of the device gradients. The optimizer update is not
+    part of the reference step (reference_train_step returns the gradients) and the gradients stay
+    on the device. FLOPs counted as 3x the forward (forward + input and weight gradients), the
+    backward's recompute of the block internals excluded."""
+    import torch
+    import paper_2509_13523_b200 as swf
+    from paper_2509_13523_b200.train import _DeviceView
+
+    TH, TW = args.train_grid
+    dist = None
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = swf.ModelConfig(**CFG)
+    dn = swf.Denoiser(cfg, TH, TW, device=local_rank, precision=swf.PREC_FP32)
+    dn.init_params(SEED, mode=2, scale=0.02 / math.sqrt(CFG["time_dim"]))
+    rng = np.random.default_rng(SEED + rank)
+    cp, cf = CFG["out_channels"], CFG["in_channels"] - 2 * CFG["out_channels"]
+    fields = [(rng.standard_normal((TH * TW, cp), dtype=np.float32),
+               rng.standard_normal((TH * TW, cp), dtype=np.float32),
+               rng.standard_normal((TH * TW, cf), dtype=np.float32)) for _ in range(2)]
+    w = swf.LossWeights.make(TH, np.ones(cp))
+    dc = swf.DiffusionConfig()
+    ptr, n = dn.train_grads_device()
+    grads = torch.as_tensor(_DeviceView(ptr, n), device=torch.device("cuda", local_rank))
+    stream = torch.cuda.ExternalStream(dn.stream, device=torch.device("cuda", local_rank))
+    gas = args.gas
+    losses = []
+
+    def step(k):
+        dn.train_reset()
+        for g in range(gas):
+            sid = (k * world + rank) * gas + g
+            xp, x0, fo = fields[sid % 2]
+            losses.append(dn.train_accumulate(xp, x0, fo, w, dc, SEED, sid))
+        if dist is not None:
+            dist.all_reduce(grads)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k)
+        e1.record(torch.cuda.current_stream())  # after the all-reduce (NCCL orders after the current stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    samples = world * gas
+    model_flops = 3.0 * flops_per_step(CFG, TH * TW) * samples
+    fp32_peak = 148 * 128 * 2 * 1965e6 / 1e12  # FFMA lanes x 2 x max SM clock (no measured FP32 peak)
+    if rank == 0:
+        tf = model_flops / (ms * 1e-3) / world / 1e12
+        print(json.dumps({
+            "metric": "training samples/sec", "value": samples / (ms * 1e-3), "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "f3 training step (reference_train_step, FP32 validation mode), "
+                                   "AERIS-1.3B widths / 20 blocks on a grid slice",
+                       "grid": [TH, TW], "gas": gas, "parallelism": f"dp{world}", "model": "swin-dit-1.3B (C2)",
+                       "l2": "inputs far larger than L2 (weights 5.3 GB fp32 + activations)"},
+            "roofline": {"bound": "fp32", "achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s", "frac": tf / fp32_peak,
+                         "peak_kind": "computed: 148 SMs x 128 FFMA lanes x 2 x 1965 MHz (no measured FP32 peak)",
+                         "traffic": None, "flops": "3 x forward per sample (perf_model.cpp:63-74), recompute excluded"},
+            "e2e": {"value": samples / (ms * 1e-3), "unit": "samples/s",
+                    "h2d_bytes_per_step": int(sum(a.nbytes for a in fields[0])) * samples, "d2h_bytes_per_step": 8 * samples},
+            "loss_finite": bool(np.isfinite(losses).all()),
+            "clocks": clk.summary(),
+        }), flush=True)
+    dn.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -433,11 +521,14 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sp", type=int, default=1, help="sequence-parallel degree (window rows split into SP bands)")
-    ap.add_argument("--workload", choices=["c2", "c4", "c5"], default="c2",
+    ap.add_argument("--workload", choices=["c2", "c4", "c5", "train"], default="c2",
                     help="c2: AERIS-1.3B 20-block step (headline); c4: 40B-shaped 2-block wide-layer slice; "
-                         "c5: ensemble generation (members x sampler evaluations, replicas)")
+                         "c5: ensemble generation (members x sampler evaluations, replicas); "
+                         "train: FP32 data-parallel training step (f3)")
     ap.add_argument("--members", type=int, default=16, help="c5: ensemble members over all ranks")
     ap.add_argument("--solver-steps", type=int, default=10, help="c5: DPM-Solver++ 2S steps (2 evaluations each)")
+    ap.add_argument("--gas", type=int, default=1, help="train: microbatches per rank")
+    ap.add_argument("--train-grid", type=int, nargs=2, default=[120, 240], help="train: grid slice (H W)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -446,6 +537,8 @@ def main():
         run_reference(args, rank, world)
     elif args.workload == "c5":
         run_c5(args, rank, world, local_rank)
+    elif args.workload == "train":
+        run_train(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 

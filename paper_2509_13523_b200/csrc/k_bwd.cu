@@ -26,13 +26,15 @@ __global__ void __launch_bounds__(256) k_gemm_strided(int M, int N, int K, const
     __shared__ float As[TK][TB + 1], Bs[TK][TB + 1];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int i0 = blockIdx.y * TB, j0 = blockIdx.x * TB;
+    const bool a_k_fast = sak == 1, b_k_fast = sbk == 1;
     float acc[4][4] = {};
     for (int k0 = 0; k0 < K; k0 += TK) {
+        // consecutive threads walk the operand's contiguous dimension (coalesced loads)
         for (int t = threadIdx.x; t < TB * TK; t += 256) {
-            const int r = t / TK, k = t % TK;  // A: row r of the tile, column k
+            const int r = a_k_fast ? t / TK : t % TB, k = a_k_fast ? t % TK : t / TB;
             const int gi = i0 + r, gk = k0 + k;
             As[k][r] = (gi < M && gk < K) ? A[gi * sai + gk * sak] : 0.f;
-            const int c = t / TK, kk = t % TK;
+            const int c = b_k_fast ? t / TK : t % TB, kk = b_k_fast ? t % TK : t / TB;
             const int gj = j0 + c, gk2 = k0 + kk;
             Bs[kk][c] = (gj < N && gk2 < K) ? B[gk2 * sbk + gj * sbj] : 0.f;
         }
@@ -201,84 +203,230 @@ __device__ __forceinline__ void seam(const AttnBwd& p, int lw, int& split, bool&
     masked = p.lay.g.shift > 0 && (gw / p.lay.g.nx) == p.lay.g.ny - 1;  // window.hpp:60
     split = (p.w - p.lay.g.shift) * p.w;
 }
-__global__ void k_attn_bwd_q(AttnBwd p) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x, head = blockIdx.y, lw = blockIdx.z;
-    if (i >= p.s) return;
-    const int s = p.s, d = p.d;
-    const i64 base = (i64(lw) * p.heads + head) * s;
-    const float* qi = p.q + (base + i) * d;
-    int split;
-    bool masked;
-    seam(p, lw, split, masked);
-    const int gq = i < split ? 0 : 1;
-    float m = -INFINITY;
-    for (int j = 0; j < s; ++j) {
-        if (masked && (j < split ? 0 : 1) != gq) continue;
-        const float* kj = p.k + (base + j) * d;
-        float acc = 0.f;
-        for (int e = 0; e < d; ++e) acc = fmaf(qi[e], kj[e], acc);
-        m = fmaxf(m, acc * p.scale);
-    }
-    float l = 0.f;
-    for (int j = 0; j < s; ++j) {
-        if (masked && (j < split ? 0 : 1) != gq) continue;
-        const float* kj = p.k + (base + j) * d;
-        float acc = 0.f;
-        for (int e = 0; e < d; ++e) acc = fmaf(qi[e], kj[e], acc);
-        l += expf(acc * p.scale - m);
-    }
-    const float* oi = p.o + (i64(lw) * s + i) * p.ldo + head * d;
-    const float* doi = p.dO + (i64(lw) * s + i) * p.ldo + head * d;
-    float D = 0.f;
-    for (int e = 0; e < d; ++e) D = fmaf(doi[e], oi[e], D);
-    float* dqi = p.dq + (base + i) * d;
-    for (int e = 0; e < d; ++e) dqi[e] = 0.f;
-    for (int j = 0; j < s; ++j) {
-        if (masked && (j < split ? 0 : 1) != gq) continue;
-        const float* kj = p.k + (base + j) * d;
-        const float* vj = p.v + (base + j) * d;
-        float acc = 0.f, dp = 0.f;
-        for (int e = 0; e < d; ++e) {
-            acc = fmaf(qi[e], kj[e], acc);
-            dp = fmaf(doi[e], vj[e], dp);
-        }
-        const float pij = expf(acc * p.scale - m) / l;
-        const float da = pij * (dp - D) * p.scale;
-        for (int e = 0; e < d; ++e) dqi[e] = fmaf(da, kj[e], dqi[e]);
-    }
-    p.m[base + i] = m;
-    p.l[base + i] = l;
-    p.D[base + i] = D;
+// Tiled flash-style backward (FP32 SIMT): 64-token tiles staged in shared memory with a padded row
+// pitch d+1, 256 threads, each owning a 4 x 4 block of the 64 x 64 score tile (rows ty*4+u, columns
+// tx*4+v; the 16 threads of a row group are one half-warp, so row reductions are shuffles) and a
+// 4 x ceil(d/16) block of the 64 x d output tile (columns tx + 16*w). d <= 128.
+constexpr int AT = 64, ADW = 8;  // tile, output columns per thread (d / 16)
+
+__device__ __forceinline__ float hw_max(float v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
 }
-__global__ void k_attn_bwd_kv(AttnBwd p) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x, head = blockIdx.y, lw = blockIdx.z;
-    if (j >= p.s) return;
-    const int s = p.s, d = p.d;
+__device__ __forceinline__ float hw_sum(float v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// rows [r0, r0+64) of a plane ([s][d], row pitch d) or of O / dO ([token][ldo] at column off) into smem
+__device__ __forceinline__ void load_tile(float* dst, const float* src, i64 pitch, int r0, int s, int d) {
+    const int ld = d + 1;
+    for (int idx = threadIdx.x; idx < AT * d; idx += blockDim.x) {
+        const int r = idx / d, e = idx - (idx / d) * d;
+        dst[r * ld + e] = r0 + r < s ? src[i64(r0 + r) * pitch + e] : 0.f;
+    }
+}
+
+// pass 1 (query tiles): row statistics m, l (online over key tiles), D = dO . O, and dQ
+__global__ void __launch_bounds__(256) k_attn_bwd_q(AttnBwd p) {
+    extern __shared__ float smf[];
+    const int d = p.d, ld = d + 1, s = p.s;
+    float *Qs = smf, *dOs = Qs + AT * ld, *Ks = dOs + AT * ld, *Vs = Ks + AT * ld, *Ss = Vs + AT * ld;
+    float* Dr = Ss + AT * (AT + 1);
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4, warp = tid >> 5, lane = tid & 31;
+    const int head = blockIdx.y, lw = blockIdx.z, i0 = blockIdx.x * AT;
     const i64 base = (i64(lw) * p.heads + head) * s;
-    const float* kj = p.k + (base + j) * d;
-    const float* vj = p.v + (base + j) * d;
     int split;
     bool masked;
     seam(p, lw, split, masked);
-    const int gk = j < split ? 0 : 1;
-    float* dkj = p.dk + (base + j) * d;
-    float* dvj = p.dv + (base + j) * d;
-    for (int e = 0; e < d; ++e) dkj[e] = dvj[e] = 0.f;
-    for (int i = 0; i < s; ++i) {
-        if (masked && (i < split ? 0 : 1) != gk) continue;
-        const float* qi = p.q + (base + i) * d;
-        const float* doi = p.dO + (i64(lw) * s + i) * p.ldo + head * d;
-        float acc = 0.f, dp = 0.f;
-        for (int e = 0; e < d; ++e) {
-            acc = fmaf(qi[e], kj[e], acc);
-            dp = fmaf(doi[e], vj[e], dp);
+    load_tile(Qs, p.q + base * d, d, i0, s, d);
+    load_tile(dOs, p.dO + i64(lw) * s * p.ldo + head * d, p.ldo, i0, s, d);
+    __syncthreads();
+    for (int r = warp; r < AT; r += 8) {  // D_i = dO_i . O_i
+        float acc = 0.f;
+        if (i0 + r < s) {
+            const float* o = p.o + (i64(lw) * s + i0 + r) * p.ldo + head * d;
+            for (int e = lane; e < d; e += 32) acc = fmaf(dOs[r * ld + e], o[e], acc);
         }
-        const float pij = expf(acc * p.scale - p.m[base + i]) / p.l[base + i];
-        const float da = pij * (dp - p.D[base + i]) * p.scale;
+        acc = warp_sum(acc);
+        if (lane == 0) Dr[r] = acc;
+    }
+    int gq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) gq[u] = i0 + ty * 4 + u < split ? 0 : 1;
+    float mr[4], lr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) mr[u] = -INFINITY, lr[u] = 0.f;
+    __syncthreads();
+    for (int j0 = 0; j0 < s; j0 += AT) {  // statistics
+        load_tile(Ks, p.k + base * d, d, j0, s, d);
+        __syncthreads();
+        float acc[4][4] = {};
         for (int e = 0; e < d; ++e) {
-            dkj[e] = fmaf(da, qi[e], dkj[e]);
-            dvj[e] = fmaf(pij, doi[e], dvj[e]);
+            float a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = Qs[(ty * 4 + u) * ld + e], b[u] = Ks[(tx * 4 + u) * ld + e];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float x[4], tm = -INFINITY;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int j = j0 + tx * 4 + v;
+                const bool ok = j < s && (!masked || (j < split ? 0 : 1) == gq[u]);
+                x[v] = ok ? acc[u][v] * p.scale : -INFINITY;
+                tm = fmaxf(tm, x[v]);
+            }
+            const float mn = fmaxf(mr[u], hw_max(tm));
+            float sum = 0.f;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) sum += x[v] == -INFINITY ? 0.f : expf(x[v] - mn);
+            sum = hw_sum(sum);
+            lr[u] = (mr[u] == -INFINITY ? 0.f : lr[u] * expf(mr[u] - mn)) + sum;
+            mr[u] = mn;
+        }
+        __syncthreads();
+    }
+    float dq[4][ADW] = {};
+    for (int j0 = 0; j0 < s; j0 += AT) {  // dQ = sum_j dS_ij k_j
+        load_tile(Ks, p.k + base * d, d, j0, s, d);
+        load_tile(Vs, p.v + base * d, d, j0, s, d);
+        __syncthreads();
+        float acc[4][4] = {}, dp[4][4] = {};
+        for (int e = 0; e < d; ++e) {
+            float a[4], b[4], g[4], h[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a[u] = Qs[(ty * 4 + u) * ld + e], g[u] = dOs[(ty * 4 + u) * ld + e];
+                b[u] = Ks[(tx * 4 + u) * ld + e], h[u] = Vs[(tx * 4 + u) * ld + e];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]), dp[u][v] = fmaf(g[u], h[v], dp[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int r = ty * 4 + u, j = j0 + tx * 4 + v;
+                const bool ok = j < s && (!masked || (j < split ? 0 : 1) == gq[u]);
+                const float pij = ok ? expf(acc[u][v] * p.scale - mr[u]) / lr[u] : 0.f;
+                Ss[r * (AT + 1) + tx * 4 + v] = pij * (dp[u][v] - Dr[r]) * p.scale;
+            }
+        __syncthreads();
+        for (int c = 0; c < AT; ++c) {
+            float kr[ADW];
+#pragma unroll
+            for (int w = 0; w < ADW; ++w) kr[w] = tx + 16 * w < d ? Ks[c * ld + tx + 16 * w] : 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float ds = Ss[(ty * 4 + u) * (AT + 1) + c];
+#pragma unroll
+                for (int w = 0; w < ADW; ++w) dq[u][w] = fmaf(ds, kr[w], dq[u][w]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int i = i0 + ty * 4 + u;
+        if (i >= s) continue;
+#pragma unroll
+        for (int w = 0; w < ADW; ++w)
+            if (tx + 16 * w < d) p.dq[(base + i) * d + tx + 16 * w] = dq[u][w];
+        if (tx == 0) {
+            p.m[base + i] = mr[u];
+            p.l[base + i] = lr[u];
+            p.D[base + i] = Dr[ty * 4 + u];
+        }
+    }
+}
+
+// pass 2 (key tiles): dV = sum_i P_ij dO_i, dK = sum_i dS_ij q_i
+__global__ void __launch_bounds__(256) k_attn_bwd_kv(AttnBwd p) {
+    extern __shared__ float smf[];
+    const int d = p.d, ld = d + 1, s = p.s;
+    float *Ks = smf, *Vs = Ks + AT * ld, *Qs = Vs + AT * ld, *dOs = Qs + AT * ld, *Ps = dOs + AT * ld;
+    float *dSs = Ps + AT * (AT + 1), *Mq = dSs + AT * (AT + 1), *Lq = Mq + AT, *Dq = Lq + AT;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int head = blockIdx.y, lw = blockIdx.z, j0 = blockIdx.x * AT;
+    const i64 base = (i64(lw) * p.heads + head) * s;
+    int split;
+    bool masked;
+    seam(p, lw, split, masked);
+    load_tile(Ks, p.k + base * d, d, j0, s, d);
+    load_tile(Vs, p.v + base * d, d, j0, s, d);
+    int gk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) gk[u] = j0 + ty * 4 + u < split ? 0 : 1;
+    float dk[4][ADW] = {}, dv[4][ADW] = {};
+    for (int i0 = 0; i0 < s; i0 += AT) {
+        load_tile(Qs, p.q + base * d, d, i0, s, d);
+        load_tile(dOs, p.dO + i64(lw) * s * p.ldo + head * d, p.ldo, i0, s, d);
+        for (int r = tid; r < AT; r += blockDim.x) {
+            const bool in = i0 + r < s;
+            Mq[r] = in ? p.m[base + i0 + r] : 0.f;
+            Lq[r] = in ? p.l[base + i0 + r] : 1.f;
+            Dq[r] = in ? p.D[base + i0 + r] : 0.f;
+        }
+        __syncthreads();
+        float acc[4][4] = {}, dp[4][4] = {};  // rows: keys ty*4+u, columns: queries tx*4+v
+        for (int e = 0; e < d; ++e) {
+            float a[4], b[4], g[4], h[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a[u] = Ks[(ty * 4 + u) * ld + e], g[u] = Vs[(ty * 4 + u) * ld + e];
+                b[u] = Qs[(tx * 4 + u) * ld + e], h[u] = dOs[(tx * 4 + u) * ld + e];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]), dp[u][v] = fmaf(g[u], h[v], dp[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int c = tx * 4 + v, i = i0 + c;
+                const bool ok = i < s && j0 + ty * 4 + u < s && (!masked || (i < split ? 0 : 1) == gk[u]);
+                const float pij = ok ? expf(acc[u][v] * p.scale - Mq[c]) / Lq[c] : 0.f;
+                Ps[(ty * 4 + u) * (AT + 1) + c] = pij;
+                dSs[(ty * 4 + u) * (AT + 1) + c] = pij * (dp[u][v] - Dq[c]) * p.scale;
+            }
+        __syncthreads();
+        for (int c = 0; c < AT; ++c) {
+            float qr[ADW], gr[ADW];
+#pragma unroll
+            for (int w = 0; w < ADW; ++w) {
+                const bool in = tx + 16 * w < d;
+                qr[w] = in ? Qs[c * ld + tx + 16 * w] : 0.f;
+                gr[w] = in ? dOs[c * ld + tx + 16 * w] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float pp = Ps[(ty * 4 + u) * (AT + 1) + c], ds = dSs[(ty * 4 + u) * (AT + 1) + c];
+#pragma unroll
+                for (int w = 0; w < ADW; ++w) dv[u][w] = fmaf(pp, gr[w], dv[u][w]), dk[u][w] = fmaf(ds, qr[w], dk[u][w]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int j = j0 + ty * 4 + u;
+        if (j >= s) continue;
+#pragma unroll
+        for (int w = 0; w < ADW; ++w)
+            if (tx + 16 * w < d) {
+                p.dk[(base + j) * d + tx + 16 * w] = dk[u][w];
+                p.dv[(base + j) * d + tx + 16 * w] = dv[u][w];
+            }
     }
 }
 // dQ, dK, dV planes -> dqkv token rows [lw*s + tok][3h] (rows [q; k; v], head-major), with the
@@ -445,10 +593,16 @@ void attention_bwd_f32(const float* q, const float* k, const float* v, const flo
     p.w = w;
     p.scale = 1.0f / sqrtf(float(d));
     p.lay = lay;
-    dim3 grid(unsigned((s + 63) / 64), unsigned(heads), unsigned(nloc));
-    k_attn_bwd_q<<<grid, 64, 0, st>>>(p);
+    if (d > 16 * ADW) throw CudaError("attention backward: head dim must be <= 128");
+    dim3 grid(unsigned((s + AT - 1) / AT), unsigned(heads), unsigned(nloc));
+    const size_t ld = size_t(d) + 1;
+    const size_t smq = (4 * AT * ld + AT * (AT + 1) + AT) * sizeof(float);
+    const size_t smkv = (4 * AT * ld + 2 * AT * (AT + 1) + 3 * AT) * sizeof(float);
+    SWF_CUDA(cudaFuncSetAttribute(k_attn_bwd_q, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smq)));
+    SWF_CUDA(cudaFuncSetAttribute(k_attn_bwd_kv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smkv)));
+    k_attn_bwd_q<<<grid, 256, smq, st>>>(p);
     SWF_LAUNCH_CHECK();
-    k_attn_bwd_kv<<<grid, 64, 0, st>>>(p);
+    k_attn_bwd_kv<<<grid, 256, smkv, st>>>(p);
     SWF_LAUNCH_CHECK();
     EpiParams e = ep;
     e.cur = lay;

@@ -70,55 +70,119 @@ __global__ void __launch_bounds__(256) k_gemm_f32(const float* __restrict__ A, c
     }
 }
 
-// One warp per query row: logits row, max-subtracted softmax normalised by the sum, then
-// O = sum_j p_j v_j -- the reference's per-row order (swin.hpp:176-186).
-__global__ void k_attn_f32(AttnParams p) {
-    extern __shared__ float sm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nw = blockDim.x >> 5;
-    const int s = p.s, d = p.d;
-    float* prow = sm + warp * (s + d);
-    float* qrow = prow + s;
-    const int tok = blockIdx.x * nw + warp;
-    const int head = blockIdx.y, lw = blockIdx.z;
-    if (tok >= s) return;
+// Windowed attention (swin.hpp:160-187) on 64-query tiles: 256 threads, K / V tiles of 64 keys
+// staged in shared memory (row pitch d+1). Pass 1 computes each row's max m and sum l of
+// exp(s - m) (online over key tiles); pass 2 accumulates O = sum_j (exp(s_j - m) / l) v_j in
+// ascending key order, the reference's normalise-then-multiply order. Each thread owns a 4 x 4 block
+// of the 64 x 64 score tile (rows ty*4+u, keys tx*4+v; a row group is one half-warp) and a
+// 4 x ceil(d/16) block of the output tile (columns tx + 16*w). d <= 128.
+constexpr int AT = 64, ADW = 8;
+
+__device__ __forceinline__ float hw_max(float v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float hw_sum(float v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ void load_tile(float* dst, const float* src, int r0, int s, int d) {
+    const int ld = d + 1;
+    for (int idx = threadIdx.x; idx < AT * d; idx += blockDim.x) {
+        const int r = idx / d, e = idx - (idx / d) * d;
+        dst[r * ld + e] = r0 + r < s ? src[i64(r0 + r) * d + e] : 0.f;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_attn_f32(AttnParams p) {
+    extern __shared__ float smf[];
+    const int d = p.d, ld = d + 1, s = p.s;
+    float *Qs = smf, *Ks = Qs + AT * ld, *Ps = Ks + AT * ld;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int head = blockIdx.y, lw = blockIdx.z, i0 = blockIdx.x * AT;
     const i64 base = (i64(lw) * p.heads + head) * s;
     const float* Q = reinterpret_cast<const float*>(p.q) + base * d;
     const float* Kp = reinterpret_cast<const float*>(p.k) + base * d;
     const float* Vp = reinterpret_cast<const float*>(p.v) + base * d;
-    for (int e = lane; e < d; e += 32) qrow[e] = Q[i64(tok) * d + e];
-    __syncwarp();
     const int gw = p.lay.loc2glob[lw];
     const bool masked = p.lay.g.shift > 0 && (gw / p.lay.g.nx) == p.lay.g.ny - 1;  // window.hpp:60
     const int split = (p.w - p.lay.g.shift) * p.w;  // seam groups are [0,split) and [split,s)
-    const int gq = tok < split ? 0 : 1;
-    float mx = -INFINITY;
-    for (int j = lane; j < s; j += 32) {
-        const float* kr = Kp + i64(j) * d;
-        float acc = 0.f;
-        for (int e = 0; e < d; ++e) acc = fmaf(qrow[e], kr[e], acc);
-        float l = acc * p.scale;
-        if (masked && ((j < split ? 0 : 1) != gq)) l = -INFINITY;
-        prow[j] = l;
-        mx = fmaxf(mx, l);
-    }
+    int gq[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.f;
-    for (int j = lane; j < s; j += 32) {
-        const float e = expf(prow[j] - mx);
-        prow[j] = e;
-        sum += e;
-    }
+    for (int u = 0; u < 4; ++u) gq[u] = i0 + ty * 4 + u < split ? 0 : 1;
+    load_tile(Qs, Q, i0, s, d);
+    float mr[4], lr[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    for (int j = lane; j < s; j += 32) prow[j] = prow[j] / sum;
-    __syncwarp();
-    float* O = reinterpret_cast<float*>(p.o) + (i64(lw) * s + tok) * p.ldo + head * d;
-    for (int e = lane; e < d; e += 32) {
-        float acc = 0.f;
-        for (int j = 0; j < s; ++j) acc = fmaf(Vp[i64(j) * d + e], prow[j], acc);
-        O[e] = acc;
+    for (int u = 0; u < 4; ++u) mr[u] = -INFINITY, lr[u] = 0.f;
+    float o[4][ADW] = {};
+    for (int pass = 0; pass < 2; ++pass)
+        for (int j0 = 0; j0 < s; j0 += AT) {
+            __syncthreads();
+            load_tile(Ks, Kp, j0, s, d);
+            __syncthreads();
+            float acc[4][4] = {};
+            for (int e = 0; e < d; ++e) {
+                float a[4], b[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[u] = Qs[(ty * 4 + u) * ld + e], b[u] = Ks[(tx * 4 + u) * ld + e];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
+            }
+            float x[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int j = j0 + tx * 4 + v;
+                    const bool ok = j < s && (!masked || (j < split ? 0 : 1) == gq[u]);
+                    x[u][v] = ok ? acc[u][v] * p.scale : -INFINITY;
+                }
+            if (pass == 0) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float mn = fmaxf(mr[u], hw_max(fmaxf(fmaxf(x[u][0], x[u][1]), fmaxf(x[u][2], x[u][3]))));
+                    float sum = 0.f;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) sum += x[u][v] == -INFINITY ? 0.f : expf(x[u][v] - mn);
+                    sum = hw_sum(sum);
+                    lr[u] = (mr[u] == -INFINITY ? 0.f : lr[u] * expf(mr[u] - mn)) + sum;
+                    mr[u] = mn;
+                }
+                continue;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    Ps[(ty * 4 + u) * (AT + 1) + tx * 4 + v] =
+                        x[u][v] == -INFINITY ? 0.f : expf(x[u][v] - mr[u]) / lr[u];
+            __syncthreads();
+            load_tile(Ks, Vp, j0, s, d);  // V tile over the K buffer
+            __syncthreads();
+            for (int c = 0; c < AT; ++c) {
+                float vr[ADW];
+#pragma unroll
+                for (int w = 0; w < ADW; ++w) vr[w] = tx + 16 * w < d ? Ks[c * ld + tx + 16 * w] : 0.f;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float pp = Ps[(ty * 4 + u) * (AT + 1) + c];
+#pragma unroll
+                    for (int w = 0; w < ADW; ++w) o[u][w] = fmaf(pp, vr[w], o[u][w]);
+                }
+            }
+        }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int i = i0 + ty * 4 + u;
+        if (i >= s) continue;
+        float* O = reinterpret_cast<float*>(p.o) + (i64(lw) * s + i) * p.ldo + head * d;
+#pragma unroll
+        for (int w = 0; w < ADW; ++w)
+            if (tx + 16 * w < d) O[tx + 16 * w] = o[u][w];
     }
 }
 
@@ -140,15 +204,11 @@ void gemm_f32(const float* A, const float* B, i64 M, int N, int K, int mode, con
 }
 
 void attention_f32(const AttnParams& p, cudaStream_t st) {
-    const int nw = 4;
-    const size_t smem = size_t(nw) * (p.s + p.d) * sizeof(float);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        SWF_CUDA(cudaFuncSetAttribute(k_attn_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        configured = smem;
-    }
-    dim3 grid(unsigned((p.s + nw - 1) / nw), unsigned(p.heads), unsigned(p.nloc));
-    k_attn_f32<<<grid, nw * 32, smem, st>>>(p);
+    if (p.d > 16 * ADW) throw CudaError("attention (FP32 mode): head dim must be <= 128");
+    const size_t smem = (2 * size_t(AT) * (p.d + 1) + AT * (AT + 1)) * sizeof(float);
+    SWF_CUDA(cudaFuncSetAttribute(k_attn_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    dim3 grid(unsigned((p.s + AT - 1) / AT), unsigned(p.heads), unsigned(p.nloc));
+    k_attn_f32<<<grid, 256, smem, st>>>(p);
     SWF_LAUNCH_CHECK();
 }
 
