@@ -22,6 +22,7 @@
 #ifndef SWINFLOW_CAPI_H
 #define SWINFLOW_CAPI_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -107,6 +108,12 @@ long long swf_param_count(const swf_model_cfg* cfg); /* parameter_count_formula 
 int swf_load_checkpoint(swf_ctx* ctx, const char* base);
 /* The same checks on the host only (no GPU needed). */
 int swf_verify_checkpoint(const swf_model_cfg* cfg, const char* base);
+/* fnv1a64 of n bytes continuing from h (0xcbf29ce484222325 to start; checkpoint.hpp / chunked_file.cpp
+ * checksums), for writers of either format. Host only. */
+uint64_t swf_fnv1a64(const void* data, size_t n, uint64_t h);
+/* parameter_arrays (model.hpp:140-168): name and shape (rows x cols, column-major) of canonical
+ * array i; rc 2 past the last array. */
+int swf_param_array(const swf_model_cfg* cfg, int i, char* name, int name_len, long long* rows, long long* cols);
 /* init_parameters (model.hpp:185-209) generated on the device with the reference counter RNG:
  * mode 0 = init_parameters(seed); 1 = init_parameters_random(seed, scale) (model.hpp:213-223);
  * 2 = init_parameters(seed) + scale*N(0,1) added only to the arrays it leaves at zero except the

@@ -142,6 +142,9 @@ def lib():
         L.swf_bench_kernel.argtypes = [vp, i, i, i, C.POINTER(d)]
         L.swf_profile.argtypes = [vp, i]
         L.swf_set_graphs.argtypes = [vp, i]
+        L.swf_fnv1a64.argtypes = [vp, C.c_size_t, u64]
+        L.swf_fnv1a64.restype = u64
+        L.swf_param_array.argtypes = [vp, i, C.c_char_p, i, C.POINTER(ll), C.POINTER(ll)]
         L.swf_profile_read.argtypes = [vp, vp, vp, i]
         L.swf_profile_launches.argtypes = [vp, vp, vp, i, C.POINTER(i)]
         L.swf_noise_field.argtypes = [vp, u64, u64, i, d, vp]
@@ -492,6 +495,41 @@ class ChunkedReader:
             self.close()
         except Exception:
             pass
+
+
+def param_arrays(cfg: ModelConfig) -> list[tuple[str, int, int]]:
+    """parameter_arrays (model.hpp:140-168): (name, rows, cols) in canonical order."""
+    out, i = [], 0
+    c = _Cfg(*astuple(cfg))
+    buf, r, k = C.create_string_buffer(64), C.c_longlong(), C.c_longlong()
+    while lib().swf_param_array(C.byref(c), i, buf, 64, C.byref(r), C.byref(k)) == OK:
+        out.append((buf.value.decode(), r.value, k.value))
+        i += 1
+    return out
+
+
+def fnv1a64(data, h: int = 0xcbf29ce484222325) -> int:
+    """fnv1a64 of a bytes-like object or contiguous numpy array (host)."""
+    a = np.ascontiguousarray(np.frombuffer(data, np.uint8) if isinstance(data, (bytes, bytearray)) else data)
+    return int(lib().swf_fnv1a64(a.ctypes.data_as(C.c_void_p), a.nbytes, h))
+
+
+def save_checkpoint(base: str, cfg: ModelConfig, arrays):
+    """save_params / save_named_arrays (checkpoint.hpp:29-47, 78-81): `arrays` yields the canonical
+    arrays (column-major, f32 or f64) one at a time; writes base.manifest + base.bin."""
+    off = 0
+    with open(base + ".bin", "wb") as fb, open(base + ".manifest", "w") as fm:
+        first = True
+        for (name, r, c), a in zip(param_arrays(cfg), arrays):
+            a = np.ascontiguousarray(a)
+            if a.size != r * c:
+                raise ConfigError(ERR_CONFIG, f"save_checkpoint: `{name}` has {a.size} elements, expected {r}x{c}")
+            if first:
+                fm.write("dtype f64\n" if a.dtype == np.float64 else "dtype f32\n")
+                first = False
+            fm.write(f"{name} {r}x{c} {off} {fnv1a64(a)}\n")
+            fb.write(a.tobytes())
+            off += a.nbytes
 
 
 def verify_checkpoint(cfg: ModelConfig, base: str):

@@ -128,21 +128,29 @@ public:
     // read_window_slice (chunked_file.cpp:156-188): out = [h*w][C] (FieldTensor of the rect)
     void read(const Rect& r, float* out) {
         check(r);
-        const int cy0 = r.y0 / ch_, cy1 = (r.y0 + r.h - 1) / ch_;
-        const int cx0 = r.x0 / cw_, cx1 = (r.x0 + r.w - 1) / cw_;
+        int cy0, cy1, cx0, cx1;
+        chunk_range(r, cy0, cy1, cx0, cx1);
         for (int cy = cy0; cy <= cy1; ++cy)
-            for (int cx = cx0; cx <= cx1; ++cx) {
-                const int y0 = cy * ch_, x0 = cx * cw_;
-                const int hh = std::min(ch_, H_ - y0), ww = std::min(cw_, W_ - x0);
-                load(cy, cx, hh, ww);
-                const int ys = std::max(r.y0, y0), ye = std::min(r.y0 + r.h, y0 + hh);
-                const int xs = std::max(r.x0, x0), xe = std::min(r.x0 + r.w, x0 + ww);
-                for (int c = 0; c < C_; ++c)
-                    for (int y = ys; y < ye; ++y) {
-                        const float* src = buf_.data() + (size_t(c) * hh + (y - y0)) * ww;
-                        float* dst = out + (size_t(y - r.y0) * r.w) * C_ + c;
-                        for (int x = xs; x < xe; ++x) dst[size_t(x - r.x0) * C_] = src[x - x0];
-                    }
+            for (int cx = cx0; cx <= cx1; ++cx) read_chunk(r, cy, cx, out);
+    }
+    // chunk rows / columns covering a (checked) rect
+    void chunk_range(const Rect& r, int& cy0, int& cy1, int& cx0, int& cx1) const {
+        cy0 = r.y0 / ch_, cy1 = (r.y0 + r.h - 1) / ch_;
+        cx0 = r.x0 / cw_, cx1 = (r.x0 + r.w - 1) / cw_;
+    }
+    // one chunk's part of read(): load + verify chunk (cy, cx), copy its intersection with r into out
+    // (disjoint from every other chunk's part, so readers on separate handles may fill one out)
+    void read_chunk(const Rect& r, int cy, int cx, float* out) {
+        const int y0 = cy * ch_, x0 = cx * cw_;
+        const int hh = std::min(ch_, H_ - y0), ww = std::min(cw_, W_ - x0);
+        load(cy, cx, hh, ww);
+        const int ys = std::max(r.y0, y0), ye = std::min(r.y0 + r.h, y0 + hh);
+        const int xs = std::max(r.x0, x0), xe = std::min(r.x0 + r.w, x0 + ww);
+        for (int c = 0; c < C_; ++c)
+            for (int y = ys; y < ye; ++y) {
+                const float* src = buf_.data() + (size_t(c) * hh + (y - y0)) * ww;
+                float* dst = out + (size_t(y - r.y0) * r.w) * C_ + c;
+                for (int x = xs; x < xe; ++x) dst[size_t(x - r.x0) * C_] = src[x - x0];
             }
     }
 

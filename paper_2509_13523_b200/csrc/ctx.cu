@@ -13,12 +13,15 @@
 //   rms(x) -> xm ; decode GEMM (+bias) -> out (window order of layout 0) ; scatter to pixels
 #include <cuda.h>
 
+#include <algorithm>
 #include <cmath>
 #include <fstream>
 #include <sstream>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -648,36 +651,91 @@ std::vector<CkptEntry> read_manifest(const std::string& base, const Dims& m, int
     return out;
 }
 
+// Read-ahead over a checkpoint's arrays: up to `depth` arrays are read, fnv1a64-verified and
+// converted to f32 by worker threads (one stream per thread) while the caller consumes earlier
+// ones in canonical order, so the serial checksum of load_named_arrays (checkpoint.hpp:50-80) runs
+// in parallel with the H2D copies and the device repack. Errors surface on the consuming call.
+class CkptReader {
+public:
+    CkptReader(const std::string& base, const std::vector<CkptEntry>& ent, int dtype, std::vector<std::string> names)
+        : base_(base), ent_(ent), es_(dtype == SWF_F64 ? 8 : 4), names_(std::move(names)), slot_(ent.size()) {
+        depth_ = int(std::max(2u, std::min(8u, std::thread::hardware_concurrency())));
+        if (const char* e = std::getenv("SWF_CKPT_THREADS")) depth_ = std::max(0, std::atoi(e) - 1);
+    }
+    ~CkptReader() {
+        for (auto& s : slot_)
+            if (s.th.joinable()) s.th.join();
+    }
+    // f32 contents of array ai (valid until the next call)
+    const float* get(int ai) {
+        while (next_ < int(slot_.size()) && next_ <= ai + depth_) {  // arrays ai .. ai + depth_ in flight
+            const int k = next_++;
+            slot_[k].th = std::thread([this, k] { work(k); });
+        }
+        Slot& s = slot_[ai];
+        if (s.th.joinable()) s.th.join();
+        if (!s.err.empty()) throw IoError(s.err);
+        if (prev_ >= 0 && prev_ != ai) release(prev_);
+        prev_ = ai;
+        return s.f32.data();
+    }
+
+private:
+    struct Slot {
+        std::vector<float> f32;
+        std::string err;
+        std::thread th;
+    };
+    void release(int k) { std::vector<float>().swap(slot_[k].f32); }
+    void work(int k) {
+        Slot& s = slot_[k];
+        const CkptEntry& e = ent_[k];
+        std::ifstream bin(base_ + ".bin", std::ios::binary);
+        std::vector<char> raw(e.n * es_);
+        if (bin) {
+            bin.seekg(std::streamoff(e.offset));
+            bin.read(raw.data(), std::streamsize(raw.size()));
+        }
+        if (!bin) {
+            s.err = "checkpoint truncated at `" + names_[k] + "` in " + base_;
+            return;
+        }
+        if (fnv1a64(raw.data(), raw.size()) != e.sum) {
+            s.err = "IntegrityError: checksum mismatch for `" + names_[k] + "` in " + base_;
+            return;
+        }
+        s.f32.resize(e.n);
+        if (es_ == 8) {
+            const double* d = reinterpret_cast<const double*>(raw.data());
+            for (size_t i = 0; i < e.n; ++i) s.f32[i] = static_cast<float>(d[i]);
+        } else {
+            std::memcpy(s.f32.data(), raw.data(), raw.size());
+        }
+    }
+    std::string base_;
+    const std::vector<CkptEntry>& ent_;
+    size_t es_;
+    std::vector<std::string> names_;
+    std::vector<Slot> slot_;
+    int depth_ = 4, next_ = 0, prev_ = -1;
+};
+
 void load_checkpoint(swf_ctx* c, const std::string& base) {
     allocate(c);
     const Dims& m = c->m;
     int dtype = SWF_F32;
     const auto ent = read_manifest(base, m, &dtype);
-    std::ifstream bin(base + ".bin", std::ios::binary);
-    if (!bin) throw IoError("cannot open checkpoint: " + base + ".bin");
-    const size_t es = dtype == SWF_F64 ? 8 : 4;
+    {
+        std::ifstream bin(base + ".bin", std::ios::binary);
+        if (!bin) throw IoError("cannot open checkpoint: " + base + ".bin");
+    }
     float* stage = nullptr;
     SWF_CUDA(cudaMalloc(&stage, max_array(m) * sizeof(float)));
-    std::vector<char> raw;
-    std::vector<float> f32;
     try {
+        CkptReader rd(base, ent, dtype, param_names(m));
         load_params_from(c, [&](int ai, size_t n) -> float* {
-            SWF_CUDA(cudaStreamSynchronize(c->st));
-            const CkptEntry& e = ent[ai];
-            raw.resize(n * es);
-            bin.seekg(std::streamoff(e.offset));
-            bin.read(raw.data(), std::streamsize(raw.size()));
-            if (!bin) throw IoError("checkpoint truncated at `" + param_names(m)[ai] + "` in " + base);
-            if (fnv1a64(raw.data(), raw.size()) != e.sum)
-                throw IoError("IntegrityError: checksum mismatch for `" + param_names(m)[ai] + "` in " + base);
-            const float* src = reinterpret_cast<const float*>(raw.data());
-            if (dtype == SWF_F64) {
-                f32.resize(n);
-                const double* d = reinterpret_cast<const double*>(raw.data());
-                for (size_t i = 0; i < n; ++i) f32[i] = static_cast<float>(d[i]);
-                src = f32.data();
-            }
-            SWF_CUDA(cudaMemcpyAsync(stage, src, n * 4, cudaMemcpyHostToDevice, c->st));
+            SWF_CUDA(cudaStreamSynchronize(c->st));  // the previous array's repack is done with stage
+            SWF_CUDA(cudaMemcpyAsync(stage, rd.get(ai), n * 4, cudaMemcpyHostToDevice, c->st));
             SWF_CUDA(cudaStreamSynchronize(c->st));
             return stage;
         });
@@ -1489,45 +1547,57 @@ unsigned long long read_local_chunked(const swf_ctx* c, const std::string& path,
         }
         runs.swap(st);
     }
+    // every run's covering chunks are split over T readers (own file handles; chunk parts are
+    // disjoint in the run buffer), then the run's windows are gathered into the local order
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const int T = std::max(1, std::min<int>(int(runs.size()), int(std::min(16u, hw))));
-    std::vector<unsigned long long> reads(T, 0);
+    const int T = int(std::min(16u, hw));
+    std::vector<std::unique_ptr<chunked::Reader>> rds(T);
     std::vector<std::exception_ptr> errs(T);
-    auto work = [&](int t) {
-        try {
-            chunked::Reader rd(path);
-            require(rd.height() == c->H && rd.width() == c->W,
-                    "chunked input " + path + ": grid " + std::to_string(rd.height()) + "x" +
-                        std::to_string(rd.width()) + " != model grid " + std::to_string(c->H) + "x" +
-                        std::to_string(c->W));
-            require(rd.channels() == C, "chunked input " + path + ": " + std::to_string(rd.channels()) +
-                                            " channels, expected " + std::to_string(C));
-            std::vector<float> buf;
-            for (size_t j = t; j < runs.size(); j += T) {
-                const Run& u = runs[j];
-                const chunked::Rect rc{u.wy0 * w + c->band * R, u.wx0 * w, u.nwy * R, u.nwx * w};
-                buf.resize(size_t(rc.h) * rc.w * C);
-                rd.read(rc, buf.data());
-                for (int a = 0; a < u.nwy; ++a)
-                    for (int b = 0; b < u.nwx; ++b) {
-                        const int lw = g2l[(u.wy0 + a) * nx + u.wx0 + b];
-                        for (int k = 0; k < R; ++k)
-                            std::memcpy(dst + (size_t(lw) * R * w + size_t(k) * w) * C,
-                                        buf.data() + (size_t(a * R + k) * rc.w + size_t(b) * w) * C,
-                                        size_t(w) * C * sizeof(float));
-                    }
+    auto parallel = [&](int n, auto&& fn) {  // fn(t, i) for i = t, t + T, ... < n on min(T, n) threads
+        const int nt = std::max(1, std::min(T, n));
+        auto body = [&](int t) {
+            try {
+                for (int i = t; i < n; i += nt) fn(t, i);
+            } catch (...) {
+                errs[t] = std::current_exception();
             }
-            reads[t] = rd.chunk_reads();
-        } catch (...) {
-            errs[t] = std::current_exception();
-        }
+        };
+        std::vector<std::thread> ths;
+        for (int t = 1; t < nt; ++t) ths.emplace_back(body, t);
+        body(0);
+        for (auto& th : ths) th.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
     };
-    std::vector<std::thread> ths;
-    for (int t = 1; t < T; ++t) ths.emplace_back(work, t);
-    work(0);
-    for (auto& th : ths) th.join();
-    for (auto& e : errs)
-        if (e) std::rethrow_exception(e);
+    parallel(T, [&](int t, int) {
+        rds[t] = std::make_unique<chunked::Reader>(path);
+        require(rds[t]->height() == c->H && rds[t]->width() == c->W,
+                "chunked input " + path + ": grid " + std::to_string(rds[t]->height()) + "x" +
+                    std::to_string(rds[t]->width()) + " != model grid " + std::to_string(c->H) + "x" +
+                    std::to_string(c->W));
+        require(rds[t]->channels() == C, "chunked input " + path + ": " + std::to_string(rds[t]->channels()) +
+                                             " channels, expected " + std::to_string(C));
+    });
+    std::vector<float> buf;
+    for (const Run& u : runs) {
+        const chunked::Rect rc{u.wy0 * w + c->band * R, u.wx0 * w, u.nwy * R, u.nwx * w};
+        rds[0]->check(rc);
+        int cy0, cy1, cx0, cx1;
+        rds[0]->chunk_range(rc, cy0, cy1, cx0, cx1);
+        const int ncx = cx1 - cx0 + 1, nch = (cy1 - cy0 + 1) * ncx;
+        buf.resize(size_t(rc.h) * rc.w * C);
+        parallel(nch, [&](int t, int i) { rds[t]->read_chunk(rc, cy0 + i / ncx, cx0 + i % ncx, buf.data()); });
+        parallel(u.nwy * u.nwx, [&](int, int i) {
+            const int a = i / u.nwx, b = i % u.nwx;
+            const int lw = g2l[(u.wy0 + a) * nx + u.wx0 + b];
+            for (int k = 0; k < R; ++k)
+                std::memcpy(dst + (size_t(lw) * R * w + size_t(k) * w) * C,
+                            buf.data() + (size_t(a * R + k) * rc.w + size_t(b) * w) * C, size_t(w) * C * sizeof(float));
+        });
+    }
+    std::vector<unsigned long long> reads;
+    for (auto& r : rds)
+        if (r) reads.push_back(r->chunk_reads());
     unsigned long long n = 0;
     for (auto v : reads) n += v;
     return n;
@@ -1886,25 +1956,33 @@ int swf_load_checkpoint(swf_ctx* c, const char* base) {
 
 // Host-only verification of a checkpoint against a model config (no GPU): manifest layout and
 // every array's fnv1a64 checksum.
+uint64_t swf_fnv1a64(const void* data, size_t n, uint64_t h) { return fnv1a64(data, n, h); }
+
+int swf_param_array(const swf_model_cfg* cfg, int i, char* name, int name_len, long long* rows, long long* cols) {
+    SWF_API_TRY({
+        require(cfg && name && rows && cols && name_len > 0, "null argument");
+        const Dims m = make_dims(*cfg, SWF_PREC_FP32);
+        const auto names = param_names(m);
+        const auto shapes = param_shapes(m);
+        if (i < 0 || i >= int(names.size())) throw ConfigError("param_array: index out of range");
+        std::snprintf(name, size_t(name_len), "%s", names[i].c_str());
+        *rows = shapes[i].first;
+        *cols = shapes[i].second;
+    })
+}
+
 int swf_verify_checkpoint(const swf_model_cfg* cfg, const char* base) {
     SWF_API_TRY({
         require(cfg && base, "null argument");
         const Dims m = make_dims(*cfg, SWF_PREC_FP32);
         int dtype = SWF_F32;
         const auto ent = read_manifest(base, m, &dtype);
-        std::ifstream bin(std::string(base) + ".bin", std::ios::binary);
-        if (!bin) throw IoError(std::string("cannot open checkpoint: ") + base + ".bin");
-        const size_t es = dtype == SWF_F64 ? 8 : 4;
-        std::vector<char> raw;
-        const auto names = param_names(m);
-        for (size_t i = 0; i < ent.size(); ++i) {
-            raw.resize(ent[i].n * es);
-            bin.seekg(std::streamoff(ent[i].offset));
-            bin.read(raw.data(), std::streamsize(raw.size()));
-            if (!bin) throw IoError("checkpoint truncated at `" + names[i] + "`");
-            if (fnv1a64(raw.data(), raw.size()) != ent[i].sum)
-                throw IoError("IntegrityError: checksum mismatch for `" + names[i] + "`");
+        {
+            std::ifstream bin(std::string(base) + ".bin", std::ios::binary);
+            if (!bin) throw IoError(std::string("cannot open checkpoint: ") + base + ".bin");
         }
+        CkptReader rd(base, ent, dtype, param_names(m));
+        for (size_t i = 0; i < ent.size(); ++i) rd.get(int(i));
     })
 }
 

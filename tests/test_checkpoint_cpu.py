@@ -55,3 +55,18 @@ def test_missing_and_truncated(ckpt, tmp_path):
         f.truncate(os.path.getsize(base + ".bin") // 2)
     with pytest.raises(swf.IoError, match="truncated"):
         swf.verify_checkpoint(swf.ModelConfig(**TINY), base)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_save_checkpoint_matches_reference_format(tmp_path, dtype):
+    """save_checkpoint writes the bytes the reference's save_named_arrays writes (restated by the
+    oracle), and param_arrays lists parameter_arrays' names and shapes."""
+    oc, sc = o.ModelConfig(**TINY), swf.ModelConfig(**TINY)
+    assert swf.param_arrays(sc) == [(n, r, c) for n, r, c in o.param_shapes(oc)]
+    p = o.init_params(oc, 9, random=True, dtype=dtype)
+    o.save_named_arrays(str(tmp_path / "ref"), oc, p)
+    swf.save_checkpoint(str(tmp_path / "ours"), sc, o.split_params(oc, p))
+    for ext in (".manifest", ".bin"):
+        assert (tmp_path / ("ref" + ext)).read_bytes() == (tmp_path / ("ours" + ext)).read_bytes()
+    swf.verify_checkpoint(sc, str(tmp_path / "ours"))
+    assert swf.fnv1a64(b"") == 0xcbf29ce484222325
