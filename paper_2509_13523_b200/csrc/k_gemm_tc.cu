@@ -78,6 +78,25 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
+// release-ordered arrive (cluster scope): publishes shared-memory writes made before it to the
+// waiting threads of either CTA (the tile queue, once per tile)
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t bar_cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acquire_cluster(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void tma_load_2cta(uint32_t dst, const void* tmap, uint32_t bar_cluster, int c0, int c1,
                                               uint64_t policy) {
     asm volatile(
@@ -325,11 +344,52 @@ __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, i
     return ss;
 }
 
+// Dynamic tile schedule: the leader CTA's producer thread takes tile indices from a global counter
+// (atomicAdd, one per tile) and publishes them through a kQ-slot ring in both CTAs' shared memory;
+// every consumer role (the peer's producer, the MMA thread, the 16 epilogue warps) reads its next
+// tile from the ring. Clusters then take tiles in index order as they free up, so the clusters
+// sharing an A row block (consecutive indices) start it together and its K slices are fetched from
+// HBM once, instead of drifting apart over the static round-robin schedule (which re-read A ~3x).
+constexpr int kQ = 4;
+constexpr uint32_t kQConsumers = 1 /*peer producer*/ + 1 /*MMA*/ + 2 * kEpiWarps;
+struct TileQueue {
+    uint64_t* full;  // [kQ], one arrival (the scheduler) per round, in each CTA
+    uint64_t* empty; // [kQ], kQConsumers arrivals per round, leader CTA only
+    int* tile;       // [kQ]
+    int* counter;    // global; nullptr -> static round-robin schedule
+    i64 total;
+    int cluster_id, n_clusters;
+    // scheduler (leader producer): publish the i-th tile of this cluster
+    __device__ void publish(int i) {
+        const int slot = i % kQ;
+        const uint32_t round = uint32_t(i / kQ);
+        mbar_wait_acquire_cluster(smem_u32(&empty[slot]), (round & 1) ^ 1);
+        const i64 t = atomicAdd(counter, 1);
+        const int v = t < total ? int(t) : -1;
+        tile[slot] = v;
+        st_cluster_u32(map_to_rank(smem_u32(&tile[slot]), 1), uint32_t(v));
+        mbar_arrive_release_cluster(map_to_rank(smem_u32(&full[slot]), 1));
+        mbar_arrive_release_cluster(smem_u32(&full[slot]));
+    }
+    // consumer: the i-th tile (-1: done); arrive = whether this thread signals the slot free
+    __device__ i64 next(int i, bool arrive) {
+        if (!counter) {
+            const i64 t = cluster_id + i64(i) * n_clusters;
+            return t < total ? t : -1;
+        }
+        const int slot = i % kQ;
+        mbar_wait_acquire_cluster(smem_u32(&full[slot]), uint32_t(i / kQ) & 1);
+        const int v = *reinterpret_cast<volatile int*>(&tile[slot]);
+        if (arrive) mbar_arrive_release_cluster(map_to_rank(smem_u32(&empty[slot]), 0));
+        return v;
+    }
+};
+
 // ---------------------------------------------------------------- the kernel
 template <int BN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, i64 M, int n_tiles,
-              int num_k, EpiParams ep) {
+              int num_k, EpiParams ep, int* sched) {
     using C = Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -341,6 +401,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tfull_bar = bars + 2 * C::kStages;
     uint64_t* tempty_bar = bars + 2 * C::kStages + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
+    uint64_t* q_full = bars + 2 * C::kStages + 5;
+    uint64_t* q_empty = q_full + kQ;
+    int* q_tile = reinterpret_cast<int*>(q_empty + kQ);
+    static_assert((2 * C::kStages + 5 + 2 * kQ) * 8 + kQ * 4 <= 256, "barrier region");
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = cluster_rank();
@@ -358,6 +422,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_init(smem_u32(&tfull_bar[a]), 1);
             mbar_init(smem_u32(&tempty_bar[a]), 2 * kEpiWarps);
         }
+        for (int a = 0; a < kQ; ++a) {
+            mbar_init(smem_u32(&q_full[a]), 1);
+            mbar_init(smem_u32(&q_empty[a]), kQConsumers);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
@@ -373,6 +441,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    TileQueue tq{q_full, q_empty, q_tile, sched, total, cluster_id, n_clusters};
 
     if (warp == 0) {
         // ===== TMA producer (both CTAs; each loads its A half and B half, signalling the leader)
@@ -381,7 +450,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
-            for (i64 t = cluster_id; t < total; t += n_clusters) {
+            const bool sched_here = sched && leader;
+            if (sched_here) tq.publish(0);
+            for (int i = 0;; ++i) {
+                const i64 t = tq.next(i, !leader);
+                if (t < 0) break;
+                if (sched_here) tq.publish(i + 1);  // one tile ahead: the atomic's latency is hidden
                 int m_blk, n_blk;
                 tile_coords(t, n_tiles, m_tiles, m_blk, n_blk);
                 const int row_a = m_blk * 2 * BM + int(crank) * BM;
@@ -406,7 +480,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (i64 t = cluster_id; t < total; t += n_clusters) {
+            for (int i = 0;; ++i) {
+                if (tq.next(i, true) < 0) break;
                 mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t dtm = tmem_base + uint32_t(acc * BN);
@@ -441,7 +516,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t tempty_leader = map_to_rank(smem_u32(&tempty_bar[0]), 0);
         float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256) + (warp - kEpiWarp0) * 32 * 33;
         const uint64_t pol_out = policy_evict_first();
-        for (i64 t = cluster_id; t < total; t += n_clusters) {
+        for (int i = 0;; ++i) {
+            const i64 t = tq.next(i, lane == 0);
+            if (t < 0) break;
             int m_blk, n_blk;
             tile_coords(t, n_tiles, m_tiles, m_blk, n_blk);
             mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
@@ -562,6 +639,18 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+// per-device tile counter of the dynamic schedule (reset by a memset node before every launch;
+// GEMMs of one device are stream-ordered)
+int* sched_counter() {
+    static std::mutex mu;
+    static int* ctr[64] = {};
+    int dev = 0;
+    SWF_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ctr[dev]) SWF_CUDA(cudaMalloc(&ctr[dev], 256));
+    return ctr[dev];
+}
+
 template <int BN, int MODE>
 void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiParams& ep, cudaStream_t st) {
     using C = Cfg<BN>;
@@ -590,7 +679,13 @@ void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiP
     cfg.numAttrs = 0;
     const CUtensorMap* a = reinterpret_cast<const CUtensorMap*>(&A);
     const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(&B);
-    SWF_CUDA(cudaLaunchKernelEx(&cfg, kern, *a, *b, M, n_tiles, K / BK, ep));
+    int* sched = nullptr;
+    static const bool dynamic = getenv("SWF_GEMM_STATIC") == nullptr;
+    if (dynamic) {
+        sched = sched_counter();
+        SWF_CUDA(cudaMemsetAsync(sched, 0, sizeof(int), st));
+    }
+    SWF_CUDA(cudaLaunchKernelEx(&cfg, kern, *a, *b, M, n_tiles, K / BK, ep, sched));
 }
 
 template <int BN>
