@@ -281,17 +281,18 @@ __device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0,
     }
 }
 
-// Rasterisation: bands of kGroupM m-blocks are swept n-block by n-block. With kGroupM = 1 the
-// concurrently running clusters cover one A row-block across all N tiles (A read once from HBM),
-// while the weights B stay L2-resident under the evict_last policy.
-constexpr int kGroupM = 1;
-__device__ __forceinline__ void tile_coords(i64 t, int n_tiles, i64 m_tiles, int& m_blk, int& n_blk) {
-    const i64 per_group = i64(kGroupM) * n_tiles;
+// Rasterisation: bands of group_m m-blocks are swept n-block by n-block (m fastest inside a band).
+// With the dynamic schedule the concurrently running clusters take consecutive tile indices, i.e.
+// group_m row blocks x (clusters / group_m) N tiles: each A slice is shared by fewer clusters at
+// the same instant (group_m = 1: every cluster on one row block), while the weights B stay
+// L2-resident under the evict_last policy.
+__device__ __forceinline__ void tile_coords(i64 t, int n_tiles, i64 m_tiles, int group_m, int& m_blk, int& n_blk) {
+    const i64 per_group = i64(group_m) * n_tiles;
     const i64 g = t / per_group;
     const i64 r = t - g * per_group;
-    const i64 gm = min(i64(kGroupM), m_tiles - g * kGroupM);
+    const i64 gm = min(i64(group_m), m_tiles - g * group_m);
     n_blk = int(r / gm);
-    m_blk = int(g * kGroupM + r % gm);
+    m_blk = int(g * group_m + r % gm);
 }
 
 // fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)
@@ -389,7 +390,7 @@ struct TileQueue {
 template <int BN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, i64 M, int n_tiles,
-              int num_k, EpiParams ep, int* sched) {
+              int num_k, EpiParams ep, int* sched, int group_m) {
     using C = Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -457,7 +458,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (t < 0) break;
                 if (sched_here) tq.publish(i + 1);  // one tile ahead: the atomic's latency is hidden
                 int m_blk, n_blk;
-                tile_coords(t, n_tiles, m_tiles, m_blk, n_blk);
+                tile_coords(t, n_tiles, m_tiles, group_m, m_blk, n_blk);
                 const int row_a = m_blk * 2 * BM + int(crank) * BM;
                 const int row_b = n_blk * BN + int(crank) * (BN / 2);
                 for (int kb = 0; kb < num_k; ++kb) {
@@ -520,7 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const i64 t = tq.next(i, lane == 0);
             if (t < 0) break;
             int m_blk, n_blk;
-            tile_coords(t, n_tiles, m_tiles, m_blk, n_blk);
+            tile_coords(t, n_tiles, m_tiles, group_m, m_blk, n_blk);
             mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
             tc_fence_after();
             const i64 row = i64(m_blk) * 2 * BM + crank * BM + q * 32 + lane;
@@ -685,7 +686,9 @@ void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiP
         sched = sched_counter();
         SWF_CUDA(cudaMemsetAsync(sched, 0, sizeof(int), st));
     }
-    SWF_CUDA(cudaLaunchKernelEx(&cfg, kern, *a, *b, M, n_tiles, K / BK, ep, sched));
+    static const int env_gm = getenv("SWF_GEMM_GROUPM") ? std::max(1, atoi(getenv("SWF_GEMM_GROUPM"))) : 0;
+    const int group_m = env_gm ? env_gm : 1;
+    SWF_CUDA(cudaLaunchKernelEx(&cfg, kern, *a, *b, M, n_tiles, K / BK, ep, sched, group_m));
 }
 
 template <int BN>
