@@ -184,7 +184,7 @@ def run_reference(args, rank: int, world: int):
               "swin.hpp forward; pixels/s extrapolated per FLOP to the 20-block 720x1440 step")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pixels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "AERIS-1.3B denoiser step, 720x1440, w=60 (sampled on CPU)",
                        "grid": [H, W], "model": "swin-dit-1.3B", "window": 60},
             "cpu_baseline": {"value": v, "unit": "pixels/s", "cores": o.num_threads(), "kind": "port",
@@ -256,7 +256,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         t = torch.tensor([ms], device=f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    pixels = H * W  # weak scaling unit: the whole grid is one step (WP shards it)
+    pixels = H * W  # strong scaling: the whole grid is one step at every N (WP shards it)
     value = pixels / (ms / 1e3)
     step_flops = flops_per_step(CFG, H * W)
     peaks = measured_peaks()
@@ -306,7 +306,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "pixels/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": ("AERIS-1.3B-shaped denoiser step (BASELINE.json configs[1])" if args.workload == "c2"
                                     else "AERIS-40B-shaped wide-layer slice, 2 blocks (BASELINE.json configs[3])"),
@@ -406,7 +406,7 @@ def run_c5(args, rank: int, world: int, local_rank: int):
         step_flops = flops_per_step(CFG, H * W)
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "pixels/s", "n_gpus": world, "steps": 1, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "ensemble generation (BASELINE.json configs[4]), replicas",
                        "grid": [H, W], "members": args.members, "members_per_gpu": per,
