@@ -456,7 +456,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int i = 0;; ++i) {
                 const i64 t = tq.next(i, !leader);
                 if (t < 0) break;
-                if (sched_here) tq.publish(i + 1);  // one tile ahead: the atomic's latency is hidden
                 int m_blk, n_blk;
                 tile_coords(t, n_tiles, m_tiles, group_m, m_blk, n_blk);
                 const int row_a = m_blk * 2 * BM + int(crank) * BM;
@@ -467,6 +466,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (leader) mbar_expect_tx(smem_u32(&full_bar[stage]), 2 * C::kStage);
                     tma_load_2cta(smem_u32(sA + stage * C::kStageA), &tmA, fb, kb * BK, row_a, pol_a);
                     tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK, row_b, pol_b);
+                    // the next tile is taken once this tile's first stage is in flight, so the
+                    // atomic's round trip overlaps the loads (one tile ahead of every consumer)
+                    if (sched_here && kb == 0) tq.publish(i + 1);
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
