@@ -80,7 +80,10 @@ constexpr int kPoly8 = SWF_ATTN_POLY8;
 constexpr int kKPT = 128 / kSplit;  // keys per thread per tile
 constexpr int kThreads = 128 + 128 * kSplit;
 constexpr int kNS = 3;       // S buffers in TMEM
-constexpr uint32_t kBackoffNs = 40;  // poll back-off of the control warps' barrier waits
+#ifndef SWF_ATTN_BACKOFF
+#define SWF_ATTN_BACKOFF 40
+#endif
+constexpr uint32_t kBackoffNs = SWF_ATTN_BACKOFF;  // poll back-off of the control warps' barrier waits
 constexpr uint32_t kTO = 384;  // TMEM column of O
 constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
 
@@ -184,7 +187,7 @@ __device__ __forceinline__ void mbar_sleep_wait(uint32_t bar, uint32_t parity) {
             : "r"(bar), "r"(parity)
             : "memory");
         if (done) break;
-        __nanosleep(kBackoffNs);
+        if constexpr (kBackoffNs > 0) __nanosleep(kBackoffNs);
     }
 }
 // named barrier of the kSplit warps sharing a TMEM lane quadrant (one per key split)
