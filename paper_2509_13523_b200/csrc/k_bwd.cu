@@ -16,51 +16,76 @@ namespace swf {
 
 namespace {
 
-constexpr int TB = 64, TK = 16;
 
 // C[i][j] = beta * C[i][j] + sum_k A(i,k) B(k,j); A(i,k) = A[i*sai + k*sak], B(k,j) = B[k*sbk + j*sbj],
-// C row stride ldc. 256 threads, 64 x 64 tile, 4 x 4 per thread.
+// C row stride ldc. 256 threads, 128 x 128 tile, 8 x 8 per thread (rows ty*4 + {0..3, 64..67},
+// columns tx*4 + {0..3, 64..67}: two float4 shared-memory reads per operand per k), k slices of 8
+// double-buffered in shared memory; each operand is loaded along its contiguous dimension.
+constexpr int GB = 128, GK = 8;
 __global__ void __launch_bounds__(256) k_gemm_strided(int M, int N, int K, const float* __restrict__ A, i64 sai,
                                                       i64 sak, const float* __restrict__ B, i64 sbk, i64 sbj,
                                                       float* __restrict__ C, i64 ldc, float beta) {
-    __shared__ float As[TK][TB + 1], Bs[TK][TB + 1];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int i0 = blockIdx.y * TB, j0 = blockIdx.x * TB;
+    __shared__ __align__(16) float As[2][GK][GB + 4], Bs[2][GK][GB + 4];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int i0 = blockIdx.y * GB, j0 = blockIdx.x * GB;
     const bool a_k_fast = sak == 1, b_k_fast = sbk == 1;
-    float acc[4][4] = {};
-    for (int k0 = 0; k0 < K; k0 += TK) {
-        // consecutive threads walk the operand's contiguous dimension (coalesced loads)
-        for (int t = threadIdx.x; t < TB * TK; t += 256) {
-            const int r = a_k_fast ? t / TK : t % TB, k = a_k_fast ? t % TK : t / TB;
+    float ra[4], rb[4];  // this thread's 4 elements of each operand's next k slice
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = tid + 256 * u;  // 1024 elements = 128 rows x 8 k
+            const int r = a_k_fast ? t / GK : t % GB, k = a_k_fast ? t % GK : t / GB;
             const int gi = i0 + r, gk = k0 + k;
-            As[k][r] = (gi < M && gk < K) ? A[gi * sai + gk * sak] : 0.f;
-            const int c = b_k_fast ? t / TK : t % TB, kk = b_k_fast ? t % TK : t / TB;
+            ra[u] = (gi < M && gk < K) ? A[gi * sai + gk * sak] : 0.f;
+            const int c = b_k_fast ? t / GK : t % GB, kk = b_k_fast ? t % GK : t / GB;
             const int gj = j0 + c, gk2 = k0 + kk;
-            Bs[kk][c] = (gj < N && gk2 < K) ? B[gk2 * sbk + gj * sbj] : 0.f;
+            rb[u] = (gj < N && gk2 < K) ? B[gk2 * sbk + gj * sbj] : 0.f;
         }
-        __syncthreads();
+    };
+    auto stash = [&](int buf) {
 #pragma unroll
-        for (int k = 0; k < TK; ++k) {
-            float a[4], b[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                a[u] = As[k][ty * 4 + u];
-                b[u] = Bs[k][tx * 4 + u];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
+        for (int u = 0; u < 4; ++u) {
+            const int t = tid + 256 * u;
+            const int r = a_k_fast ? t / GK : t % GB, k = a_k_fast ? t % GK : t / GB;
+            As[buf][k][r] = ra[u];
+            const int c = b_k_fast ? t / GK : t % GB, kk = b_k_fast ? t % GK : t / GB;
+            Bs[buf][kk][c] = rb[u];
         }
-        __syncthreads();
+    };
+    float acc[8][8] = {};
+    fetch(0);
+    stash(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < K; k0 += GK) {
+        const bool more = k0 + GK < K;
+        if (more) fetch(k0 + GK);  // global loads in flight during this slice's FMAs
+#pragma unroll
+        for (int k = 0; k < GK; ++k) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(av[u], bv[v], acc[u][v]);
+        }
+        if (more) {
+            stash(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int gi = i0 + ty * 4 + u;
+    for (int u = 0; u < 8; ++u) {
+        const int gi = i0 + (u < 4 ? ty * 4 + u : 64 + ty * 4 + u - 4);
         if (gi >= M) continue;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int gj = j0 + tx * 4 + v;
+        for (int v = 0; v < 8; ++v) {
+            const int gj = j0 + (v < 4 ? tx * 4 + v : 64 + tx * 4 + v - 4);
             if (gj >= N) continue;
             float* c = C + gi * ldc + gj;
             *c = beta == 0.f ? acc[u][v] : beta * *c + acc[u][v];
@@ -537,7 +562,7 @@ __global__ void k_axpy(const float* __restrict__ x, i64 n, float a, float* __res
 void gemm_strided_f32(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj,
                       float* C, i64 ldc, float beta, cudaStream_t st) {
     if (M <= 0 || N <= 0) return;
-    dim3 grid(unsigned((N + TB - 1) / TB), unsigned((M + TB - 1) / TB));
+    dim3 grid(unsigned((N + GB - 1) / GB), unsigned((M + GB - 1) / GB));
     k_gemm_strided<<<grid, 256, 0, st>>>(M, N, K, A, sai, sak, B, sbk, sbj, C, ldc, beta);
     SWF_LAUNCH_CHECK();
 }
