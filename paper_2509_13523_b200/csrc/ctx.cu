@@ -109,6 +109,7 @@ struct swf_ctx {
     void** d_qkv_dst = nullptr;      // device table: attention planes of every rank
     void** d_o_dst = nullptr;        // device table: attention-output (xm) buffer of every rank
     int* d_epoch = nullptr;          // device barrier epoch (advanced by k_peer_barrier; graph-safe)
+    int* d_sched = nullptr;          // GEMM dynamic-schedule tile counter (reset before every launch)
     // TMA maps (BF16 path)
     TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec, tm_q, tm_k, tm_vt;
     TmaMap tm_so;  // sbuf viewed as [M][hp] (attention output of the kernel benchmark)
@@ -416,6 +417,7 @@ void allocate(swf_ctx* c) {
     c->bar_flags = dalloc<int>(c, 64);
     c->d_flag_table = dalloc<int*>(c, 8);
     c->d_epoch = dalloc<int>(c, 1);
+    c->d_sched = dalloc<int>(c, 1);
     c->d_churn_key = dalloc<u64>(c, 1);
     SWF_CUDA(cudaMallocHost(&c->h_churn_key, sizeof(u64)));
     c->peer.assign(c->world, Peer{{nullptr, nullptr}, nullptr, nullptr, nullptr});
@@ -855,6 +857,7 @@ EpiParams base_ep(swf_ctx* c) {
     ep.h = c->m.h;
     ep.d = c->m.d;
     ep.heads = c->m.heads;
+    ep.sched = c->d_sched;
     ep.rope_row = reinterpret_cast<const float2*>(c->rope_row);
     ep.rope_col = reinterpret_cast<const float2*>(c->rope_col);
     ep.rope_nrow = c->H + c->m.w;

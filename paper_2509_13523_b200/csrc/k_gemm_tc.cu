@@ -642,8 +642,8 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// per-device tile counter of the dynamic schedule (reset by a memset node before every launch;
-// GEMMs of one device are stream-ordered)
+// per-device tile counter of the dynamic schedule for callers without a context (self-test); a
+// context passes its own counter in EpiParams::sched, so contexts on one device may run concurrently
 int* sched_counter() {
     static std::mutex mu;
     static int* ctr[64] = {};
@@ -685,7 +685,7 @@ void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiP
     int* sched = nullptr;
     static const bool dynamic = getenv("SWF_GEMM_STATIC") == nullptr;
     if (dynamic) {
-        sched = sched_counter();
+        sched = ep.sched ? ep.sched : sched_counter();
         SWF_CUDA(cudaMemsetAsync(sched, 0, sizeof(int), st));
     }
     static const int env_gm = getenv("SWF_GEMM_GROUPM") ? std::max(1, atoi(getenv("SWF_GEMM_GROUPM"))) : 0;

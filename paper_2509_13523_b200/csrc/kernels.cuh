@@ -118,6 +118,9 @@ struct EpiParams {
     i64 off_xb, off_ss;
     const float* inv_r;
     const float* beta;
+    // tile counter of the persistent GEMM's dynamic schedule, owned by the context (GEMMs of one
+    // context are stream-ordered); nullptr -> a per-device counter (single-stream callers only)
+    int* sched;
 };
 // inv_r[m] = 1 / sqrt(sum_i ss[m][i] / h + 1e-8) over the nss partials; non-finite rows flag
 // flags[slot] (check_finite, swin.hpp:295-300)
