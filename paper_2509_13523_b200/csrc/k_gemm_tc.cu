@@ -352,6 +352,9 @@ __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, i
 // sharing an A row block (consecutive indices) start it together and its K slices are fetched from
 // HBM once, instead of drifting apart over the static round-robin schedule (which re-read A ~3x).
 constexpr int kQ = 4;
+#ifndef SWF_GEMM_XPF
+#define SWF_GEMM_XPF 1
+#endif
 constexpr uint32_t kQConsumers = 1 /*peer producer*/ + 1 /*MMA*/ + 2 * kEpiWarps;
 struct TileQueue {
     uint64_t* full;  // [kQ], one arrival (the scheduler) per round, in each CTA
@@ -524,9 +527,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (t < 0) break;
             int m_blk, n_blk;
             tile_coords(t, n_tiles, m_tiles, group_m, m_blk, n_blk);
+            const i64 row = i64(m_blk) * 2 * BM + crank * BM + q * 32 + lane;
+#if SWF_GEMM_XPF
+            // out projection (short K): pull this tile's rows of the residual x (this warp's half: BN/2
+            // floats per row) into L2 while the accumulator is computed, so the epilogue's loads hit L2
+            // (A/B: out GEMM -4%; for the down projection's long K the lines are evicted before use)
+            if constexpr (MODE == EPI_RESID)
+                if (row < ep.M) {
+                    const float* xr = ep.x + row * ep.h + n_blk * BN + half * (BN / 2);
+#pragma unroll
+                    for (int c = 0; c < BN / 64; ++c)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + c * 32) : "memory");
+                }
+#endif
             mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
             tc_fence_after();
-            const i64 row = i64(m_blk) * 2 * BM + crank * BM + q * 32 + lane;
             const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
             // fused RMSNorm + AdaLN of operand A's rows (consumers): 1 / rms from the producer partials
             float inv_r = 1.f;
