@@ -698,7 +698,11 @@ void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiP
     const CUtensorMap* a = reinterpret_cast<const CUtensorMap*>(&A);
     const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(&B);
     int* sched = nullptr;
-    static const bool dynamic = getenv("SWF_GEMM_STATIC") == nullptr;
+    // SWF_GEMM_STATIC=1: static round-robin schedule for every GEMM; SWF_GEMM_STATIC_MASK=bits: for the
+    // epilogue modes whose bit is set (A/B knobs)
+    static const bool all_static = getenv("SWF_GEMM_STATIC") != nullptr;
+    static const int static_mask = getenv("SWF_GEMM_STATIC_MASK") ? atoi(getenv("SWF_GEMM_STATIC_MASK")) : 0;
+    const bool dynamic = !all_static && !((static_mask >> MODE) & 1);
     if (dynamic) {
         sched = ep.sched ? ep.sched : sched_counter();
         SWF_CUDA(cudaMemsetAsync(sched, 0, sizeof(int), st));
