@@ -70,3 +70,15 @@ def test_save_checkpoint_matches_reference_format(tmp_path, dtype):
         assert (tmp_path / ("ref" + ext)).read_bytes() == (tmp_path / ("ours" + ext)).read_bytes()
     swf.verify_checkpoint(sc, str(tmp_path / "ours"))
     assert swf.fnv1a64(b"") == 0xcbf29ce484222325
+
+
+def test_save_checkpoint_rejects_wrong_shapes(tmp_path):
+    sc = swf.ModelConfig(**TINY)
+    arrays = [np.zeros(r * c, np.float32) for _, r, c in swf.param_arrays(sc)]
+    arrays[3] = np.zeros(arrays[3].size + 1, np.float32)
+    with pytest.raises(swf.ConfigError):
+        swf.save_checkpoint(str(tmp_path / "bad"), sc, arrays)
+    c = swf._Cfg(*swf.astuple(sc))
+    buf, r, k = swf.C.create_string_buffer(64), swf.C.c_longlong(), swf.C.c_longlong()
+    n = len(swf.param_arrays(sc))
+    assert swf.lib().swf_param_array(swf.C.byref(c), n, buf, 64, swf.C.byref(r), swf.C.byref(k)) == swf.ERR_CONFIG
