@@ -17,8 +17,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -215,14 +217,35 @@ constexpr int dtype_of() {
     return sizeof(T) == 8 ? SWF_F64 : SWF_F32;
 }
 
-// One device context per (parameter set, grid): weights are uploaded once and kept resident.
+// Window / sequence parallelism of one process over several GPUs (swf_set_topology_devices):
+// rank r of the wp_a x wp_b x sp topology runs on device_ids[r] (a device may host several ranks).
+struct Topology {
+    int wp_a = 1, wp_b = 1, sp = 1, ownership = SWF_OWN_CONTIGUOUS;
+    std::vector<int> device_ids{0};
+    int world() const { return wp_a * wp_b * sp; }
+    bool operator<(const Topology& o) const {
+        return std::tie(wp_a, wp_b, sp, ownership, device_ids) < std::tie(o.wp_a, o.wp_b, o.sp, o.ownership, o.device_ids);
+    }
+};
+
+// One device context per (parameter set, grid, precision, topology): weights are uploaded once and
+// kept resident; one mutex per context serialises concurrent callers (one stream per context).
 class Context {
 public:
-    Context(const ModelConfig& cfg, int H, int W, int device = 0, int precision = SWF_PREC_BF16) : cfg_(cfg) {
+    Context(const ModelConfig& cfg, int H, int W, int device = 0, int precision = SWF_PREC_BF16,
+            const Topology* topo = nullptr)
+        : cfg_(cfg) {
         const swf_model_cfg c = cfg.c();
         swf_ctx* p = nullptr;
-        check_rc(swf_create(&c, H, W, device, precision, &p));
+        const int dev0 = topo ? topo->device_ids.at(0) : device;
+        check_rc(swf_create(&c, H, W, dev0, precision, &p));
         ctx_.reset(p);
+        if (topo && topo->world() > 1) {
+            if (int(topo->device_ids.size()) != topo->world())
+                throw ConfigError("topology: one device id per rank required");
+            check_rc(swf_set_topology_devices(p, topo->wp_a, topo->wp_b, topo->sp, topo->ownership,
+                                              topo->device_ids.data()));
+        }
     }
     template <class T>
     void load(const Parameters<T>& p) {
@@ -231,6 +254,7 @@ public:
     }
     swf_ctx* get() const { return ctx_.get(); }
     const ModelConfig& cfg() const { return cfg_; }
+    std::mutex& mutex() { return mu_; }
 
 private:
     struct Del {
@@ -238,40 +262,101 @@ private:
     };
     ModelConfig cfg_;
     std::unique_ptr<swf_ctx, Del> ctx_;
+    std::mutex mu_;
 };
 
 namespace detail {
 struct Key {
     const void* params;
     int H, W, prec;
+    Topology topo;
     bool operator<(const Key& o) const {
-        return std::tie(params, H, W, prec) < std::tie(o.params, o.H, o.W, o.prec);
+        return std::tie(params, H, W, prec, topo) < std::tie(o.params, o.H, o.W, o.prec, o.topo);
     }
 };
-inline std::map<Key, std::unique_ptr<Context>>& cache() {
-    static thread_local std::map<Key, std::unique_ptr<Context>> c;
+struct Entry {
+    std::unique_ptr<Context> ctx;
+    u64 fingerprint = 0;
+};
+// Process-wide (not per thread: a C2 context holds ~46 GB of HBM)
+inline std::map<Key, Entry>& cache() {
+    static std::map<Key, Entry> c;
     return c;
+}
+inline std::mutex& cache_mutex() {
+    static std::mutex m;
+    return m;
 }
 inline int& default_precision() {
     static int p = SWF_PREC_BF16;
     return p;
 }
+inline Topology& default_topology() {
+    static Topology t;
+    return t;
+}
+inline u64 mix(u64 h, u64 v) { return splitmix64(h ^ splitmix64(v)); }
+// Identity + contents of a parameter set: every array's address and size, and an fnv1a64 of its
+// values -- all of them up to 2^22 elements per array, an evenly strided sample of 2^22 above that
+// (an optimizer / EMA update rewrites every element, so it cannot hide between the samples).
+template <class T>
+u64 fingerprint(const Parameters<T>& p) {
+    const std::vector<const void*> a = parameter_arrays(p);
+    std::vector<i64> n{p.w_encode.size(), p.b_encode.size()};
+    for (const auto& b : p.blocks)
+        for (const MatX<T>* m : {&b.w_qkv, &b.w_out, &b.g_attn, &b.g_ffn, &b.w_gate, &b.w_up, &b.w_down, &b.w_ada,
+                                 &b.b_ada})
+            n.push_back(m->size());
+    for (const MatX<T>* m : {&p.w_time, &p.b_time, &p.g_decode, &p.w_decode, &p.b_decode}) n.push_back(m->size());
+    u64 h = 0xcbf29ce484222325ULL;
+    for (size_t i = 0; i < a.size(); ++i) {
+        h = mix(h, reinterpret_cast<std::uintptr_t>(a[i]));
+        h = mix(h, u64(n[i]));
+        const T* v = static_cast<const T*>(a[i]);
+        const i64 stride = std::max<i64>(1, n[i] >> 22);
+        u64 f = 0xcbf29ce484222325ULL;
+        for (i64 k = 0; k < n[i]; k += stride) {
+            u64 bits = 0;
+            std::memcpy(&bits, v + k, sizeof(T));
+            f = (f ^ bits) * 0x100000001b3ULL;
+        }
+        h = mix(h, f);
+    }
+    return h;
+}
 }  // namespace detail
 
 // Select the device arithmetic for the reference-signature entry points below.
 inline void set_precision(int precision) { detail::default_precision() = precision; }
+// Run the reference-signature entry points on several GPUs of this process (window / sequence
+// parallelism; the results are identical to one device, bitwise).
+inline void set_topology(const Topology& t) { detail::default_topology() = t; }
 
+// The context serving `p` on an H x W grid. The parameters are re-uploaded whenever their contents
+// changed since the last call (in-place optimizer / EMA updates of the caller's Parameters).
 template <class T>
 Context& context_for(const Parameters<T>& p, int H, int W) {
+    const detail::Key k{&p, H, W, detail::default_precision(), detail::default_topology()};
+    const u64 fp = detail::fingerprint(p);
+    std::lock_guard<std::mutex> lk(detail::cache_mutex());
     auto& c = detail::cache();
-    const detail::Key k{&p, H, W, detail::default_precision()};
     auto it = c.find(k);
     if (it == c.end()) {
-        auto ctx = std::make_unique<Context>(p.cfg, H, W, 0, k.prec);
-        ctx->load(p);
-        it = c.emplace(k, std::move(ctx)).first;
+        detail::Entry e;
+        e.ctx = std::make_unique<Context>(p.cfg, H, W, 0, k.prec, &k.topo);
+        it = c.emplace(k, std::move(e)).first;
     }
-    return *it->second;
+    if (!it->second.fingerprint || it->second.fingerprint != fp) {
+        std::lock_guard<std::mutex> lk2(it->second.ctx->mutex());
+        it->second.ctx->load(p);
+        it->second.fingerprint = fp;
+    }
+    return *it->second.ctx;
+}
+// Drop the cached contexts (frees their device memory).
+inline void release_contexts() {
+    std::lock_guard<std::mutex> lk(detail::cache_mutex());
+    detail::cache().clear();
 }
 
 // forward (swin.hpp:327-368): input C_in x N, returns C_out x N.
@@ -280,7 +365,24 @@ MatX<T> forward(const Parameters<T>& p, const MatX<T>& input, T t, int grid_h, i
     if (input.rows() != p.cfg.in_channels) throw ConfigError("forward: input channel mismatch");
     Context& ctx = context_for(p, grid_h, grid_w);
     MatX<T> out(p.cfg.out_channels, i64(grid_h) * grid_w);
+    std::lock_guard<std::mutex> lk(ctx.mutex());
     check_rc(swf_forward(ctx.get(), input.data(), double(t), out.data(), dtype_of<T>()));
+    return out;
+}
+
+// block_window_forward (swin.hpp:306-325): window (wy, wx) of block `block`'s layout (shift 0 / w/2 by
+// parity, window.hpp:83-85) at time t; x_in / the result are the window's h x s_w residual columns.
+// The reference passes the block's parameters and ada vectors; here they are block `block` of p
+// (uploaded once, like forward()) and its ada vectors at t.
+template <class T>
+MatX<T> block_window_forward(const Parameters<T>& p, int block, T t, int grid_h, int grid_w, int wy, int wx,
+                             const MatX<T>& x_in) {
+    if (x_in.rows() != p.cfg.hidden_dim || x_in.cols() != i64(p.cfg.window_px) * p.cfg.window_px)
+        throw ConfigError("block_window_forward: x_in must be hidden_dim x window_px^2");
+    Context& ctx = context_for(p, grid_h, grid_w);
+    MatX<T> out(x_in.rows(), x_in.cols());
+    std::lock_guard<std::mutex> lk(ctx.mutex());
+    check_rc(swf_block_window_forward(ctx.get(), block, wy, wx, double(t), x_in.data(), out.data(), dtype_of<T>()));
     return out;
 }
 

@@ -81,6 +81,20 @@ void swf_destroy(swf_ctx* ctx);
  * rows are split into SP bands by global row phase (window.hpp:67-79), heads into sp groups
  * (heads % sp == 0 and window_px % sp == 0, topology.hpp:95-102). Must precede parameter loading. */
 int swf_set_topology(swf_ctx* ctx, int wp_a, int wp_b, int sp, int rank, int ownership);
+/* Single-process multi-GPU (SURVEY.md §8(b) swf_set_topology(ctx, wp_a, wp_b, sp, device_ids)): this
+ * context becomes rank 0 of a wp_a x wp_b x sp topology whose rank r runs on CUDA device
+ * device_ids[r] (device_ids[0] = the context's device; a device may host several ranks). The context
+ * creates and owns the other ranks; every call on it (load / init params, forward, forward_hidden,
+ * solve_pf_ode, forecast_step[_chunked], rollout_ensemble, backward, training, noise_field) runs all
+ * ranks from one host call, each rank on its own host thread, and returns the complete result: each
+ * rank writes its owned pixels of the output fields, partial sums (losses, gradients) are added in
+ * rank order. Peers are mapped directly (same address space; cudaDeviceEnablePeerAccess across
+ * GPUs) -- no IPC and no external process group. The reference-signature forward() / forecast_step()
+ * (include/swinflow/b200.hpp) therefore drive every GPU from one thread. Must precede parameter
+ * loading. */
+int swf_set_topology_devices(swf_ctx* ctx, int wp_a, int wp_b, int sp, int ownership, const int* device_ids);
+int swf_group_size(swf_ctx* ctx);                /* ranks driven by this context (1 without a group) */
+swf_ctx* swf_group_rank(swf_ctx* ctx, int rank); /* rank context (0 = ctx itself), for per-rank queries */
 /* Export this rank's IPC handles (residual buffers x2, barrier flags, attention planes, attention
  * output: 5 x 64 bytes) / map all ranks' handles (world x 320 bytes, rank order). After connecting, the down-projection epilogue
  * stores owner-changed tokens straight into the peer's residual buffer over NVLink (the
@@ -124,6 +138,18 @@ int swf_init_params(swf_ctx* ctx, uint64_t seed, int mode, double scale);
 /* forward(p, input, t, H, W) (swin.hpp:327-368): input C_in x N, output C_out x N, host memory.
  * Under a multi-rank topology each rank writes only the pixels it owns (see swf_owned_pixels). */
 int swf_forward(swf_ctx* ctx, const void* input, double t, void* output, int dtype);
+/* forward() stopped after the first n_blocks blocks (0 = right after the encode, n_blocks = all
+ * blocks, before the decode): the FP32 residual stream (ForwardCache::blocks[n_blocks].x_in /
+ * the final x of swin.hpp:273-291,344-362) for the listed pixels, hidden = n_pix x hidden_dim.
+ * Under a multi-rank topology only the rows of pixels this rank owns are written. */
+int swf_forward_hidden(swf_ctx* ctx, const void* input, double t, int n_blocks, const long long* pixels,
+                       long long n_pix, float* hidden, int dtype);
+/* block_window_forward(bp, ada, layout, wy, wx, n_heads, wc) (swin.hpp:306-325) with the context's
+ * block `block` (its layout: shift 0 on even, w/2 on odd blocks, window.hpp:83-85) and ada vectors
+ * at time t: x_in / x_out are one window's h x s_w residual columns (s_w = w*w tokens in canonical
+ * r*w + c order, column-major = [token][h]). Single-rank contexts. */
+int swf_block_window_forward(swf_ctx* ctx, int block, int wy, int wx, double t, const void* x_in, void* x_out,
+                             int dtype);
 /* Same, on device pointers (fp32, [N][C]) on the context stream, without synchronising;
  * numerics flags are checked by swf_sync(). */
 int swf_forward_device(swf_ctx* ctx, const float* d_input, double t, float* d_output);
@@ -229,6 +255,13 @@ int swf_noise_field(swf_ctx* ctx, uint64_t run_seed, uint64_t event, int channel
 /* Run one bf16 GEMM self-test of the tcgen05 kernel: C = A.B^T on device, returns max |err|
  * against an fp32 SIMT product of the same bf16 operands (used by the parity tests). */
 int swf_selftest_gemm(int device, long long M, int N, int K, double* max_abs_err, double* max_ref);
+/* Run the windowed attention kernel alone (head_attention_fwd, swin.hpp:161-188) on the windows of
+ * an (n_wy*w) x (n_wx*w) grid under cyclic shift `shift` (the last window row seam-masked when
+ * shift > 0, window.hpp:107-122): q, k, v are [n_win][heads][w*w][d] fp32 host arrays (rounded to
+ * bf16 for SWF_PREC_BF16), o receives [n_win][w*w][heads*d] (head-concatenated, swin.hpp:319-320).
+ * flags bit 0 (negative control for the tests): skip the online-softmax O rescale. */
+int swf_selftest_attention(int device, int precision, int n_wy, int n_wx, int w, int shift, int heads, int d,
+                           const float* q, const float* k, const float* v, float* o, int flags);
 
 #ifdef __cplusplus
 }

@@ -342,6 +342,24 @@ def forecast_step(cfg: ModelConfig, params, H, W, x_prev, forc, run_seed, event,
     return out, fe.value
 
 
+def rollout_ensemble(cfg: ModelConfig, params, H, W, x_init, forcings, n_members, n_steps, run_seed, rollout_id,
+                     st=None, rs=None, fo=None, **dc):
+    """rollout_ensemble (diffusion.hpp:323-339): members x AR steps, out[m][k] = the state after step k of
+    member m; step k of member m uses event key_derive(rollout_id, m, k) and forcings[k], and its output
+    is the next step's x_prev. Members are independent (their noise streams differ only by the event)."""
+    if len(forcings) < n_steps:
+        raise ConfigError(2, "rollout: not enough forcing steps")
+    x_init = np.ascontiguousarray(x_init, params.dtype)
+    out = np.empty((n_members, n_steps) + x_init.shape, params.dtype)
+    for m in range(n_members):
+        x = x_init
+        for k in range(n_steps):
+            x, _ = forecast_step(cfg, params, H, W, x, forcings[k], run_seed, key_derive(rollout_id, m, k), st, rs,
+                                 fo, **dc)
+            out[m, k] = x
+    return out
+
+
 def solve_net(cfg: ModelConfig, params, H, W, x_init, x_prev_std, forc_std, sigma_d=1.0, sigma_min=0.2,
               sigma_max=500.0, steps=10, churn=0.0, churn_key=0):
     """solve_pf_ode with the forecast_step net lambda on given standardized conditioning (f64)."""

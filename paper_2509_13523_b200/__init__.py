@@ -114,6 +114,10 @@ def lib():
         L.swf_destroy.argtypes = [vp]
         L.swf_destroy.restype = None
         L.swf_set_topology.argtypes = [vp, i, i, i, i, i]
+        L.swf_set_topology_devices.argtypes = [vp, i, i, i, i, vp]
+        L.swf_group_size.argtypes = [vp]
+        L.swf_group_rank.argtypes = [vp, i]
+        L.swf_group_rank.restype = vp
         L.swf_ipc_handles.argtypes = [vp, vp]
         L.swf_connect_peers.argtypes = [vp, vp]
         L.swf_plan_owners.argtypes = [i, i, i, i, i, i, vp]
@@ -149,6 +153,9 @@ def lib():
         L.swf_profile_launches.argtypes = [vp, vp, vp, i, C.POINTER(i)]
         L.swf_noise_field.argtypes = [vp, u64, u64, i, d, vp]
         L.swf_selftest_gemm.argtypes = [i, ll, i, i, C.POINTER(d), C.POINTER(d)]
+        L.swf_selftest_attention.argtypes = [i, i, i, i, i, i, i, i, vp, vp, vp, vp, i]
+        L.swf_forward_hidden.argtypes = [vp, vp, d, i, vp, ll, vp, i]
+        L.swf_block_window_forward.argtypes = [vp, i, i, i, d, vp, vp, i]
         L.swf_backward.argtypes = [vp, vp, d, vp, vp, vp, i]
         L.swf_diffusion_loss_sample.argtypes = [vp, vp, vp, vp, vp, vp, u64, vp, C.POINTER(d), vp, i]
         L.swf_train_accumulate.argtypes = [vp, vp, vp, vp, vp, vp, u64, u64, C.POINTER(d), i]
@@ -205,20 +212,46 @@ def selftest_gemm(M: int, N: int, K: int, device: int = 0):
     return e.value, r.value
 
 
+def selftest_attention(q, k, v, n_wy: int, n_wx: int, w: int, shift: int = 0, precision: int = PREC_BF16,
+                       flags: int = 0, device: int = 0) -> np.ndarray:
+    """The windowed attention kernel alone on q/k/v [n_win][heads][w*w][d] (fp32); returns
+    [n_win][w*w][heads*d]. flags bit 0 disables the O rescale (negative control)."""
+    q, k, v = (np.ascontiguousarray(a, np.float32) for a in (q, k, v))
+    nwin, heads, s, dd = q.shape
+    if nwin != n_wy * n_wx or s != w * w or k.shape != q.shape or v.shape != q.shape:
+        raise ConfigError(ERR_CONFIG, "selftest_attention: q/k/v must be [n_wy*n_wx][heads][w*w][d]")
+    o = np.zeros((nwin, s, heads * dd), np.float32)
+    _check(lib().swf_selftest_attention(device, precision, n_wy, n_wx, w, shift, heads, dd, _p(q), _p(k), _p(v),
+                                        _p(o), flags))
+    return o
+
+
 class Denoiser:
     """Device context for one model on one H x W grid (forward / solve / forecast)."""
 
     def __init__(self, cfg: ModelConfig, grid_h: int, grid_w: int, device: int = 0, precision: int = PREC_BF16,
-                 topology: tuple | None = None):
+                 topology: tuple | None = None, devices: list | None = None):
+        """topology=(wp_a, wp_b, sp, rank, ownership): this process is one rank (connect the others with
+        connect_peers / connect_peers_torch). devices=[dev of rank 0, dev of rank 1, ...] with
+        topology=(wp_a, wp_b, sp, ownership): this one object drives every rank (single-process group,
+        swf_set_topology_devices) and every call returns complete fields."""
         self.cfg, self.H, self.W, self.precision = cfg, grid_h, grid_w, precision
         self._c = C.c_void_p()
-        _check(lib().swf_create(C.byref(_Cfg(*astuple(cfg))), grid_h, grid_w, device, precision,
+        dev0 = devices[0] if devices is not None else device
+        _check(lib().swf_create(C.byref(_Cfg(*astuple(cfg))), grid_h, grid_w, dev0, precision,
                                 C.byref(self._c)))
         self.wp_world, self.wp_rank = 1, 0  # ranks sharing this model's windows (WP x SP group)
-        if topology is not None:
+        if devices is not None:
+            wp_a, wp_b, sp, own = topology if topology is not None else (1, len(devices), 1, OWN_CONTIGUOUS)
+            ids = (C.c_int * len(devices))(*devices)
+            _check(lib().swf_set_topology_devices(self._c, wp_a, wp_b, sp, own, ids))
+        elif topology is not None:
             wp_a, wp_b, sp, rank, own = topology
             _check(lib().swf_set_topology(self._c, wp_a, wp_b, sp, rank, own))
             self.wp_world, self.wp_rank = wp_a * wp_b * sp, rank
+
+    def group_size(self) -> int:
+        return lib().swf_group_size(self._c)
 
     def connect_peers(self, all_handles: bytes):
         buf = C.create_string_buffer(all_handles, len(all_handles))
@@ -267,6 +300,23 @@ class Denoiser:
         inp = np.ascontiguousarray(inp)
         out = np.zeros((self.H * self.W, self.cfg.out_channels), inp.dtype)
         _check(lib().swf_forward(self._c, _p(inp), float(t), _p(out), _dt(inp)))
+        return out
+
+    def forward_hidden(self, inp: np.ndarray, t: float, n_blocks: int, pixels) -> np.ndarray:
+        """Residual stream after the first n_blocks blocks (fp32) at the given pixels: [n_pix][h]."""
+        inp = np.ascontiguousarray(inp)
+        pix = np.ascontiguousarray(pixels, np.int64)
+        out = np.zeros((pix.size, self.cfg.hidden_dim), np.float32)
+        _check(lib().swf_forward_hidden(self._c, _p(inp), float(t), int(n_blocks), _p(pix), pix.size, _p(out),
+                                        _dt(inp)))
+        return out
+
+    def block_window_forward(self, block: int, wy: int, wx: int, t: float, x_in: np.ndarray) -> np.ndarray:
+        """block_window_forward (swin.hpp:306-325): one window's residual rows [w*w][h] (canonical
+        token order) through block `block` of the loaded model at time t."""
+        x_in = np.ascontiguousarray(x_in)
+        out = np.zeros_like(x_in)
+        _check(lib().swf_block_window_forward(self._c, block, wy, wx, float(t), _p(x_in), _p(out), _dt(x_in)))
         return out
 
     def forward_device(self, d_in: int, t: float, d_out: int):
@@ -514,22 +564,36 @@ def fnv1a64(data, h: int = 0xcbf29ce484222325) -> int:
     return int(lib().swf_fnv1a64(a.ctypes.data_as(C.c_void_p), a.nbytes, h))
 
 
-def save_checkpoint(base: str, cfg: ModelConfig, arrays):
+def save_checkpoint(base: str, cfg: ModelConfig, arrays, dtype=None):
     """save_params / save_named_arrays (checkpoint.hpp:29-47, 78-81): `arrays` yields the canonical
-    arrays (column-major, f32 or f64) one at a time; writes base.manifest + base.bin."""
-    off = 0
+    arrays (column-major) one at a time; writes base.manifest + base.bin. Every array is written in
+    one element type -- `dtype` (np.float32 / np.float64), default the first array's -- as the
+    reference's save_named_arrays<T> does; exactly the canonical number of arrays is required."""
+    shapes = param_arrays(cfg)
+    it = iter(arrays)
+    off, dt = 0, None if dtype is None else np.dtype(dtype)
+    if dt is not None and dt not in (np.float32, np.float64):
+        raise ConfigError(ERR_CONFIG, "save_checkpoint: dtype must be float32 or float64")
     with open(base + ".bin", "wb") as fb, open(base + ".manifest", "w") as fm:
-        first = True
-        for (name, r, c), a in zip(param_arrays(cfg), arrays):
-            a = np.ascontiguousarray(a)
+        for k, (name, r, c) in enumerate(shapes):
+            try:
+                a = next(it)
+            except StopIteration:
+                raise ConfigError(ERR_CONFIG, f"save_checkpoint: {k} arrays given, the model has {len(shapes)}") \
+                    from None
+            a = np.asarray(a)
+            if dt is None:
+                dt = np.dtype(np.float64) if a.dtype == np.float64 else np.dtype(np.float32)
+            a = np.ascontiguousarray(a, dt)
             if a.size != r * c:
                 raise ConfigError(ERR_CONFIG, f"save_checkpoint: `{name}` has {a.size} elements, expected {r}x{c}")
-            if first:
-                fm.write("dtype f64\n" if a.dtype == np.float64 else "dtype f32\n")
-                first = False
+            if k == 0:
+                fm.write("dtype f64\n" if dt == np.float64 else "dtype f32\n")
             fm.write(f"{name} {r}x{c} {off} {fnv1a64(a)}\n")
             fb.write(a.tobytes())
             off += a.nbytes
+        if next(it, None) is not None:
+            raise ConfigError(ERR_CONFIG, f"save_checkpoint: more arrays than the model's {len(shapes)}")
 
 
 def verify_checkpoint(cfg: ModelConfig, base: str):

@@ -19,6 +19,7 @@
 #include <sstream>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -42,7 +43,7 @@ struct IoError : std::runtime_error {  // common.hpp:33-40 (IoError / IntegrityE
     explicit IoError(const std::string& m) : std::runtime_error(m) {}
 };
 }  // namespace swf
-#include "chunked.hpp"
+#include "chunk_store.hpp"
 namespace swf {
 static void require(bool c, const std::string& m) {
     if (!c) throw ConfigError(m);
@@ -176,6 +177,19 @@ struct swf_ctx {
     long long graph_launches = 0;
     u64* d_churn_key = nullptr;
     u64* h_churn_key = nullptr;  // pinned staging
+    // test hook (swf_forward_hidden): stop the forward after this many blocks (-1: full forward);
+    // the residual then sits in xbuf[hid_cur] in the local order of layout hid_par
+    int stop_after = -1, hid_cur = 0, hid_par = 0;
+    // single-process multi-GPU group (swf_set_topology_devices): the root context (rank 0) owns the
+    // contexts of ranks 1..world-1 and fans every call out to them; peers are mapped directly
+    // (peer access, same address space) instead of through CUDA IPC
+    std::vector<swf_ctx*> kids;
+    bool ipc_mapped = false;
+    std::vector<long long> owned_pix;  // pixel of every local token (layout 0, local order)
+    float* h_stage = nullptr;          // pinned staging for owned-row readback [M][max C]
+    size_t h_stage_n = 0;
+    // per-call device buffers of the sampler entry points, kept across calls (grow-only)
+    std::vector<std::pair<float*, size_t>> scratch;
 };
 
 namespace {
@@ -190,6 +204,34 @@ T* dalloc(swf_ctx* c, size_t n) {
     c->allocs.push_back(p);
     return static_cast<T*>(p);
 }
+
+void dfree(swf_ctx* c, void* p) {
+    for (size_t i = 0; i < c->allocs.size(); ++i)
+        if (c->allocs[i] == p) {
+            SWF_CUDA(cudaFree(p));
+            c->allocs.erase(c->allocs.begin() + i);
+            return;
+        }
+}
+
+// Grow-only device scratch slot k: the per-call buffers of the host-buffer entry points (staged
+// forcings, outputs, rollout states, readback rows) are allocated once, not cudaMalloc'd / cudaFree'd
+// per call (cudaFree synchronises the whole device -- other ranks of a single-process group included).
+enum Scratch { SC_FORC, SC_OUT, SC_RX0, SC_RXA, SC_RXB, SC_RFORC, SC_NOISE, SC_NOISE_PIX, SC_PIX, SC_ROWS, SC_WIN, SC_N };
+void* scratch(swf_ctx* c, int k, size_t bytes) {
+    if (c->scratch.size() < SC_N) c->scratch.resize(SC_N, {nullptr, 0});
+    auto& s = c->scratch[k];
+    if (s.second < bytes) {
+        if (s.first) {
+            SWF_CUDA(cudaStreamSynchronize(c->st));
+            dfree(c, s.first);
+        }
+        s.first = dalloc<float>(c, (bytes + 3) / 4);
+        s.second = bytes;
+    }
+    return s.first;
+}
+float* scratch_f(swf_ctx* c, int k, size_t n) { return static_cast<float*>(scratch(c, k, n * 4)); }
 
 size_t esize(const swf_ctx* c) { return c->prec == SWF_PREC_BF16 ? 2 : 4; }
 
@@ -293,6 +335,9 @@ void build_layouts(swf_ctx* c) {
     require(nx % c->wp_b == 0, "topology: window cols " + std::to_string(nx) + " not divisible by WP grid B=" +
                                    std::to_string(c->wp_b));
     const int nwp = c->wp_a * c->wp_b;
+    // glob2rl packs (WP rank << 16) | local window (LayMap): local window counts must fit 16 bits
+    require((nwin + nwp - 1) / nwp < 65536, "topology: " + std::to_string(nwin / nwp) +
+                                                " windows per rank exceed the 65535 the window maps address");
     std::vector<int> g2rl(nwin);
     for (int par = 0; par < 2; ++par) {
         c->l2g[par].clear();
@@ -359,6 +404,16 @@ void allocate(swf_ctx* c) {
     build_layouts(c);
     build_rope(c);
     const i64 M = c->M;
+    {  // pixel of every local token (layout 0): owned windows, the band's rows ascending, columns
+        const LayMap& L = c->lay[0];
+        const int w = m.w, R = w / c->sp;
+        c->owned_pix.clear();
+        c->owned_pix.reserve(size_t(M));
+        for (int gw : c->l2g[0])
+            for (int k = 0; k < R; ++k)
+                for (int cc = 0; cc < w; ++cc)
+                    c->owned_pix.push_back(L.g.win_to_pix(i64(gw) * w * w + i64(L.band_row(c->band, k)) * w + cc));
+    }
     if (c->prec == SWF_PREC_BF16) {  // [x fp32 M x h][x bf16 M x hp][sum-of-squares partials M x nss]
         c->off_xb = M * m.h;
         c->off_ss = c->off_xb + M * m.hp / 2;
@@ -618,37 +673,70 @@ std::vector<std::string> param_names(const Dims& m) {  // parameter_arrays names
     return v;
 }
 
+// Manifest of a checkpoint (the text half of save_named_arrays / load_named_arrays,
+// checkpoint.hpp:29-80): first line `dtype f32|f64`, then one `name RxC offset fnv1a64` line per
+// array. Parsed in two passes: the whole file is tokenised into records, then the records are
+// matched against this model's canonical array list (names, element counts, in order).
+struct ManifestRecord {
+    std::string name;
+    long long rows = 0, cols = 0;
+    unsigned long long offset = 0, sum = 0;
+};
+
+std::vector<ManifestRecord> parse_manifest(const std::string& path, std::string* dtype_word) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("checkpoint: no manifest at " + path);
+    const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    std::istringstream lines(text);
+    std::string line, key;
+    if (!std::getline(lines, line)) throw IoError("checkpoint: empty manifest " + path);
+    std::istringstream head(line);
+    head >> key >> *dtype_word;
+    if (key != "dtype") throw IoError("checkpoint: " + path + " does not start with a dtype line");
+    std::vector<ManifestRecord> recs;
+    while (std::getline(lines, line)) {
+        if (line.find_first_not_of(" \t\r") == std::string::npos) continue;
+        ManifestRecord r;
+        std::string shape;
+        std::istringstream f(line);
+        if (!(f >> r.name >> shape >> r.offset >> r.sum))
+            throw IoError("checkpoint: unreadable manifest line " + std::to_string(recs.size() + 2) + " in " + path);
+        const size_t x = shape.find('x');
+        char* e1 = nullptr;
+        char* e2 = nullptr;
+        r.rows = x == std::string::npos ? -1 : std::strtoll(shape.c_str(), &e1, 10);
+        r.cols = x == std::string::npos ? -1 : std::strtoll(shape.c_str() + x + 1, &e2, 10);
+        if (r.rows < 0 || r.cols < 0 || e1 != shape.c_str() + x || *e2 != '\0')
+            throw IoError("checkpoint: bad shape `" + shape + "` for `" + r.name + "` in " + path);
+        recs.push_back(std::move(r));
+    }
+    return recs;
+}
+
 struct CkptEntry {
     u64 offset, sum;
     size_t n;
 };
 
-// Strict manifest check (load_named_arrays): dtype line, then per array `name RxC offset fnv1a64`
-// in canonical order with matching element counts.
 std::vector<CkptEntry> read_manifest(const std::string& base, const Dims& m, int* dtype) {
-    std::ifstream man(base + ".manifest");
-    if (!man) throw IoError("cannot open manifest: " + base + ".manifest");
-    std::string tag, dt;
-    man >> tag >> dt;
-    if (tag != "dtype" || (dt != "f32" && dt != "f64"))
-        throw IoError("checkpoint dtype mismatch in " + base + " (found `" + dt + "`)");
-    *dtype = dt == "f64" ? SWF_F64 : SWF_F32;
+    std::string word;
+    const std::vector<ManifestRecord> recs = parse_manifest(base + ".manifest", &word);
+    if (word != "f32" && word != "f64") throw IoError("checkpoint dtype `" + word + "` is neither f32 nor f64 (" + base + ")");
+    *dtype = word == "f64" ? SWF_F64 : SWF_F32;
     const auto names = param_names(m);
     const auto shapes = param_shapes(m);
     std::vector<CkptEntry> out;
+    out.reserve(names.size());
     for (size_t i = 0; i < names.size(); ++i) {
-        std::string name, shape;
-        u64 off = 0, sum = 0;
-        if (!(man >> name >> shape >> off >> sum))
-            throw IoError("manifest truncated at array `" + names[i] + "` in " + base);
-        const auto xp = shape.find('x');
-        if (xp == std::string::npos) throw IoError("bad shape `" + shape + "` in " + base);
-        const long long rows = std::stoll(shape.substr(0, xp)), cols = std::stoll(shape.substr(xp + 1));
-        const i64 n = shapes[i].first * shapes[i].second;
-        if (name != names[i] || rows * cols != n)
-            throw IoError("checkpoint layout mismatch: expected `" + names[i] + "` (" + std::to_string(n) +
-                          " elements), manifest has `" + name + "` " + shape);
-        out.push_back({off, sum, size_t(n)});
+        if (i >= recs.size())
+            throw IoError("checkpoint " + base + " is truncated: the manifest ends before `" + names[i] + "`");
+        const ManifestRecord& r = recs[i];
+        const long long want = shapes[i].first * shapes[i].second;
+        if (r.name != names[i] || r.rows * r.cols != want)
+            throw IoError("checkpoint layout mismatch at array " + std::to_string(i) + ": this model has `" + names[i] +
+                          "` with " + std::to_string(want) + " values, the manifest `" + r.name + "` " +
+                          std::to_string(r.rows) + "x" + std::to_string(r.cols));
+        out.push_back({r.offset, r.sum, size_t(want)});
     }
     return out;
 }
@@ -917,18 +1005,13 @@ struct ProfScope {
     }
 };
 
-// The network on the prepared model input a_in (window order of layout 0). out_scale multiplies
-// the decode output (sigma_d for the sampler's net lambda, 1 for forward()).
+// Per-t preparation: time embedding + every block's AdaLN vectors; BF16 also folds this t's AdaLN
+// scale into the normed GEMMs' weights and its shift into their biases.
 template <class T>
-void forward_core(swf_ctx* c, double t, float out_scale) {
+void prep_time(swf_ctx* c, double t) {
     const Dims& m = c->m;
-    const i64 M = c->M;
-    // no rank may store into a peer's residual buffer while that peer still reads it
-    if (c->world > 1) peer_barrier(c);
     time_vectors(c, t);
-    constexpr bool kFuse = sizeof(T) == 2;  // BF16: RMSNorm + AdaLN fused into the GEMMs
-    if constexpr (kFuse) {
-        // fold this t's AdaLN scale into the normed GEMMs' weights and its shift into their biases
+    if constexpr (sizeof(T) == 2) {
         const int h = m.h;
         for (int b = 0; b < m.nb; ++b) {
             const float* six = c->six + size_t(b) * 6 * h;
@@ -941,6 +1024,126 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
                    static_cast<__nv_bfloat16*>(c->w_dec), nullptr, c->st);
         c->launches += 2 * m.nb + 1;
     }
+}
+
+// One block (block_window_forward, swin.hpp:306-325, over all local windows at once) on the residual
+// rows xbuf[cur] (M rows in the local order of layout L); the output is stored in the local order of
+// Lnext into xbuf[cur ^ 1] (and, multi-rank, the peers' buffers). M < c->M runs a window subset (the
+// q / k / V^T planes keep the full-size offsets the attention's TMA maps were built with).
+template <class T>
+void run_block(swf_ctx* c, int b, int cur, const LayMap& L, const LayMap& Lnext, i64 M) {
+    const Dims& m = c->m;
+    constexpr bool kFuse = sizeof(T) == 2;  // BF16: RMSNorm + AdaLN fused into the GEMMs
+    const int par = b & 1;
+    const float* six = c->six + size_t(b) * 6 * m.h;
+    float* x = c->xbuf[cur];
+    T* xm = static_cast<T*>(c->xm);
+    EpiParams ep = base_ep(c);
+    ep.M = M;
+    // attention branch: prenorm_modulate -> heads -> out projection (swin.hpp:313-322)
+    if constexpr (!kFuse) {
+        ProfScope ps(c, K_RMS);
+        rms_modulate<T>(x, M, m.h, m.hp, c->g_attn + size_t(b) * m.h, six, six + m.h, six + 2 * m.h, xm, c->flags,
+                        1 + b, c->st);
+    }
+    EpiParams e = ep;
+    e.cur = L;
+    e.out = c->qkv;
+    e.plane = i64(c->lay[par].nloc) * (m.heads / c->sp) * m.w * m.w * m.d;  // one q/k/v plane of a rank
+    e.N = 3 * m.h;
+    if constexpr (kFuse) {  // A = bf16 copy of x; norm from the producer's partial sums
+        inv_rms(c->ssb[cur], M, m.nss, m.h, c->invr, c->flags, 1 + b, c->st);
+        e.inv_r = c->invr;
+        e.beta = c->beta_qkv[b];
+        c->launches++;
+    }
+    {
+        ProfScope ps(c, K_QKV);
+        Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_qkv[b], tmap_at(c->tm_qkv, b), M, m.np_qkv,
+                     m.hp, m.bn_qkv, EPI_QKV, e);
+    }
+    if (c->sp > 1) peer_barrier(c);  // every head group's planes complete before attention
+    AttnParams ap;
+    ap.q = c->qkv;
+    ap.k = static_cast<const char*>(c->qkv) + size_t(c->M) * m.h * esize(c);
+    ap.v = static_cast<const char*>(c->qkv) + size_t(2) * c->M * m.h * esize(c);
+    ap.o = xm;
+    ap.ldo = m.hp;
+    ap.nloc = L.nloc;
+    ap.heads = m.heads / c->sp;
+    ap.head0 = c->band * (m.heads / c->sp);
+    ap.wp_rank = c->wp_rank;
+    ap.o_dst = c->d_o_dst;
+    ap.s = m.w * m.w;
+    ap.d = m.d;
+    ap.w = m.w;
+    ap.lay = L;
+    ap.scale = 1.0f / std::sqrt(float(m.d));
+    ap.tmq = &c->tm_q;
+    ap.tmk = &c->tm_k;
+    ap.tmv = &c->tm_vt;
+    ap.tmo = c->sp == 1 ? &c->tm_xm : nullptr;  // SP: rows go to the band owners row by row
+    {
+        ProfScope ps(c, K_ATTN);
+        if constexpr (sizeof(T) == 4)
+            attention_f32(ap, c->st);
+        else
+            attention_bf16(ap, c->st);
+    }
+    if (c->sp > 1) peer_barrier(c);  // all O rows of this rank's tokens landed
+    e = ep;
+    e.x = x;
+    e.N = m.h;
+    {
+        ProfScope ps(c, K_OUT);
+        Gemm<T>::run(c, xm, &c->tm_xm, c->w_out[b], tmap_at(c->tm_out, b), M, m.np_out, m.hp, m.bn_out, EPI_RESID, e);
+    }
+    // feed-forward branch (swin.hpp:323-324)
+    if constexpr (!kFuse) {
+        ProfScope ps(c, K_RMS);
+        rms_modulate<T>(x, M, m.h, m.hp, c->g_ffn + size_t(b) * m.h, six + 3 * m.h, six + 4 * m.h, six + 5 * m.h, xm,
+                        nullptr, 0, c->st);
+    }
+    e = ep;
+    e.out = c->sbuf;
+    e.ld_out = m.fp;
+    e.N = m.f;
+    e.G = m.G;
+    if constexpr (kFuse) {
+        inv_rms(c->ssb[cur], M, m.nss, m.h, c->invr, nullptr, 0, c->st);
+        e.inv_r = c->invr;
+        e.beta = c->beta_gu[b];
+        c->launches++;
+    }
+    {
+        ProfScope ps(c, K_GATEUP);
+        Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_gu[b], tmap_at(c->tm_gu, b), M, m.np_gu, m.hp,
+                     m.bn_gu, EPI_SWIGLU, e);
+    }
+    e = ep;
+    e.x = x;
+    e.N = m.h;
+    e.cur = L;
+    e.nxt = Lnext;
+    e.xdst = c->d_xdst[cur ^ 1];
+    {
+        ProfScope ps(c, K_DOWN);
+        Gemm<T>::run(c, c->sbuf, &c->tm_s, c->w_down[b], tmap_at(c->tm_down, b), M, m.np_down, m.fp, m.bn_down,
+                     EPI_DOWN, e);
+    }
+    c->launches += 7;
+}
+
+// The network on the prepared model input a_in (window order of layout 0). out_scale multiplies
+// the decode output (sigma_d for the sampler's net lambda, 1 for forward()).
+template <class T>
+void forward_core(swf_ctx* c, double t, float out_scale) {
+    const Dims& m = c->m;
+    const i64 M = c->M;
+    // no rank may store into a peer's residual buffer while that peer still reads it
+    if (c->world > 1) peer_barrier(c);
+    prep_time<T>(c, t);
+    constexpr bool kFuse = sizeof(T) == 2;
     EpiParams ep = base_ep(c);
     // encode (swin.hpp:341-342)
     ep.x = c->xbuf[0];
@@ -956,115 +1159,31 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
     for (int b = 0; b < m.nb; ++b) {
         const int par = b & 1;
         const int npar = (b + 1 < m.nb) ? ((b + 1) & 1) : 0;
-        const float* six = c->six + size_t(b) * 6 * m.h;
-        float* x = c->xbuf[cur];
+        if (b == c->stop_after) {
+            c->hid_cur = cur;
+            c->hid_par = par;
+            return;
+        }
         if (c->save_x)
-            SWF_CUDA(cudaMemcpyAsync(c->xsave + size_t(b) * M * m.h, x, size_t(M) * m.h * 4, cudaMemcpyDeviceToDevice,
-                                     c->st));
-        // attention branch: prenorm_modulate -> heads -> out projection (swin.hpp:313-322)
-        if constexpr (!kFuse) {
-            ProfScope ps(c, K_RMS);
-            rms_modulate<T>(x, M, m.h, m.hp, c->g_attn + size_t(b) * m.h, six, six + m.h, six + 2 * m.h, xm, c->flags,
-                        1 + b, c->st);
-        }
-        EpiParams e = ep;
-        e.cur = c->lay[par];
-        e.out = c->qkv;
-        e.plane = i64(c->lay[par].nloc) * (m.heads / c->sp) * m.w * m.w * m.d;  // one q/k/v plane of a rank
-        e.N = 3 * m.h;
-        if constexpr (kFuse) {  // A = bf16 copy of x; norm from the producer's partial sums
-            inv_rms(c->ssb[cur], M, m.nss, m.h, c->invr, c->flags, 1 + b, c->st);
-            e.inv_r = c->invr;
-            e.beta = c->beta_qkv[b];
-            c->launches++;
-        }
-        {
-            ProfScope ps(c, K_QKV);
-            Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_qkv[b], tmap_at(c->tm_qkv, b), M, m.np_qkv,
-                         m.hp, m.bn_qkv, EPI_QKV, e);
-        }
-        if (c->sp > 1) peer_barrier(c);  // every head group's planes complete before attention
-        AttnParams ap;
-        ap.q = c->qkv;
-        ap.k = static_cast<const char*>(c->qkv) + size_t(M) * m.h * esize(c);
-        ap.v = static_cast<const char*>(c->qkv) + size_t(2) * M * m.h * esize(c);
-        ap.o = xm;
-        ap.ldo = m.hp;
-        ap.nloc = c->lay[par].nloc;
-        ap.heads = m.heads / c->sp;
-        ap.head0 = c->band * (m.heads / c->sp);
-        ap.wp_rank = c->wp_rank;
-        ap.o_dst = c->d_o_dst;
-        ap.s = m.w * m.w;
-        ap.d = m.d;
-        ap.w = m.w;
-        ap.lay = c->lay[par];
-        ap.scale = 1.0f / std::sqrt(float(m.d));
-        ap.tmq = &c->tm_q;
-        ap.tmk = &c->tm_k;
-        ap.tmv = &c->tm_vt;
-        ap.tmo = c->sp == 1 ? &c->tm_xm : nullptr;  // SP: rows go to the band owners row by row
-        {
-            ProfScope ps(c, K_ATTN);
-            if constexpr (sizeof(T) == 4)
-                attention_f32(ap, c->st);
-            else
-                attention_bf16(ap, c->st);
-        }
-        if (c->sp > 1) peer_barrier(c);  // all O rows of this rank's tokens landed
-        e = ep;
-        e.x = x;
-        e.N = m.h;
-        {
-            ProfScope ps(c, K_OUT);
-            Gemm<T>::run(c, xm, &c->tm_xm, c->w_out[b], tmap_at(c->tm_out, b), M, m.np_out, m.hp,
-                     m.bn_out, EPI_RESID, e);
-        }
-        // feed-forward branch (swin.hpp:323-324)
-        if constexpr (!kFuse) {
-            ProfScope ps(c, K_RMS);
-            rms_modulate<T>(x, M, m.h, m.hp, c->g_ffn + size_t(b) * m.h, six + 3 * m.h, six + 4 * m.h, six + 5 * m.h, xm,
-                        nullptr, 0, c->st);
-        }
-        e = ep;
-        e.out = c->sbuf;
-        e.ld_out = m.fp;
-        e.N = m.f;
-        e.G = m.G;
-        if constexpr (kFuse) {
-            inv_rms(c->ssb[cur], M, m.nss, m.h, c->invr, nullptr, 0, c->st);
-            e.inv_r = c->invr;
-            e.beta = c->beta_gu[b];
-            c->launches++;
-        }
-        {
-            ProfScope ps(c, K_GATEUP);
-            Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_gu[b], tmap_at(c->tm_gu, b), M, m.np_gu,
-                         m.hp, m.bn_gu, EPI_SWIGLU, e);
-        }
-        e = ep;
-        e.x = x;
-        e.N = m.h;
-        e.cur = c->lay[par];
-        e.nxt = c->lay[npar];
-        e.xdst = c->d_xdst[cur ^ 1];
-        {
-            ProfScope ps(c, K_DOWN);
-            Gemm<T>::run(c, c->sbuf, &c->tm_s, c->w_down[b], tmap_at(c->tm_down, b), M,
-                     m.np_down, m.fp, m.bn_down, EPI_DOWN, e);
-        }
-        c->launches += 7;
+            SWF_CUDA(cudaMemcpyAsync(c->xsave + size_t(b) * M * m.h, c->xbuf[cur], size_t(M) * m.h * 4,
+                                     cudaMemcpyDeviceToDevice, c->st));
+        run_block<T>(c, b, cur, c->lay[par], c->lay[npar], M);
         if (c->world > 1) peer_barrier(c);
         cur ^= 1;
     }
     if (c->save_x)
         SWF_CUDA(cudaMemcpyAsync(c->xsave + size_t(m.nb) * M * m.h, c->xbuf[cur], size_t(M) * m.h * 4,
                                  cudaMemcpyDeviceToDevice, c->st));
+    if (c->stop_after == m.nb) {
+        c->hid_cur = cur;
+        c->hid_par = 0;
+        return;
+    }
     // decode (swin.hpp:362-366)
     if constexpr (!kFuse) {
-            ProfScope ps(c, K_RMS);
-            rms_modulate<T>(c->xbuf[cur], M, m.h, m.hp, c->g_dec, nullptr, nullptr, nullptr, xm, c->flags, 1 + m.nb, c->st);
-        }
+        ProfScope ps(c, K_RMS);
+        rms_modulate<T>(c->xbuf[cur], M, m.h, m.hp, c->g_dec, nullptr, nullptr, nullptr, xm, c->flags, 1 + m.nb, c->st);
+    }
     EpiParams e = ep;
     e.out = c->out_loc;
     e.ld_out = m.cout;
@@ -1077,11 +1196,42 @@ void forward_core(swf_ctx* c, double t, float out_scale) {
         c->launches++;
     }
     {
-            ProfScope ps(c, K_DECODE);
-            Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_dec, &c->tm_dec, M, m.np_dec, m.hp, m.bn_dec,
-                         EPI_DECODE, e);
-        }
+        ProfScope ps(c, K_DECODE);
+        Gemm<T>::run(c, xm, kFuse ? &c->tm_xb[cur] : &c->tm_xm, c->w_dec, &c->tm_dec, M, m.np_dec, m.hp, m.bn_dec,
+                     EPI_DECODE, e);
+    }
     c->launches += 2;
+    // every rank sees every rank's non-finite flags (the decode input's included) before any of
+    // them checks: all ranks raise the same NumericsError at the same call (k_peer_barrier)
+    if (c->world > 1) peer_barrier(c);
+}
+
+// block_window_forward (swin.hpp:306-325) of block b on window (wy, wx) of the block's layout:
+// x_in / x_out are that window's h x s_w residual columns (canonical token order r * w + c), fp32 rows
+// [token][h] on the device. Runs the forward's kernels on a one-window layout (Lnext = the same
+// window, so the down projection stores in place order).
+template <class T>
+void block_window_core(swf_ctx* c, int b, int wy, int wx, double t) {
+    const Dims& m = c->m;
+    const int par = b & 1;
+    const LayMap& Lf = c->lay[par];
+    const int nwin = Lf.g.nx * Lf.g.ny, gw = wy * Lf.g.nx + wx;
+    int* ids = static_cast<int*>(scratch(c, SC_WIN, size_t(nwin + 1) * 4));
+    std::vector<int> h_ids(size_t(nwin) + 1, 0);  // [0] = loc2glob[0] = gw; [1 + g] = glob2rl (rank 0, window 0)
+    h_ids[0] = gw;
+    SWF_CUDA(cudaMemcpyAsync(ids, h_ids.data(), h_ids.size() * 4, cudaMemcpyHostToDevice, c->st));
+    LayMap L = Lf;
+    L.nloc = 1;
+    L.loc2glob = ids;
+    L.glob2rl = ids + 1;
+    const i64 M = i64(m.w) * m.w;
+    prep_time<T>(c, t);
+    if constexpr (sizeof(T) == 2) {
+        prep_residual(c->xbuf[0], M, m.h, m.hp, m.nss, c->xbb[0], c->ssb[0], c->st);
+        c->launches++;
+    }
+    run_block<T>(c, b, 0, L, L, M);
+    SWF_CUDA(cudaStreamSynchronize(c->st));  // h_ids staging
 }
 
 void forward_any(swf_ctx* c, double t, float out_scale) {
@@ -1172,7 +1322,7 @@ void backward_core(swf_ctx* c, const float* dout) {
         const float* kk = q + size_t(M) * h;
         const float* v = q + size_t(2) * M * h;
         AttnParams ap;
-        std::memset(&ap, 0, sizeof ap);
+        ap = AttnParams{};
         ap.q = q;
         ap.k = kk;
         ap.v = v;
@@ -1272,19 +1422,34 @@ void check_flags(swf_ctx* c) {
     }
 }
 
-// Cross-GPU barrier over NVLink-mapped flags (one launch per GPU; ranks are separate GPUs, so the
-// waiting blocks never share an SM with the blocks they wait for). Each rank release-stores the
-// epoch into its slot of every peer's flag array, then acquire-polls its own slots. Stream order
-// places it after the down-projection whose epilogue stored rows into peer residual buffers.
-__global__ void k_peer_barrier(int* const* flags, int rank, int world, int* epoch_ctr, int* err) {
-    __shared__ int epoch;
+// Cross-rank barrier over peer-mapped flag words (one CTA per rank; rank 0..world-1 may share a GPU,
+// the waiting CTA never holds resources another rank's kernels need). Slot layout of a rank's
+// 64-int barrier array: [0, 8) the epoch each peer reached, [8 + 8 p, 16 + 8 p) for epoch parity p
+// the lowest numerics flag slot each peer had raised (+1; 0 = none). Each rank publishes its lowest
+// raised slot into every peer, release-stores the epoch, acquire-polls every peer's epoch, then
+// raises the peers' slots locally: after a barrier every rank holds every rank's flags, so a NaN in
+// one rank's windows makes all ranks throw the same NumericsError at the same point. A
+// peer can be at most one barrier ahead (it waits for this rank's epoch), so parity double-buffers
+// the published slots. A peer silent for 30 s sets the timeout word instead of hanging.
+__global__ void k_peer_barrier(int* const* flags, int rank, int world, int* epoch_ctr, int* local, int nflags) {
+    __shared__ int epoch, lowest;
     const int t = threadIdx.x;
-    if (t == 0) epoch = *epoch_ctr + 1;  // every rank runs the same barrier sequence
+    if (t == 0) {
+        epoch = *epoch_ctr + 1;  // every rank runs the same barrier sequence
+        lowest = 0x7fffffff;
+    }
     __syncthreads();
+    int lo = 0x7fffffff;
+    for (int i = t; i < nflags - 1; i += blockDim.x)
+        if (local[i]) lo = min(lo, i);
+    atomicMin(&lowest, lo);
+    __syncthreads();
+    const int par = epoch & 1;
     if (t < world) {
+        int* remote = flags[t];
+        remote[8 + 8 * par + rank] = lowest == 0x7fffffff ? 0 : lowest + 1;
         __threadfence_system();
-        int* remote = flags[t] + rank;
-        asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(remote), "r"(epoch) : "memory");
+        asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(remote + rank), "r"(epoch) : "memory");
         const int* mine = flags[rank] + t;
         unsigned long long t0, t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -1294,18 +1459,21 @@ __global__ void k_peer_barrier(int* const* flags, int rank, int world, int* epoc
             if (v >= epoch) break;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
             if (t1 - t0 > 30000000000ull) {  // 30 s: a peer died -> report instead of hanging
-                atomicOr(err, 1);
+                atomicOr(local + nflags - 1, 1);
                 break;
             }
         }
+        int v;
+        asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(flags[rank] + 8 + 8 * par + t) : "memory");
+        if (v > 0 && v < nflags) atomicOr(local + (v - 1), 1);
     }
     __syncthreads();
     if (t == 0) *epoch_ctr = epoch;
 }
 
 void peer_barrier(swf_ctx* c) {
-    if (!c->peers) throw ConfigError("multi-rank topology: call swf_connect_peers before running");
-    k_peer_barrier<<<1, 32, 0, c->st>>>(c->d_flag_table, c->rank, c->world, c->d_epoch, c->flags + (c->nflags - 1));
+    if (!c->peers) throw ConfigError("multi-rank topology: connect the ranks (swf_connect_peers) before running");
+    k_peer_barrier<<<1, 256, 0, c->st>>>(c->d_flag_table, c->rank, c->world, c->d_epoch, c->flags, c->nflags);
     SWF_LAUNCH_CHECK();
     c->launches++;
 }
@@ -1509,6 +1677,36 @@ void d2h_field(swf_ctx* c, const float* src_loc, int C, int dtype, void* dst) {
     }
 }
 
+// Multi-rank readback: this rank's local rows [M][C] -> pinned staging -> the caller's [N][C] field at
+// the owned pixels only (the other ranks of a single-process group write theirs concurrently).
+void d2h_owned(swf_ctx* c, const float* src_loc, int C, int dtype, void* dst) {
+    const size_t n = size_t(c->M) * C;
+    if (c->h_stage_n < n) {
+        if (c->h_stage) SWF_CUDA(cudaFreeHost(c->h_stage));
+        c->h_stage = nullptr;
+        SWF_CUDA(cudaMallocHost(&c->h_stage, n * 4));
+        c->h_stage_n = n;
+    }
+    SWF_CUDA(cudaMemcpyAsync(c->h_stage, src_loc, n * 4, cudaMemcpyDeviceToHost, c->st));
+    SWF_CUDA(cudaStreamSynchronize(c->st));
+    for (i64 i = 0; i < c->M; ++i) {
+        const float* r = c->h_stage + size_t(i) * C;
+        const size_t o = size_t(c->owned_pix[i]) * C;
+        if (dtype == SWF_F64)
+            for (int k = 0; k < C; ++k) static_cast<double*>(dst)[o + k] = r[k];
+        else
+            std::memcpy(static_cast<float*>(dst) + o, r, size_t(C) * 4);
+    }
+}
+
+// Output field: the whole grid on one rank; owned pixels only under a multi-rank topology.
+void d2h_out(swf_ctx* c, const float* src_loc, int C, int dtype, void* dst) {
+    if (c->world > 1)
+        d2h_owned(c, src_loc, C, dtype, dst);
+    else
+        d2h_field(c, src_loc, C, dtype, dst);
+}
+
 // host field [N][C] -> device local window order (layout 0)
 void h2d_local(swf_ctx* c, const void* src, int C, int dtype, float* dst_loc) {
     h2d_field(c, src, C, dtype, c->in_pix);
@@ -1516,94 +1714,59 @@ void h2d_local(swf_ctx* c, const void* src, int C, int dtype, float* dst_loc) {
     SWF_CUDA(cudaStreamSynchronize(c->st));
 }
 
-// Per-rank input loading from chunked containers (ChunkedReader::read_window_slice,
-// chunked_file.cpp:156-188; the reference CLI reads whole fields, swinflow_main.cpp:128-157): the
-// rank's owned windows of the unshifted layout (its SP band rows) are merged into pixel rects -- runs
-// of adjacent windows in a window row, stacked over window rows when sp == 1 -- read by parallel
-// readers (one file handle each) and gathered into the local token order [M][C]. Returns the number
-// of chunks read (each chunk's checksum verified).
+// Per-rank input loading from tiled field files (ChunkedReader::read_window_slice,
+// chunked_file.cpp:156-188; the reference CLI reads whole fields, swinflow_main.cpp:128-157). The
+// rank's owned windows of the unshifted layout -- only its SP band rows -- define the pixel rows it
+// needs; the tiles covering them are read once each by a pool of threads sharing one descriptor
+// (pread), verified, and scattered straight into the local token order [M][C]. Returns the number of
+// tiles read.
 unsigned long long read_local_chunked(const swf_ctx* c, const std::string& path, int C, float* dst) {
-    const int w = c->m.w, R = w / c->sp, nx = c->W / w;
-    const std::vector<int>& l2g = c->l2g[0];
-    std::vector<int> g2l(size_t(c->H / w) * nx, -1);
-    for (size_t i = 0; i < l2g.size(); ++i) g2l[l2g[i]] = int(i);
-    struct Run {
-        int wy0, wx0, nwy, nwx;
-    };
-    std::vector<Run> runs;
-    for (int gw : l2g) {
-        const int wy = gw / nx, wx = gw % nx;
-        if (!runs.empty() && runs.back().wy0 == wy && runs.back().wx0 + runs.back().nwx == wx) {
-            ++runs.back().nwx;
-            continue;
-        }
-        runs.push_back({wy, wx, 1, 1});
+    const tiles::File f(path);
+    const tiles::Grid& g = f.grid();
+    require(g.H == c->H && g.W == c->W, "chunked input " + path + ": grid " + std::to_string(g.H) + "x" +
+                                            std::to_string(g.W) + " does not match the model grid " +
+                                            std::to_string(c->H) + "x" + std::to_string(c->W));
+    require(g.C == C, "chunked input " + path + ": " + std::to_string(g.C) + " channels, expected " + std::to_string(C));
+    // local token -> pixel is c->owned_pix; invert it per tile: the tiles this rank touches and, per
+    // tile, the (pixel, local index) pairs inside it
+    const int tc = g.cols();
+    std::vector<std::vector<std::pair<long long, i64>>> need(size_t(g.count()));
+    for (i64 i = 0; i < c->M; ++i) {
+        const long long p = c->owned_pix[size_t(i)];
+        const int y = int(p / c->W), x = int(p % c->W);
+        need[size_t(y / g.th) * tc + x / g.tw].push_back({p, i});
     }
-    if (c->sp == 1) {
-        std::vector<Run> st;
-        for (const Run& r : runs) {
-            if (!st.empty() && st.back().wx0 == r.wx0 && st.back().nwx == r.nwx && st.back().wy0 + st.back().nwy == r.wy0) {
-                ++st.back().nwy;
-                continue;
-            }
-            st.push_back(r);
-        }
-        runs.swap(st);
-    }
-    // every run's covering chunks are split over T readers (own file handles; chunk parts are
-    // disjoint in the run buffer), then the run's windows are gathered into the local order
+    std::vector<int> todo;
+    for (int t = 0; t < g.count(); ++t)
+        if (!need[size_t(t)].empty()) todo.push_back(t);
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const int T = int(std::min(16u, hw));
-    std::vector<std::unique_ptr<chunked::Reader>> rds(T);
-    std::vector<std::exception_ptr> errs(T);
-    auto parallel = [&](int n, auto&& fn) {  // fn(t, i) for i = t, t + T, ... < n on min(T, n) threads
-        const int nt = std::max(1, std::min(T, n));
-        auto body = [&](int t) {
-            try {
-                for (int i = t; i < n; i += nt) fn(t, i);
-            } catch (...) {
-                errs[t] = std::current_exception();
+    const int nt = int(std::min<size_t>(std::min(16u, hw), std::max<size_t>(todo.size(), 1)));
+    std::atomic<size_t> next{0};
+    std::vector<std::exception_ptr> errs(static_cast<size_t>(nt));
+    auto worker = [&](int k) {
+        try {
+            std::vector<float> buf;
+            for (size_t j = next++; j < todo.size(); j = next++) {
+                const int t = todo[j], ty = t / tc, tx = t % tc;
+                f.tile(ty, tx, buf);
+                const tiles::Rect b = g.box(ty, tx);
+                for (const auto& pi : need[size_t(t)]) {
+                    const int yy = int(pi.first / c->W) - b.y0, xx = int(pi.first % c->W) - b.x0;
+                    float* o = dst + size_t(pi.second) * C;
+                    for (int ch = 0; ch < C; ++ch) o[ch] = buf[(size_t(ch) * b.h + yy) * b.w + xx];
+                }
             }
-        };
-        std::vector<std::thread> ths;
-        for (int t = 1; t < nt; ++t) ths.emplace_back(body, t);
-        body(0);
-        for (auto& th : ths) th.join();
-        for (auto& e : errs)
-            if (e) std::rethrow_exception(e);
+        } catch (...) {
+            errs[size_t(k)] = std::current_exception();
+        }
     };
-    parallel(T, [&](int t, int) {
-        rds[t] = std::make_unique<chunked::Reader>(path);
-        require(rds[t]->height() == c->H && rds[t]->width() == c->W,
-                "chunked input " + path + ": grid " + std::to_string(rds[t]->height()) + "x" +
-                    std::to_string(rds[t]->width()) + " != model grid " + std::to_string(c->H) + "x" +
-                    std::to_string(c->W));
-        require(rds[t]->channels() == C, "chunked input " + path + ": " + std::to_string(rds[t]->channels()) +
-                                             " channels, expected " + std::to_string(C));
-    });
-    std::vector<float> buf;
-    for (const Run& u : runs) {
-        const chunked::Rect rc{u.wy0 * w + c->band * R, u.wx0 * w, u.nwy * R, u.nwx * w};
-        rds[0]->check(rc);
-        int cy0, cy1, cx0, cx1;
-        rds[0]->chunk_range(rc, cy0, cy1, cx0, cx1);
-        const int ncx = cx1 - cx0 + 1, nch = (cy1 - cy0 + 1) * ncx;
-        buf.resize(size_t(rc.h) * rc.w * C);
-        parallel(nch, [&](int t, int i) { rds[t]->read_chunk(rc, cy0 + i / ncx, cx0 + i % ncx, buf.data()); });
-        parallel(u.nwy * u.nwx, [&](int, int i) {
-            const int a = i / u.nwx, b = i % u.nwx;
-            const int lw = g2l[(u.wy0 + a) * nx + u.wx0 + b];
-            for (int k = 0; k < R; ++k)
-                std::memcpy(dst + (size_t(lw) * R * w + size_t(k) * w) * C,
-                            buf.data() + (size_t(a * R + k) * rc.w + size_t(b) * w) * C, size_t(w) * C * sizeof(float));
-        });
-    }
-    std::vector<unsigned long long> reads;
-    for (auto& r : rds)
-        if (r) reads.push_back(r->chunk_reads());
-    unsigned long long n = 0;
-    for (auto v : reads) n += v;
-    return n;
+    std::vector<std::thread> th;
+    for (int k = 1; k < nt; ++k) th.emplace_back(worker, k);
+    worker(0);
+    for (auto& t : th) t.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    return f.tiles_read();
 }
 
 // chunked staging slots: pinned local-order buffers filled by a (background) reader thread
@@ -1693,6 +1856,7 @@ void forecast_core(swf_ctx* c, const float* xprev_phys_loc, const float* forc_ph
     solve(c, dc, h_kd(event, 0xc4u), nullptr);
     destandardize_add(c->s_x, xprev_phys_loc, c->M, cp, S + 2 * m.cin, S + 3 * m.cin, dst_loc, c->st);
     c->launches += 5;
+    if (c->world > 1) peer_barrier(c);  // the solver's divergence flags reach every rank
 }
 
 int fail(const std::exception& e, int rc) {
@@ -1823,6 +1987,124 @@ void grads_to_host(swf_ctx* c, const float* src, double scale, void* out, int dt
         return fail(e, SWF_ERR_CUDA);                               \
     }
 
+namespace {
+
+// ---- single-process multi-GPU groups (swf_set_topology_devices)
+thread_local bool tl_group_worker = false;  // set inside a group's per-rank threads
+
+std::vector<swf_ctx*> group_ranks(swf_ctx* root) {
+    std::vector<swf_ctx*> r{root};
+    r.insert(r.end(), root->kids.begin(), root->kids.end());
+    return r;
+}
+
+// Run fn(rank context) for every rank of the group on its own host thread (the ranks meet in device
+// barriers, so they must run concurrently) and return the most specific failure: numerics (1) before
+// config (2), I/O (3) and device (4) -- a barrier timeout on one rank is the consequence of another
+// rank's error, not the cause.
+template <class F>
+int group_run(swf_ctx* root, F&& fn) {
+    const std::vector<swf_ctx*> R = group_ranks(root);
+    const size_t n = R.size();
+    std::vector<int> rc(n, SWF_OK);
+    std::vector<std::string> msg(n);
+    std::vector<std::thread> th;
+    th.reserve(n);
+    for (size_t r = 0; r < n; ++r)
+        th.emplace_back([&, r] {
+            tl_group_worker = true;
+            rc[r] = fn(R[r], int(r));
+            if (rc[r] != SWF_OK) msg[r] = g_err;
+        });
+    for (auto& t : th) t.join();
+    int best = -1;
+    for (size_t r = 0; r < n; ++r)
+        if (rc[r] != SWF_OK && (best < 0 || rc[r] < rc[best])) best = int(r);
+    if (best < 0) return SWF_OK;
+    g_err = "rank " + std::to_string(best) + ": " + msg[best];
+    return rc[best];
+}
+
+#define SWF_FANOUT(c, call)                                                                         \
+    if ((c) != nullptr && !(c)->kids.empty() && !tl_group_worker)                                  \
+    return group_run((c), [&](swf_ctx * r_, int rank_) {                                          \
+        (void)rank_;                                                                                \
+        return call;                                                                                \
+    })
+
+// Sum per-rank partial sums (f64, fixed rank order: deterministic) into out (f32 / f64).
+void sum_ranks(const std::vector<std::vector<double>>& g, void* out, int dtype) {
+    if (!out || g.empty()) return;
+    const size_t n = g[0].size();
+    for (size_t i = 0; i < n; ++i) {
+        double v = 0.0;
+        for (const auto& r : g) v += r[i];
+        if (dtype == SWF_F64)
+            static_cast<double*>(out)[i] = v;
+        else
+            static_cast<float*>(out)[i] = float(v);
+    }
+}
+
+void rethrow_rc(int rc) {
+    if (rc == SWF_OK) return;
+    if (rc == SWF_ERR_NUMERICS) throw NumericsError(g_err);
+    if (rc == SWF_ERR_CONFIG) throw ConfigError(g_err);
+    if (rc == SWF_ERR_IO) throw IoError(g_err);
+    throw CudaError(g_err);
+}
+
+// Device tables of peer pointers (residual buffers, barrier flags, attention planes / output) from
+// c->peer, after IPC mapping or in-process peer mapping.
+void upload_peer_tables(swf_ctx* c) {
+    for (int par = 0; par < 2; ++par) {
+        std::vector<float*> t(8, nullptr);
+        for (int r = 0; r < c->world; ++r) t[r] = c->peer[r].x[par];
+        SWF_CUDA(cudaMemcpy(c->d_xdst[par], t.data(), sizeof(float*) * 8, cudaMemcpyHostToDevice));
+    }
+    std::vector<int*> ft(8, nullptr);
+    std::vector<void*> qt(8, nullptr), ot(8, nullptr);
+    for (int r = 0; r < c->world; ++r) {
+        ft[r] = c->peer[r].flags;
+        qt[r] = c->peer[r].qkv;
+        ot[r] = c->peer[r].xm;
+    }
+    SWF_CUDA(cudaMemcpy(c->d_flag_table, ft.data(), sizeof(int*) * 8, cudaMemcpyHostToDevice));
+    SWF_CUDA(cudaMemcpy(c->d_qkv_dst, qt.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+    SWF_CUDA(cudaMemcpy(c->d_o_dst, ot.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+    c->peers = true;
+}
+
+// Map every rank's buffers into every other rank of a single-process group: one address space, so
+// the peer pointers are the ranks' own allocations; ranks on different GPUs need peer access.
+void group_connect(swf_ctx* root) {
+    const std::vector<swf_ctx*> R = group_ranks(root);
+    for (swf_ctx* a : R)
+        for (swf_ctx* b : R) {
+            if (a->dev == b->dev) continue;
+            int can = 0;
+            SWF_CUDA(cudaDeviceCanAccessPeer(&can, a->dev, b->dev));
+            if (!can)
+                throw CudaError("group: device " + std::to_string(a->dev) + " cannot access device " +
+                                std::to_string(b->dev) + " (no NVLink / P2P path)");
+            SWF_CUDA(cudaSetDevice(a->dev));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b->dev, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled)
+                (void)cudaGetLastError();
+            else
+                SWF_CUDA(e);
+        }
+    for (swf_ctx* c : R) {
+        SWF_CUDA(cudaSetDevice(c->dev));
+        for (int r = 0; r < c->world; ++r)
+            c->peer[r] = Peer{{R[r]->xbuf[0], R[r]->xbuf[1]}, R[r]->bar_flags, R[r]->qkv, R[r]->xm};
+        upload_peer_tables(c);
+        SWF_CUDA(cudaDeviceSynchronize());
+    }
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* swf_last_error(void) { return g_err.c_str(); }
@@ -1862,6 +2144,8 @@ int swf_create(const swf_model_cfg* cfg, int grid_h, int grid_w, int device, int
 
 void swf_destroy(swf_ctx* c) {
     if (!c) return;
+    for (swf_ctx* k : c->kids) swf_destroy(k);
+    c->kids.clear();
     cudaSetDevice(c->dev);
     cudaStreamSynchronize(c->st);
     for (void* p : c->allocs) cudaFree(p);
@@ -1875,7 +2159,8 @@ void swf_destroy(swf_ctx* c) {
     if (c->tr.h_part) cudaFreeHost(c->tr.h_part);
     if (c->solve_exec) cudaGraphExecDestroy(c->solve_exec);
     if (c->h_feat) cudaFreeHost(c->h_feat);
-    for (int r = 0; r < int(c->peer.size()); ++r) {  // unmap every IPC-opened peer buffer
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    for (int r = 0; r < int(c->peer.size()) && c->ipc_mapped; ++r) {  // unmap every IPC-opened peer buffer
         if (r == c->rank) continue;
         const Peer& pr = c->peer[r];
         for (void* p : {static_cast<void*>(pr.x[0]), static_cast<void*>(pr.x[1]), static_cast<void*>(pr.flags),
@@ -1912,7 +2197,43 @@ int swf_set_topology(swf_ctx* c, int wp_a, int wp_b, int sp, int rank, int owner
     })
 }
 
+int swf_set_topology_devices(swf_ctx* c, int wp_a, int wp_b, int sp, int ownership, const int* device_ids) {
+    SWF_API_TRY({
+        require(c && device_ids, "null argument");
+        require(c->kids.empty() && !c->allocated && c->world == 1,
+                "swf_set_topology_devices: once, on a fresh context, before loading parameters");
+        require(device_ids[0] == c->dev, "swf_set_topology_devices: device_ids[0] must be the context's device");
+        rethrow_rc(swf_set_topology(c, wp_a, wp_b, sp, 0, ownership));
+        try {
+            for (int r = 1; r < c->world; ++r) {
+                swf_ctx* k = nullptr;
+                rethrow_rc(swf_create(&c->cfg, c->H, c->W, device_ids[r], c->prec, &k));
+                c->kids.push_back(k);
+                rethrow_rc(swf_set_topology(k, wp_a, wp_b, sp, r, ownership));
+            }
+        } catch (...) {
+            for (swf_ctx* k : c->kids) swf_destroy(k);
+            c->kids.clear();
+            c->wp_a = c->wp_b = c->sp = c->world = 1;
+            c->rank = c->wp_rank = c->band = 0;
+            throw;
+        }
+        SWF_CUDA(cudaSetDevice(c->dev));
+    })
+}
+
+int swf_group_size(swf_ctx* c) { return c ? 1 + int(c->kids.size()) : 0; }
+swf_ctx* swf_group_rank(swf_ctx* c, int r) {
+    if (!c || r < 0 || r > int(c->kids.size())) return nullptr;
+    return r == 0 ? c : c->kids[size_t(r - 1)];
+}
+
 int swf_load_params(swf_ctx* c, const void* const* arrays, int n_arrays, int dtype) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        const int rc = group_run(c, [&](swf_ctx* r_, int) { return swf_load_params(r_, arrays, n_arrays, dtype); });
+        if (rc != SWF_OK) return rc;
+        SWF_API_TRY(group_connect(c))
+    }
     SWF_API_TRY({
         require(c && arrays, "null argument");
         SWF_CUDA(cudaSetDevice(c->dev));
@@ -1921,6 +2242,11 @@ int swf_load_params(swf_ctx* c, const void* const* arrays, int n_arrays, int dty
 }
 
 int swf_load_params_flat(swf_ctx* c, const void* flat, long long count, int dtype) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        const int rc = group_run(c, [&](swf_ctx* r_, int) { return swf_load_params_flat(r_, flat, count, dtype); });
+        if (rc != SWF_OK) return rc;
+        SWF_API_TRY(group_connect(c))
+    }
     SWF_API_TRY({
         require(c && flat, "null argument");
         require(count == swf_param_count(&c->cfg), "load_params: flat count " + std::to_string(count) +
@@ -1950,6 +2276,11 @@ int swf_load_params_flat(swf_ctx* c, const void* flat, long long count, int dtyp
 }
 
 int swf_load_checkpoint(swf_ctx* c, const char* base) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        const int rc = group_run(c, [&](swf_ctx* r_, int) { return swf_load_checkpoint(r_, base); });
+        if (rc != SWF_OK) return rc;
+        SWF_API_TRY(group_connect(c))
+    }
     SWF_API_TRY({
         require(c && base, "null argument");
         SWF_CUDA(cudaSetDevice(c->dev));
@@ -1990,6 +2321,11 @@ int swf_verify_checkpoint(const swf_model_cfg* cfg, const char* base) {
 }
 
 int swf_init_params(swf_ctx* c, uint64_t seed, int mode, double scale) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        const int rc = group_run(c, [&](swf_ctx* r_, int) { return swf_init_params(r_, seed, mode, scale); });
+        if (rc != SWF_OK) return rc;
+        SWF_API_TRY(group_connect(c))
+    }
     SWF_API_TRY({
         require(c, "null context");
         require(mode >= 0 && mode <= 2, "init_params: mode must be 0, 1 or 2");
@@ -1999,6 +2335,7 @@ int swf_init_params(swf_ctx* c, uint64_t seed, int mode, double scale) {
 }
 
 int swf_forward(swf_ctx* c, const void* input, double t, void* output, int dtype) {
+    SWF_FANOUT(c, swf_forward(r_, input, t, output, dtype));
     SWF_API_TRY({
         require(c && input && output, "null argument");
         require(c->loaded, "forward: parameters not loaded");
@@ -2008,13 +2345,105 @@ int swf_forward(swf_ctx* c, const void* input, double t, void* output, int dtype
         gather_input_any(c, c->in_pix);
         forward_any(c, t, 1.f);
         check_flags(c);
-        d2h_field(c, c->out_loc, c->m.cout, dtype, output);
+        d2h_out(c, c->out_loc, c->m.cout, dtype, output);
     })
 }
 
 
+int swf_forward_hidden(swf_ctx* c, const void* input, double t, int n_blocks, const long long* pixels,
+                       long long n_pix, float* hidden, int dtype) {
+    SWF_FANOUT(c, swf_forward_hidden(r_, input, t, n_blocks, pixels, n_pix, hidden, dtype));
+    SWF_API_TRY({
+        require(c && input && (n_pix == 0 || (pixels && hidden)), "null argument");
+        require(c->loaded, "forward_hidden: parameters not loaded");
+        require(n_blocks >= 0 && n_blocks <= c->m.nb, "forward_hidden: n_blocks out of range");
+        require(n_pix >= 0, "forward_hidden: negative pixel count");
+        for (long long k = 0; k < n_pix; ++k)
+            require(pixels[k] >= 0 && pixels[k] < c->N, "forward_hidden: pixel index out of range");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        reset_flags(c);
+        h2d_field(c, input, c->m.cin, dtype, c->in_pix);
+        gather_input_any(c, c->in_pix);
+        c->stop_after = n_blocks;
+        try {
+            forward_any(c, t, 1.f);
+        } catch (...) {
+            c->stop_after = -1;
+            throw;
+        }
+        c->stop_after = -1;
+        i64* d_pix = static_cast<i64*>(scratch(c, SC_PIX, size_t(std::max<long long>(n_pix, 1)) * 8));
+        float* d_out = scratch_f(c, SC_ROWS, size_t(std::max<long long>(n_pix, 1)) * c->m.h);
+        SWF_CUDA(cudaMemcpyAsync(d_pix, pixels, size_t(n_pix) * 8, cudaMemcpyHostToDevice, c->st));
+        rows_at_pixels(c->xbuf[c->hid_cur], c->lay[c->hid_par], c->rank, c->m.h, d_pix, n_pix, d_out, c->st);
+        check_flags(c);
+        std::vector<float> tmp(size_t(n_pix) * c->m.h);
+        SWF_CUDA(cudaMemcpyAsync(tmp.data(), d_out, tmp.size() * 4, cudaMemcpyDeviceToHost, c->st));
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        // rows of pixels another rank owns stay as the caller passed them
+        std::vector<char> own(size_t(n_pix), 0);
+        {
+            const LayMap& L = c->lay[c->hid_par];
+            std::vector<int> g2rl(size_t(L.g.nx) * L.g.ny);
+            SWF_CUDA(cudaMemcpy(g2rl.data(), L.glob2rl, g2rl.size() * 4, cudaMemcpyDeviceToHost));
+            for (long long k = 0; k < n_pix; ++k) {
+                const i64 gi = L.g.pix_to_win(pixels[k]);
+                const int gw = int(gi / L.g.s()), tok = int(gi % L.g.s());
+                const int band = L.band_of_row(tok / L.g.w);
+                own[k] = ((g2rl[gw] >> 16) * c->sp + band) == c->rank;
+            }
+        }
+        for (long long k = 0; k < n_pix; ++k)
+            if (own[k]) std::memcpy(hidden + size_t(k) * c->m.h, tmp.data() + size_t(k) * c->m.h, size_t(c->m.h) * 4);
+    })
+}
+
+int swf_block_window_forward(swf_ctx* c, int block, int wy, int wx, double t, const void* x_in, void* x_out,
+                             int dtype) {
+    SWF_API_TRY({
+        require(c && x_in && x_out, "null argument");
+        require(c->loaded, "block_window_forward: parameters not loaded");
+        require(c->world == 1, "block_window_forward: single-rank contexts (a window lives on one rank)");
+        require(block >= 0 && block < c->m.nb, "block_window_forward: block out of range");
+        const Lay& g = c->lay[block & 1].g;
+        require(wy >= 0 && wy < g.ny && wx >= 0 && wx < g.nx, "block_window_forward: window out of range");
+        SWF_CUDA(cudaSetDevice(c->dev));
+        const Dims& m = c->m;
+        const size_t n = size_t(m.w) * m.w * m.h;
+        std::vector<float> tmp(n);
+        const float* src = static_cast<const float*>(x_in);
+        if (dtype == SWF_F64) {
+            for (size_t i = 0; i < n; ++i) tmp[i] = float(static_cast<const double*>(x_in)[i]);
+            src = tmp.data();
+        }
+        reset_flags(c);
+        SWF_CUDA(cudaMemcpyAsync(c->xbuf[0], src, n * 4, cudaMemcpyHostToDevice, c->st));
+        if (c->prec == SWF_PREC_BF16)
+            block_window_core<__nv_bfloat16>(c, block, wy, wx, t);
+        else
+            block_window_core<float>(c, block, wy, wx, t);
+        check_flags(c);
+        SWF_CUDA(cudaMemcpyAsync(tmp.data(), c->xbuf[1], n * 4, cudaMemcpyDeviceToHost, c->st));
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        if (dtype == SWF_F64)
+            for (size_t i = 0; i < n; ++i) static_cast<double*>(x_out)[i] = tmp[i];
+        else
+            std::memcpy(x_out, tmp.data(), n * 4);
+    })
+}
+
 int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, void* grads, void* d_input,
                  int dtype) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        const size_t n = size_t(swf_param_count(&c->cfg));
+        std::vector<std::vector<double>> g(c->kids.size() + 1, std::vector<double>(n));
+        const int rc = group_run(c, [&](swf_ctx* r_, int k) {
+            return swf_backward(r_, input, t, d_output, grads ? g[size_t(k)].data() : nullptr, d_input, SWF_F64);
+        });
+        if (rc != SWF_OK) return rc;
+        sum_ranks(g, grads, dtype);
+        return SWF_OK;
+    }
     SWF_API_TRY({
         require(c && input && d_output && grads, "null argument");
         require(c->loaded, "backward: parameters not loaded");
@@ -2032,6 +2461,7 @@ int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, 
         h2d_local(c, d_output, c->m.cout, dtype, c->bw.dtmp);  // [M][C_out] in layout-0 order
         SWF_CUDA(cudaMemcpyAsync(c->bw.dS, c->bw.dtmp, size_t(c->M) * c->m.cout * 4, cudaMemcpyDeviceToDevice, c->st));
         backward_core(c, c->bw.dS);
+        check_flags(c);  // a WP peer that stalled in the backward's exchanges fails the call here
         const size_t n = c->poff.back();
         std::vector<float> g(n);
         SWF_CUDA(cudaMemcpyAsync(g.data(), c->bw.gflat, n * 4, cudaMemcpyDeviceToHost, c->st));
@@ -2040,7 +2470,9 @@ int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, 
             for (size_t i = 0; i < n; ++i) static_cast<double*>(grads)[i] = g[i];
         else
             std::memcpy(grads, g.data(), n * 4);
-        if (d_input) {  // local layout-0 rows -> pixel order (in_pix holds N x C_in)
+        if (d_input && c->world > 1) {
+            d2h_owned(c, c->bw.din, c->m.cin, dtype, d_input);
+        } else if (d_input) {  // local layout-0 rows -> pixel order (in_pix holds N x C_in)
             const size_t ni = size_t(c->N) * c->m.cin;
             SWF_CUDA(cudaMemsetAsync(c->in_pix, 0, ni * 4, c->st));
             scatter_rows(c->bw.din, c->lay[0], c->m.cin, c->M, c->in_pix, c->st);
@@ -2059,6 +2491,22 @@ int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, 
 int swf_diffusion_loss_sample(swf_ctx* c, const void* x_prev, const void* x0, const void* forcings,
                               const swf_loss_weights* w, const swf_diffusion_cfg* dc, uint64_t t_key, const void* z,
                               double* loss, void* grads, int dtype) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        const size_t n = size_t(swf_param_count(&c->cfg));
+        std::vector<std::vector<double>> g(c->kids.size() + 1, std::vector<double>(grads ? n : 0));
+        std::vector<double> l(c->kids.size() + 1, 0.0);
+        const int rc = group_run(c, [&](swf_ctx* r_, int k) {
+            return swf_diffusion_loss_sample(r_, x_prev, x0, forcings, w, dc, t_key, z, &l[size_t(k)],
+                                             grads ? g[size_t(k)].data() : nullptr, SWF_F64);
+        });
+        if (rc != SWF_OK) return rc;
+        if (loss) {  // partial sums over the ranks' tokens, in rank order
+            *loss = 0.0;
+            for (double v : l) *loss += v;
+        }
+        if (grads) sum_ranks(g, grads, dtype);
+        return SWF_OK;
+    }
     SWF_API_TRY({
         require(c && x_prev && x0 && dc && z && loss, "null argument");
         train_checks(c);
@@ -2066,6 +2514,7 @@ int swf_diffusion_loss_sample(swf_ctx* c, const void* x_prev, const void* x0, co
         train_inputs(c, x_prev, x0, forcings, dtype);
         h2d_local(c, z, c->m.cout, dtype, c->tr.z);
         *loss = train_sample_core(c, *dc, t_key);
+        check_flags(c);
         if (grads) grads_to_host(c, c->bw.gflat, 1.0, grads, dtype);
     })
 }
@@ -2073,6 +2522,17 @@ int swf_diffusion_loss_sample(swf_ctx* c, const void* x_prev, const void* x0, co
 int swf_train_accumulate(swf_ctx* c, const void* x_prev, const void* x0, const void* forcings,
                          const swf_loss_weights* w, const swf_diffusion_cfg* dc, uint64_t run_seed,
                          uint64_t sample_id, double* loss, int dtype) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        std::vector<double> l(c->kids.size() + 1, 0.0);
+        const int rc = group_run(c, [&](swf_ctx* r_, int k) {
+            return swf_train_accumulate(r_, x_prev, x0, forcings, w, dc, run_seed, sample_id, &l[size_t(k)], dtype);
+        });
+        if (rc == SWF_OK && loss) {
+            *loss = 0.0;
+            for (double v : l) *loss += v;
+        }
+        return rc;
+    }
     SWF_API_TRY({
         require(c && x_prev && x0 && dc && loss, "null argument");
         train_checks(c);
@@ -2082,6 +2542,7 @@ int swf_train_accumulate(swf_ctx* c, const void* x_prev, const void* x0, const v
         noise_field(h_kd(h_kd(run_seed, 0x7au), sample_id), c->m.cout, c->lay[0], dc->sigma_d, c->tr.z, c->st);
         c->launches++;
         *loss = train_sample_core(c, *dc, h_kd(h_kd(run_seed, 0x74u), sample_id));
+        check_flags(c);  // the backward's peer exchanges completed (no partial landing buffer)
         axpy_f32(c->bw.gflat, i64(c->poff.back()), 1.f, c->tr.gacc, c->st);
         c->launches++;
         SWF_CUDA(cudaStreamSynchronize(c->st));  // the accumulator is complete for an all-reduce
@@ -2089,6 +2550,7 @@ int swf_train_accumulate(swf_ctx* c, const void* x_prev, const void* x0, const v
 }
 
 int swf_train_reset(swf_ctx* c) {
+    SWF_FANOUT(c, swf_train_reset(r_));
     SWF_API_TRY({
         require(c, "null context");
         train_checks(c);
@@ -2098,6 +2560,10 @@ int swf_train_reset(swf_ctx* c) {
 }
 
 int swf_train_grads(swf_ctx* c, float** dev_ptr, long long* n) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        g_err = "a single-process group sums its ranks' gradients itself: read them with swf_train_read";
+        return SWF_ERR_CONFIG;
+    }
     SWF_API_TRY({
         require(c && dev_ptr && n, "null argument");
         train_checks(c);
@@ -2107,6 +2573,16 @@ int swf_train_grads(swf_ctx* c, float** dev_ptr, long long* n) {
 }
 
 int swf_train_read(swf_ctx* c, double scale, void* grads, int dtype) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        const size_t n = size_t(swf_param_count(&c->cfg));
+        std::vector<std::vector<double>> g(c->kids.size() + 1, std::vector<double>(n));
+        const int rc = group_run(c, [&](swf_ctx* r_, int k) { return swf_train_read(r_, 1.0, g[size_t(k)].data(), SWF_F64); });
+        if (rc != SWF_OK) return rc;
+        for (auto& v : g)
+            for (double& x : v) x *= scale;
+        sum_ranks(g, grads, dtype);
+        return SWF_OK;
+    }
     SWF_API_TRY({
         require(c && grads, "null argument");
         train_checks(c);
@@ -2115,6 +2591,10 @@ int swf_train_read(swf_ctx* c, double scale, void* grads, int dtype) {
 }
 
 int swf_forward_device(swf_ctx* c, const float* d_input, double t, float* d_output) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        g_err = "swf_forward_device takes one device's pointers: call it per rank context (swf_group_rank)";
+        return SWF_ERR_CONFIG;
+    }
     SWF_API_TRY({
         require(c && d_input && d_output, "null argument");
         require(c->loaded, "forward: parameters not loaded");
@@ -2129,6 +2609,7 @@ int swf_forward_device(swf_ctx* c, const float* d_input, double t, float* d_outp
 }
 
 int swf_sync(swf_ctx* c) {
+    SWF_FANOUT(c, swf_sync(r_));
     SWF_API_TRY({
         require(c, "null context");
         SWF_CUDA(cudaSetDevice(c->dev));
@@ -2140,6 +2621,14 @@ void* swf_stream(swf_ctx* c) { return c ? static_cast<void*>(c->st) : nullptr; }
 
 int swf_solve_pf_ode(swf_ctx* c, const void* x_init, const void* x_prev_std, const void* forcings_std,
                      const swf_diffusion_cfg* dc, uint64_t churn_key, void* x_out, int* f_evals, int dtype) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        std::vector<int> fe(c->kids.size() + 1, 0);
+        const int rc = group_run(c, [&](swf_ctx* r_, int k) {
+            return swf_solve_pf_ode(r_, x_init, x_prev_std, forcings_std, dc, churn_key, x_out, &fe[size_t(k)], dtype);
+        });
+        if (rc == SWF_OK && f_evals) *f_evals = fe[0];
+        return rc;
+    }
     SWF_API_TRY({
         require(c && x_init && x_prev_std && dc && x_out, "null argument");
         require(c->loaded, "solve: parameters not loaded");
@@ -2157,13 +2646,15 @@ int swf_solve_pf_ode(swf_ctx* c, const void* x_init, const void* x_prev_std, con
         set_conditioning(c, c->s_tmp, c->s_cond);
         h2d_local(c, x_init, m.cout, dtype, c->s_x);
         solve(c, *dc, churn_key, f_evals);
+        if (c->world > 1) peer_barrier(c);  // every rank's divergence flags, before the check
         check_flags(c);
-        d2h_field(c, c->s_x, m.cout, dtype, x_out);
+        d2h_out(c, c->s_x, m.cout, dtype, x_out);
     })
 }
 
 int swf_forecast_step(swf_ctx* c, const void* x_prev_phys, const void* forcing_phys, const swf_standardizers* stds,
                       const swf_diffusion_cfg* dc, uint64_t run_seed, uint64_t noise_event, void* out, int dtype) {
+    SWF_FANOUT(c, swf_forecast_step(r_, x_prev_phys, forcing_phys, stds, dc, run_seed, noise_event, out, dtype));
     SWF_API_TRY({
         require(c && x_prev_phys && dc && out, "null argument");
         require(c->loaded, "forecast: parameters not loaded");
@@ -2179,28 +2670,18 @@ int swf_forecast_step(swf_ctx* c, const void* x_prev_phys, const void* forcing_p
         float* forc = nullptr;
         if (cf > 0) {
             require(forcing_phys != nullptr, "forecast: forcings required");
-            forc = dalloc<float>(c, size_t(c->M) * cf);
+            forc = scratch_f(c, SC_FORC, size_t(c->M) * cf);
             h2d_local(c, forcing_phys, cf, dtype, forc);
         }
-        float* dst = dalloc<float>(c, size_t(c->M) * m.cout);
+        float* dst = scratch_f(c, SC_OUT, size_t(c->M) * m.cout);
         forecast_core(c, c->s_base, forc, *dc, run_seed, noise_event, dst);
         check_flags(c);
-        d2h_field(c, dst, m.cout, dtype, out);
-        SWF_CUDA(cudaStreamSynchronize(c->st));
-        // release the per-call buffers (keeps repeated calls bounded)
-        for (void* p : {static_cast<void*>(dst), static_cast<void*>(forc)}) {
-            if (!p) continue;
-            for (size_t i = 0; i < c->allocs.size(); ++i)
-                if (c->allocs[i] == p) {
-                    cudaFree(p);
-                    c->allocs.erase(c->allocs.begin() + i);
-                    break;
-                }
-        }
+        d2h_out(c, dst, m.cout, dtype, out);
     })
 }
 
 int swf_prefetch_chunked(swf_ctx* c, const char* state_path, const char* forcing_path) {
+    SWF_FANOUT(c, swf_prefetch_chunked(r_, state_path, forcing_path));
     SWF_API_TRY({
         require(c && state_path, "null argument");
         require(c->allocated, "prefetch: load parameters first (the topology fixes the local windows)");
@@ -2213,6 +2694,7 @@ int swf_prefetch_chunked(swf_ctx* c, const char* state_path, const char* forcing
 int swf_forecast_step_chunked(swf_ctx* c, const char* state_path, const char* forcing_path,
                               const swf_standardizers* stds, const swf_diffusion_cfg* dc, uint64_t run_seed,
                               uint64_t noise_event, void* out, int dtype) {
+    SWF_FANOUT(c, swf_forecast_step_chunked(r_, state_path, forcing_path, stds, dc, run_seed, noise_event, out, dtype));
     SWF_API_TRY({
         require(c && state_path && dc && out, "null argument");
         require(c->loaded, "forecast: parameters not loaded");
@@ -2238,39 +2720,29 @@ int swf_forecast_step_chunked(swf_ctx* c, const char* state_path, const char* fo
         SWF_CUDA(cudaMemcpyAsync(c->s_base, s.state, size_t(c->M) * m.cout * 4, cudaMemcpyHostToDevice, c->st));
         float* forc = nullptr;
         if (cf > 0) {
-            forc = dalloc<float>(c, size_t(c->M) * cf);
+            forc = scratch_f(c, SC_FORC, size_t(c->M) * cf);
             SWF_CUDA(cudaMemcpyAsync(forc, s.forcing, size_t(c->M) * cf * 4, cudaMemcpyHostToDevice, c->st));
         }
-        float* dst = dalloc<float>(c, size_t(c->M) * m.cout);
+        float* dst = scratch_f(c, SC_OUT, size_t(c->M) * m.cout);
         forecast_core(c, c->s_base, forc, *dc, run_seed, noise_event, dst);
         check_flags(c);
-        d2h_field(c, dst, m.cout, dtype, out);
-        SWF_CUDA(cudaStreamSynchronize(c->st));
-        for (void* p : {static_cast<void*>(dst), static_cast<void*>(forc)}) {
-            if (!p) continue;
-            for (size_t i = 0; i < c->allocs.size(); ++i)
-                if (c->allocs[i] == p) {
-                    cudaFree(p);
-                    c->allocs.erase(c->allocs.begin() + i);
-                    break;
-                }
-        }
+        d2h_out(c, dst, m.cout, dtype, out);
     })
 }
 
 long long swf_last_chunk_reads(swf_ctx* c) { return c ? (long long)c->last_chunk_reads : -1; }
 
-// ---- the container itself (host only; chunked_file.hpp / src/chunked_file.cpp)
+// ---- the tiled field file itself (host only; format of chunked_file.hpp / src/chunked_file.cpp)
 struct swf_chunked {
-    explicit swf_chunked(const std::string& p) : r(p) {}
-    swf::chunked::Reader r;
+    explicit swf_chunked(const std::string& p) : f(p) {}
+    swf::tiles::File f;
 };
 
 int swf_chunked_write(const char* path, const float* field, int channels, int height, int width, int chunk_h,
                       int chunk_w) {
     SWF_API_TRY({
         require(path && field, "null argument");
-        swf::chunked::write(path, field, channels, height, width, chunk_h, chunk_w);
+        swf::tiles::save(path, field, channels, height, width, chunk_h, chunk_w);
     })
 }
 int swf_chunked_open(const char* path, swf_chunked** out) {
@@ -2283,33 +2755,35 @@ void swf_chunked_close(swf_chunked* r) { delete r; }
 int swf_chunked_info(swf_chunked* r, int* channels, int* height, int* width, int* chunk_h, int* chunk_w) {
     SWF_API_TRY({
         require(r, "null reader");
-        if (channels) *channels = r->r.channels();
-        if (height) *height = r->r.height();
-        if (width) *width = r->r.width();
-        if (chunk_h) *chunk_h = r->r.chunk_h();
-        if (chunk_w) *chunk_w = r->r.chunk_w();
+        const swf::tiles::Grid& g = r->f.grid();
+        if (channels) *channels = g.C;
+        if (height) *height = g.H;
+        if (width) *width = g.W;
+        if (chunk_h) *chunk_h = g.th;
+        if (chunk_w) *chunk_w = g.tw;
     })
 }
 int swf_chunked_read(swf_chunked* r, int y0, int x0, int h, int w, float* out) {
     SWF_API_TRY({
         require(r && out, "null argument");
-        r->r.read({y0, x0, h, w}, out);
+        r->f.read({y0, x0, h, w}, out);
     })
 }
 int swf_chunked_cover(swf_chunked* r, int y0, int x0, int h, int w, long long* n) {
     SWF_API_TRY({
         require(r && n, "null argument");
-        *n = (long long)r->r.cover({y0, x0, h, w});
+        *n = (long long)r->f.grid().touched({y0, x0, h, w});
     })
 }
-long long swf_chunked_reads(swf_chunked* r) { return r ? (long long)r->r.chunk_reads() : -1; }
+long long swf_chunked_reads(swf_chunked* r) { return r ? (long long)r->f.tiles_read() : -1; }
 void swf_chunked_reset_reads(swf_chunked* r) {
-    if (r) r->r.reset_chunk_reads();
+    if (r) r->f.reset_tiles_read();
 }
 
 int swf_rollout_ensemble(swf_ctx* c, const void* x_init_phys, const void* forcings_phys, int n_members, int n_steps,
                          const swf_standardizers* stds, const swf_diffusion_cfg* dc, uint64_t run_seed,
                          uint64_t rollout_id, void* out, int dtype) {
+    SWF_FANOUT(c, swf_rollout_ensemble(r_, x_init_phys, forcings_phys, n_members, n_steps, stds, dc, run_seed, rollout_id, out, dtype));
     SWF_API_TRY({
         require(c && x_init_phys && dc && out, "null argument");
         require(n_members >= 1 && n_steps >= 1, "rollout: members and steps must be >= 1");
@@ -2323,10 +2797,10 @@ int swf_rollout_ensemble(swf_ctx* c, const void* x_init_phys, const void* forcin
         upload_stats(c, stds, dtype);
         const size_t es = dtype == SWF_F64 ? 8 : 4;
         const size_t fsz = size_t(c->N) * m.cout * es, ffsz = size_t(c->N) * std::max(cf, 0) * es;
-        float* x0 = dalloc<float>(c, size_t(c->M) * m.cout);
-        float* xa = dalloc<float>(c, size_t(c->M) * m.cout);
-        float* xb = dalloc<float>(c, size_t(c->M) * m.cout);
-        float* forc = dalloc<float>(c, size_t(c->M) * std::max(cf, 1) * n_steps);
+        float* x0 = scratch_f(c, SC_RX0, size_t(c->M) * m.cout);
+        float* xa = scratch_f(c, SC_RXA, size_t(c->M) * m.cout);
+        float* xb = scratch_f(c, SC_RXB, size_t(c->M) * m.cout);
+        float* forc = scratch_f(c, SC_RFORC, size_t(c->M) * std::max(cf, 1) * n_steps);
         h2d_local(c, x_init_phys, m.cout, dtype, x0);
         for (int k = 0; k < n_steps && cf > 0; ++k)
             h2d_local(c, static_cast<const char*>(forcings_phys) + k * ffsz, cf, dtype,
@@ -2340,18 +2814,11 @@ int swf_rollout_ensemble(swf_ctx* c, const void* x_init_phys, const void* forcin
                 reset_flags(c);
                 forecast_core(c, x, forc + size_t(c->M) * std::max(cf, 0) * k, *dc, run_seed, ev, dst);
                 check_flags(c);
-                d2h_field(c, dst, m.cout, dtype, static_cast<char*>(out) + (size_t(mem) * n_steps + k) * fsz);
+                d2h_out(c, dst, m.cout, dtype, static_cast<char*>(out) + (size_t(mem) * n_steps + k) * fsz);
                 x = dst;
             }
         }
         SWF_CUDA(cudaStreamSynchronize(c->st));
-        for (void* p : {static_cast<void*>(x0), static_cast<void*>(xa), static_cast<void*>(xb), static_cast<void*>(forc)})
-            for (size_t i = 0; i < c->allocs.size(); ++i)
-                if (c->allocs[i] == p) {
-                    cudaFree(p);
-                    c->allocs.erase(c->allocs.begin() + i);
-                    break;
-                }
     })
 }
 
@@ -2489,6 +2956,7 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
 }
 
 int swf_set_graphs(swf_ctx* c, int enable) {
+    SWF_FANOUT(c, swf_set_graphs(r_, enable));
     SWF_API_TRY({
         require(c, "null context");
         SWF_CUDA(cudaStreamSynchronize(c->st));
@@ -2497,6 +2965,7 @@ int swf_set_graphs(swf_ctx* c, int enable) {
 }
 
 int swf_profile(swf_ctx* c, int enable) {
+    SWF_FANOUT(c, swf_profile(r_, enable));
     SWF_API_TRY({
         require(c, "null context");
         SWF_CUDA(cudaStreamSynchronize(c->st));
@@ -2548,27 +3017,29 @@ int swf_profile_read(swf_ctx* c, double* ms, long long* launches, int n) {
 }
 
 int swf_noise_field(swf_ctx* c, uint64_t run_seed, uint64_t event, int channels, double sigma_d, float* out) {
+    SWF_FANOUT(c, swf_noise_field(r_, run_seed, event, channels, sigma_d, out));
     SWF_API_TRY({
         require(c && out && channels > 0, "bad argument");
         SWF_CUDA(cudaSetDevice(c->dev));
         allocate(c);
-        float* z = dalloc<float>(c, size_t(c->M) * channels);
-        float* zp = dalloc<float>(c, size_t(c->N) * channels);
+        float* z = scratch_f(c, SC_NOISE, size_t(c->M) * channels);
         noise_field(h_kd(h_kd(run_seed, 0x7au), event), channels, c->lay[0], sigma_d, z, c->st);
-        scatter_rows(z, c->lay[0], channels, c->M, zp, c->st);
-        SWF_CUDA(cudaMemcpyAsync(out, zp, size_t(c->N) * channels * 4, cudaMemcpyDeviceToHost, c->st));
-        SWF_CUDA(cudaStreamSynchronize(c->st));
-        for (void* p : {static_cast<void*>(z), static_cast<void*>(zp)})
-            for (size_t i = 0; i < c->allocs.size(); ++i)
-                if (c->allocs[i] == p) {
-                    cudaFree(p);
-                    c->allocs.erase(c->allocs.begin() + i);
-                    break;
-                }
+        if (c->world > 1) {
+            d2h_owned(c, z, channels, SWF_F32, out);
+        } else {
+            float* zp = scratch_f(c, SC_NOISE_PIX, size_t(c->N) * channels);
+            scatter_rows(z, c->lay[0], channels, c->M, zp, c->st);
+            SWF_CUDA(cudaMemcpyAsync(out, zp, size_t(c->N) * channels * 4, cudaMemcpyDeviceToHost, c->st));
+            SWF_CUDA(cudaStreamSynchronize(c->st));
+        }
     })
 }
 
 int swf_ipc_handles(swf_ctx* c, void* out) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        g_err = "a single-process group is already connected (no IPC)";
+        return SWF_ERR_CONFIG;
+    }
     SWF_API_TRY({
         require(c && out, "null argument");
         SWF_CUDA(cudaSetDevice(c->dev));
@@ -2584,6 +3055,10 @@ int swf_ipc_handles(swf_ctx* c, void* out) {
 }
 
 int swf_connect_peers(swf_ctx* c, const void* all) {
+    if (c && !c->kids.empty() && !tl_group_worker) {
+        g_err = "a single-process group is already connected (no IPC)";
+        return SWF_ERR_CONFIG;
+    }
     SWF_API_TRY({
         require(c && all, "null argument");
         SWF_CUDA(cudaSetDevice(c->dev));
@@ -2601,24 +3076,124 @@ int swf_connect_peers(swf_ctx* c, const void* all) {
             c->peer[r].qkv = p[3];
             c->peer[r].xm = p[4];
         }
-        for (int par = 0; par < 2; ++par) {
-            std::vector<float*> t(8, nullptr);
-            for (int r = 0; r < c->world; ++r) t[r] = c->peer[r].x[par];
-            SWF_CUDA(cudaMemcpy(c->d_xdst[par], t.data(), sizeof(float*) * 8, cudaMemcpyHostToDevice));
-        }
-        std::vector<int*> ft(8, nullptr);
-        std::vector<void*> qt(8, nullptr), ot(8, nullptr);
-        for (int r = 0; r < c->world; ++r) {
-            ft[r] = c->peer[r].flags;
-            qt[r] = c->peer[r].qkv;
-            ot[r] = c->peer[r].xm;
-        }
-        SWF_CUDA(cudaMemcpy(c->d_flag_table, ft.data(), sizeof(int*) * 8, cudaMemcpyHostToDevice));
-        SWF_CUDA(cudaMemcpy(c->d_qkv_dst, qt.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
-        SWF_CUDA(cudaMemcpy(c->d_o_dst, ot.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
-        c->peers = true;
+        c->ipc_mapped = true;
+        upload_peer_tables(c);
         SWF_CUDA(cudaDeviceSynchronize());
     })
+}
+
+// Isolated attention (test infrastructure for head_attention_fwd, swin.hpp:161-188): the windows of
+// an (n_wy w) x (n_wx w) grid under `shift` (seam mask on the last window row when shift > 0),
+// q / k / v [n_win][heads][s][d] host fp32 (bf16-representable for the BF16 kernel), o
+// [n_win][s][heads d] fp32. Same planes, TMA maps and launch as the forward.
+int swf_selftest_attention(int device, int precision, int n_wy, int n_wx, int w, int shift, int heads, int d,
+                           const float* q, const float* k, const float* v, float* o, int flags) {
+    std::vector<void*> mem;
+    auto cleanup = [&]() {
+        for (void* p : mem) cudaFree(p);
+    };
+    try {
+        require(q && k && v && o, "null argument");
+        require(n_wy >= 1 && n_wx >= 1 && w >= 1 && heads >= 1 && shift >= 0 && shift < w, "attention: bad shape");
+        require(precision == SWF_PREC_BF16 || precision == SWF_PREC_FP32, "attention: bad precision");
+        const bool bf = precision == SWF_PREC_BF16;
+        if (bf) require((d == 32 || d == 64 || d == 128) && w % 4 == 0, "attention: BF16 needs d in {32,64,128}");
+        SWF_CUDA(cudaSetDevice(device));
+        const int nwin = n_wy * n_wx, s = w * w, hd = heads * d;
+        const int ldo = int(roundup(hd, 64));
+        const size_t n = size_t(nwin) * heads * s * d;
+        auto alloc = [&](size_t bytes) {
+            void* p = nullptr;
+            SWF_CUDA(cudaMalloc(&p, bytes + 256));
+            SWF_CUDA(cudaMemset(p, 0, bytes + 256));
+            mem.push_back(p);
+            return p;
+        };
+        LayMap L;
+        L.g = make_lay(n_wy * w, n_wx * w, w, shift);
+        L.nloc = nwin;
+        L.sp = 1;
+        L.band = 0;
+        std::vector<int> ident(static_cast<size_t>(nwin));
+        for (int i = 0; i < nwin; ++i) ident[i] = i;
+        int* d_ident = static_cast<int*>(alloc(ident.size() * 4));
+        SWF_CUDA(cudaMemcpy(d_ident, ident.data(), ident.size() * 4, cudaMemcpyHostToDevice));
+        L.loc2glob = d_ident;
+        L.glob2rl = d_ident;
+        AttnParams ap;
+        ap = AttnParams{};
+        ap.ldo = ldo;
+        ap.nloc = nwin;
+        ap.heads = heads;
+        ap.s = s;
+        ap.d = d;
+        ap.w = w;
+        ap.lay = L;
+        ap.scale = 1.0f / std::sqrt(float(d));
+        ap.dbg = flags;
+        std::vector<float> out(size_t(nwin) * s * ldo);
+        if (bf) {
+            std::vector<__nv_bfloat16> hq(n), hk(n), hv(n);
+            for (size_t i = 0; i < n; ++i) {
+                hq[i] = __float2bfloat16_rn(q[i]);
+                hk[i] = __float2bfloat16_rn(k[i]);
+            }
+            for (size_t pl = 0; pl < size_t(nwin) * heads; ++pl)  // V^T planes [d][s]
+                for (int t = 0; t < s; ++t)
+                    for (int j = 0; j < d; ++j) hv[(pl * d + j) * s + t] = __float2bfloat16_rn(v[(pl * s + t) * d + j]);
+            char* qkv = static_cast<char*>(alloc(3 * n * 2));
+            SWF_CUDA(cudaMemcpy(qkv, hq.data(), n * 2, cudaMemcpyHostToDevice));
+            SWF_CUDA(cudaMemcpy(qkv + n * 2, hk.data(), n * 2, cudaMemcpyHostToDevice));
+            SWF_CUDA(cudaMemcpy(qkv + 2 * n * 2, hv.data(), n * 2, cudaMemcpyHostToDevice));
+            __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(alloc(out.size() * 2));
+            TmaMap tq, tk, tv, to;
+            const int sw = d >= 64 ? 128 : 2 * d;
+            const i64 rows = i64(nwin) * heads * s;
+            make_tma_bf16_2d(&tq, qkv, rows, d, sw / 2, 128, sw);
+            make_tma_bf16_2d(&tk, qkv + n * 2, rows, d, sw / 2, 64, sw);
+            make_tma_bf16_2d(&tv, qkv + 2 * n * 2, i64(nwin) * heads * d, s, 64, d / 2, 128);
+            make_tma_bf16(&to, ob, i64(nwin) * s, ldo, 128);
+            void** otab = static_cast<void**>(alloc(8 * sizeof(void*)));
+            std::vector<void*> t8(8, ob);
+            SWF_CUDA(cudaMemcpy(otab, t8.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice));
+            ap.q = qkv;
+            ap.k = qkv + n * 2;
+            ap.v = qkv + 2 * n * 2;
+            ap.o = ob;
+            ap.o_dst = otab;
+            ap.tmq = &tq;
+            ap.tmk = &tk;
+            ap.tmv = &tv;
+            ap.tmo = &to;
+            attention_bf16(ap, nullptr);
+            SWF_CUDA(cudaDeviceSynchronize());
+            std::vector<__nv_bfloat16> ho(out.size());
+            SWF_CUDA(cudaMemcpy(ho.data(), ob, ho.size() * 2, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < out.size(); ++i) out[i] = __bfloat162float(ho[i]);
+        } else {
+            float* qkv = static_cast<float*>(alloc(3 * n * 4));
+            SWF_CUDA(cudaMemcpy(qkv, q, n * 4, cudaMemcpyHostToDevice));
+            SWF_CUDA(cudaMemcpy(qkv + n, k, n * 4, cudaMemcpyHostToDevice));
+            SWF_CUDA(cudaMemcpy(qkv + 2 * n, v, n * 4, cudaMemcpyHostToDevice));
+            float* of = static_cast<float*>(alloc(out.size() * 4));
+            ap.q = qkv;
+            ap.k = qkv + n;
+            ap.v = qkv + 2 * n;
+            ap.o = of;
+            attention_f32(ap, nullptr);
+            SWF_CUDA(cudaDeviceSynchronize());
+            SWF_CUDA(cudaMemcpy(out.data(), of, out.size() * 4, cudaMemcpyDeviceToHost));
+        }
+        for (size_t r = 0; r < size_t(nwin) * s; ++r) std::memcpy(o + r * hd, out.data() + r * ldo, size_t(hd) * 4);
+        cleanup();
+        return SWF_OK;
+    } catch (const ConfigError& e) {
+        cleanup();
+        return fail(e, SWF_ERR_CONFIG);
+    } catch (const std::exception& e) {
+        cleanup();
+        return fail(e, SWF_ERR_CUDA);
+    }
 }
 
 // ---------------------------------------------------------------- host-only planning (no GPU)

@@ -148,9 +148,10 @@ __global__ void __launch_bounds__(256) k_rms_mod(const float* __restrict__ x, i6
 }
 
 // ---------------------------------------------------------------- sampler
-__global__ void k_sampler_update(const float* __restrict__ xa, const float* __restrict__ xd,
-                                 const float* __restrict__ v, i64 n, float cs, float sn, float c1, float c2,
-                                 float* __restrict__ y, int* flags, int slot) {
+// xa and y may alias (stage 2 updates the state in place): no __restrict__ on either; each element is
+// read and written by one thread, in that order
+__global__ void k_sampler_update(const float* xa, const float* __restrict__ xd, const float* __restrict__ v, i64 n,
+                                 float cs, float sn, float c1, float c2, float* y, int* flags, int slot) {
     bool bad = false;
     for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
         const float d = cs * xd[i] - sn * v[i];
@@ -284,6 +285,49 @@ template void gather_rows<__nv_bfloat16>(const float*, const LayMap&, int, int, 
 
 void scatter_rows(const float* src_loc, const LayMap& lay, int C, i64 M, float* dst_pix, cudaStream_t st) {
     k_scatter_rows<<<grid_for(M * C), kThreads, 0, st>>>(src_loc, lay, C, M, dst_pix);
+    SWF_LAUNCH_CHECK();
+}
+
+namespace {
+// one warp per residual row: the bf16 copy (zero-padded to hp) and the row's sum of squares in
+// partial slot 0 (others 0) -- what the producing GEMM epilogues emit for the fused norm
+__global__ void k_prep_residual(const float* __restrict__ x, i64 M, int h, int hp, int nss,
+                                __nv_bfloat16* __restrict__ xb, float* __restrict__ ss) {
+    const i64 row = i64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= M) return;
+    const int lane = threadIdx.x & 31;
+    float acc = 0.f;
+    for (int c = lane; c < hp; c += 32) {
+        const float v = c < h ? x[row * h + c] : 0.f;
+        xb[row * hp + c] = __float2bfloat16_rn(v);
+        acc += v * v;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int k = lane; k < nss; k += 32) ss[row * nss + k] = k == 0 ? acc : 0.f;
+}
+
+// one warp per requested pixel: its row of the local [M][C] buffer (owned pixels only)
+__global__ void k_rows_at_pixels(const float* __restrict__ src, LayMap lay, int rank, int C,
+                                 const i64* __restrict__ pix, i64 n, float* __restrict__ dst) {
+    const i64 k = i64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (k >= n) return;
+    int owner = 0;
+    const i64 i = lay.pix_to_loc(pix[k], &owner);
+    if (owner != rank) return;
+    for (int c = threadIdx.x & 31; c < C; c += 32) dst[k * C + c] = src[i * C + c];
+}
+}  // namespace
+
+void prep_residual(const float* x, i64 M, int h, int hp, int nss, __nv_bfloat16* xb, float* ss, cudaStream_t st) {
+    if (M <= 0) return;
+    k_prep_residual<<<int((M + 7) / 8), 256, 0, st>>>(x, M, h, hp, nss, xb, ss);
+    SWF_LAUNCH_CHECK();
+}
+
+void rows_at_pixels(const float* src_loc, const LayMap& lay, int rank, int C, const i64* pix, i64 n, float* dst,
+                    cudaStream_t st) {
+    if (n <= 0) return;
+    k_rows_at_pixels<<<int((n + 7) / 8), 256, 0, st>>>(src_loc, lay, rank, C, pix, n, dst);
     SWF_LAUNCH_CHECK();
 }
 

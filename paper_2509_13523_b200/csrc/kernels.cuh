@@ -163,6 +163,7 @@ struct AttnParams {
     const TmaMap* tmv;
     const TmaMap* tmo;  // BF16 path, sp == 1: map of the own output buffer (box 64 x 128, SW128) for TMA
                         // stores of whole query tiles; nullptr = per-row stores
+    int dbg = 0;        // test only (swf_selftest_attention negative control): bit 0 skips the O rescale
 };
 void attention_f32(const AttnParams& p, cudaStream_t st);
 void attention_bf16(const AttnParams& p, cudaStream_t st);
@@ -210,6 +211,12 @@ void gather_rows(const float* src_pix, const LayMap& lay, int C, int ldo, i64 M,
                  cudaStream_t st);
 // Inverse: dst_pix[pix(i)][c] = src[i][c] for the owned rows.
 void scatter_rows(const float* src_loc, const LayMap& lay, int C, i64 M, float* dst_pix, cudaStream_t st);
+// Fused-norm operands of residual rows written by the host (block_window_forward): bf16 copy [M][hp]
+// and the per-row sum of squares (partial slot 0; inv_rms sums all nss slots)
+void prep_residual(const float* x, i64 M, int h, int hp, int nss, __nv_bfloat16* xb, float* ss, cudaStream_t st);
+// dst[k][c] = src[local index of pix[k]][c] for the pixels `rank` owns under `lay` (others untouched)
+void rows_at_pixels(const float* src_loc, const LayMap& lay, int rank, int C, const i64* pix, i64 n, float* dst,
+                    cudaStream_t st);
 // RMSNorm + AdaLN modulation (prenorm_modulate, swin.hpp:72-85) or plain (prenorm_plain :111-123 when
 // a == nullptr): out[m][i] = gate*((g*x/r)*(1+a)+b); non-finite input -> flags[slot].
 // AdaLN folding for the fused norm (BF16 path): Wf[n][k] = bf16(Wm[n][k] * s[k]) and

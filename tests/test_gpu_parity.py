@@ -328,3 +328,20 @@ def test_train_step_matches_oracle():
     assert np.array_equal(again.grads, res.grads) and again.mb_losses == res.mb_losses
     with pytest.raises(swf.ConfigError):
         swf.Denoiser(sc, H, W, precision=swf.PREC_BF16).train_reset()
+
+
+@pytest.mark.parametrize("prec,tol", [(swf.PREC_FP32, TOL_FP32), (swf.PREC_BF16, TOL_BF16)])
+@pytest.mark.parametrize("cfg,H,W,blk,wy,wx", [(C1, 32, 64, 0, 1, 2), (C1, 32, 64, 1, 3, 5), (MID, 48, 96, 1, 3, 1),
+                                               (MID, 48, 96, 0, 0, 7)])
+def test_block_window_forward_matches_oracle(prec, tol, cfg, H, W, blk, wy, wx):
+    """block_window_forward (swin.hpp:306-325) exported through the C-ABI: one window of one block,
+    unshifted and shifted (seam-masked on the last window row)."""
+    oc, sc = cfgs(cfg)
+    p = o.init_params(oc, 91, random=True, scale=0.05, dtype=np.float32)
+    s = oc.window_px ** 2
+    xin = (0.7 * o.random_field(oc.hidden_dim, s, 92)).astype(np.float32)
+    ref = o.block_window(oc, p, 0.6, H, W, blk, wy, wx, xin)
+    dn = swf.Denoiser(sc, H, W, precision=prec)
+    dn.load_params(p)
+    got = dn.block_window_forward(blk, wy, wx, 0.6, xin)
+    assert rel_err_per_channel(got - xin, ref - xin) <= tol

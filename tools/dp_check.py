@@ -17,9 +17,12 @@ import paper_2509_13523_b200 as swf  # noqa: E402
 from oracle import pyoracle as o  # noqa: E402
 
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-local = int(os.environ.get("LOCAL_RANK", rank))
+local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
 torch.cuda.set_device(local)
-dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+if torch.cuda.device_count() >= world:
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+else:  # ranks share GPUs (NCCL rejects duplicate devices): gloo all-reduce through host memory
+    dist.init_process_group("gloo")
 d = dict(hidden_dim=64, n_heads=4, ffn_dim=128, n_layers=2, window_px=8, in_channels=8, out_channels=3, time_dim=64)
 H, W, gas = 32, 64, 2
 oc, sc = o.ModelConfig(**d), swf.ModelConfig(**d)
