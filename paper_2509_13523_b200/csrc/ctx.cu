@@ -112,7 +112,7 @@ struct swf_ctx {
     int* d_epoch = nullptr;          // device barrier epoch (advanced by k_peer_barrier; graph-safe)
     int* d_sched = nullptr;          // GEMM dynamic-schedule tile counter (reset before every launch)
     // TMA maps (BF16 path)
-    TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec, tm_q, tm_k, tm_vt;
+    TmaMap tm_ain, tm_xm, tm_s, tm_enc, tm_dec, tm_q, tm_k, tm_k2, tm_vt;
     TmaMap tm_so;  // sbuf viewed as [M][hp] (attention output of the kernel benchmark)
     // fused RMSNorm + AdaLN (BF16): bf16 copy + row partial sums of squares of each residual buffer
     // (inside xbuf[par] at off_xb / off_ss floats), fp32 masters of the folded weights, shift biases
@@ -513,6 +513,7 @@ void allocate(swf_ctx* c) {
             make_tma_bf16_2d(&c->tm_q, qb, rows_qk, m.d, sw / 2, 128, sw);
             // K and V^T tiles are fetched half per CTA of a 2-CTA cluster and multicast (k_attn.cu)
             make_tma_bf16_2d(&c->tm_k, qb + size_t(M) * m.h * 2, rows_qk, m.d, sw / 2, 64, sw);
+            make_tma_bf16_2d(&c->tm_k2, qb + size_t(M) * m.h * 2, rows_qk, m.d, sw / 2, 32, sw);
             make_tma_bf16_2d(&c->tm_vt, qb + size_t(2) * M * m.h * 2, i64(c->lay[0].nloc) * hl * m.d,
                              i64(m.w) * m.w, 64, m.d / 2, 128);
         }
@@ -1081,6 +1082,7 @@ void run_block(swf_ctx* c, int b, int cur, const LayMap& L, const LayMap& Lnext,
     ap.scale = 1.0f / std::sqrt(float(m.d));
     ap.tmq = &c->tm_q;
     ap.tmk = &c->tm_k;
+    ap.tmk2 = &c->tm_k2;
     ap.tmv = &c->tm_vt;
     ap.tmo = c->sp == 1 ? &c->tm_xm : nullptr;  // SP: rows go to the band owners row by row
     {
@@ -2022,6 +2024,8 @@ int group_run(swf_ctx* root, F&& fn) {
         if (rc[r] != SWF_OK && (best < 0 || rc[r] < rc[best])) best = int(r);
     if (best < 0) return SWF_OK;
     g_err = "rank " + std::to_string(best) + ": " + msg[best];
+    for (size_t r = 0; r < n; ++r)  // the other ranks' failures, for diagnosis
+        if (rc[r] != SWF_OK && int(r) != best) g_err += " [rank " + std::to_string(r) + ": " + msg[r] + "]";
     return rc[best];
 }
 
@@ -2039,6 +2043,21 @@ void sum_ranks(const std::vector<std::vector<double>>& g, void* out, int dtype) 
     for (size_t i = 0; i < n; ++i) {
         double v = 0.0;
         for (const auto& r : g) v += r[i];
+        if (dtype == SWF_F64)
+            static_cast<double*>(out)[i] = v;
+        else
+            static_cast<float*>(out)[i] = float(v);
+    }
+}
+
+// Same for per-rank buffers already in the output element type.
+void sum_ranks_typed(const std::vector<std::vector<char>>& g, size_t n, void* out, int dtype) {
+    if (!out) return;
+    for (size_t i = 0; i < n; ++i) {
+        double v = 0.0;
+        for (const auto& r : g)
+            v += dtype == SWF_F64 ? reinterpret_cast<const double*>(r.data())[i]
+                                  : double(reinterpret_cast<const float*>(r.data())[i]);
         if (dtype == SWF_F64)
             static_cast<double*>(out)[i] = v;
         else
@@ -2129,6 +2148,23 @@ int swf_create(const swf_model_cfg* cfg, int grid_h, int grid_w, int device, int
         SWF_CUDA(cudaGetDeviceProperties(&prop, device));
         if (prop.major != 10) throw CudaError("swf_create: this build targets sm_100a (B200); found sm_" +
                                                std::to_string(prop.major) + std::to_string(prop.minor));
+        {  // load every kernel into this device's context once (see preload_elem_kernels, kernels.cuh)
+            static std::mutex mu;
+            static std::vector<char> done(64, 0);
+            std::lock_guard<std::mutex> lk(mu);
+            if (device < 64 && !done[size_t(device)]) {
+                preload_elem_kernels();
+                preload_bwd_kernels();
+                preload_simt_kernels();
+                preload_gemm_kernels();
+                preload_attn_kernels();
+                cudaFuncAttributes a;
+                for (const void* f : {(const void*)k_repack<float>, (const void*)k_repack<__nv_bfloat16>,
+                                      (const void*)k_init_fill, (const void*)k_peer_barrier})
+                    SWF_CUDA(cudaFuncGetAttributes(&a, f));
+                done[size_t(device)] = 1;
+            }
+        }
         swf_ctx* c = new swf_ctx();
         c->cfg = *cfg;
         c->m = make_dims(*cfg, precision);
@@ -2435,13 +2471,15 @@ int swf_block_window_forward(swf_ctx* c, int block, int wy, int wx, double t, co
 int swf_backward(swf_ctx* c, const void* input, double t, const void* d_output, void* grads, void* d_input,
                  int dtype) {
     if (c && !c->kids.empty() && !tl_group_worker) {
-        const size_t n = size_t(swf_param_count(&c->cfg));
-        std::vector<std::vector<double>> g(c->kids.size() + 1, std::vector<double>(n));
+        // per-rank partial gradients in the caller's element type (the call's dtype also types the
+        // input and output-gradient fields); the input gradient rows are disjoint per rank
+        const size_t n = size_t(swf_param_count(&c->cfg)), es = dtype == SWF_F64 ? 8 : 4;
+        std::vector<std::vector<char>> g(c->kids.size() + 1, std::vector<char>(n * es));
         const int rc = group_run(c, [&](swf_ctx* r_, int k) {
-            return swf_backward(r_, input, t, d_output, grads ? g[size_t(k)].data() : nullptr, d_input, SWF_F64);
+            return swf_backward(r_, input, t, d_output, g[size_t(k)].data(), d_input, dtype);
         });
         if (rc != SWF_OK) return rc;
-        sum_ranks(g, grads, dtype);
+        sum_ranks_typed(g, n, grads, dtype);
         return SWF_OK;
     }
     SWF_API_TRY({
@@ -2492,19 +2530,19 @@ int swf_diffusion_loss_sample(swf_ctx* c, const void* x_prev, const void* x0, co
                               const swf_loss_weights* w, const swf_diffusion_cfg* dc, uint64_t t_key, const void* z,
                               double* loss, void* grads, int dtype) {
     if (c && !c->kids.empty() && !tl_group_worker) {
-        const size_t n = size_t(swf_param_count(&c->cfg));
-        std::vector<std::vector<double>> g(c->kids.size() + 1, std::vector<double>(grads ? n : 0));
+        const size_t n = size_t(swf_param_count(&c->cfg)), es = dtype == SWF_F64 ? 8 : 4;
+        std::vector<std::vector<char>> g(c->kids.size() + 1, std::vector<char>(grads ? n * es : 0));
         std::vector<double> l(c->kids.size() + 1, 0.0);
         const int rc = group_run(c, [&](swf_ctx* r_, int k) {
             return swf_diffusion_loss_sample(r_, x_prev, x0, forcings, w, dc, t_key, z, &l[size_t(k)],
-                                             grads ? g[size_t(k)].data() : nullptr, SWF_F64);
+                                             grads ? g[size_t(k)].data() : nullptr, dtype);
         });
         if (rc != SWF_OK) return rc;
         if (loss) {  // partial sums over the ranks' tokens, in rank order
             *loss = 0.0;
             for (double v : l) *loss += v;
         }
-        if (grads) sum_ranks(g, grads, dtype);
+        if (grads) sum_ranks_typed(g, n, grads, dtype);
         return SWF_OK;
     }
     SWF_API_TRY({
@@ -2907,6 +2945,7 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
                     ap.scale = 1.0f / std::sqrt(float(m.d));
                     ap.tmq = &c->tm_q;
                     ap.tmk = &c->tm_k;
+                    ap.tmk2 = &c->tm_k2;
                     ap.tmv = &c->tm_vt;
                     ap.tmo = c->sp == 1 ? &c->tm_so : nullptr;
                     attention_bf16(ap, c->st);
@@ -3146,11 +3185,12 @@ int swf_selftest_attention(int device, int precision, int n_wy, int n_wx, int w,
             SWF_CUDA(cudaMemcpy(qkv + n * 2, hk.data(), n * 2, cudaMemcpyHostToDevice));
             SWF_CUDA(cudaMemcpy(qkv + 2 * n * 2, hv.data(), n * 2, cudaMemcpyHostToDevice));
             __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(alloc(out.size() * 2));
-            TmaMap tq, tk, tv, to;
+            TmaMap tq, tk, tk2, tv, to;
             const int sw = d >= 64 ? 128 : 2 * d;
             const i64 rows = i64(nwin) * heads * s;
             make_tma_bf16_2d(&tq, qkv, rows, d, sw / 2, 128, sw);
             make_tma_bf16_2d(&tk, qkv + n * 2, rows, d, sw / 2, 64, sw);
+            make_tma_bf16_2d(&tk2, qkv + n * 2, rows, d, sw / 2, 32, sw);
             make_tma_bf16_2d(&tv, qkv + 2 * n * 2, i64(nwin) * heads * d, s, 64, d / 2, 128);
             make_tma_bf16(&to, ob, i64(nwin) * s, ldo, 128);
             void** otab = static_cast<void**>(alloc(8 * sizeof(void*)));
@@ -3163,6 +3203,7 @@ int swf_selftest_attention(int device, int precision, int n_wy, int n_wx, int w,
             ap.o_dst = otab;
             ap.tmq = &tq;
             ap.tmk = &tk;
+            ap.tmk2 = &tk2;
             ap.tmv = &tv;
             ap.tmo = &to;
             attention_bf16(ap, nullptr);

@@ -697,17 +697,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const float mx = mxr * sl2;
                 pair_sync(wq);  // every split read before the next exchange overwrites
                 if (tr) SWF_TR(1, g);
-                // both halves take the same rescale decision (same mx, same m)
-                if (mx > m + kRescale || (m == -INFINITY && mx != -INFINITY)) {
-                    if (m != -INFINITY) {
-                        // O *= 2^(m - mx): P(g-1) V must have landed
-                        mbar_wait(bar(B_OD), (g - 1) & 1);
-                        fence_after();
-                        const float f = ex2(m - mx);
-                        if (!(p.dbg & 1)) o_scale<C::kOC>(tO, f);
-                        l *= f;
-                    }
-                    m = mx;
+                // Lazy rescale, decided per WARP: the O rescale is a tcgen05.ld / st pair, warp-collective
+                // (.sync.aligned), so a row that needs it (running max grew by > 2^kRescale) takes its
+                // whole warp along; every lane then moves to max(m, mx). Both key halves of a row sit in
+                // warps holding the same 32 rows, so they take the same decision and factor.
+                const bool grow = m != -INFINITY && mx > m + kRescale;
+                if (__any_sync(0xffffffffu, grow)) {
+                    // O *= 2^(m - m_new): P(g-1) V must have landed
+                    mbar_wait(bar(B_OD), (g - 1) & 1);
+                    fence_after();
+                    const float mn = fmaxf(m, mx);
+                    const float f = m == -INFINITY ? 0.f : ex2(m - mn);  // m = -inf: O and l are still 0
+                    if (!(p.dbg & 1)) o_scale<C::kOC>(tO, f);
+                    l *= f;
+                    m = mn;
+                } else if (m == -INFINITY && mx != -INFINITY) {
+                    m = mx;  // first unmasked keys of this row: O and l are still 0, nothing to scale
                 }
                 const float nb = m == -INFINITY ? 0.f : -m;
                 const unsigned long long sl2x2 = f2_pack(sl2, sl2), nbx2 = f2_pack(nb, nb);
@@ -818,21 +823,484 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
 }
 
+// ============================================================================================
+// Ping-pong kernel (default). The 8 softmax warps of a CTA form two groups that take alternate
+// 64-key tiles of an item -- group 0 the even tiles, group 1 the odd ones -- each thread owning a
+// whole query row of its tile, with its own running max / sum and its own O accumulator in TMEM
+// (O0 / O1). The groups run out of phase: while one loads S and reduces its row maximum, the other's
+// exponentials keep the sub-partition's MUFU and FMA pipes busy; there is no per-tile max exchange
+// and no named barrier between warps. S is a ring of four 64-column buffers, so QK^T runs two tiles
+// ahead of each group (QK^T(g) waits only for P(g-4) V), which takes the tensor-core round trip
+// (P V of a tile, QK^T of the group's next tile) off the softmax critical path. The two partial
+// outputs are merged once per item in the epilogue:
+//   O = (O0 2^(m0-M) + O1 2^(m1-M)) / (l0 2^(m0-M) + l1 2^(m1-M)),  M = max(m0, m1)
+// (each group writes half of the head's columns).
+// TMEM (per CTA): S ring [0, 256) (buffer b at 64 b), O0 [256, 256+D), O1 [256+D, 256+2D).
+// Operands per 64-key tile: each CTA loads its 32 keys of K (QK^T: M = 256 pair-wide, N = 64 split
+// 32 / 32 across the pair) and its D/2 rows of V^T (P V: N = D split across the pair, K = 64 keys).
+namespace pp {
+constexpr int KT = 64;  // keys per tile
+constexpr int kNS = 4;  // S buffers
+enum : int {
+    QF = 0, QE = 2, KF = 4, KE = 12, VF = 20, VE = 28, SF = 36, PF = 40, SFREE = 44, OD = 48, OF = 50, NUM = 51
+};
+constexpr uint32_t kTO = 256;
+constexpr int kThreads = 384;
+template <int D>
+struct Cfg {
+    static constexpr int kSw = D >= 64 ? 128 : 2 * D;
+    static constexpr int kColsPerBox = kSw / 2;
+    static constexpr int kBoxes = D / kColsPerBox;
+    static constexpr int kQBytes = BQ * D * 2;
+    static constexpr int kKHalf = (KT / 2) * D * 2;  // this CTA's 32 keys of a K tile
+    static constexpr int kVHalf = (D / 2) * KT * 2;  // this CTA's D/2 rows of a V^T tile
+    static constexpr int kNK = 8, kNV = 8;
+    static constexpr int kRedBytes = 4 * BQ * 4;  // (m, l) x 2 groups x BQ rows
+    static constexpr int kSmem = 2 * kQBytes + kNK * kKHalf + kNV * kVHalf + kRedBytes + 512 + 1024;
+    static constexpr int kOC = D / 2;  // O columns per thread in the epilogue (its group's half)
+    static constexpr uint32_t kIdescS = idesc_bf16(2 * BQ, KT);
+    static constexpr uint32_t kIdescO = idesc_bf16(2 * BQ, D);
+};
+// QK^T of one 64-key tile: D/16 k-steps; A = Q (BQ rows per box), B = this CTA's 32 keys per box
+template <int D>
+__device__ __forceinline__ void issue_s(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    if constexpr (D == 128)
+        mma2_ss_x8<2, 4, 6, 1024, 1026, 1028, 1030, 2, 4, 6, 256, 258, 260, 262>(d, a, b, idesc);
+    else if constexpr (D == 64)
+        mma2_ss_x4<2, 4, 6, 2, 4, 6>(d, a, b, idesc);
+    else
+        mma2_ss_x2<2, 2>(d, a, b, idesc);
+}
+// P V of one tile: 4 pair-wide TS MMAs (K = 16 keys each); P of keys [16 kk, 16 kk + 16) at S
+// columns [8 kk, 8 kk + 8) (bf16 pairs in key order), B = the V^T half (one SW128 box, 64 keys)
+__device__ __forceinline__ void issue_pv(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, p0, pt;\n"
+        ".reg .b64 b;\n"
+        ".reg .b32 a;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p0, %4, 0;\n"
+        "setp.eq.b32 pt, %3, %3;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p0;\n"
+        "add.u32 a, %1, 8;\n"
+        "add.s64 b, %2, 2;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.u32 a, %1, 16;\n"
+        "add.s64 b, %2, 4;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.u32 a, %1, 24;\n"
+        "add.s64 b, %2, 6;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, pt;\n"
+        "}\n" ::"r"(d),
+        "r"(a), "l"(b), "r"(idesc), "r"(acc0));
+}
+__device__ __forceinline__ void quad_sync(int quadrant) {  // the two warps (one per group) of a lane quadrant
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quadrant) : "memory");
+}
+__device__ __forceinline__ void all_softmax_sync() { asm volatile("bar.sync 5, 256;" ::: "memory"); }
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// key range of a work item (seam groups) in 64-key tiles, the union over the pair
+__device__ __forceinline__ Range range_of(const AttnParams& p, const Item& it) {
+    Range r;
+    const int s = p.s;
+    const int gw = p.lay.loc2glob[it.lw];
+    r.masked = p.lay.g.shift > 0 && (gw / p.lay.g.nx) == p.lay.g.ny - 1;
+    r.split = r.masked ? (p.w - p.lay.g.shift) * p.w : s;
+    const int qlast = min(it.qp0 + 2 * BQ, s) - 1;
+    const int kv_lo = (r.masked && it.qp0 >= r.split) ? r.split : 0;
+    const int kv_hi = (r.masked && qlast < r.split) ? r.split : s;
+    r.t_lo = kv_lo / KT;
+    r.ntiles = (kv_hi + KT - 1) / KT - r.t_lo;
+    return r;
+}
+}  // namespace pp
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
+    k_attn_pp(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, AttnParams p,
+              int n_items) {
+    using C = pp::Cfg<D>;
+    constexpr int KT = pp::KT;
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = sm;
+    uint8_t* sK = sm + 2 * C::kQBytes;
+    uint8_t* sV = sK + C::kNK * C::kKHalf;
+    float* red = reinterpret_cast<float*>(sV + C::kNV * C::kVHalf);  // [m0 | m1 | l0 | l1][BQ]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::kNV * C::kVHalf + C::kRedBytes);
+    auto bar = [&](int slot) { return smem_u32(&bars[slot]); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[pp::NUM]);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = p.s;
+    const int npairs = (s + 2 * BQ - 1) / (2 * BQ);
+    const int crank = int(cta_rank());
+    const bool lead = crank == 0;
+    auto lbar = [&](int slot) { return map_to_rank(bar(slot), 0); };
+    const int cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+
+    if (warp == 1 && lane == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar(pp::QF + i), 1);
+            mbar_init(bar(pp::QE + i), 1);
+            mbar_init(bar(pp::OD + i), 1);
+        }
+        for (int i = 0; i < pp::kNS; ++i) {
+            mbar_init(bar(pp::SF + i), 1);
+            mbar_init(bar(pp::PF + i), 2 * 4);
+            mbar_init(bar(pp::SFREE + i), 1);
+        }
+        for (int i = 0; i < C::kNK; ++i) {
+            mbar_init(bar(pp::KF + i), 1);
+            mbar_init(bar(pp::KE + i), 1);
+        }
+        for (int i = 0; i < C::kNV; ++i) {
+            mbar_init(bar(pp::VF + i), 1);
+            mbar_init(bar(pp::VE + i), 1);
+        }
+        mbar_init(bar(pp::OF), 2 * 8);
+        fence_barrier_init();
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    fence_before();
+    cluster_sync_all();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+
+    if (warp == 0) {
+        // ===== TMA: Q (double-buffered across items) and the K ring (this CTA's 32 keys of a tile)
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+            int g = 0, n = 0;
+            for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
+                const Item it = item_of(itx, npairs, p.heads, crank);
+                const Range rg = pp::range_of(p, it);
+                const int plane = it.lw * p.heads + it.head;
+                const int qb = n & 1;
+                mbar_sleep_wait(bar(pp::QE + qb), ((n >> 1) & 1) ^ 1);
+                if (lead) mbar_expect_tx(bar(pp::QF + qb), 2 * C::kQBytes);
+                for (int b = 0; b < C::kBoxes; ++b)
+                    tma_load_2cta(smem_u32(sQ + qb * C::kQBytes + b * BQ * C::kSw), &tmQ, lbar(pp::QF + qb),
+                                  b * C::kColsPerBox, plane * s + it.q0);
+                for (int j = 0; j < rg.ntiles; ++j, ++g) {
+                    const int st = g % C::kNK;
+                    mbar_sleep_wait(bar(pp::KE + st), ((g / C::kNK) & 1) ^ 1);
+                    if (lead) mbar_expect_tx(bar(pp::KF + st), 2 * C::kKHalf);
+                    for (int b = 0; b < C::kBoxes; ++b)
+                        tma_load_2cta(smem_u32(sK + st * C::kKHalf + b * (KT / 2) * C::kSw), &tmK, lbar(pp::KF + st),
+                                      b * C::kColsPerBox, plane * s + (rg.t_lo + j) * KT + crank * (KT / 2));
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ===== TMA: the V^T ring (this CTA's D/2 rows x 64 keys, one SW128 box)
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+            int g = 0;
+            for (int itx = cluster_id; itx < n_items; itx += n_clusters) {
+                const Item it = item_of(itx, npairs, p.heads, crank);
+                const Range rg = pp::range_of(p, it);
+                const int plane = it.lw * p.heads + it.head;
+                for (int j = 0; j < rg.ntiles; ++j, ++g) {
+                    const int st = g % C::kNV;
+                    mbar_sleep_wait(bar(pp::VE + st), ((g / C::kNV) & 1) ^ 1);
+                    if (lead) mbar_expect_tx(bar(pp::VF + st), 2 * C::kVHalf);
+                    tma_load_2cta(smem_u32(sV + st * C::kVHalf), &tmV, lbar(pp::VF + st), (rg.t_lo + j) * KT,
+                                  plane * D + crank * (D / 2));
+                }
+            }
+        }
+    } else if (warp == 1 && lead) {
+        // ===== QK^T issuer for the pair: S(g) into ring buffer g % 4 once P(g-4) V has completed
+        if (tmem != 0) __trap();
+        const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK);
+        int g = 0, n = 0;
+        for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
+            const Range rg = pp::range_of(p, item_of(itx, npairs, p.heads, crank));
+            const int qb = n & 1;
+            mbar_sleep_wait(bar(pp::QF + qb), (n >> 1) & 1);
+            for (int j = 0; j < rg.ntiles; ++j, ++g) {
+                const int st = g % C::kNK, b = g % pp::kNS;
+                mbar_sleep_wait(bar(pp::KF + st), (g / C::kNK) & 1);
+                mbar_sleep_wait(bar(pp::SFREE + b), ((g / pp::kNS) & 1) ^ 1);
+                fence_after();
+                const uint64_t a0 = desc_kmajor(sQa + uint32_t(qb * C::kQBytes), C::kSw);
+                const uint64_t b0 = desc_kmajor(sKa + uint32_t(st * C::kKHalf), C::kSw);
+                pp::issue_s<D>(uint32_t(b * KT), a0, b0, C::kIdescS);
+                commit2_mc(bar(pp::SF + b));
+                commit2_mc(bar(pp::KE + st));
+            }
+        }
+    } else if (warp == 2 && lead) {
+        // ===== P V issuer: tile j of an item accumulates into O[j % 2]
+        const uint32_t sVa = smem_u32(sV);
+        int g = 0, n = 0;
+        for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
+            const Range rg = pp::range_of(p, item_of(itx, npairs, p.heads, crank));
+            for (int j = 0; j < rg.ntiles; ++j, ++g) {
+                const int b = g % pp::kNS, vs = g % C::kNV, par = j & 1;
+                if (j == 0 && n >= 1) mbar_sleep_wait(bar(pp::OF), (n - 1) & 1);  // O0 / O1 of the last item read
+                mbar_sleep_wait(bar(pp::PF + b), (g / pp::kNS) & 1);
+                mbar_sleep_wait(bar(pp::VF + vs), (g / C::kNV) & 1);
+                fence_after();
+                const uint64_t b0 = desc_kmajor(sVa + uint32_t(vs * C::kVHalf), 128);
+                pp::issue_pv(pp::kTO + uint32_t(par * D), uint32_t(b * KT), b0, C::kIdescO, j >= 2 ? 1u : 0u);
+                commit2_mc(bar(pp::OD + par));
+                commit2_mc(bar(pp::VE + vs));
+                commit2(bar(pp::SFREE + b));
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== softmax: group grp takes the tiles j % 2 == grp, one query row per thread
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+        const int grp = (warp - 4) >> 2;
+        const int wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_off = uint32_t(wq * 32) << 16;
+        const float sl2 = p.scale * 1.4426950408889634f;
+        const bool leader = threadIdx.x == 128;  // issues the O TMA stores, releases Q buffers
+        int qe_pending = -1;
+        auto release_q = [&]() {
+            if (qe_pending >= 0) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(bar(pp::QE + qe_pending));
+                qe_pending = -1;
+            }
+        };
+        int g = 0, n = 0;
+        int cnt[2] = {0, 0};  // P V products issued into O0 / O1 so far (all items)
+        for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
+            const Item it = item_of(itx, npairs, p.heads, crank);
+            const Range rg = pp::range_of(p, it);
+            const int q = it.q0 + r;
+            const int rlo = (rg.masked && q >= rg.split) ? rg.split : 0;
+            const int rhi = (rg.masked && q < rg.split) ? rg.split : s;
+            int orank = 0;
+            const i64 oloc = q < s ? p.lay.wtok_to_loc(p.wp_rank, it.lw, q, &orank) : 0;
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < rg.ntiles; ++j, ++g) {
+                const int par = j & 1;
+                ++cnt[par];
+                if (par != grp) continue;
+                const int b = g % pp::kNS;
+                const uint32_t tS = lane_off + uint32_t(b * KT);
+                mbar_wait(bar(pp::SF + b), (g / pp::kNS) & 1);
+                fence_after();
+                uint32_t sa[KT];
+                ld32(tS, sa);
+                ld32(tS + 32u, sa + 32);
+                wait_ld_dep(sa);
+                wait_ld_dep(sa + 32);
+                const int kb = (rg.t_lo + j) * KT;
+                if (kb < rlo || kb + KT > rhi) {  // boundary tile: keys outside [rlo, rhi) get -inf
+#pragma unroll
+                    for (int i = 0; i < KT; ++i)
+                        if (kb + i < rlo || kb + i >= rhi) sa[i] = __float_as_uint(-INFINITY);
+                }
+                float mx4[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)  // 3-input max (FMNMX3) over 16 keys per chain
+                    mx4[c] = pp::max3(__uint_as_float(sa[16 * c]), __uint_as_float(sa[16 * c + 1]),
+                                      __uint_as_float(sa[16 * c + 2]));
+#pragma unroll
+                for (int i = 3; i < 16; i += 2)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        mx4[c] = i + 1 < 16 ? pp::max3(mx4[c], __uint_as_float(sa[16 * c + i]),
+                                                       __uint_as_float(sa[16 * c + i + 1]))
+                                            : fmaxf(mx4[c], __uint_as_float(sa[16 * c + i]));
+                const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+                // lazy rescale, warp-uniform (tcgen05.ld / st are warp-collective): O[grp] *= 2^(m - m_new)
+                // once this group's previous P V into O[grp] has landed
+                const bool grow = m != -INFINITY && mx > m + kRescale;
+                if (__any_sync(0xffffffffu, grow)) {
+                    mbar_wait(bar(pp::OD + grp), (cnt[grp] - 2) & 1);
+                    fence_after();
+                    const float mn = fmaxf(m, mx);
+                    const float f = m == -INFINITY ? 0.f : ex2(m - mn);
+                    if (!(p.dbg & 1)) o_scale<D>(lane_off + pp::kTO + uint32_t(grp * D), f);
+                    l *= f;
+                    m = mn;
+                } else if (m == -INFINITY && mx != -INFINITY) {
+                    m = mx;
+                }
+                const float nb = m == -INFINITY ? 0.f : -m;
+                const unsigned long long sl2x2 = f2_pack(sl2, sl2), nbx2 = f2_pack(nb, nb);
+                unsigned long long ls2 = 0ull, ls2b = 0ull;
+#pragma unroll
+                for (int c = 0; c < KT / 32; ++c) {  // 32 keys -> 16 packed bf16x2 columns per store
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const unsigned long long sv =
+                            (unsigned long long)sa[32 * c + 2 * i] | ((unsigned long long)sa[32 * c + 2 * i + 1] << 32);
+                        const unsigned long long z = ffma2(sv, sl2x2, nbx2);
+                        unsigned long long pv;
+                        if ((i & 7) < kPoly8)
+                            pv = ex2_poly2(z);
+                        else
+                            pv = f2_pack(ex2(lo_f(z)), ex2(hi_f(z)));
+                        if (i & 1)
+                            ls2b = fadd2(ls2b, pv);
+                        else
+                            ls2 = fadd2(ls2, pv);
+                        pk[i] = pack_bf16x2(lo_f(pv), hi_f(pv));
+                    }
+                    st16(tS + uint32_t(16 * c), pk);
+                }
+                const unsigned long long lsum = fadd2(ls2, ls2b);
+                l += lo_f(lsum) + hi_f(lsum);
+                wait_st();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(lbar(pp::PF + b));
+                if (leader) release_q();
+            }
+            // ---- epilogue: merge the two groups' partial softmax states, O / l -> bf16
+            red[grp * BQ + r] = m;
+            red[(2 + grp) * BQ + r] = l;
+            pp::quad_sync(wq);
+            const float m0 = red[r], m1 = red[BQ + r], l0 = red[2 * BQ + r], l1 = red[3 * BQ + r];
+            pp::quad_sync(wq);  // both read before the next item's epilogue overwrites
+            const float M = fmaxf(m0, m1);
+            const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
+            const float inv = 1.f / (l0 * f0 + l1 * f1);
+            const bool has1 = rg.ntiles >= 2;  // item-uniform: O1 holds this item's odd tiles
+            mbar_wait(bar(pp::OD + 0), (cnt[0] - 1) & 1);
+            if (has1) mbar_wait(bar(pp::OD + 1), (cnt[1] - 1) & 1);
+            fence_after();
+            const uint32_t tO0 = lane_off + pp::kTO + uint32_t(grp * C::kOC), tO1 = tO0 + uint32_t(D);
+            const int qb = n & 1;
+            constexpr int CW = C::kOC < 16 ? C::kOC : 16;  // columns per TMEM load
+            auto combined = [&](int c, uint32_t* o) {      // this thread's columns [c CW, c CW + CW), merged
+                uint32_t o1[CW];
+                if constexpr (CW == 16) {
+                    ld16(tO0 + uint32_t(c * CW), o);
+                    if (has1) ld16(tO1 + uint32_t(c * CW), o1);
+                    wait_ld_dep16(o);
+                    if (has1) wait_ld_dep16(o1);
+                } else {
+                    ld8(tO0 + uint32_t(c * CW), o);
+                    if (has1) ld8(tO1 + uint32_t(c * CW), o1);
+                    wait_ld_dep8(o);
+                    if (has1) wait_ld_dep8(o1);
+                }
+#pragma unroll
+                for (int i = 0; i < CW; ++i) {
+                    float v = __uint_as_float(o[i]) * f0;
+                    if (has1) v = fmaf(__uint_as_float(o1[i]), f1, v);
+                    o[i] = __float_as_uint(v * inv);
+                }
+            };
+            if (D >= 64 && p.tmo != nullptr && it.q0 + BQ <= s) {
+                uint8_t* stg = sQ + qb * C::kQBytes;  // SW128 staging in this item's Q buffer (TMA box layout)
+#pragma unroll 1
+                for (int c = 0; c < C::kOC / CW; ++c) {
+                    uint32_t o[CW];
+                    combined(c, o);
+#pragma unroll
+                    for (int v = 0; v < CW / 8; ++v) {
+                        const int col = grp * C::kOC + c * CW + v * 8;
+                        const int ch = (col & 63) >> 3;
+                        uint4* dst = reinterpret_cast<uint4*>(stg + (col >> 6) * (BQ * 128) + r * 128 +
+                                                              ((ch ^ (r & 7)) << 4));
+                        *dst = make_uint4(pack_bf16x2(__uint_as_float(o[8 * v]), __uint_as_float(o[8 * v + 1])),
+                                          pack_bf16x2(__uint_as_float(o[8 * v + 2]), __uint_as_float(o[8 * v + 3])),
+                                          pack_bf16x2(__uint_as_float(o[8 * v + 4]), __uint_as_float(o[8 * v + 5])),
+                                          pack_bf16x2(__uint_as_float(o[8 * v + 6]), __uint_as_float(o[8 * v + 7])));
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                fence_before();
+                pp::all_softmax_sync();
+                if (leader) {
+                    for (int bx = 0; bx < D / 64; ++bx)
+                        tma_store_2d(&tmO, smem_u32(stg + bx * (BQ * 128)), (p.head0 + it.head) * D + bx * 64,
+                                     int(oloc));
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    qe_pending = qb;
+                }
+            } else {
+                __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(p.o_dst[orank]) + oloc * p.ldo +
+                                   (p.head0 + it.head) * D + grp * C::kOC;
+#pragma unroll 1
+                for (int c = 0; c < C::kOC / CW; ++c) {
+                    uint32_t o[CW];
+                    combined(c, o);
+                    if (q < s) {
+                        uint4* d4 = reinterpret_cast<uint4*>(O + c * CW);
+#pragma unroll
+                        for (int v = 0; v < CW / 8; ++v)
+                            d4[v] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * v]), __uint_as_float(o[8 * v + 1])),
+                                               pack_bf16x2(__uint_as_float(o[8 * v + 2]), __uint_as_float(o[8 * v + 3])),
+                                               pack_bf16x2(__uint_as_float(o[8 * v + 4]), __uint_as_float(o[8 * v + 5])),
+                                               pack_bf16x2(__uint_as_float(o[8 * v + 6]), __uint_as_float(o[8 * v + 7])));
+                    }
+                }
+                fence_before();
+                pp::all_softmax_sync();  // both groups done with this item's Q buffer and O columns
+                if (leader) mbar_arrive(bar(pp::QE + qb));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(lbar(pp::OF));  // O0 / O1 may be overwritten
+        }
+        if (leader && qe_pending >= 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    fence_before();
+    cluster_sync_all();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+// SWF_ATTN=split selects the key-split kernel (two threads per query row, one shared O); the default
+// is the ping-pong kernel.
+inline bool use_split_kernel() {
+    static const bool v = [] {
+        const char* e = std::getenv("SWF_ATTN");
+        return e && std::string(e) == "split";
+    }();
+    return v;
+}
+
+inline int pp_grid(const AttnParams& p) {
+    const int npairs = (p.s + 2 * BQ - 1) / (2 * BQ);
+    return 2 * std::min(npairs * p.heads * p.nloc, 74);
+}
+
 template <int D>
 void launch(const AttnParams& p, cudaStream_t st) {
     using C = ACfg<D>;
     static bool configured = false;
     if (!configured) {
         SWF_CUDA(cudaFuncSetAttribute(k_attn_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        SWF_CUDA(cudaFuncSetAttribute(k_attn_pp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, pp::Cfg<D>::kSmem));
         configured = true;
     }
     const int npairs = (p.s + 2 * BQ - 1) / (2 * BQ);
     const int n_items = npairs * p.heads * p.nloc;
     const int grid = 2 * std::min(n_items, 74);  // 2-CTA clusters, one CTA per SM
-    k_attn_tc<D><<<grid, kThreads, C::kSmem, st>>>(*reinterpret_cast<const CUtensorMap*>(p.tmq),
-                                                  *reinterpret_cast<const CUtensorMap*>(p.tmk),
-                                                  *reinterpret_cast<const CUtensorMap*>(p.tmv),
-                                                  *reinterpret_cast<const CUtensorMap*>(p.tmo ? p.tmo : p.tmv), p, n_items);
+    const CUtensorMap& tq = *reinterpret_cast<const CUtensorMap*>(p.tmq);
+    const CUtensorMap& tk = *reinterpret_cast<const CUtensorMap*>(p.tmk);
+    const CUtensorMap& tk2 = *reinterpret_cast<const CUtensorMap*>(p.tmk2 ? p.tmk2 : p.tmk);
+    const CUtensorMap& tv = *reinterpret_cast<const CUtensorMap*>(p.tmv);
+    const CUtensorMap& to = *reinterpret_cast<const CUtensorMap*>(p.tmo ? p.tmo : p.tmv);
+    if (use_split_kernel())
+        k_attn_tc<D><<<grid, kThreads, C::kSmem, st>>>(tq, tk, tv, to, p, n_items);
+    else
+        k_attn_pp<D><<<pp_grid(p), pp::kThreads, pp::Cfg<D>::kSmem, st>>>(tq, tk2, tv, to, p, n_items);
     SWF_LAUNCH_CHECK();
 #ifdef SWF_ATTN_TRACE
     if (const char* path = getenv("SWF_ATTN_TRACE_OUT")) {
@@ -851,8 +1319,16 @@ void launch(const AttnParams& p, cudaStream_t st) {
 
 }  // namespace
 
+void preload_attn_kernels() {
+    cudaFuncAttributes a;
+    const void* k[] = {(const void*)k_attn_tc<32>, (const void*)k_attn_tc<64>, (const void*)k_attn_tc<128>,
+                       (const void*)k_attn_pp<32>, (const void*)k_attn_pp<64>, (const void*)k_attn_pp<128>};
+    for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
+}
+
 void attention_bf16(const AttnParams& p, cudaStream_t st) {
     if (!p.tmq || !p.tmk || !p.tmv) throw CudaError("attention_bf16: TMA descriptors missing");
+    if (!use_split_kernel() && !p.tmk2) throw CudaError("attention_bf16: the K map with 32-row boxes is missing");
     switch (p.d) {
         case 32: launch<32>(p, st); break;
         case 64: launch<64>(p, st); break;

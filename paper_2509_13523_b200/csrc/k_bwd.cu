@@ -662,4 +662,14 @@ void axpy_f32(const float* x, i64 n, float a, float* y, cudaStream_t st) {
     SWF_LAUNCH_CHECK();
 }
 
+void preload_bwd_kernels() {
+    cudaFuncAttributes a;
+    const void* k[] = {(const void*)k_gemm_strided, (const void*)k_norm_bwd_rows, (const void*)k_norm_bwd_cols,
+                       (const void*)k_colsum, (const void*)k_swiglu_bwd, (const void*)k_relayout,
+                       (const void*)k_relayout_push, (const void*)k_attn_bwd_q, (const void*)k_attn_bwd_kv,
+                       (const void*)k_attn_bwd_pack, (const void*)k_ada_bwd, (const void*)k_time_bwd,
+                       (const void*)k_train_prep, (const void*)k_train_loss, (const void*)k_axpy};
+    for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
+}
+
 }  // namespace swf

@@ -69,27 +69,63 @@ template <>
 __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 template <class T>
-__global__ void k_gather_rows(const float* __restrict__ src, LayMap lay, int C, int ldo, i64 M, T* __restrict__ dst,
-                              int* flags, int slot) {
-    const i64 total = M * ldo;
-    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
-        const i64 i = e / ldo;
-        const int c = int(e - i * ldo);
-        float v = 0.f;
-        if (c < C) {
-            v = src[lay.loc_to_pix(i) * C + c];
-            if (flags && !isfinite(v)) flag_nonfinite(flags, slot);
-        }
-        dst[e] = cvt<T>(v);
-    }
+__device__ __forceinline__ void store_cvt4(T* p, float4 v);
+template <>
+__device__ __forceinline__ void store_cvt4<float>(float* p, float4 v) {
+    *reinterpret_cast<float4*>(p) = v;
+}
+template <>
+__device__ __forceinline__ void store_cvt4<__nv_bfloat16>(__nv_bfloat16* p, float4 v) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
 }
 
-__global__ void k_scatter_rows(const float* __restrict__ src, LayMap lay, int C, i64 M, float* __restrict__ dst) {
-    const i64 total = M * C;
-    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
-        const i64 i = e / C;
-        const int c = int(e - i * C);
-        dst[lay.loc_to_pix(i) * C + c] = src[e];
+// One warp per local row: the row's pixel is resolved once (not per element), then the C source
+// values are read as 16-byte vectors (C % 4 == 0 and ldo % 4 == 0) or scalars, cast and zero-padded to
+// ldo. Source rows are contiguous [pixel][C] runs, so each warp reads / writes whole rows coalesced.
+template <class T>
+__global__ void __launch_bounds__(256) k_gather_rows(const float* __restrict__ src, LayMap lay, int C, int ldo, i64 M,
+                                                     T* __restrict__ dst, int* flags, int slot) {
+    const int lane = threadIdx.x & 31;
+    const bool vec = (C % 4 == 0) && (ldo % 4 == 0);
+    bool bad = false;
+    for (i64 i = i64(blockIdx.x) * 8 + (threadIdx.x >> 5); i < M; i += i64(gridDim.x) * 8) {
+        const float* row = src + lay.loc_to_pix(i) * C;
+        T* o = dst + i * ldo;
+        if (vec) {
+            for (int q = lane; q < ldo / 4; q += 32) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (4 * q < C) {
+                    v = __ldg(reinterpret_cast<const float4*>(row) + q);
+                    bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+                }
+                store_cvt4<T>(o + 4 * q, v);
+            }
+        } else {
+            for (int c = lane; c < ldo; c += 32) {
+                float v = 0.f;
+                if (c < C) {
+                    v = __ldg(row + c);
+                    bad |= !isfinite(v);
+                }
+                o[c] = cvt<T>(v);
+            }
+        }
+    }
+    if (flags && __any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(flags, slot);
+}
+
+// One warp per local row, the inverse of k_gather_rows.
+__global__ void __launch_bounds__(256) k_scatter_rows(const float* __restrict__ src, LayMap lay, int C, i64 M,
+                                                      float* __restrict__ dst) {
+    const int lane = threadIdx.x & 31;
+    for (i64 i = i64(blockIdx.x) * 8 + (threadIdx.x >> 5); i < M; i += i64(gridDim.x) * 8) {
+        float* o = dst + lay.loc_to_pix(i) * C;
+        const float* r = src + i * C;
+        if (C % 4 == 0)
+            for (int q = lane; q < C / 4; q += 32)
+                reinterpret_cast<float4*>(o)[q] = __ldg(reinterpret_cast<const float4*>(r) + q);
+        else
+            for (int c = lane; c < C; c += 32) o[c] = __ldg(r + c);
     }
 }
 
@@ -276,7 +312,7 @@ void ada_vectors(const float* emb, const float* w_ada_t, const float* b_ada, int
 template <class T>
 void gather_rows(const float* src_pix, const LayMap& lay, int C, int ldo, i64 M, T* dst, int* flags, int slot,
                  cudaStream_t st) {
-    k_gather_rows<T><<<grid_for(M * ldo), kThreads, 0, st>>>(src_pix, lay, C, ldo, M, dst, flags, slot);
+    k_gather_rows<T><<<grid_for(M, 8), kThreads, 0, st>>>(src_pix, lay, C, ldo, M, dst, flags, slot);
     SWF_LAUNCH_CHECK();
 }
 template void gather_rows<float>(const float*, const LayMap&, int, int, i64, float*, int*, int, cudaStream_t);
@@ -284,7 +320,7 @@ template void gather_rows<__nv_bfloat16>(const float*, const LayMap&, int, int, 
                                          cudaStream_t);
 
 void scatter_rows(const float* src_loc, const LayMap& lay, int C, i64 M, float* dst_pix, cudaStream_t st) {
-    k_scatter_rows<<<grid_for(M * C), kThreads, 0, st>>>(src_loc, lay, C, M, dst_pix);
+    k_scatter_rows<<<grid_for(M, 8), kThreads, 0, st>>>(src_loc, lay, C, M, dst_pix);
     SWF_LAUNCH_CHECK();
 }
 
@@ -447,6 +483,20 @@ void destandardize_add(const float* r, const float* base, i64 M, int C, const fl
 void check_finite(const float* x, i64 n, int* flags, int slot, cudaStream_t st) {
     k_check_finite<<<grid_for(n), kThreads, 0, st>>>(x, n, flags, slot);
     SWF_LAUNCH_CHECK();
+}
+
+// Load every kernel of this file into the current device's context now (see preload_kernels).
+void preload_elem_kernels() {
+    cudaFuncAttributes a;
+    const void* k[] = {
+        (const void*)k_time_features, (const void*)k_time_embed, (const void*)k_ada,
+        (const void*)k_gather_rows<float>, (const void*)k_gather_rows<__nv_bfloat16>, (const void*)k_scatter_rows,
+        (const void*)k_rms_mod<float>, (const void*)k_rms_mod<__nv_bfloat16>, (const void*)k_sampler_update,
+        (const void*)k_build_static<float>, (const void*)k_build_static<__nv_bfloat16>,
+        (const void*)k_assemble_state<float>, (const void*)k_assemble_state<__nv_bfloat16>, (const void*)k_noise,
+        (const void*)k_churn, (const void*)k_standardize, (const void*)k_destd_add, (const void*)k_check_finite,
+        (const void*)k_prep_residual, (const void*)k_rows_at_pixels, (const void*)k_fold_adaln, (const void*)k_inv_rms};
+    for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
 }
 
 }  // namespace swf

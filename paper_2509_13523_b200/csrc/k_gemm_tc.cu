@@ -757,6 +757,19 @@ void make_tma_bf16_2d(TmaMap* m, const void* base, i64 rows, i64 inner, int box_
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (2d) failed: " + std::to_string(int(r)));
 }
 
+template <int BN>
+void preload_bn(cudaFuncAttributes& a) {
+    const void* k[] = {(const void*)k_gemm_tc<BN, EPI_ENCODE>, (const void*)k_gemm_tc<BN, EPI_QKV>,
+                       (const void*)k_gemm_tc<BN, EPI_RESID>, (const void*)k_gemm_tc<BN, EPI_SWIGLU>,
+                       (const void*)k_gemm_tc<BN, EPI_DOWN>, (const void*)k_gemm_tc<BN, EPI_DECODE>};
+    for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
+}
+void preload_gemm_kernels() {
+    cudaFuncAttributes a;
+    preload_bn<128>(a);
+    preload_bn<256>(a);
+}
+
 void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int BN, int mode, const EpiParams& ep,
                   cudaStream_t st) {
     if (K % BK != 0) throw CudaError("gemm_bf16_tc: K must be a multiple of 64");

@@ -212,4 +212,13 @@ void attention_f32(const AttnParams& p, cudaStream_t st) {
     SWF_LAUNCH_CHECK();
 }
 
+void preload_simt_kernels() {
+    cudaFuncAttributes a;
+    const void* k[] = {(const void*)k_gemm_f32<EPI_ENCODE>, (const void*)k_gemm_f32<EPI_QKV>,
+                       (const void*)k_gemm_f32<EPI_RESID>, (const void*)k_gemm_f32<EPI_SWIGLU>,
+                       (const void*)k_gemm_f32<EPI_DOWN>, (const void*)k_gemm_f32<EPI_DECODE>,
+                       (const void*)k_attn_f32};
+    for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
+}
+
 }  // namespace swf

@@ -161,6 +161,7 @@ struct AttnParams {
     const TmaMap* tmq;  // BF16 path: TMA maps of the q / k planes ([rows][d]) and of V^T ([rows][s])
     const TmaMap* tmk;
     const TmaMap* tmv;
+    const TmaMap* tmk2; // BF16 path: K planes with 32-row boxes (the ping-pong kernel's 64-key tiles)
     const TmaMap* tmo;  // BF16 path, sp == 1: map of the own output buffer (box 64 x 128, SW128) for TMA
                         // stores of whole query tiles; nullptr = per-row stores
     int dbg = 0;        // test only (swf_selftest_attention negative control): bit 0 skips the O rescale
@@ -252,5 +253,15 @@ void destandardize_add(const float* r, const float* base, i64 M, int C, const fl
                        float* y, cudaStream_t st);
 // Count non-finite values of a buffer into flags[slot] (cheap guard for device-entry inputs).
 void check_finite(const float* x, i64 n, int* flags, int slot, cudaStream_t st);
+
+// Load every kernel into the current device's context (cudaFuncGetAttributes per kernel). CUDA's
+// lazy module loading would otherwise load a kernel at its first launch, which needs the context idle
+// -- and with ranks of one process meeting in spin barriers on a shared GPU, a rank's first launch of
+// a kernel can wait behind a peer's barrier that waits for that rank: a deadlock.
+void preload_elem_kernels();
+void preload_bwd_kernels();
+void preload_simt_kernels();
+void preload_gemm_kernels();
+void preload_attn_kernels();
 
 }  // namespace swf

@@ -150,3 +150,26 @@ def test_group_c4_width_sp2_vs_oracle():
     p = o.init_params(oc, 2024, random=True, scale=0.004, dtype=np.float32)
     ref = o.forward(oc, p, x, np.float32(0.9), H, W)
     assert rel_err_per_channel(y, ref) <= 2e-2
+
+
+def test_group_train_step_matches_single():
+    """reference_train_step (simulator.hpp:50-86) on a WP 1x2 single-process group: the ranks' partial
+    losses / gradients over their own windows are summed by the group, no process group needed."""
+    d = dict(hidden_dim=64, n_heads=4, ffn_dim=128, n_layers=2, window_px=8, in_channels=8, out_channels=3,
+             time_dim=64)
+    H, W = 32, 64
+    oc, sc = o.ModelConfig(**d), swf.ModelConfig(**d)
+    p = o.init_params(oc, 57, random=True, scale=0.05, dtype=np.float32)
+    data = swf.DataSet(*[[o.random_field(c, H * W, 900 + 3 * i + j).astype(np.float32) for i in range(3)]
+                         for j, c in ((0, 3), (1, 2), (2, 3))])
+    w = swf.LossWeights.make(H, [1.0, 0.6, 1.7])
+    res = {}
+    for grp in (False, True):
+        kw = dict(topology=(1, 2, 1, swf.OWN_CONTIGUOUS), devices=devices(2)) if grp else {}
+        dn = swf.Denoiser(sc, H, W, precision=swf.PREC_FP32, **kw)
+        dn.load_params(p)
+        res[grp] = dn.train_step(data, 3, 2, 2, w, swf.DiffusionConfig(), 31)
+        dn.close()
+    a, b = res[False], res[True]
+    assert np.allclose(a.mb_losses, b.mb_losses, rtol=1e-6, atol=0)
+    assert float(np.abs(a.grads - b.grads).max()) <= 1e-5 * float(np.abs(a.grads).max())

@@ -52,7 +52,7 @@ def test_forecast_step_churn_fp32_mode(churn):
     assert fe == 18
     assert rel_err_per_channel(got, ref) <= TOL_FP32
     # the churn changes the result well beyond the tolerance (the comparison sees the rotation)
-    assert rel_err_per_channel(ref0, ref) > 100 * TOL_FP32
+    assert rel_err_per_channel(ref0, ref) > 20 * TOL_FP32
 
 
 def test_forecast_step_standardizers_fp32_mode():

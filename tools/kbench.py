@@ -17,7 +17,7 @@ classes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["attention", "qkv_ge
                                                              "down_gemm", "rms_adaln"]
 cfg = swf.ModelConfig(**bench.CFG)
 dn = swf.Denoiser(cfg, bench.H, bench.W, precision=swf.PREC_BF16)
-dn.init_params(bench.SEED, mode=2, scale=0.02 / math.sqrt(bench.CFG["time_dim"]))
+dn.init_params(bench.SEED, mode=1, scale=bench.WEIGHT_SCALE)
 x = bench.synthetic_input(dn, bench.CFG)
 d_in = torch.from_numpy(x).cuda()
 d_out = torch.empty(bench.H * bench.W * bench.CFG["out_channels"], device="cuda")
