@@ -252,6 +252,21 @@ int swf_profile_launches(swf_ctx* ctx, int* classes, double* ms, int max_n, int*
 int swf_bench_kernel(swf_ctx* ctx, int kernel_class, int block, int reps, double* ms);
 /* Noise field (diffusion.hpp:91-108) for (run_seed, event) into a host C x N buffer (fp32). */
 int swf_noise_field(swf_ctx* ctx, uint64_t run_seed, uint64_t event, int channels, double sigma_d, float* out);
+/* Leaves of the reference's ops namespace (swin.hpp:49-234), as the SWiPe simulator calls them per
+ * sequence band (simulator.hpp:466-506): standalone device calls on host buffers, column-major like
+ * the reference (a C x n matrix is n*C floats, token j's C values contiguous). precision selects the
+ * BF16 tensor-core or the FP32 SIMT arithmetic.
+ *   linear_cols(W, X) = W X           W: out x in (W[k*out + o]), X: in x n, Y: out x n  (swin.hpp:49-54)
+ *   prenorm_modulate(x; g, a, b, gate) = gate*((g*x/rms(x))*(1+a)+b), rms with eps 1e-8;
+ *                                      a = b = gate = NULL for prenorm_plain      (swin.hpp:72-85,111-123)
+ *   swiglu_fwd(x) = W_down (silu(W_gate x) * (W_up x))                              (swin.hpp:228-234)
+ * head_attention_fwd's attention core is swf_selftest_attention below (flags 0). */
+int swf_op_linear_cols(int device, int precision, const float* W, int out, int in, const float* X, long long n,
+                       float* Y);
+int swf_op_prenorm_modulate(int device, const float* X, int h, long long n, const float* g, const float* a,
+                            const float* b, const float* gate, float* Y);
+int swf_op_swiglu_fwd(int device, int precision, const float* W_gate, const float* W_up, const float* W_down,
+                      int h, int f, const float* X, long long n, float* Y);
 /* Run one bf16 GEMM self-test of the tcgen05 kernel: C = A.B^T on device, returns max |err|
  * against an fp32 SIMT product of the same bf16 operands (used by the parity tests). */
 int swf_selftest_gemm(int device, long long M, int N, int K, double* max_abs_err, double* max_ref);

@@ -156,6 +156,9 @@ def lib():
         L.swf_selftest_attention.argtypes = [i, i, i, i, i, i, i, i, vp, vp, vp, vp, i]
         L.swf_forward_hidden.argtypes = [vp, vp, d, i, vp, ll, vp, i]
         L.swf_block_window_forward.argtypes = [vp, i, i, i, d, vp, vp, i]
+        L.swf_op_linear_cols.argtypes = [i, i, vp, i, i, vp, ll, vp]
+        L.swf_op_prenorm_modulate.argtypes = [i, vp, i, ll, vp, vp, vp, vp, vp]
+        L.swf_op_swiglu_fwd.argtypes = [i, i, vp, vp, vp, i, i, vp, ll, vp]
         L.swf_backward.argtypes = [vp, vp, d, vp, vp, vp, i]
         L.swf_diffusion_loss_sample.argtypes = [vp, vp, vp, vp, vp, vp, u64, vp, C.POINTER(d), vp, i]
         L.swf_train_accumulate.argtypes = [vp, vp, vp, vp, vp, vp, u64, u64, C.POINTER(d), i]
@@ -224,6 +227,39 @@ def selftest_attention(q, k, v, n_wy: int, n_wx: int, w: int, shift: int = 0, pr
     _check(lib().swf_selftest_attention(device, precision, n_wy, n_wx, w, shift, heads, dd, _p(q), _p(k), _p(v),
                                         _p(o), flags))
     return o
+
+
+class ops:
+    """The reference's ops leaves (swin.hpp:49-234) on the device. Matrices are numpy arrays in the
+    reference's column-major storage: W (out x in) as W.reshape(in, out) [in][out], fields (C x n) as
+    [n][C] rows."""
+
+    @staticmethod
+    def linear_cols(W, out: int, inp: int, X, precision: int = PREC_BF16, device: int = 0):
+        W = np.ascontiguousarray(W, np.float32).reshape(-1)
+        X = np.ascontiguousarray(X, np.float32)
+        n = X.size // inp
+        Y = np.zeros((n, out), np.float32)
+        _check(lib().swf_op_linear_cols(device, precision, _p(W), out, inp, _p(X), n, _p(Y)))
+        return Y
+
+    @staticmethod
+    def prenorm_modulate(X, g, a=None, b=None, gate=None, device: int = 0):
+        X = np.ascontiguousarray(X, np.float32)
+        n, h = X.shape
+        Y = np.zeros_like(X)
+        v = [None if t is None else np.ascontiguousarray(t, np.float32) for t in (g, a, b, gate)]
+        _check(lib().swf_op_prenorm_modulate(device, _p(X), h, n, *[_p(t) for t in v], _p(Y)))
+        return Y
+
+    @staticmethod
+    def swiglu_fwd(W_gate, W_up, W_down, h: int, f: int, X, precision: int = PREC_BF16, device: int = 0):
+        W = [np.ascontiguousarray(t, np.float32).reshape(-1) for t in (W_gate, W_up, W_down)]
+        X = np.ascontiguousarray(X, np.float32)
+        n = X.size // h
+        Y = np.zeros((n, h), np.float32)
+        _check(lib().swf_op_swiglu_fwd(device, precision, *[_p(t) for t in W], h, f, _p(X), n, _p(Y)))
+        return Y
 
 
 class Denoiser:

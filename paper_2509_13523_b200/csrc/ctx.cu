@@ -196,12 +196,17 @@ namespace {
 
 thread_local std::string g_err;
 
+// Zeroed device allocation owned by the context. The zero fill is complete on return: cudaMemset on
+// the legacy stream is not ordered with the context's non-blocking stream (and may still be pending
+// when cudaMemset returns), so a fill racing the first writes of the new buffer on c->st could zero
+// them (seen as a zero loss on the first training call with two ranks on one GPU).
 template <class T>
 T* dalloc(swf_ctx* c, size_t n) {
     void* p = nullptr;
     SWF_CUDA(cudaMalloc(&p, n * sizeof(T) + 256));
-    SWF_CUDA(cudaMemset(p, 0, n * sizeof(T) + 256));
     c->allocs.push_back(p);
+    SWF_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T) + 256, c->st));
+    SWF_CUDA(cudaStreamSynchronize(c->st));
     return static_cast<T*>(p);
 }
 
@@ -232,6 +237,13 @@ void* scratch(swf_ctx* c, int k, size_t bytes) {
     return s.first;
 }
 float* scratch_f(swf_ctx* c, int k, size_t n) { return static_cast<float*>(scratch(c, k, n * 4)); }
+
+// Host -> device copy complete on return and ordered with the context stream (a legacy-stream
+// cudaMemcpy from pageable memory may return before its DMA lands, unordered with c->st).
+void h2d_sync(swf_ctx* c, void* dst, const void* src, size_t bytes) {
+    SWF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st));
+    SWF_CUDA(cudaStreamSynchronize(c->st));
+}
 
 size_t esize(const swf_ctx* c) { return c->prec == SWF_PREC_BF16 ? 2 : 4; }
 
@@ -361,8 +373,8 @@ void build_layouts(swf_ctx* c) {
             c->d_l2g[par] = dalloc<int>(c, nwin);
             c->d_g2rl[par] = dalloc<int>(c, nwin);
         }
-        SWF_CUDA(cudaMemcpy(c->d_l2g[par], c->l2g[par].data(), sizeof(int) * c->l2g[par].size(), cudaMemcpyHostToDevice));
-        SWF_CUDA(cudaMemcpy(c->d_g2rl[par], g2rl.data(), sizeof(int) * nwin, cudaMemcpyHostToDevice));
+        h2d_sync(c, c->d_l2g[par], c->l2g[par].data(), sizeof(int) * c->l2g[par].size());
+        h2d_sync(c, c->d_g2rl[par], g2rl.data(), sizeof(int) * nwin);
         LayMap& L = c->lay[par];
         L.g = make_lay(c->H, c->W, m.w, par == 0 ? 0 : m.w / 2);
         L.nloc = int(c->l2g[par].size());
@@ -394,8 +406,8 @@ void build_rope(swf_ctx* c) {
     const auto tr = table(c->H + m.w), tc = table(c->W + m.w);
     c->rope_row = dalloc<float>(c, tr.size());
     c->rope_col = dalloc<float>(c, tc.size());
-    SWF_CUDA(cudaMemcpy(c->rope_row, tr.data(), tr.size() * 4, cudaMemcpyHostToDevice));
-    SWF_CUDA(cudaMemcpy(c->rope_col, tc.data(), tc.size() * 4, cudaMemcpyHostToDevice));
+    h2d_sync(c, c->rope_row, tr.data(), tr.size() * 4);
+    h2d_sync(c, c->rope_col, tc.data(), tc.size() * 4);
 }
 
 void allocate(swf_ctx* c) {
@@ -487,14 +499,14 @@ void allocate(swf_ctx* c) {
         std::vector<void*> t(8, nullptr), o(8, nullptr);
         t[c->rank] = c->qkv;
         o[c->rank] = c->xm;
-        SWF_CUDA(cudaMemcpy(c->d_qkv_dst, t.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
-        SWF_CUDA(cudaMemcpy(c->d_o_dst, o.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+        h2d_sync(c, c->d_qkv_dst, t.data(), sizeof(void*) * 8);
+        h2d_sync(c, c->d_o_dst, o.data(), sizeof(void*) * 8);
     }
     for (int par = 0; par < 2; ++par) {
         c->d_xdst[par] = dalloc<float*>(c, 8);
         std::vector<float*> t(8, nullptr);
         for (int r = 0; r < c->world; ++r) t[r] = c->peer[r].x[par];
-        SWF_CUDA(cudaMemcpy(c->d_xdst[par], t.data(), sizeof(float*) * 8, cudaMemcpyHostToDevice));
+        h2d_sync(c, c->d_xdst[par], t.data(), sizeof(float*) * 8);
     }
     if (c->prec == SWF_PREC_BF16) {
         make_tma_bf16(&c->tm_ain, c->a_in, M, m.cinp, 128);
@@ -1502,7 +1514,7 @@ void ensure_sampler(swf_ctx* c) {
                 }
         }
     c->pe_loc = dalloc<float>(c, size_t(M) * m.cin);
-    SWF_CUDA(cudaMemcpy(c->in_pix, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice));
+    h2d_sync(c, c->in_pix, pe.data(), pe.size() * 4);
     gather_rows<float>(c->in_pix, c->lay[0], m.cin, m.cin, M, c->pe_loc, nullptr, 0, c->st);
     c->s_x = dalloc<float>(c, size_t(M) * m.cout);
     c->s_xmid = dalloc<float>(c, size_t(M) * m.cout);
@@ -1831,7 +1843,7 @@ void upload_stats(swf_ctx* c, const swf_standardizers* s, int dtype) {
     get(s ? s->resid_std : nullptr, cp, size_t(3) * m.cin, 1.f);
     get(s ? s->forcing_mean : nullptr, cf, size_t(4) * m.cin, 0.f);
     get(s ? s->forcing_std : nullptr, cf, size_t(5) * m.cin, 1.f);
-    SWF_CUDA(cudaMemcpy(c->s_stats, st.data(), st.size() * 4, cudaMemcpyHostToDevice));
+    h2d_sync(c, c->s_stats, st.data(), st.size() * 4);
 }
 
 u64 h_splitmix(u64 x) {
@@ -1972,6 +1984,34 @@ void grads_to_host(swf_ctx* c, const float* src, double scale, void* out, int dt
 
 }  // namespace
 
+namespace swf {
+void set_last_error(const std::string& m) { g_err = m; }
+
+// Once per device and process, before any work runs on it: load every kernel and set the dynamic
+// shared-memory limits (per device: the attributes live in each device's context). Both would
+// otherwise happen on first use, inside the ranks' concurrent calls, and need the context idle.
+void ensure_device(int device) {
+    static std::mutex mu;
+    static std::vector<char> done(256, 0);
+    std::lock_guard<std::mutex> lk(mu);
+    if (device < 0 || device >= 256 || done[size_t(device)]) return;
+    int prev = 0;
+    SWF_CUDA(cudaGetDevice(&prev));
+    SWF_CUDA(cudaSetDevice(device));
+    preload_elem_kernels();
+    preload_bwd_kernels();
+    preload_simt_kernels();
+    preload_gemm_kernels();
+    preload_attn_kernels();
+    cudaFuncAttributes a;
+    for (const void* f : {(const void*)k_repack<float>, (const void*)k_repack<__nv_bfloat16>, (const void*)k_init_fill,
+                          (const void*)k_peer_barrier})
+        SWF_CUDA(cudaFuncGetAttributes(&a, f));
+    SWF_CUDA(cudaSetDevice(prev));
+    done[size_t(device)] = 1;
+}
+}  // namespace swf
+
 // ====================================================================== C ABI
 #define SWF_API_TRY(...)                                            \
     try {                                                           \
@@ -2079,7 +2119,7 @@ void upload_peer_tables(swf_ctx* c) {
     for (int par = 0; par < 2; ++par) {
         std::vector<float*> t(8, nullptr);
         for (int r = 0; r < c->world; ++r) t[r] = c->peer[r].x[par];
-        SWF_CUDA(cudaMemcpy(c->d_xdst[par], t.data(), sizeof(float*) * 8, cudaMemcpyHostToDevice));
+        h2d_sync(c, c->d_xdst[par], t.data(), sizeof(float*) * 8);
     }
     std::vector<int*> ft(8, nullptr);
     std::vector<void*> qt(8, nullptr), ot(8, nullptr);
@@ -2088,9 +2128,9 @@ void upload_peer_tables(swf_ctx* c) {
         qt[r] = c->peer[r].qkv;
         ot[r] = c->peer[r].xm;
     }
-    SWF_CUDA(cudaMemcpy(c->d_flag_table, ft.data(), sizeof(int*) * 8, cudaMemcpyHostToDevice));
-    SWF_CUDA(cudaMemcpy(c->d_qkv_dst, qt.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
-    SWF_CUDA(cudaMemcpy(c->d_o_dst, ot.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+    h2d_sync(c, c->d_flag_table, ft.data(), sizeof(int*) * 8);
+    h2d_sync(c, c->d_qkv_dst, qt.data(), sizeof(void*) * 8);
+    h2d_sync(c, c->d_o_dst, ot.data(), sizeof(void*) * 8);
     c->peers = true;
 }
 
@@ -2148,23 +2188,7 @@ int swf_create(const swf_model_cfg* cfg, int grid_h, int grid_w, int device, int
         SWF_CUDA(cudaGetDeviceProperties(&prop, device));
         if (prop.major != 10) throw CudaError("swf_create: this build targets sm_100a (B200); found sm_" +
                                                std::to_string(prop.major) + std::to_string(prop.minor));
-        {  // load every kernel into this device's context once (see preload_elem_kernels, kernels.cuh)
-            static std::mutex mu;
-            static std::vector<char> done(64, 0);
-            std::lock_guard<std::mutex> lk(mu);
-            if (device < 64 && !done[size_t(device)]) {
-                preload_elem_kernels();
-                preload_bwd_kernels();
-                preload_simt_kernels();
-                preload_gemm_kernels();
-                preload_attn_kernels();
-                cudaFuncAttributes a;
-                for (const void* f : {(const void*)k_repack<float>, (const void*)k_repack<__nv_bfloat16>,
-                                      (const void*)k_init_fill, (const void*)k_peer_barrier})
-                    SWF_CUDA(cudaFuncGetAttributes(&a, f));
-                done[size_t(device)] = 1;
-            }
-        }
+        ensure_device(device);
         swf_ctx* c = new swf_ctx();
         c->cfg = *cfg;
         c->m = make_dims(*cfg, precision);
@@ -2934,7 +2958,7 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
                         if (!scratch_tab) {
                             scratch_tab = dalloc<void*>(c, 8);
                             std::vector<void*> t(8, c->sbuf);
-                            SWF_CUDA(cudaMemcpy(scratch_tab, t.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice));
+                            h2d_sync(c, scratch_tab, t.data(), sizeof(void*) * 8);
                         }
                         ap.o_dst = scratch_tab;
                     }
@@ -3138,6 +3162,7 @@ int swf_selftest_attention(int device, int precision, int n_wy, int n_wx, int w,
         const bool bf = precision == SWF_PREC_BF16;
         if (bf) require((d == 32 || d == 64 || d == 128) && w % 4 == 0, "attention: BF16 needs d in {32,64,128}");
         SWF_CUDA(cudaSetDevice(device));
+        ensure_device(device);
         const int nwin = n_wy * n_wx, s = w * w, hd = heads * d;
         const int ldo = int(roundup(hd, 64));
         const size_t n = size_t(nwin) * heads * s * d;

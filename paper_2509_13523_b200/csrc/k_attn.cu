@@ -84,6 +84,18 @@ constexpr int kNS = 3;       // S buffers in TMEM
 #define SWF_ATTN_BACKOFF 40
 #endif
 constexpr uint32_t kBackoffNs = SWF_ATTN_BACKOFF;  // poll back-off of the control warps' barrier waits
+// TMA producers of the ping-pong kernel wait for free ring slots 8 tiles ahead of their consumers: a
+// long back-off costs nothing there, while each poll takes an issue slot from the softmax warp sharing
+// the sub-partition (ncu: the producers' polling was ~17% of all issued instructions at 40 ns)
+#ifndef SWF_ATTN_PBACKOFF
+#define SWF_ATTN_PBACKOFF 256
+#endif
+// ping-pong kernel: exponentials speculated against the running max before this tile's max is known
+// (1) or after it (0, default: the speculative variant measured 17% more cycles per launch and gave
+// wrong rows under sharp logits at C2 size; kept off)
+#ifndef SWF_ATTN_SPEC
+#define SWF_ATTN_SPEC 0
+#endif
 constexpr uint32_t kTO = 384;  // TMEM column of O
 constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
 
@@ -174,6 +186,7 @@ __device__ __forceinline__ void tma_load_2cta(uint32_t dst, const void* tmap, ui
 }
 // mbarrier wait for the control warps: poll with a short nanosleep back-off, so a waiting producer /
 // MMA warp leaves the issue slots of its SM sub-partition to the softmax warp pair that shares it
+template <uint32_t kNs = kBackoffNs>
 __device__ __forceinline__ void mbar_sleep_wait(uint32_t bar, uint32_t parity) {
     uint32_t done;
     for (;;) {
@@ -187,7 +200,7 @@ __device__ __forceinline__ void mbar_sleep_wait(uint32_t bar, uint32_t parity) {
             : "r"(bar), "r"(parity)
             : "memory");
         if (done) break;
-        if constexpr (kBackoffNs > 0) __nanosleep(kBackoffNs);
+        if constexpr (kNs > 0) __nanosleep(kNs);
     }
 }
 // named barrier of the kSplit warps sharing a TMEM lane quadrant (one per key split)
@@ -988,14 +1001,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
                 const Range rg = pp::range_of(p, it);
                 const int plane = it.lw * p.heads + it.head;
                 const int qb = n & 1;
-                mbar_sleep_wait(bar(pp::QE + qb), ((n >> 1) & 1) ^ 1);
+                mbar_sleep_wait<SWF_ATTN_PBACKOFF>(bar(pp::QE + qb), ((n >> 1) & 1) ^ 1);
                 if (lead) mbar_expect_tx(bar(pp::QF + qb), 2 * C::kQBytes);
                 for (int b = 0; b < C::kBoxes; ++b)
                     tma_load_2cta(smem_u32(sQ + qb * C::kQBytes + b * BQ * C::kSw), &tmQ, lbar(pp::QF + qb),
                                   b * C::kColsPerBox, plane * s + it.q0);
                 for (int j = 0; j < rg.ntiles; ++j, ++g) {
                     const int st = g % C::kNK;
-                    mbar_sleep_wait(bar(pp::KE + st), ((g / C::kNK) & 1) ^ 1);
+                    mbar_sleep_wait<SWF_ATTN_PBACKOFF>(bar(pp::KE + st), ((g / C::kNK) & 1) ^ 1);
                     if (lead) mbar_expect_tx(bar(pp::KF + st), 2 * C::kKHalf);
                     for (int b = 0; b < C::kBoxes; ++b)
                         tma_load_2cta(smem_u32(sK + st * C::kKHalf + b * (KT / 2) * C::kSw), &tmK, lbar(pp::KF + st),
@@ -1014,7 +1027,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
                 const int plane = it.lw * p.heads + it.head;
                 for (int j = 0; j < rg.ntiles; ++j, ++g) {
                     const int st = g % C::kNV;
-                    mbar_sleep_wait(bar(pp::VE + st), ((g / C::kNV) & 1) ^ 1);
+                    mbar_sleep_wait<SWF_ATTN_PBACKOFF>(bar(pp::VE + st), ((g / C::kNV) & 1) ^ 1);
                     if (lead) mbar_expect_tx(bar(pp::VF + st), 2 * C::kVHalf);
                     tma_load_2cta(smem_u32(sV + st * C::kVHalf), &tmV, lbar(pp::VF + st), (rg.t_lo + j) * KT,
                                   plane * D + crank * (D / 2));
@@ -1080,6 +1093,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
         };
         int g = 0, n = 0;
         int cnt[2] = {0, 0};  // P V products issued into O0 / O1 so far (all items)
+        const unsigned long long sl2x2 = f2_pack(sl2, sl2);
+        // P = 2^(s sl2 - m) of this thread's 64 keys into 32 packed bf16x2 registers; returns the sum
+        auto exps = [&](const uint32_t* sa, float m, uint32_t* pk) {
+            const float nb = m == -INFINITY ? 0.f : -m;
+            const unsigned long long nbx2 = f2_pack(nb, nb);
+            unsigned long long ls2 = 0ull, ls2b = 0ull;
+#pragma unroll
+            for (int i = 0; i < KT / 2; ++i) {
+                const unsigned long long sv = (unsigned long long)sa[2 * i] | ((unsigned long long)sa[2 * i + 1] << 32);
+                const unsigned long long z = ffma2(sv, sl2x2, nbx2);
+                unsigned long long pv;
+                if ((i & 7) < kPoly8)  // kPoly8 / 8 of the exponentials on the FMA pipe
+                    pv = ex2_poly2(z);
+                else
+                    pv = f2_pack(ex2(lo_f(z)), ex2(hi_f(z)));
+                if (i & 1)
+                    ls2b = fadd2(ls2b, pv);
+                else
+                    ls2 = fadd2(ls2, pv);
+                pk[i] = pack_bf16x2(lo_f(pv), hi_f(pv));
+            }
+            const unsigned long long lsum = fadd2(ls2, ls2b);
+            return lo_f(lsum) + hi_f(lsum);
+        };
+        auto tile_max = [&](const uint32_t* sa) {  // 3-input max (FMNMX3), 4 chains of 16 keys
+            float mx4[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                mx4[c] = pp::max3(__uint_as_float(sa[16 * c]), __uint_as_float(sa[16 * c + 1]),
+                                  __uint_as_float(sa[16 * c + 2]));
+#pragma unroll
+            for (int i = 3; i < 16; i += 2)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    mx4[c] = i + 1 < 16 ? pp::max3(mx4[c], __uint_as_float(sa[16 * c + i]),
+                                                   __uint_as_float(sa[16 * c + i + 1]))
+                                        : fmaxf(mx4[c], __uint_as_float(sa[16 * c + i]));
+            return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+        };
         for (int itx = cluster_id; itx < n_items; itx += n_clusters, ++n) {
             const Item it = item_of(itx, npairs, p.heads, crank);
             const Range rg = pp::range_of(p, it);
@@ -1089,13 +1141,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             int orank = 0;
             const i64 oloc = q < s ? p.lay.wtok_to_loc(p.wp_rank, it.lw, q, &orank) : 0;
             float m = -INFINITY, l = 0.f;
-            for (int j = 0; j < rg.ntiles; ++j, ++g) {
-                const int par = j & 1;
-                ++cnt[par];
-                if (par != grp) continue;
-                const int b = g % pp::kNS;
+            const int g0 = g;
+            for (int j = grp; j < rg.ntiles; j += 2) {  // this group's tiles of the item
+                const int gj = g0 + j, b = gj % pp::kNS;
+                const int k = cnt[grp] + (j >> 1) + 1;  // P V products into O[grp] once this tile's is issued
                 const uint32_t tS = lane_off + uint32_t(b * KT);
-                mbar_wait(bar(pp::SF + b), (g / pp::kNS) & 1);
+                mbar_wait(bar(pp::SF + b), (gj / pp::kNS) & 1);
                 fence_after();
                 uint32_t sa[KT];
                 ld32(tS, sa);
@@ -1108,65 +1159,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
                     for (int i = 0; i < KT; ++i)
                         if (kb + i < rlo || kb + i >= rhi) sa[i] = __float_as_uint(-INFINITY);
                 }
-                float mx4[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c)  // 3-input max (FMNMX3) over 16 keys per chain
-                    mx4[c] = pp::max3(__uint_as_float(sa[16 * c]), __uint_as_float(sa[16 * c + 1]),
-                                      __uint_as_float(sa[16 * c + 2]));
-#pragma unroll
-                for (int i = 3; i < 16; i += 2)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        mx4[c] = i + 1 < 16 ? pp::max3(mx4[c], __uint_as_float(sa[16 * c + i]),
-                                                       __uint_as_float(sa[16 * c + i + 1]))
-                                            : fmaxf(mx4[c], __uint_as_float(sa[16 * c + i]));
-                const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
-                // lazy rescale, warp-uniform (tcgen05.ld / st are warp-collective): O[grp] *= 2^(m - m_new)
-                // once this group's previous P V into O[grp] has landed
+                uint32_t pk[KT / 2];
+                float lt;
+                // Speculate on the running max (every lane of the warp has one): the exponentials then do
+                // not wait for this tile's max, which is computed alongside and only checked afterwards;
+                // a tile whose max exceeds the running max by > 2^kRescale (rare after the first tiles)
+                // takes the rescale path and recomputes P.
+                const bool spec = SWF_ATTN_SPEC && __all_sync(0xffffffffu, m != -INFINITY);
+                if (spec) lt = exps(sa, m, pk);
+                const float mx = tile_max(sa);
                 const bool grow = m != -INFINITY && mx > m + kRescale;
                 if (__any_sync(0xffffffffu, grow)) {
-                    mbar_wait(bar(pp::OD + grp), (cnt[grp] - 2) & 1);
+                    // lazy rescale, warp-uniform (tcgen05.ld / st are warp-collective): O[grp] *= 2^(m - m_new)
+                    // once this group's previous P V into O[grp] has landed
+                    mbar_wait(bar(pp::OD + grp), (k - 2) & 1);
                     fence_after();
                     const float mn = fmaxf(m, mx);
                     const float f = m == -INFINITY ? 0.f : ex2(m - mn);
                     if (!(p.dbg & 1)) o_scale<D>(lane_off + pp::kTO + uint32_t(grp * D), f);
                     l *= f;
                     m = mn;
-                } else if (m == -INFINITY && mx != -INFINITY) {
-                    m = mx;
+                    lt = exps(sa, m, pk);
+                } else if (!spec) {
+                    if (m == -INFINITY) m = mx;  // first unmasked keys of this row: O and l are still 0
+                    lt = exps(sa, m, pk);
                 }
-                const float nb = m == -INFINITY ? 0.f : -m;
-                const unsigned long long sl2x2 = f2_pack(sl2, sl2), nbx2 = f2_pack(nb, nb);
-                unsigned long long ls2 = 0ull, ls2b = 0ull;
-#pragma unroll
-                for (int c = 0; c < KT / 32; ++c) {  // 32 keys -> 16 packed bf16x2 columns per store
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const unsigned long long sv =
-                            (unsigned long long)sa[32 * c + 2 * i] | ((unsigned long long)sa[32 * c + 2 * i + 1] << 32);
-                        const unsigned long long z = ffma2(sv, sl2x2, nbx2);
-                        unsigned long long pv;
-                        if ((i & 7) < kPoly8)
-                            pv = ex2_poly2(z);
-                        else
-                            pv = f2_pack(ex2(lo_f(z)), ex2(hi_f(z)));
-                        if (i & 1)
-                            ls2b = fadd2(ls2b, pv);
-                        else
-                            ls2 = fadd2(ls2, pv);
-                        pk[i] = pack_bf16x2(lo_f(pv), hi_f(pv));
-                    }
-                    st16(tS + uint32_t(16 * c), pk);
-                }
-                const unsigned long long lsum = fadd2(ls2, ls2b);
-                l += lo_f(lsum) + hi_f(lsum);
+                l += lt;
+                st16(tS, pk);
+                st16(tS + 16u, pk + 16);
                 wait_st();
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(lbar(pp::PF + b));
                 if (leader) release_q();
             }
+            cnt[0] += (rg.ntiles + 1) >> 1;
+            cnt[1] += rg.ntiles >> 1;
+            g = g0 + rg.ntiles;
             // ---- epilogue: merge the two groups' partial softmax states, O / l -> bf16
             red[grp * BQ + r] = m;
             red[(2 + grp) * BQ + r] = l;
@@ -1283,12 +1312,6 @@ inline int pp_grid(const AttnParams& p) {
 template <int D>
 void launch(const AttnParams& p, cudaStream_t st) {
     using C = ACfg<D>;
-    static bool configured = false;
-    if (!configured) {
-        SWF_CUDA(cudaFuncSetAttribute(k_attn_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        SWF_CUDA(cudaFuncSetAttribute(k_attn_pp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, pp::Cfg<D>::kSmem));
-        configured = true;
-    }
     const int npairs = (p.s + 2 * BQ - 1) / (2 * BQ);
     const int n_items = npairs * p.heads * p.nloc;
     const int grid = 2 * std::min(n_items, 74);  // 2-CTA clusters, one CTA per SM
@@ -1319,11 +1342,19 @@ void launch(const AttnParams& p, cudaStream_t st) {
 
 }  // namespace
 
+template <int D>
+void configure_attn() {  // dynamic shared memory limits of this head size's kernels (current device)
+    SWF_CUDA(cudaFuncSetAttribute(k_attn_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<D>::kSmem));
+    SWF_CUDA(cudaFuncSetAttribute(k_attn_pp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, pp::Cfg<D>::kSmem));
+}
 void preload_attn_kernels() {
     cudaFuncAttributes a;
     const void* k[] = {(const void*)k_attn_tc<32>, (const void*)k_attn_tc<64>, (const void*)k_attn_tc<128>,
                        (const void*)k_attn_pp<32>, (const void*)k_attn_pp<64>, (const void*)k_attn_pp<128>};
     for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
+    configure_attn<32>();
+    configure_attn<64>();
+    configure_attn<128>();
 }
 
 void attention_bf16(const AttnParams& p, cudaStream_t st) {

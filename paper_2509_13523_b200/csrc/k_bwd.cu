@@ -623,8 +623,6 @@ void attention_bwd_f32(const float* q, const float* k, const float* v, const flo
     const size_t ld = size_t(d) + 1;
     const size_t smq = (4 * AT * ld + AT * (AT + 1) + AT) * sizeof(float);
     const size_t smkv = (4 * AT * ld + 2 * AT * (AT + 1) + 3 * AT) * sizeof(float);
-    SWF_CUDA(cudaFuncSetAttribute(k_attn_bwd_q, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smq)));
-    SWF_CUDA(cudaFuncSetAttribute(k_attn_bwd_kv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smkv)));
     k_attn_bwd_q<<<grid, 256, smq, st>>>(p);
     SWF_LAUNCH_CHECK();
     k_attn_bwd_kv<<<grid, 256, smkv, st>>>(p);
@@ -670,6 +668,11 @@ void preload_bwd_kernels() {
                        (const void*)k_attn_bwd_pack, (const void*)k_ada_bwd, (const void*)k_time_bwd,
                        (const void*)k_train_prep, (const void*)k_train_loss, (const void*)k_axpy};
     for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
+    int dev = 0, mx = 0;
+    SWF_CUDA(cudaGetDevice(&dev));
+    SWF_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    for (const void* f : {(const void*)k_attn_bwd_q, (const void*)k_attn_bwd_kv})
+        SWF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
 }
 
 }  // namespace swf

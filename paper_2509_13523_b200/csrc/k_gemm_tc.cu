@@ -295,7 +295,7 @@ __device__ __forceinline__ void tile_coords(i64 t, int n_tiles, i64 m_tiles, int
     m_blk = int(g * group_m + r % gm);
 }
 
-// fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)
+// fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)// fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)
 // is transposed through shared memory so each global access is one contiguous 128-byte row segment.
 template <int MODE>
 __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, int n0, const float* v, float* stg,
@@ -672,12 +672,7 @@ int* sched_counter() {
 template <int BN, int MODE>
 void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiParams& ep, cudaStream_t st) {
     using C = Cfg<BN>;
-    static bool configured = false;
-    auto kern = k_gemm_tc<BN, MODE>;
-    if (!configured) {
-        SWF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        configured = true;
-    }
+    auto kern = k_gemm_tc<BN, MODE>;  // shared-memory limit set per device by preload_gemm_kernels
     const int n_tiles = Npad / BN;
     const i64 m_tiles = (M + 2 * BM - 1) / (2 * BM);
     const i64 total = m_tiles * n_tiles;
@@ -762,7 +757,10 @@ void preload_bn(cudaFuncAttributes& a) {
     const void* k[] = {(const void*)k_gemm_tc<BN, EPI_ENCODE>, (const void*)k_gemm_tc<BN, EPI_QKV>,
                        (const void*)k_gemm_tc<BN, EPI_RESID>, (const void*)k_gemm_tc<BN, EPI_SWIGLU>,
                        (const void*)k_gemm_tc<BN, EPI_DOWN>, (const void*)k_gemm_tc<BN, EPI_DECODE>};
-    for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
+    for (const void* f : k) {
+        SWF_CUDA(cudaFuncGetAttributes(&a, f));
+        SWF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem));
+    }
 }
 void preload_gemm_kernels() {
     cudaFuncAttributes a;
@@ -814,6 +812,7 @@ extern "C" int swf_selftest_gemm(int device, long long M, int N, int K, double* 
     using namespace swf;
     try {
         SWF_CUDA(cudaSetDevice(device));
+        ensure_device(device);
         if (N % 128 != 0 || K % 64 != 0) throw CudaError("selftest: N % 128 and K % 64 required");
         __nv_bfloat16 *A, *B;
         float *Af, *Bf, *C1, *C2, *bias, *res;

@@ -206,7 +206,6 @@ void gemm_f32(const float* A, const float* B, i64 M, int N, int K, int mode, con
 void attention_f32(const AttnParams& p, cudaStream_t st) {
     if (p.d > 16 * ADW) throw CudaError("attention (FP32 mode): head dim must be <= 128");
     const size_t smem = (2 * size_t(AT) * (p.d + 1) + AT * (AT + 1)) * sizeof(float);
-    SWF_CUDA(cudaFuncSetAttribute(k_attn_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     dim3 grid(unsigned((p.s + AT - 1) / AT), unsigned(p.heads), unsigned(p.nloc));
     k_attn_f32<<<grid, 256, smem, st>>>(p);
     SWF_LAUNCH_CHECK();
@@ -219,6 +218,10 @@ void preload_simt_kernels() {
                        (const void*)k_gemm_f32<EPI_DOWN>, (const void*)k_gemm_f32<EPI_DECODE>,
                        (const void*)k_attn_f32};
     for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
+    int dev = 0, mx = 0;
+    SWF_CUDA(cudaGetDevice(&dev));
+    SWF_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    SWF_CUDA(cudaFuncSetAttribute(k_attn_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
 }
 
 }  // namespace swf

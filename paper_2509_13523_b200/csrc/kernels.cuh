@@ -259,6 +259,10 @@ void check_finite(const float* x, i64 n, int* flags, int slot, cudaStream_t st);
 // -- and with ranks of one process meeting in spin barriers on a shared GPU, a rank's first launch of
 // a kernel can wait behind a peer's barrier that waits for that rank: a deadlock.
 void preload_elem_kernels();
+// the calling thread's swf_last_error() message (ctx.cu)
+void set_last_error(const std::string& m);
+// load all kernels and set their shared-memory limits on `device`, once per process (ctx.cu)
+void ensure_device(int device);
 void preload_bwd_kernels();
 void preload_simt_kernels();
 void preload_gemm_kernels();

@@ -52,6 +52,8 @@ if rank == 0:
     ref = single.train_step(data, 3, dp, gas, w, dc, 31)
     rel = float(np.abs(res.grads - ref.grads).max() / np.abs(ref.grads).max())
     mb_rel = float(np.max(np.abs(np.array(res.mb_losses) - np.array(ref.mb_losses)) / np.abs(ref.mb_losses)))
+    print(f"mb_losses sharded={[round(v, 9) for v in res.mb_losses]} single={[round(v, 9) for v in ref.mb_losses]}",
+          flush=True)
     print(f"world={world} wp={wp} dp={dp} gas={gas} loss={res.loss:.9e} ref={ref.loss:.9e} "
           f"mb_loss_rel_err={mb_rel:.3e} grad_rel_err={rel:.3e}", flush=True)
     ok = mb_rel <= (0.0 if wp == 1 else 1e-6) and abs(res.loss - ref.loss) <= 1e-6 * abs(ref.loss) and rel <= 1e-5
