@@ -90,12 +90,6 @@ constexpr uint32_t kBackoffNs = SWF_ATTN_BACKOFF;  // poll back-off of the contr
 #ifndef SWF_ATTN_PBACKOFF
 #define SWF_ATTN_PBACKOFF 256
 #endif
-// ping-pong kernel: exponentials speculated against the running max before this tile's max is known
-// (1) or after it (0, default: the speculative variant measured 17% more cycles per launch and gave
-// wrong rows under sharp logits at C2 size; kept off)
-#ifndef SWF_ATTN_SPEC
-#define SWF_ATTN_SPEC 0
-#endif
 constexpr uint32_t kTO = 384;  // TMEM column of O
 constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
 
@@ -1092,7 +1086,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             }
         };
         int g = 0, n = 0;
-        int cnt[2] = {0, 0};  // P V products issued into O0 / O1 so far (all items)
+        int cnt0 = 0, cnt1 = 0;  // P V products issued into O0 / O1 so far (all items); scalars, not an
+                                 // array: indexed by the group it would live in local memory
         const unsigned long long sl2x2 = f2_pack(sl2, sl2);
         // P = 2^(s sl2 - m) of this thread's 64 keys into 32 packed bf16x2 registers; returns the sum
         auto exps = [&](const uint32_t* sa, float m, uint32_t* pk) {
@@ -1142,34 +1137,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             const i64 oloc = q < s ? p.lay.wtok_to_loc(p.wp_rank, it.lw, q, &orank) : 0;
             float m = -INFINITY, l = 0.f;
             const int g0 = g;
-            for (int j = grp; j < rg.ntiles; j += 2) {  // this group's tiles of the item
-                const int gj = g0 + j, b = gj % pp::kNS;
-                const int k = cnt[grp] + (j >> 1) + 1;  // P V products into O[grp] once this tile's is issued
-                const uint32_t tS = lane_off + uint32_t(b * KT);
-                mbar_wait(bar(pp::SF + b), (gj / pp::kNS) & 1);
+            auto s_col = [&](int jj) { return lane_off + uint32_t(((g0 + jj) % pp::kNS) * KT); };
+            auto s_bar = [&](int jj) { return bar(pp::SF + (g0 + jj) % pp::kNS); };
+            auto s_par = [&](int jj) { return uint32_t(((g0 + jj) / pp::kNS) & 1); };
+            auto s_load = [&](int jj, uint32_t* s) {  // wait for S of tile jj, start its TMEM load
+                mbar_wait(s_bar(jj), s_par(jj));
                 fence_after();
-                uint32_t sa[KT];
-                ld32(tS, sa);
-                ld32(tS + 32u, sa + 32);
-                wait_ld_dep(sa);
-                wait_ld_dep(sa + 32);
+                ld32(s_col(jj), s);
+                ld32(s_col(jj) + 32u, s + 32);
+            };
+            // one tile whose S is in registers: seam mask, row max, lazy rescale, P, hand-off to P V
+            auto tile = [&](int j, uint32_t* sa) {
+                const int b = (g0 + j) % pp::kNS;
+                const int k = (grp ? cnt1 : cnt0) + (j >> 1) + 1;  // P V products into O[grp] incl. this tile's
+                const uint32_t tS = s_col(j);
                 const int kb = (rg.t_lo + j) * KT;
                 if (kb < rlo || kb + KT > rhi) {  // boundary tile: keys outside [rlo, rhi) get -inf
 #pragma unroll
                     for (int i = 0; i < KT; ++i)
                         if (kb + i < rlo || kb + i >= rhi) sa[i] = __float_as_uint(-INFINITY);
                 }
-                uint32_t pk[KT / 2];
-                float lt;
-                // Speculate on the running max (every lane of the warp has one): the exponentials then do
-                // not wait for this tile's max, which is computed alongside and only checked afterwards;
-                // a tile whose max exceeds the running max by > 2^kRescale (rare after the first tiles)
-                // takes the rescale path and recomputes P.
-                const bool spec = SWF_ATTN_SPEC && __all_sync(0xffffffffu, m != -INFINITY);
-                if (spec) lt = exps(sa, m, pk);
                 const float mx = tile_max(sa);
-                const bool grow = m != -INFINITY && mx > m + kRescale;
-                if (__any_sync(0xffffffffu, grow)) {
+                if (__any_sync(0xffffffffu, m != -INFINITY && mx > m + kRescale)) {
                     // lazy rescale, warp-uniform (tcgen05.ld / st are warp-collective): O[grp] *= 2^(m - m_new)
                     // once this group's previous P V into O[grp] has landed
                     mbar_wait(bar(pp::OD + grp), (k - 2) & 1);
@@ -1179,22 +1168,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
                     if (!(p.dbg & 1)) o_scale<D>(lane_off + pp::kTO + uint32_t(grp * D), f);
                     l *= f;
                     m = mn;
-                    lt = exps(sa, m, pk);
-                } else if (!spec) {
-                    if (m == -INFINITY) m = mx;  // first unmasked keys of this row: O and l are still 0
-                    lt = exps(sa, m, pk);
+                } else if (m == -INFINITY) {
+                    m = mx;  // first unmasked keys of this row: O and l are still 0
                 }
-                l += lt;
-                st16(tS, pk);
-                st16(tS + 16u, pk + 16);
+                l += exps(sa, m, sa);  // P packed in place: pair i reads sa[2i], sa[2i+1], writes sa[i]
+                st16(tS, sa);
+                st16(tS + 16u, sa + 16);
                 wait_st();
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(lbar(pp::PF + b));
                 if (leader) release_q();
+            };
+            // this group's tiles j = grp, grp + 2, ... (prefetching the next S from TMEM during a tile
+            // measured +21% cycles per launch: register pressure; dropped)
+            for (int j = grp; j < rg.ntiles; j += 2) {
+                uint32_t sa[KT];
+                s_load(j, sa);
+                wait_ld_dep(sa);
+                wait_ld_dep(sa + 32);
+                tile(j, sa);
             }
-            cnt[0] += (rg.ntiles + 1) >> 1;
-            cnt[1] += rg.ntiles >> 1;
+            cnt0 += (rg.ntiles + 1) >> 1;
+            cnt1 += rg.ntiles >> 1;
             g = g0 + rg.ntiles;
             // ---- epilogue: merge the two groups' partial softmax states, O / l -> bf16
             red[grp * BQ + r] = m;
@@ -1206,8 +1202,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
             const float inv = 1.f / (l0 * f0 + l1 * f1);
             const bool has1 = rg.ntiles >= 2;  // item-uniform: O1 holds this item's odd tiles
-            mbar_wait(bar(pp::OD + 0), (cnt[0] - 1) & 1);
-            if (has1) mbar_wait(bar(pp::OD + 1), (cnt[1] - 1) & 1);
+            mbar_wait(bar(pp::OD + 0), (cnt0 - 1) & 1);
+            if (has1) mbar_wait(bar(pp::OD + 1), (cnt1 - 1) & 1);
             fence_after();
             const uint32_t tO0 = lane_off + pp::kTO + uint32_t(grp * C::kOC), tO1 = tO0 + uint32_t(D);
             const int qb = n & 1;
