@@ -66,11 +66,12 @@ def class_flops(c: dict, M: int) -> dict:
 
 
 def attention_executed(c: dict, H_: int, W_: int, nloc_frac: float = 1.0) -> dict:
-    """Executed vs algorithmic attention FLOPs per step for the BF16 kernel (k_attn.cu): a work item is
-    a pair of 128-query tiles (M = 256) of one (window, head) over 128-key tiles; the last pair and
+    """Executed vs algorithmic attention FLOPs per step for the BF16 kernel (k_attn_pp, k_attn.cu): a work
+    item is a pair of 128-query tiles (M = 256) of one (window, head) over 64-key tiles; the last pair and
     the last key tile are partly padding, and on the shifted blocks the seam-masked bottom window row
-    skips the key tiles outside each query range (range_of, k_attn.cu). Counts 2 x 2 x 256 x 128 x d
-    per (item, key tile) (QK^T and PV), against perf_model's 4 s w^2 h."""
+    skips the key tiles outside each query range (pp::range_of). Counts 2 x 2 x 256 x 64 x d per (item,
+    key tile) (QK^T and PV), against perf_model's 4 s w^2 h."""
+    KT = 64
     w, h, d = c["window_px"], c["hidden_dim"], c["hidden_dim"] // c["n_heads"]
     s = w * w
     ny, nx = H_ // w, W_ // w
@@ -90,8 +91,8 @@ def attention_executed(c: dict, H_: int, W_: int, nloc_frac: float = 1.0) -> dic
                 qlast = min(qp0 + 256, s) - 1
                 lo = split if (masked and qp0 >= split) else 0
                 hi = split if (masked and qlast < split) else s
-                tiles += -(-hi // 128) - lo // 128
-            ex += nwin * c["n_heads"] * tiles * 2 * 2 * 256 * 128 * d
+                tiles += -(-hi // KT) - lo // KT
+            ex += nwin * c["n_heads"] * tiles * 2 * 2 * 256 * KT * d
     alg = nb * 4.0 * H_ * W_ * s * h
     return {"algorithmic_per_step": alg * nloc_frac, "executed_per_step": ex * nloc_frac, "executed_over_algorithmic": ex / alg}
 
