@@ -47,7 +47,10 @@ using namespace tc;
 // written to $SWF_ATTN_TRACE_OUT after each launch. Per key tile g: 0 S ready, 1 row max exchanged,
 // 2 P stores issued, 3 P stored, 4 P seen by the MMA issuer, 5 P V issued; per item n: 6 MMA saw
 // Q, 7 MMA saw O free, 8 epilogue start, 9 epilogue end; MMA warp per tile: 10 S issue entry,
-// 11 K landed, 12 S issued, 13 P V entry, 14 P seen.
+// 11 K landed, 12 S issued, 13 P V entry, 14 P seen. The ping-pong kernel (tools/attn_pp_trace.py):
+// 1 first global tile of item n, 10/11/12 QK^T issuer entry / K landed / ring slot free, 13/14/15 P V
+// issuer entry / P seen / V landed, 7 O free; per softmax warp w (g_trace_w): w S ready, 8 + w S in
+// registers, 16 + w P handed over; 8 / 9 item epilogue start / end.
 constexpr int kTrN = 1024;
 __device__ unsigned long long g_trace[2][16][kTrN];  // [CTA 0 / 1 of the first cluster]
 __device__ unsigned long long g_trace_w[2][32][kTrN];  // per softmax warp: [cta][warp-4 (S ready) / 8+warp-4 (P done)]
@@ -55,9 +58,16 @@ __device__ unsigned long long g_trace_w[2][32][kTrN];  // per softmax warp: [cta
     do {                                                                                 \
         if (blockIdx.x < 2 && (idx) < kTrN) g_trace[blockIdx.x][row][idx] = clock64(); \
     } while (0)
+#define SWF_TRW(row, idx)                                                                    \
+    do {                                                                                     \
+        if (blockIdx.x < 2 && (idx) < kTrN) g_trace_w[blockIdx.x][row][idx] = clock64();   \
+    } while (0)
 #else
 #define SWF_TR(row, idx) \
     do {                 \
+    } while (0)
+#define SWF_TRW(row, idx) \
+    do {                  \
     } while (0)
 #endif
 
@@ -1037,10 +1047,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             const Range rg = pp::range_of(p, item_of(itx, npairs, p.heads, crank));
             const int qb = n & 1;
             mbar_sleep_wait(bar(pp::QF + qb), (n >> 1) & 1);
+            if (lane == 0) SWF_TR(6, n);
+#ifdef SWF_ATTN_TRACE
+            if (lane == 0 && blockIdx.x < 2 && n < kTrN) g_trace[blockIdx.x][1][n] = (unsigned long long)g;
+#endif
             for (int j = 0; j < rg.ntiles; ++j, ++g) {
                 const int st = g % C::kNK, b = g % pp::kNS;
+                if (lane == 0) SWF_TR(10, g);
                 mbar_sleep_wait(bar(pp::KF + st), (g / C::kNK) & 1);
+                if (lane == 0) SWF_TR(11, g);
                 mbar_sleep_wait(bar(pp::SFREE + b), ((g / pp::kNS) & 1) ^ 1);
+                if (lane == 0) SWF_TR(12, g);
                 fence_after();
                 const uint64_t a0 = desc_kmajor(sQa + uint32_t(qb * C::kQBytes), C::kSw);
                 const uint64_t b0 = desc_kmajor(sKa + uint32_t(st * C::kKHalf), C::kSw);
@@ -1058,8 +1075,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             for (int j = 0; j < rg.ntiles; ++j, ++g) {
                 const int b = g % pp::kNS, vs = g % C::kNV, par = j & 1;
                 if (j == 0 && n >= 1) mbar_sleep_wait(bar(pp::OF), (n - 1) & 1);  // O0 / O1 of the last item read
+                if (j == 0 && lane == 0) SWF_TR(7, n);
+                if (lane == 0) SWF_TR(13, g);
                 mbar_sleep_wait(bar(pp::PF + b), (g / pp::kNS) & 1);
+                if (lane == 0) SWF_TR(14, g);
                 mbar_sleep_wait(bar(pp::VF + vs), (g / C::kNV) & 1);
+                if (lane == 0) SWF_TR(15, g);
                 fence_after();
                 const uint64_t b0 = desc_kmajor(sVa + uint32_t(vs * C::kVHalf), 128);
                 pp::issue_pv(pp::kTO + uint32_t(par * D), uint32_t(b * KT), b0, C::kIdescO, j >= 2 ? 1u : 0u);
@@ -1142,6 +1163,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             auto s_par = [&](int jj) { return uint32_t(((g0 + jj) / pp::kNS) & 1); };
             auto s_load = [&](int jj, uint32_t* s) {  // wait for S of tile jj, start its TMEM load
                 mbar_wait(s_bar(jj), s_par(jj));
+                if (lane == 0) SWF_TRW(warp - 4, g0 + jj);
                 fence_after();
                 ld32(s_col(jj), s);
                 ld32(s_col(jj) + 32u, s + 32);
@@ -1178,6 +1200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(lbar(pp::PF + b));
+                if (lane == 0) SWF_TRW(16 + warp - 4, g0 + j);
                 if (leader) release_q();
             };
             // this group's tiles j = grp, grp + 2, ... (prefetching the next S from TMEM during a tile
@@ -1187,11 +1210,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
                 s_load(j, sa);
                 wait_ld_dep(sa);
                 wait_ld_dep(sa + 32);
+                if (lane == 0) SWF_TRW(8 + warp - 4, g0 + j);
                 tile(j, sa);
             }
             cnt0 += (rg.ntiles + 1) >> 1;
             cnt1 += rg.ntiles >> 1;
             g = g0 + rg.ntiles;
+            if (warp == 4 && lane == 0) SWF_TR(8, n);
             // ---- epilogue: merge the two groups' partial softmax states, O / l -> bf16
             red[grp * BQ + r] = m;
             red[(2 + grp) * BQ + r] = l;
@@ -1279,6 +1304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(lbar(pp::OF));  // O0 / O1 may be overwritten
+            if (warp == 4 && lane == 0) SWF_TR(9, n);
         }
         if (leader && qe_pending >= 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
@@ -1328,8 +1354,9 @@ void launch(const AttnParams& p, cudaStream_t st) {
         SWF_CUDA(cudaMemcpyFromSymbol(h, g_trace, sizeof(h)));
         if (FILE* f = fopen(path, "wb")) {
             fwrite(h, sizeof(h), 1, f);
-            SWF_CUDA(cudaMemcpyFromSymbol(h, g_trace_w, sizeof(h)));
-            fwrite(h, sizeof(h), 1, f);
+            static unsigned long long hw[2][32][kTrN];
+            SWF_CUDA(cudaMemcpyFromSymbol(hw, g_trace_w, sizeof(hw)));
+            fwrite(hw, sizeof(hw), 1, f);
             fclose(f);
         }
     }
