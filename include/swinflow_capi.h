@@ -160,6 +160,13 @@ int swf_forward_device(swf_ctx* ctx, const float* d_input, double t, float* d_ou
  * recomputed from them in the backward (no s x s probabilities are stored). */
 int swf_backward(swf_ctx* ctx, const void* input, double t, const void* d_output, void* grads, void* d_input,
                  int dtype);
+/* Arithmetic of the backward's linears (not a reference interface; the reference backward runs in T,
+ * swin.hpp:370-467): SWF_PREC_FP32 (default, FP32 validation mode, SIMT) or SWF_PREC_BF16 -- the
+ * data and weight gradients of the QKV, out, gate/up and down projections as tcgen05 GEMMs with bf16
+ * operands and fp32 accumulation (weight gradients with MN-major operands, K = tokens). Applies to
+ * swf_backward, swf_diffusion_loss_sample and the training entry points; hidden_dim and ffn_dim must
+ * be multiples of 8. */
+int swf_set_backward_precision(swf_ctx* ctx, int precision);
 
 /* LossWeights (grid.hpp:76-96): alpha_row = per-row latitude weights (H entries, unit mean),
  * kappa = per-variable weights (C_out entries, > 0); element type given by the call's dtype. */
@@ -267,6 +274,11 @@ int swf_op_prenorm_modulate(int device, const float* X, int h, long long n, cons
                             const float* b, const float* gate, float* Y);
 int swf_op_swiglu_fwd(int device, int precision, const float* W_gate, const float* W_up, const float* W_down,
                       int h, int f, const float* X, long long n, float* Y);
+/* Test hook for the backward's tensor-core GEMM (gemm_bf16_general, not a reference interface):
+ * C[M][N] (+)= A . B with A = [M][lda] and B = [N][ldb] (K-major, mn_major = 0) or A = [K][lda] and
+ * B = [K][ldb] (MN-major, mn_major = 1); operands rounded to bf16, fp32 accumulation. */
+int swf_op_gemm_bf16(int device, int mn_major, long long M, long long N, long long K, const float* A, long long lda,
+                     const float* B, long long ldb, float* C, long long ldc, int accumulate);
 /* Run one bf16 GEMM self-test of the tcgen05 kernel: C = A.B^T on device, returns max |err|
  * against an fp32 SIMT product of the same bf16 operands (used by the parity tests). */
 int swf_selftest_gemm(int device, long long M, int N, int K, double* max_abs_err, double* max_ref);

@@ -159,6 +159,8 @@ def lib():
         L.swf_op_linear_cols.argtypes = [i, i, vp, i, i, vp, ll, vp]
         L.swf_op_prenorm_modulate.argtypes = [i, vp, i, ll, vp, vp, vp, vp, vp]
         L.swf_op_swiglu_fwd.argtypes = [i, i, vp, vp, vp, i, i, vp, ll, vp]
+        L.swf_op_gemm_bf16.argtypes = [i, i, ll, ll, ll, vp, ll, vp, ll, vp, ll, i]
+        L.swf_set_backward_precision.argtypes = [vp, i]
         L.swf_backward.argtypes = [vp, vp, d, vp, vp, vp, i]
         L.swf_diffusion_loss_sample.argtypes = [vp, vp, vp, vp, vp, vp, u64, vp, C.POINTER(d), vp, i]
         L.swf_train_accumulate.argtypes = [vp, vp, vp, vp, vp, vp, u64, u64, C.POINTER(d), i]
@@ -260,6 +262,21 @@ class ops:
         Y = np.zeros((n, h), np.float32)
         _check(lib().swf_op_swiglu_fwd(device, precision, *[_p(t) for t in W], h, f, _p(X), n, _p(Y)))
         return Y
+
+    @staticmethod
+    def gemm_bf16(A, B, mn_major: bool, C=None, accumulate: bool = False, device: int = 0):
+        """The backward's tensor-core GEMM: returns C (+)= op(A) . op(B) in fp32 with bf16-rounded operands.
+        K-major: A [M][K], B [N][K] (C = A B^T); MN-major: A [K][M], B [K][N] (C = A^T B)."""
+        A = np.ascontiguousarray(A, np.float32)
+        B = np.ascontiguousarray(B, np.float32)
+        if mn_major:
+            (K, M), N = A.shape, B.shape[1]
+        else:
+            (M, K), N = A.shape, B.shape[0]
+        C = np.zeros((M, N), np.float32) if C is None else np.ascontiguousarray(C, np.float32).copy()
+        _check(lib().swf_op_gemm_bf16(device, int(mn_major), M, N, K, _p(A), A.shape[1], _p(B), B.shape[1], _p(C),
+                                      N, int(accumulate)))
+        return C
 
 
 class Denoiser:
@@ -373,6 +390,11 @@ class Denoiser:
 
     KERNEL_CLASSES = ("encode_gemm", "rms_adaln", "qkv_gemm", "attention", "out_gemm", "gateup_gemm",
                       "down_gemm", "decode_gemm", "other")
+
+    def set_backward_precision(self, precision: int):
+        """PREC_BF16: the backward's linear-layer GEMMs on the tensor cores (bf16 operands, fp32
+        accumulation); PREC_FP32: the FP32 validation mode (default)."""
+        _check(lib().swf_set_backward_precision(self._c, precision))
 
     def set_graphs(self, enable: bool = True):
         """CUDA-graph replay of the sampler's evaluations (default on)."""

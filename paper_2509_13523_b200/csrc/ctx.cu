@@ -153,6 +153,12 @@ struct swf_ctx {
             *rms, *d6, *demb, *zero, *gflat, *din;
     } bw = {};
     bool bw_alloc = false;
+    // swf_set_backward_precision(BF16): the backward's linears on the tensor cores (bf16 operand
+    // copies in bt_a / bt_b, allocated with the work buffers)
+    bool bwd_tc = false;
+    __nv_bfloat16 *bt_a = nullptr, *bt_b = nullptr;
+    float* bt_c = nullptr;  // plain fp32 product of the two-pass linears (gemm_f32_ctx)
+    size_t bt_c_n = 0;
     // diffusion training loss (FP32 validation mode): residual target x0, noise z, velocity target v,
     // loss weights, per-block loss partials, and the gradient accumulator of the training step
     struct Train {
@@ -936,11 +942,27 @@ const TmaMap* tmap_at(const std::vector<TmaMap>& v, int b) { return b < int(v.si
 template <class T>
 struct Gemm;
 
+// FP32-context linear layer. In the BF16 training mode (swf_set_backward_precision(BF16)) the
+// forwards of the training entry points (activations saved) and the backward's recomputation run
+// their GEMMs on the tensor cores: bf16 operands, plain fp32 product, then the same epilogue.
+void gemm_f32_ctx(swf_ctx* c, const float* A, const float* W, i64 M, int Np, int K, int mode, const EpiParams& ep) {
+    if (c->bwd_tc && c->bt_c && K % 8 == 0 && size_t(M) * Np <= c->bt_c_n) {
+        gemm_strided_tc(int(M), Np, K, A, K, 1, W, 1, K, c->bt_c, Np, 0.f, c->bt_a, c->bt_b, c->d_sched, c->st);
+        epi_rows_f32(c->bt_c, Np, M, Np, mode, ep, c->st);
+        c->launches += 4;
+        return;
+    }
+    gemm_f32(A, W, M, Np, K, mode, ep, c->st);
+}
+
 template <>
 struct Gemm<float> {
     static void run(swf_ctx* c, const void* A, const TmaMap*, const void* B, const TmaMap*, i64 M, int Np, int K, int,
                     int mode, const EpiParams& ep) {
-        gemm_f32(static_cast<const float*>(A), static_cast<const float*>(B), M, Np, K, mode, ep, c->st);
+        if (c->save_x)
+            gemm_f32_ctx(c, static_cast<const float*>(A), static_cast<const float*>(B), M, Np, K, mode, ep);
+        else
+            gemm_f32(static_cast<const float*>(A), static_cast<const float*>(B), M, Np, K, mode, ep, c->st);
     }
 };
 template <>
@@ -1260,6 +1282,21 @@ void forward_any(swf_ctx* c, double t, float out_scale) {
 // the backward recomputes each block's internals from it (no s x s probabilities are stored),
 // then runs the reference backward in reverse block order with k_bwd.cu kernels. Weight gradients
 // come out in the reference's canonical order and column-major layout.
+// bf16 operand copies and the plain-product buffer of the BF16 training mode
+void alloc_bwd_tc(swf_ctx* c) {
+    if (c->bt_a) return;
+    const Dims& m = c->m;
+    const size_t M = size_t(c->M);
+    const size_t wide = size_t(std::max({m.np_gu, m.np_qkv, 3 * m.h, m.hp, m.cinp, m.np_dec}));
+    const size_t w_max = std::max({size_t(m.np_gu) * m.hp, size_t(m.np_qkv) * m.hp, size_t(m.f) * m.h,
+                                   size_t(m.np_dec) * m.hp, size_t(m.np_enc) * m.cinp});
+    const size_t n = std::max(M * wide, w_max);
+    c->bt_a = dalloc<__nv_bfloat16>(c, n);
+    c->bt_b = dalloc<__nv_bfloat16>(c, n);
+    c->bt_c_n = M * wide;
+    c->bt_c = dalloc<float>(c, c->bt_c_n);
+}
+
 void ensure_bwd(swf_ctx* c) {
     if (c->bw_alloc) return;
     const Dims& m = c->m;
@@ -1289,6 +1326,7 @@ void ensure_bwd(swf_ctx* c) {
     b.zero = dalloc<float>(c, size_t(m.np_gu) + m.np_dec + 64);
     b.gflat = dalloc<float>(c, c->poff.back());
     b.din = dalloc<float>(c, size_t(M) * m.cin);
+    if (c->bwd_tc) alloc_bwd_tc(c);
     c->bw_alloc = true;
 }
 
@@ -1303,6 +1341,14 @@ void backward_core(swf_ctx* c, const float* dout) {
     auto pa = [&](int ai) { return P + c->poff[ai]; };
     auto ga = [&](int ai) { return G + c->poff[ai]; };
     const int kHead = 2, kPer = 9, tail = kHead + nb * kPer;
+    // the linears' GEMMs: SIMT FP32 (validation mode) or tcgen05 BF16 (swf_set_backward_precision)
+    auto lin = [&](int Mg, int Ng, int Kg, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj, float* C,
+                   i64 ldc, float beta) {
+        if (c->bwd_tc)
+            gemm_strided_tc(Mg, Ng, Kg, A, sai, sak, B, sbk, sbj, C, ldc, beta, c->bt_a, c->bt_b, c->d_sched, st);
+        else
+            gemm_strided_f32(Mg, Ng, Kg, A, sai, sak, B, sbk, sbj, C, ldc, beta, st);
+    };
     // WP: every rank's gradients are partial sums over its tokens (all-reduced by the caller); no
     // rank may store into a peer's landing buffer while that peer still runs its forward
     if (c->world > 1) peer_barrier(c);
@@ -1331,7 +1377,7 @@ void backward_core(swf_ctx* c, const float* dout) {
         e.out = c->qkv;
         e.plane = i64(c->lay[par].nloc) * m.heads * m.w * m.w * m.d;
         e.N = 3 * h;
-        gemm_f32(bw.xm1, static_cast<const float*>(c->w_qkv[b]), M, m.np_qkv, hp, EPI_QKV, e, st);
+        gemm_f32_ctx(c, bw.xm1, static_cast<const float*>(c->w_qkv[b]), M, m.np_qkv, hp, EPI_QKV, e);
         const float* q = static_cast<const float*>(c->qkv);
         const float* kk = q + size_t(M) * h;
         const float* v = q + size_t(2) * M * h;
@@ -1354,7 +1400,7 @@ void backward_core(swf_ctx* c, const float* dout) {
         e = ep;
         e.x = bw.xmid;
         e.N = h;
-        gemm_f32(bw.obuf, static_cast<const float*>(c->w_out[b]), M, m.np_out, hp, EPI_RESID, e, st);
+        gemm_f32_ctx(c, bw.obuf, static_cast<const float*>(c->w_out[b]), M, m.np_out, hp, EPI_RESID, e);
         rms_modulate<float>(bw.xmid, M, h, hp, c->g_ffn + size_t(b) * h, six + 3 * h, six + 4 * h, six + 5 * h, bw.x2m,
                             nullptr, 0, st);
         e = ep;
@@ -1362,7 +1408,7 @@ void backward_core(swf_ctx* c, const float* dout) {
         e.ld_out = m.np_gu;
         e.N = m.np_gu;
         e.bias = bw.zero;
-        gemm_f32(bw.x2m, static_cast<const float*>(c->w_gu[b]), M, m.np_gu, hp, EPI_DECODE, e, st);
+        gemm_f32_ctx(c, bw.x2m, static_cast<const float*>(c->w_gu[b]), M, m.np_gu, hp, EPI_DECODE, e);
         // ---- backward (block_window_backward, swin.hpp:370-417)
         float* dXp = bw.dtmp;  // output gradient in this block's layout
         if (c->world > 1) {    // WP: owners change between the layouts -> peer stores, then a barrier
@@ -1374,26 +1420,26 @@ void backward_core(swf_ctx* c, const float* dout) {
             relayout_rows(bw.dx[cur], c->lay[npar], c->lay[par], M, h, dXp, st);
         }
         // feed-forward branch: swiglu_bwd (:236-252)
-        gemm_strided_f32(int(M), f, h, dXp, h, 1, pa(base + 6), 1, h, bw.dS, f, 0.f, st);
+        lin(int(M), f, h, dXp, h, 1, pa(base + 6), 1, h, bw.dS, f, 0.f);
         swiglu_bwd(bw.gu, m.np_gu, bw.dS, f, M, f, m.G, bw.act, bw.dG, bw.dU, st);
-        gemm_strided_f32(f, h, int(M), bw.act, 1, f, dXp, h, 1, ga(base + 6), h, 1.f, st);     // dW_down
-        gemm_strided_f32(h, f, int(M), bw.x2m, 1, hp, bw.dG, f, 1, ga(base + 4), f, 1.f, st);  // dW_gate
-        gemm_strided_f32(h, f, int(M), bw.x2m, 1, hp, bw.dU, f, 1, ga(base + 5), f, 1.f, st);  // dW_up
-        gemm_strided_f32(int(M), h, f, bw.dG, f, 1, pa(base + 4), 1, f, bw.dxm, h, 0.f, st);
-        gemm_strided_f32(int(M), h, f, bw.dU, f, 1, pa(base + 5), 1, f, bw.dxm, h, 1.f, st);
+        lin(f, h, int(M), bw.act, 1, f, dXp, h, 1, ga(base + 6), h, 1.f);     // dW_down
+        lin(h, f, int(M), bw.x2m, 1, hp, bw.dG, f, 1, ga(base + 4), f, 1.f);  // dW_gate
+        lin(h, f, int(M), bw.x2m, 1, hp, bw.dU, f, 1, ga(base + 5), f, 1.f);  // dW_up
+        lin(int(M), h, f, bw.dG, f, 1, pa(base + 4), 1, f, bw.dxm, h, 0.f);
+        lin(int(M), h, f, bw.dU, f, 1, pa(base + 5), 1, f, bw.dxm, h, 1.f);
         SWF_CUDA(cudaMemsetAsync(bw.d6, 0, size_t(6) * h * 4, st));
         float* dxmid = bw.dx[cur ^ 1];
         SWF_CUDA(cudaMemcpyAsync(dxmid, dXp, size_t(M) * h * 4, cudaMemcpyDeviceToDevice, st));
         norm_bwd(bw.xmid, h, bw.dxm, h, M, h, c->g_ffn + size_t(b) * h, six + 3 * h, six + 4 * h, six + 5 * h, dxmid,
                  h, bw.rms, ga(base + 3), bw.d6 + 3 * h, bw.d6 + 4 * h, bw.d6 + 5 * h, st);
         // attention branch: out projection, head_attention_bwd (:189-226), prenorm_modulate_bwd
-        gemm_strided_f32(h, h, int(M), bw.obuf, 1, hp, dxmid, h, 1, ga(base + 1), h, 1.f, st);  // dW_out
-        gemm_strided_f32(int(M), h, h, dxmid, h, 1, pa(base + 1), 1, h, bw.dO, hp, 0.f, st);
+        lin(h, h, int(M), bw.obuf, 1, hp, dxmid, h, 1, ga(base + 1), h, 1.f);  // dW_out
+        lin(int(M), h, h, dxmid, h, 1, pa(base + 1), 1, h, bw.dO, hp, 0.f);
         float* dq = bw.dplanes;
         attention_bwd_f32(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h, bw.stats,
                           c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, st);
-        gemm_strided_f32(h, 3 * h, int(M), bw.xm1, 1, hp, bw.dqkv, 3 * h, 1, ga(base + 0), 3 * h, 1.f, st);  // dW_qkv
-        gemm_strided_f32(int(M), h, 3 * h, bw.dqkv, 3 * h, 1, pa(base + 0), 1, 3 * h, bw.dxm, h, 0.f, st);
+        lin(h, 3 * h, int(M), bw.xm1, 1, hp, bw.dqkv, 3 * h, 1, ga(base + 0), 3 * h, 1.f);  // dW_qkv
+        lin(int(M), h, 3 * h, bw.dqkv, 3 * h, 1, pa(base + 0), 1, 3 * h, bw.dxm, h, 0.f);
         // dx_in = dx_mid + prenorm_modulate_bwd(...) -- accumulated in place in dxmid
         norm_bwd(xb, h, bw.dxm, h, M, h, c->g_attn + size_t(b) * h, six, six + h, six + 2 * h, dxmid, h, bw.rms,
                  ga(base + 2), bw.d6, bw.d6 + h, bw.d6 + 2 * h, st);
@@ -3015,6 +3061,22 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
         cudaEventDestroy(a);
         cudaEventDestroy(b);
         *ms = double(t) / reps;
+    })
+}
+
+int swf_set_backward_precision(swf_ctx* c, int precision) {
+    SWF_FANOUT(c, swf_set_backward_precision(r_, precision));
+    SWF_API_TRY({
+        require(c, "null context");
+        require(precision == SWF_PREC_BF16 || precision == SWF_PREC_FP32,
+                "backward precision must be SWF_PREC_BF16 or SWF_PREC_FP32");
+        const bool tc = precision == SWF_PREC_BF16;
+        if (tc)
+            require(c->m.h % 8 == 0 && c->m.f % 8 == 0,
+                    "BF16 backward: hidden_dim and ffn_dim must be multiples of 8 (16-byte operand rows)");
+        SWF_CUDA(cudaStreamSynchronize(c->st));
+        c->bwd_tc = tc;
+        if (tc && c->bw_alloc) alloc_bwd_tc(c);  // work buffers exist already: add the operand copies
     })
 }
 

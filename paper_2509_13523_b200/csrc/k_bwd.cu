@@ -10,6 +10,10 @@
 //     results are deterministic, no atomics);
 //   * attention backward recomputes P from q, k and the stored row statistics: a query-major pass
 //     (dQ, and D_i = dO_i . O_i) and a key-major pass (dK, dV), then the inverse RoPE rotation.
+// With swf_set_backward_precision(BF16) the linears' GEMMs run on the tensor cores instead
+// (gemm_strided_tc: bf16 operands, fp32 accumulation).
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace swf {
@@ -565,6 +569,35 @@ void gemm_strided_f32(int M, int N, int K, const float* A, i64 sai, i64 sak, con
     dim3 grid(unsigned((N + GB - 1) / GB), unsigned((M + GB - 1) / GB));
     k_gemm_strided<<<grid, 256, 0, st>>>(M, N, K, A, sai, sak, B, sbk, sbj, C, ldc, beta);
     SWF_LAUNCH_CHECK();
+}
+__global__ void k_to_bf16(const float* __restrict__ x, i64 n, __nv_bfloat16* __restrict__ y) {
+    const i64 n4 = n >> 2;
+    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += i64(gridDim.x) * blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+        reinterpret_cast<uint2*>(y)[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+    }
+    for (i64 i = 4 * n4 + i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+        y[i] = __float2bfloat16_rn(x[i]);
+}
+void to_bf16(const float* x, i64 n, __nv_bfloat16* y, cudaStream_t st) {
+    if (n <= 0) return;
+    if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) throw CudaError("to_bf16: source must be 16-byte aligned");
+    const i64 blocks = std::min<i64>((n / 4 + 255) / 256 + 1, 148 * 16);
+    k_to_bf16<<<unsigned(blocks), 256, 0, st>>>(x, n, y);
+    SWF_LAUNCH_CHECK();
+}
+// gemm_strided_f32's product on the tensor cores: the FP32 operands are rounded to bf16 copies in ta /
+// tb (same layout) and multiplied by one tcgen05 GEMM with FP32 accumulation. The backward's linears
+// take this path when it runs in BF16 (swf_set_backward_precision): data gradients with both operands
+// K-major, weight gradients (K = tokens) with both MN-major, straight from the row-major activations.
+void gemm_strided_tc(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj, float* C,
+                     i64 ldc, float beta, __nv_bfloat16* ta, __nv_bfloat16* tb, int* sched, cudaStream_t st) {
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    const bool a_mn = sai == 1 && sak != 1, b_mn = sbj == 1 && sbk != 1;
+    const i64 lda = a_mn ? sak : sai, ldb = b_mn ? sbk : sbj;
+    to_bf16(A, a_mn ? i64(K) * lda : i64(M) * lda, ta, st);
+    to_bf16(B, b_mn ? i64(K) * ldb : i64(N) * ldb, tb, st);
+    gemm_bf16_general(ta, a_mn, lda, tb, b_mn, ldb, M, N, K, C, ldc, beta != 0.f, sched, st);
 }
 void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h, const float* g, const float* a,
               const float* b, const float* gate, float* dX, int lddx, float* rms, float* dg, float* da, float* db,

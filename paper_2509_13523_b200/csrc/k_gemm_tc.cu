@@ -7,6 +7,7 @@
 //   residual add + next-layout window permutation of the down projection (swin.hpp:306-366).
 #include <cuda.h>
 
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -132,6 +133,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
            | (uint64_t(1024 >> 4) << 32)                          // SBO: 8 rows x 128 B
            | (uint64_t(1) << 46)                                  // sm100 descriptor version
            | (uint64_t(2) << 61);                                 // SWIZZLE_128B
+}
+// MN-major SW128 operand (the backward's weight gradients: tokens = K run along the rows of a TMA box
+// [K rows][64 MN elements]): 64-element MN chunks LBO = one box (64 rows x 128 B) apart, 8-row K
+// groups SBO = 1024 B apart; a K step of 16 advances the start by 16 rows (2048 B)
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((BK * 128) >> 4) << 16)  // LBO: next 64-wide MN chunk
+           | (uint64_t(1024 >> 4) << 32)                                        // SBO: next 8 K rows
+           | (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 __device__ __forceinline__ void umma_2cta(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -390,7 +399,9 @@ struct TileQueue {
 };
 
 // ---------------------------------------------------------------- the kernel
-template <int BN, int MODE>
+// MN: operand majors, bit 0 = A MN-major (A stored [K][M]), bit 1 = B MN-major (B stored [K][N]); 0 =
+// both K-major (the forward's layout)
+template <int BN, int MODE, int MN = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, i64 M, int n_tiles,
               int num_k, EpiParams ep, int* sched, int group_m) {
@@ -467,8 +478,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = map_to_rank(smem_u32(&full_bar[stage]), 0);
                     if (leader) mbar_expect_tx(smem_u32(&full_bar[stage]), 2 * C::kStage);
-                    tma_load_2cta(smem_u32(sA + stage * C::kStageA), &tmA, fb, kb * BK, row_a, pol_a);
-                    tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK, row_b, pol_b);
+                    if constexpr (MN & 1) {  // [64 K rows][64 M] boxes, BM / 64 of them
+#pragma unroll
+                        for (int c = 0; c < BM / 64; ++c)
+                            tma_load_2cta(smem_u32(sA + stage * C::kStageA + c * BK * 128), &tmA, fb, row_a + 64 * c,
+                                          kb * BK, pol_a);
+                    } else {
+                        tma_load_2cta(smem_u32(sA + stage * C::kStageA), &tmA, fb, kb * BK, row_a, pol_a);
+                    }
+                    if constexpr (MN & 2) {
+#pragma unroll
+                        for (int c = 0; c < BN / 128; ++c)
+                            tma_load_2cta(smem_u32(sB + stage * C::kStageB + c * BK * 128), &tmB, fb, row_b + 64 * c,
+                                          kb * BK, pol_b);
+                    } else {
+                        tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK, row_b, pol_b);
+                    }
                     // the next tile is taken once this tile's first stage is in flight, so the
                     // atomic's round trip overlaps the loads (one tile ahead of every consumer)
                     if (sched_here && kb == 0) tq.publish(i + 1);
@@ -496,9 +521,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * C::kStageA);
                     const uint32_t b0 = smem_u32(sB + stage * C::kStageB);
+                    constexpr uint32_t kIdesc = C::kIdesc | (uint32_t(MN & 1) << 15) | (uint32_t((MN >> 1) & 1) << 16);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        umma_2cta(dtm, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), C::kIdesc,
+                        umma_2cta(dtm, (MN & 1) ? umma_desc_sw128_mn(a0 + k * 2048) : umma_desc_sw128(a0 + k * 32),
+                                  (MN & 2) ? umma_desc_sw128_mn(b0 + k * 2048) : umma_desc_sw128(b0 + k * 32), kIdesc,
                                   (kb | k) != 0);
                     umma_commit_mc(smem_u32(&empty_bar[stage]), 0x3);
                     if (++stage == C::kStages) {
@@ -533,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // floats per row) into L2 while the accumulator is computed, so the epilogue's loads hit L2
             // (A/B: out GEMM -4%; for the down projection's long K the lines are evicted before use)
             if constexpr (MODE == EPI_RESID)
-                if (row < ep.M) {
+                if (row < ep.M && n_blk * BN + (half + 1) * (BN / 2) <= ep.N) {
                     const float* xr = ep.x + row * ep.h + n_blk * BN + half * (BN / 2);
 #pragma unroll
                     for (int c = 0; c < BN / 64; ++c)
@@ -669,10 +696,10 @@ int* sched_counter() {
     return ctr[dev];
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, int MN = 0>
 void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiParams& ep, cudaStream_t st) {
     using C = Cfg<BN>;
-    auto kern = k_gemm_tc<BN, MODE>;  // shared-memory limit set per device by preload_gemm_kernels
+    auto kern = k_gemm_tc<BN, MODE, MN>;  // shared-memory limit set per device by preload_gemm_kernels
     const int n_tiles = Npad / BN;
     const i64 m_tiles = (M + 2 * BM - 1) / (2 * BM);
     const i64 total = m_tiles * n_tiles;
@@ -756,7 +783,8 @@ template <int BN>
 void preload_bn(cudaFuncAttributes& a) {
     const void* k[] = {(const void*)k_gemm_tc<BN, EPI_ENCODE>, (const void*)k_gemm_tc<BN, EPI_QKV>,
                        (const void*)k_gemm_tc<BN, EPI_RESID>, (const void*)k_gemm_tc<BN, EPI_SWIGLU>,
-                       (const void*)k_gemm_tc<BN, EPI_DOWN>, (const void*)k_gemm_tc<BN, EPI_DECODE>};
+                       (const void*)k_gemm_tc<BN, EPI_DOWN>, (const void*)k_gemm_tc<BN, EPI_DECODE>,
+                       (const void*)k_gemm_tc<BN, EPI_RESID, 3>};
     for (const void* f : k) {
         SWF_CUDA(cudaFuncGetAttributes(&a, f));
         SWF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem));
@@ -766,6 +794,53 @@ void preload_gemm_kernels() {
     cudaFuncAttributes a;
     preload_bn<128>(a);
     preload_bn<256>(a);
+}
+
+// bf16 [rows][inner] operand with row pitch `pitch` elements, box {64, box_rows}, 128-byte swizzle;
+// reads beyond `inner` / `rows` are zero filled (K and MN tails)
+void make_tma_bf16_pitch(TmaMap* m, const void* base, i64 rows, i64 inner, i64 pitch, int box_rows) {
+    if ((pitch * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0)
+        throw CudaError("make_tma_bf16_pitch: row pitch and base must be 16-byte aligned");
+    cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(pitch) * 2};
+    cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(reinterpret_cast<CUtensorMap*>(m), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (pitch) failed: " + std::to_string(int(r)));
+}
+
+void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bfloat16* B, bool b_mn, i64 ldb, i64 M,
+                       i64 N, i64 K, float* C, i64 ldc, bool accumulate, int* sched, cudaStream_t st) {
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    if (a_mn != b_mn) throw CudaError("gemm_bf16_general: mixed operand majors are not instantiated");
+    if (!accumulate) SWF_CUDA(cudaMemset2DAsync(C, size_t(ldc) * 4, 0, size_t(N) * 4, size_t(M), st));
+    const int BN = N > 128 ? 256 : 128;
+    TmaMap ta, tb;
+    if (a_mn)
+        make_tma_bf16_pitch(&ta, A, K, M, lda, BK);
+    else
+        make_tma_bf16_pitch(&ta, A, M, K, lda, BM);
+    if (b_mn)
+        make_tma_bf16_pitch(&tb, B, K, N, ldb, BK);
+    else
+        make_tma_bf16_pitch(&tb, B, N, K, ldb, BN / 2);
+    EpiParams ep;
+    std::memset(&ep, 0, sizeof ep);
+    ep.M = M;
+    ep.N = int(N);
+    ep.x = C;
+    ep.h = int(ldc);
+    ep.out_scale = 1.f;
+    ep.sched = sched;
+    const int Kp = int((K + BK - 1) / BK * BK);
+    const int Np = int((N + BN - 1) / BN * BN);
+    if (BN == 256)
+        a_mn ? launch<256, EPI_RESID, 3>(ta, tb, M, Np, Kp, ep, st) : launch<256, EPI_RESID, 0>(ta, tb, M, Np, Kp, ep, st);
+    else
+        a_mn ? launch<128, EPI_RESID, 3>(ta, tb, M, Np, Kp, ep, st) : launch<128, EPI_RESID, 0>(ta, tb, M, Np, Kp, ep, st);
 }
 
 void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int BN, int mode, const EpiParams& ep,

@@ -203,6 +203,38 @@ void gemm_f32(const float* A, const float* B, i64 M, int N, int K, int mode, con
     SWF_LAUNCH_CHECK();
 }
 
+// The SIMT GEMM's epilogue applied to a product computed elsewhere (the tensor cores): C is the plain
+// [M][ldc] fp32 product A . W^T with the same column layout (interleave G = 4 for SWIGLU).
+template <int MODE>
+__global__ void k_epi_rows(const float* __restrict__ Cm, int ldc, i64 M, int N, EpiParams ep) {
+    const int nch = (N + 7) / 8;
+    for (i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x; t < M * nch; t += i64(gridDim.x) * blockDim.x) {
+        const i64 m = t / nch;
+        const int nc = int(t - m * nch) * 8;
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = nc + j < N ? Cm[m * ldc + nc + j] : 0.f;
+        if constexpr (MODE == EPI_SWIGLU)
+            epi_swiglu<float, 4>(ep, m, nc / 2, &v[0], &v[4]);
+        else
+            epi_apply<MODE, float, 8>(ep, m, nc, v);
+    }
+}
+void epi_rows_f32(const float* Cm, int ldc, i64 M, int N, int mode, const EpiParams& ep, cudaStream_t st) {
+    const i64 work = M * ((N + 7) / 8);
+    const unsigned grid = unsigned(std::min<i64>((work + 255) / 256, 148 * 16));
+    switch (mode) {
+        case EPI_ENCODE: k_epi_rows<EPI_ENCODE><<<grid, 256, 0, st>>>(Cm, ldc, M, N, ep); break;
+        case EPI_QKV: k_epi_rows<EPI_QKV><<<grid, 256, 0, st>>>(Cm, ldc, M, N, ep); break;
+        case EPI_RESID: k_epi_rows<EPI_RESID><<<grid, 256, 0, st>>>(Cm, ldc, M, N, ep); break;
+        case EPI_SWIGLU: k_epi_rows<EPI_SWIGLU><<<grid, 256, 0, st>>>(Cm, ldc, M, N, ep); break;
+        case EPI_DOWN: k_epi_rows<EPI_DOWN><<<grid, 256, 0, st>>>(Cm, ldc, M, N, ep); break;
+        case EPI_DECODE: k_epi_rows<EPI_DECODE><<<grid, 256, 0, st>>>(Cm, ldc, M, N, ep); break;
+        default: throw CudaError("epi_rows_f32: bad epilogue mode");
+    }
+    SWF_LAUNCH_CHECK();
+}
+
 void attention_f32(const AttnParams& p, cudaStream_t st) {
     if (p.d > 16 * ADW) throw CudaError("attention (FP32 mode): head dim must be <= 128");
     const size_t smem = (2 * size_t(AT) * (p.d + 1) + AT * (AT + 1)) * sizeof(float);

@@ -129,6 +129,8 @@ void inv_rms(const float* ss, i64 M, int nss, int h, float* inv_r, int* flags, i
 // C[M][N] = A[M][K] . B[N][K]^T (both K-major), fp32 SIMT -- the FP32 validation mode GEMM.
 void gemm_f32(const float* A, const float* B, i64 M, int N, int K, int mode, const EpiParams& ep,
               cudaStream_t st);
+// gemm_f32's epilogue `mode` applied row-wise to a plain fp32 product C = A . B^T ([M][ldc])
+void epi_rows_f32(const float* C, int ldc, i64 M, int N, int mode, const EpiParams& ep, cudaStream_t st);
 
 // TMA descriptor (CUtensorMap, 128 B) of a row-major bf16 [rows][kcols] operand, box = box_rows x 64
 // with 128-byte swizzle (the canonical K-major SW128 UMMA layout).
@@ -144,6 +146,11 @@ void make_tma_bf16_2d(TmaMap* m, const void* base, i64 rows, i64 inner, int box_
 // A = [M][K] (box 128 rows), B = [Npad][K] (box BN/2 rows), BN in {128, 256}, K % 64 == 0.
 void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int BN, int mode, const EpiParams& ep,
                   cudaStream_t st);
+// General tensor-core GEMM of the backward: C[M][N] (fp32, row pitch ldc) (+)= A . B with bf16
+// operands, A K-major (A[m * lda + k]) or MN-major (A[k * lda + m]), B K-major (B[n * ldb + k]) or
+// MN-major (B[k * ldb + n]) -- both K-major or both MN-major; pitches multiples of 8 elements.
+void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bfloat16* B, bool b_mn, i64 ldb, i64 M,
+                       i64 N, i64 K, float* C, i64 ldc, bool accumulate, int* sched, cudaStream_t st);
 
 // ------------------------------------------------------------------ attention
 struct AttnParams {
@@ -173,6 +180,9 @@ void attention_bf16(const AttnParams& p, cudaStream_t st);
 // C[i][j] = beta C[i][j] + sum_k A[i*sai + k*sak] B[k*sbk + j*sbj]
 void gemm_strided_f32(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj,
                       float* C, i64 ldc, float beta, cudaStream_t st);
+void to_bf16(const float* x, i64 n, __nv_bfloat16* y, cudaStream_t st);
+void gemm_strided_tc(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj, float* C,
+                     i64 ldc, float beta, __nv_bfloat16* ta, __nv_bfloat16* tb, int* sched, cudaStream_t st);
 // prenorm_modulate_bwd / prenorm_plain_bwd (a, b, gate null): dX += ..., per-channel grads +=
 void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h, const float* g, const float* a,
               const float* b, const float* gate, float* dX, int lddx, float* rms, float* dg, float* da, float* db,

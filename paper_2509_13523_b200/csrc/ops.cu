@@ -182,4 +182,28 @@ int swf_op_swiglu_fwd(int device, int precision, const float* W_gate, const floa
     });
 }
 
+// The backward's tensor-core GEMM on host buffers (test hook for gemm_bf16_general): C[M][N] (+)= A . B,
+// A = [M][lda] K-major or [K][lda] MN-major, B = [N][ldb] K-major or [K][ldb] MN-major, operands
+// rounded to bf16, fp32 accumulation.
+int swf_op_gemm_bf16(int device, int mn_major, long long M, long long N, long long K, const float* A, long long lda,
+                     const float* B, long long ldb, float* Cm, long long ldc, int accumulate) {
+    return op_try([&] {
+        need(A && B && Cm && M > 0 && N > 0 && K > 0, "gemm_bf16: bad argument");
+        need(lda % 8 == 0 && ldb % 8 == 0 && ldc >= N, "gemm_bf16: operand pitches must be multiples of 8");
+        SWF_CUDA(cudaSetDevice(device));
+        ensure_device(device);
+        const size_t na = size_t(mn_major ? K : M) * lda, nb = size_t(mn_major ? K : N) * ldb, nc = size_t(M) * ldc;
+        DevBuf da(na * 4), db(nb * 4), dc(nc * 4), ta(na * 2), tb(nb * 2), sched(64);
+        SWF_CUDA(cudaMemcpy(da.p, A, na * 4, cudaMemcpyHostToDevice));
+        SWF_CUDA(cudaMemcpy(db.p, B, nb * 4, cudaMemcpyHostToDevice));
+        SWF_CUDA(cudaMemcpy(dc.p, Cm, nc * 4, cudaMemcpyHostToDevice));
+        to_bf16(da.as<float>(), i64(na), ta.as<__nv_bfloat16>(), nullptr);
+        to_bf16(db.as<float>(), i64(nb), tb.as<__nv_bfloat16>(), nullptr);
+        gemm_bf16_general(ta.as<__nv_bfloat16>(), mn_major != 0, lda, tb.as<__nv_bfloat16>(), mn_major != 0, ldb, M, N,
+                          K, dc.as<float>(), ldc, accumulate != 0, sched.as<int>(), nullptr);
+        SWF_CUDA(cudaDeviceSynchronize());
+        SWF_CUDA(cudaMemcpy(Cm, dc.p, nc * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
 }  // extern "C"
