@@ -150,7 +150,7 @@ struct swf_ctx {
     float* xsave = nullptr;
     struct Bwd {
         float *dx[2], *dtmp, *xmid, *dxm, *xm1, *obuf, *x2m, *dO, *gu, *act, *dS, *dG, *dU, *dqkv, *dplanes, *stats,
-            *rms, *d6, *demb, *zero, *gflat, *din;
+            *rms, *d6, *demb, *zero, *gflat, *din, *npart;
     } bw = {};
     bool bw_alloc = false;
     // swf_set_backward_precision(BF16): the backward's linears on the tensor cores (bf16 operand
@@ -159,6 +159,10 @@ struct swf_ctx {
     __nv_bfloat16 *bt_a = nullptr, *bt_b = nullptr;
     float* bt_c = nullptr;  // plain fp32 product of the two-pass linears (gemm_f32_ctx)
     size_t bt_c_n = 0;
+    // tensor-core attention of the BF16 training mode: bf16 q / k planes + V^T, bf16 output rows
+    __nv_bfloat16 *bt_qkv = nullptr, *bt_o = nullptr;
+    void** d_bt_o = nullptr;
+    TmaMap bt_tm_q, bt_tm_k, bt_tm_k2, bt_tm_vt, bt_tm_o;
     // diffusion training loss (FP32 validation mode): residual target x0, noise z, velocity target v,
     // loss weights, per-block loss partials, and the gradient accumulator of the training step
     struct Train {
@@ -942,6 +946,8 @@ const TmaMap* tmap_at(const std::vector<TmaMap>& v, int b) { return b < int(v.si
 template <class T>
 struct Gemm;
 
+void attention_ctx(swf_ctx* c, const AttnParams& ap);
+
 // FP32-context linear layer. In the BF16 training mode (swf_set_backward_precision(BF16)) the
 // forwards of the training entry points (activations saved) and the backward's recomputation run
 // their GEMMs on the tensor cores: bf16 operands, plain fp32 product, then the same epilogue.
@@ -1122,7 +1128,7 @@ void run_block(swf_ctx* c, int b, int cur, const LayMap& L, const LayMap& Lnext,
     {
         ProfScope ps(c, K_ATTN);
         if constexpr (sizeof(T) == 4)
-            attention_f32(ap, c->st);
+            attention_ctx(c, ap);
         else
             attention_bf16(ap, c->st);
     }
@@ -1295,6 +1301,51 @@ void alloc_bwd_tc(swf_ctx* c) {
     c->bt_b = dalloc<__nv_bfloat16>(c, n);
     c->bt_c_n = M * wide;
     c->bt_c = dalloc<float>(c, c->bt_c_n);
+    if (c->world == 1 && (m.d == 32 || m.d == 64 || m.d == 128)) {
+        c->bt_qkv = dalloc<__nv_bfloat16>(c, size_t(3) * M * m.h);
+        c->bt_o = dalloc<__nv_bfloat16>(c, M * size_t(m.hp));
+        c->d_bt_o = dalloc<void*>(c, 1);
+        void* o = c->bt_o;
+        h2d_sync(c, c->d_bt_o, &o, sizeof(void*));
+        const int sw = m.d >= 64 ? 128 : 2 * m.d;
+        const i64 rows = i64(c->lay[0].nloc) * m.heads * m.w * m.w;
+        const __nv_bfloat16* qb = c->bt_qkv;
+        make_tma_bf16_2d(&c->bt_tm_q, qb, rows, m.d, sw / 2, 128, sw);
+        make_tma_bf16_2d(&c->bt_tm_k, qb + M * m.h, rows, m.d, sw / 2, 64, sw);
+        make_tma_bf16_2d(&c->bt_tm_k2, qb + M * m.h, rows, m.d, sw / 2, 32, sw);
+        make_tma_bf16_2d(&c->bt_tm_vt, qb + 2 * M * m.h, i64(c->lay[0].nloc) * m.heads * m.d, i64(m.w) * m.w, 64,
+                         m.d / 2, 128);
+        make_tma_bf16(&c->bt_tm_o, c->bt_o, i64(M), m.hp, 128);
+    }
+}
+
+// FP32-context attention. The BF16 training mode runs the tensor-core kernel (k_attn_pp) on bf16
+// copies of q, k and V^T and widens its bf16 output; the FP32 validation mode runs the SIMT kernel.
+void attention_ctx(swf_ctx* c, const AttnParams& ap) {
+    if (!(c->bwd_tc && c->save_x && c->bt_qkv)) {
+        attention_f32(ap, c->st);
+        return;
+    }
+    const Dims& m = c->m;
+    const i64 M = c->M;
+    const i64 planes = i64(ap.nloc) * ap.heads;
+    to_bf16(static_cast<const float*>(ap.q), 2 * M * m.h, c->bt_qkv, c->st);  // q and k planes are adjacent
+    vt_bf16(static_cast<const float*>(ap.v), planes, ap.s, ap.d, c->bt_qkv + 2 * M * m.h, c->st);
+    AttnParams b = ap;
+    b.q = c->bt_qkv;
+    b.k = c->bt_qkv + M * m.h;
+    b.v = c->bt_qkv + 2 * M * m.h;
+    b.o_dst = c->d_bt_o;
+    b.ldo = m.hp;
+    b.head0 = 0;
+    b.tmq = &c->bt_tm_q;
+    b.tmk = &c->bt_tm_k;
+    b.tmk2 = &c->bt_tm_k2;
+    b.tmv = &c->bt_tm_vt;
+    b.tmo = &c->bt_tm_o;
+    attention_bf16(b, c->st);
+    to_f32(c->bt_o, M * m.hp, static_cast<float*>(ap.o), c->st);
+    c->launches += 4;
 }
 
 void ensure_bwd(swf_ctx* c) {
@@ -1326,6 +1377,7 @@ void ensure_bwd(swf_ctx* c) {
     b.zero = dalloc<float>(c, size_t(m.np_gu) + m.np_dec + 64);
     b.gflat = dalloc<float>(c, c->poff.back());
     b.din = dalloc<float>(c, size_t(M) * m.cin);
+    b.npart = dalloc<float>(c, size_t(kNormSlices) * 4 * m.h);
     if (c->bwd_tc) alloc_bwd_tc(c);
     c->bw_alloc = true;
 }
@@ -1362,7 +1414,7 @@ void backward_core(swf_ctx* c, const float* dout) {
     gemm_strided_f32(int(M), h, m.cout, dout, m.cout, 1, pa(tail + 3), 1, m.cout, bw.dtmp, h, 0.f, st);
     SWF_CUDA(cudaMemsetAsync(bw.dx[0], 0, size_t(M) * h * 4, st));
     norm_bwd(xf, h, bw.dtmp, h, M, h, c->g_dec, nullptr, nullptr, nullptr, bw.dx[0], h, bw.rms, ga(tail + 2), nullptr,
-             nullptr, nullptr, st);
+             nullptr, nullptr, bw.npart, st);
     int cur = 0;  // bw.dx[cur]: gradient of the current block's output, in that output's layout
     EpiParams ep = base_ep(c);
     for (int b = nb - 1; b >= 0; --b) {
@@ -1395,7 +1447,7 @@ void backward_core(swf_ctx* c, const float* dout) {
         ap.w = m.w;
         ap.lay = c->lay[par];
         ap.scale = 1.0f / std::sqrt(float(m.d));
-        attention_f32(ap, st);
+        attention_ctx(c, ap);
         SWF_CUDA(cudaMemcpyAsync(bw.xmid, xb, size_t(M) * h * 4, cudaMemcpyDeviceToDevice, st));
         e = ep;
         e.x = bw.xmid;
@@ -1431,7 +1483,7 @@ void backward_core(swf_ctx* c, const float* dout) {
         float* dxmid = bw.dx[cur ^ 1];
         SWF_CUDA(cudaMemcpyAsync(dxmid, dXp, size_t(M) * h * 4, cudaMemcpyDeviceToDevice, st));
         norm_bwd(bw.xmid, h, bw.dxm, h, M, h, c->g_ffn + size_t(b) * h, six + 3 * h, six + 4 * h, six + 5 * h, dxmid,
-                 h, bw.rms, ga(base + 3), bw.d6 + 3 * h, bw.d6 + 4 * h, bw.d6 + 5 * h, st);
+                 h, bw.rms, ga(base + 3), bw.d6 + 3 * h, bw.d6 + 4 * h, bw.d6 + 5 * h, bw.npart, st);
         // attention branch: out projection, head_attention_bwd (:189-226), prenorm_modulate_bwd
         lin(h, h, int(M), bw.obuf, 1, hp, dxmid, h, 1, ga(base + 1), h, 1.f);  // dW_out
         lin(int(M), h, h, dxmid, h, 1, pa(base + 1), 1, h, bw.dO, hp, 0.f);
@@ -1442,7 +1494,7 @@ void backward_core(swf_ctx* c, const float* dout) {
         lin(int(M), h, 3 * h, bw.dqkv, 3 * h, 1, pa(base + 0), 1, 3 * h, bw.dxm, h, 0.f);
         // dx_in = dx_mid + prenorm_modulate_bwd(...) -- accumulated in place in dxmid
         norm_bwd(xb, h, bw.dxm, h, M, h, c->g_attn + size_t(b) * h, six, six + h, six + 2 * h, dxmid, h, bw.rms,
-                 ga(base + 2), bw.d6, bw.d6 + h, bw.d6 + 2 * h, st);
+                 ga(base + 2), bw.d6, bw.d6 + h, bw.d6 + 2 * h, bw.npart, st);
         ada_bwd(bw.d6, c->emb, pa(base + 7), 6 * h, td, ga(base + 7), ga(base + 8), bw.demb, st);
         cur ^= 1;  // the block input's gradient, in layout par = the previous block's output layout
     }

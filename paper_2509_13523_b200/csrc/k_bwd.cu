@@ -134,17 +134,20 @@ __global__ void k_norm_bwd_rows(const float* __restrict__ X, int ldx, const floa
 }
 
 // per-channel pass: dg[i] += sum_j dxm gate (1+a) u ; da[i] += sum_j dxm gate g u ; db[i] += sum_j dxm gate ;
-// dgate[i] += sum_j dxm (g u (1+a) + b), u = x / r. One thread per channel, tokens in order.
+// dgate[i] += sum_j dxm (g u (1+a) + b), u = x / r. One thread per (channel, token slice): slice sl of
+// S sums its tokens in order into part[sl][4][h]; k_norm_bwd_cols_sum adds the slices in order (a fixed
+// order for given M, h: deterministic, no atomics).
 __global__ void k_norm_bwd_cols(const float* __restrict__ X, int ldx, const float* __restrict__ dXM, int lddxm,
                                 const float* __restrict__ rms, i64 M, int h, const float* __restrict__ g,
                                 const float* __restrict__ a, const float* __restrict__ b,
-                                const float* __restrict__ gate, float* __restrict__ dg, float* __restrict__ da,
-                                float* __restrict__ db, float* __restrict__ dgate) {
+                                const float* __restrict__ gate, int S, float* __restrict__ part) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int sl = blockIdx.y;
     if (i >= h) return;
     const float gi = g[i], ai = a ? a[i] : 0.f, bi = b ? b[i] : 0.f, qi = gate ? gate[i] : 1.f;
     float sg = 0.f, sa = 0.f, sb = 0.f, sq = 0.f;
-    for (i64 j = 0; j < M; ++j) {
+    const i64 j1 = M * (sl + 1) / S;
+    for (i64 j = M * sl / S; j < j1; ++j) {
         const float u = X[j * ldx + i] / rms[j];
         const float dxm = dXM[j * lddxm + i];
         const float gu = gi * u;
@@ -153,10 +156,24 @@ __global__ void k_norm_bwd_cols(const float* __restrict__ X, int ldx, const floa
         sq = fmaf(dxm, gu * (1.f + ai) + bi, sq);
         sg = fmaf(dxm * qi * (1.f + ai), u, sg);
     }
-    dg[i] += sg;
-    if (da) da[i] += sa;
-    if (db) db[i] += sb;
-    if (dgate) dgate[i] += sq;
+    float* pt = part + size_t(sl) * 4 * h;
+    pt[i] = sg;
+    pt[h + i] = sa;
+    pt[2 * h + i] = sb;
+    pt[3 * h + i] = sq;
+}
+__global__ void k_norm_bwd_cols_sum(const float* __restrict__ part, int S, int h, float* __restrict__ dg,
+                                    float* __restrict__ da, float* __restrict__ db, float* __restrict__ dgate) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= h) return;
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int sl = 0; sl < S; ++sl)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[q] += part[(size_t(sl) * 4 + q) * h + i];
+    dg[i] += s[0];
+    if (da) da[i] += s[1];
+    if (db) db[i] += s[2];
+    if (dgate) dgate[i] += s[3];
 }
 
 // column sums (bias gradients): out[i] += sum_j X[j][i]
@@ -586,6 +603,35 @@ void to_bf16(const float* x, i64 n, __nv_bfloat16* y, cudaStream_t st) {
     k_to_bf16<<<unsigned(blocks), 256, 0, st>>>(x, n, y);
     SWF_LAUNCH_CHECK();
 }
+__global__ void k_to_f32(const __nv_bfloat16* __restrict__ x, i64 n, float* __restrict__ y) {
+    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+        y[i] = __bfloat162float(x[i]);
+}
+void to_f32(const __nv_bfloat16* x, i64 n, float* y, cudaStream_t st) {
+    if (n <= 0) return;
+    k_to_f32<<<unsigned(std::min<i64>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(x, n, y);
+    SWF_LAUNCH_CHECK();
+}
+// V planes [planes][s][d] fp32 -> V^T planes [planes][d][s] bf16 (the tensor-core attention's P V
+// operand), 32 x 32 tiles through shared memory
+__global__ void k_vt_bf16(const float* __restrict__ v, int s, int d, __nv_bfloat16* __restrict__ vt) {
+    __shared__ float t[32][33];
+    const i64 pl = blockIdx.z;
+    const int s0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+    const float* src = v + pl * s * d;
+    __nv_bfloat16* dst = vt + pl * s * d;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y)
+        t[r][threadIdx.x] = (s0 + r < s && d0 + int(threadIdx.x) < d) ? src[i64(s0 + r) * d + d0 + threadIdx.x] : 0.f;
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y)
+        if (d0 + r < d && s0 + int(threadIdx.x) < s)
+            dst[i64(d0 + r) * s + s0 + threadIdx.x] = __float2bfloat16_rn(t[threadIdx.x][r]);
+}
+void vt_bf16(const float* v, i64 planes, int s, int d, __nv_bfloat16* vt, cudaStream_t st) {
+    dim3 grid(unsigned((s + 31) / 32), unsigned((d + 31) / 32), unsigned(planes));
+    k_vt_bf16<<<grid, dim3(32, 8), 0, st>>>(v, s, d, vt);
+    SWF_LAUNCH_CHECK();
+}
 // gemm_strided_f32's product on the tensor cores: the FP32 operands are rounded to bf16 copies in ta /
 // tb (same layout) and multiplied by one tcgen05 GEMM with FP32 accumulation. The backward's linears
 // take this path when it runs in BF16 (swf_set_backward_precision): data gradients with both operands
@@ -601,11 +647,15 @@ void gemm_strided_tc(int M, int N, int K, const float* A, i64 sai, i64 sak, cons
 }
 void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h, const float* g, const float* a,
               const float* b, const float* gate, float* dX, int lddx, float* rms, float* dg, float* da, float* db,
-              float* dgate, cudaStream_t st) {
+              float* dgate, float* part, cudaStream_t st) {
     k_norm_bwd_rows<<<unsigned((M + 7) / 8), 256, 0, st>>>(X, ldx, dXM, lddxm, M, h, g, a, gate, dX, lddx, rms);
     SWF_LAUNCH_CHECK();
-    k_norm_bwd_cols<<<unsigned((h + 127) / 128), 128, 0, st>>>(X, ldx, dXM, lddxm, rms, M, h, g, a, b, gate, dg, da,
-                                                               db, dgate);
+    const int cb = (h + 127) / 128;  // channel blocks; token slices fill ~4 waves, >= 64 tokens each
+    const int S = int(std::max<i64>(1, std::min<i64>({i64(kNormSlices), (M + 63) / 64, i64(148 * 4 / cb + 1)})));
+    k_norm_bwd_cols<<<dim3(unsigned(cb), unsigned(S)), 128, 0, st>>>(X, ldx, dXM, lddxm, rms, M, h, g, a, b, gate, S,
+                                                                     part);
+    SWF_LAUNCH_CHECK();
+    k_norm_bwd_cols_sum<<<unsigned(cb), 128, 0, st>>>(part, S, h, dg, da, db, dgate);
     SWF_LAUNCH_CHECK();
 }
 void colsum_f32(const float* X, int ldx, i64 M, int n, float* out, cudaStream_t st) {

@@ -181,12 +181,16 @@ void attention_bf16(const AttnParams& p, cudaStream_t st);
 void gemm_strided_f32(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj,
                       float* C, i64 ldc, float beta, cudaStream_t st);
 void to_bf16(const float* x, i64 n, __nv_bfloat16* y, cudaStream_t st);
+void to_f32(const __nv_bfloat16* x, i64 n, float* y, cudaStream_t st);
+void vt_bf16(const float* v, i64 planes, int s, int d, __nv_bfloat16* vt, cudaStream_t st);
 void gemm_strided_tc(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj, float* C,
                      i64 ldc, float beta, __nv_bfloat16* ta, __nv_bfloat16* tb, int* sched, cudaStream_t st);
 // prenorm_modulate_bwd / prenorm_plain_bwd (a, b, gate null): dX += ..., per-channel grads +=
+// part: scratch of kNormSlices * 4 * h floats (per-slice channel sums)
+constexpr int kNormSlices = 256;
 void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h, const float* g, const float* a,
               const float* b, const float* gate, float* dX, int lddx, float* rms, float* dg, float* da, float* db,
-              float* dgate, cudaStream_t st);
+              float* dgate, float* part, cudaStream_t st);
 void colsum_f32(const float* X, int ldx, i64 M, int n, float* out, cudaStream_t st);
 void swiglu_bwd(const float* gu, int ldgu, const float* dS, int ldds, i64 M, int f, int G, float* act, float* dG,
                 float* dU, cudaStream_t st);
