@@ -161,6 +161,7 @@ struct swf_ctx {
     size_t bt_c_n = 0;
     // tensor-core attention of the BF16 training mode: bf16 q / k planes + V^T, bf16 output rows
     __nv_bfloat16 *bt_qkv = nullptr, *bt_o = nullptr;
+    void* bt_att = nullptr;  // per-plane scratch of the tensor-core attention backward
     void** d_bt_o = nullptr;
     TmaMap bt_tm_q, bt_tm_k, bt_tm_k2, bt_tm_vt, bt_tm_o;
     // diffusion training loss (FP32 validation mode): residual target x0, noise z, velocity target v,
@@ -1301,6 +1302,8 @@ void alloc_bwd_tc(swf_ctx* c) {
     c->bt_b = dalloc<__nv_bfloat16>(c, n);
     c->bt_c_n = M * wide;
     c->bt_c = dalloc<float>(c, c->bt_c_n);
+    if (c->world == 1 && m.d % 8 == 0)
+        c->bt_att = dalloc<char>(c, attention_bwd_tc_scratch(m.w * m.w));
     if (c->world == 1 && (m.d == 32 || m.d == 64 || m.d == 128)) {
         c->bt_qkv = dalloc<__nv_bfloat16>(c, size_t(3) * M * m.h);
         c->bt_o = dalloc<__nv_bfloat16>(c, M * size_t(m.hp));
@@ -1488,8 +1491,13 @@ void backward_core(swf_ctx* c, const float* dout) {
         lin(h, h, int(M), bw.obuf, 1, hp, dxmid, h, 1, ga(base + 1), h, 1.f);  // dW_out
         lin(int(M), h, h, dxmid, h, 1, pa(base + 1), 1, h, bw.dO, hp, 0.f);
         float* dq = bw.dplanes;
-        attention_bwd_f32(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h, bw.stats,
-                          c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, st);
+        if (c->bwd_tc && c->bt_att)
+            attention_bwd_tc(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h,
+                             c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, c->bt_a,
+                             c->bt_b, c->bt_att, c->d_sched, st);
+        else
+            attention_bwd_f32(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h,
+                              bw.stats, c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, st);
         lin(h, 3 * h, int(M), bw.xm1, 1, hp, bw.dqkv, 3 * h, 1, ga(base + 0), 3 * h, 1.f);  // dW_qkv
         lin(int(M), h, 3 * h, bw.dqkv, 3 * h, 1, pa(base + 0), 1, 3 * h, bw.dxm, h, 0.f);
         // dx_in = dx_mid + prenorm_modulate_bwd(...) -- accumulated in place in dxmid

@@ -784,7 +784,7 @@ void preload_bn(cudaFuncAttributes& a) {
     const void* k[] = {(const void*)k_gemm_tc<BN, EPI_ENCODE>, (const void*)k_gemm_tc<BN, EPI_QKV>,
                        (const void*)k_gemm_tc<BN, EPI_RESID>, (const void*)k_gemm_tc<BN, EPI_SWIGLU>,
                        (const void*)k_gemm_tc<BN, EPI_DOWN>, (const void*)k_gemm_tc<BN, EPI_DECODE>,
-                       (const void*)k_gemm_tc<BN, EPI_RESID, 3>};
+                       (const void*)k_gemm_tc<BN, EPI_RESID, 3>, (const void*)k_gemm_tc<BN, EPI_RESID, 2>};
     for (const void* f : k) {
         SWF_CUDA(cudaFuncGetAttributes(&a, f));
         SWF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem));
@@ -815,7 +815,7 @@ void make_tma_bf16_pitch(TmaMap* m, const void* base, i64 rows, i64 inner, i64 p
 void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bfloat16* B, bool b_mn, i64 ldb, i64 M,
                        i64 N, i64 K, float* C, i64 ldc, bool accumulate, int* sched, cudaStream_t st) {
     if (M <= 0 || N <= 0 || K <= 0) return;
-    if (a_mn != b_mn) throw CudaError("gemm_bf16_general: mixed operand majors are not instantiated");
+    if (a_mn && !b_mn) throw CudaError("gemm_bf16_general: A MN-major with B K-major is not instantiated");
     if (!accumulate) SWF_CUDA(cudaMemset2DAsync(C, size_t(ldc) * 4, 0, size_t(N) * 4, size_t(M), st));
     const int BN = N > 128 ? 256 : 128;
     TmaMap ta, tb;
@@ -837,10 +837,16 @@ void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bf
     ep.sched = sched;
     const int Kp = int((K + BK - 1) / BK * BK);
     const int Np = int((N + BN - 1) / BN * BN);
-    if (BN == 256)
-        a_mn ? launch<256, EPI_RESID, 3>(ta, tb, M, Np, Kp, ep, st) : launch<256, EPI_RESID, 0>(ta, tb, M, Np, Kp, ep, st);
-    else
-        a_mn ? launch<128, EPI_RESID, 3>(ta, tb, M, Np, Kp, ep, st) : launch<128, EPI_RESID, 0>(ta, tb, M, Np, Kp, ep, st);
+    const int mn = (a_mn ? 1 : 0) | (b_mn ? 2 : 0);
+    if (BN == 256) {
+        if (mn == 3) launch<256, EPI_RESID, 3>(ta, tb, M, Np, Kp, ep, st);
+        else if (mn == 2) launch<256, EPI_RESID, 2>(ta, tb, M, Np, Kp, ep, st);
+        else launch<256, EPI_RESID, 0>(ta, tb, M, Np, Kp, ep, st);
+    } else {
+        if (mn == 3) launch<128, EPI_RESID, 3>(ta, tb, M, Np, Kp, ep, st);
+        else if (mn == 2) launch<128, EPI_RESID, 2>(ta, tb, M, Np, Kp, ep, st);
+        else launch<128, EPI_RESID, 0>(ta, tb, M, Np, Kp, ep, st);
+    }
 }
 
 void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int BN, int mode, const EpiParams& ep,

@@ -148,7 +148,7 @@ void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int 
                   cudaStream_t st);
 // General tensor-core GEMM of the backward: C[M][N] (fp32, row pitch ldc) (+)= A . B with bf16
 // operands, A K-major (A[m * lda + k]) or MN-major (A[k * lda + m]), B K-major (B[n * ldb + k]) or
-// MN-major (B[k * ldb + n]) -- both K-major or both MN-major; pitches multiples of 8 elements.
+// MN-major (B[k * ldb + n]) -- not A MN-major with B K-major; pitches multiples of 8 elements.
 void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bfloat16* B, bool b_mn, i64 ldb, i64 M,
                        i64 N, i64 K, float* C, i64 ldc, bool accumulate, int* sched, cudaStream_t st);
 
@@ -183,6 +183,14 @@ void gemm_strided_f32(int M, int N, int K, const float* A, i64 sai, i64 sak, con
 void to_bf16(const float* x, i64 n, __nv_bfloat16* y, cudaStream_t st);
 void to_f32(const __nv_bfloat16* x, i64 n, float* y, cudaStream_t st);
 void vt_bf16(const float* v, i64 planes, int s, int d, __nv_bfloat16* vt, cudaStream_t st);
+// attention backward on the tensor cores (BF16 training mode): per (window, head) plane, five tcgen05
+// GEMMs and two row passes; scratch of attention_bwd_tc_scratch(s) bytes, qkv16 3 M h and dO16 M ldo
+// bf16 elements; d % 8 == 0
+size_t attention_bwd_tc_scratch(int s);
+void attention_bwd_tc(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,
+                      float* dq, float* dk, float* dv, int nloc, int heads, int s, int d, int w, const LayMap& lay,
+                      const EpiParams& ep, float* dqkv, __nv_bfloat16* qkv16, __nv_bfloat16* dO16, void* scratch,
+                      int* sched, cudaStream_t st);
 void gemm_strided_tc(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj, float* C,
                      i64 ldc, float beta, __nv_bfloat16* ta, __nv_bfloat16* tb, int* sched, cudaStream_t st);
 // prenorm_modulate_bwd / prenorm_plain_bwd (a, b, gate null): dX += ..., per-channel grads +=
