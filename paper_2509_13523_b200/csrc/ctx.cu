@@ -161,7 +161,7 @@ struct swf_ctx {
     size_t bt_c_n = 0;
     // tensor-core attention of the BF16 training mode: bf16 q / k planes + V^T, bf16 output rows
     __nv_bfloat16 *bt_qkv = nullptr, *bt_o = nullptr;
-    void* bt_att = nullptr;  // per-plane scratch of the tensor-core attention backward
+    AttnBwdStreams bt_ws;  // worker streams / scratch of the tensor-core attention backward
     void** d_bt_o = nullptr;
     TmaMap bt_tm_q, bt_tm_k, bt_tm_k2, bt_tm_vt, bt_tm_o;
     // diffusion training loss (FP32 validation mode): residual target x0, noise z, velocity target v,
@@ -947,7 +947,7 @@ const TmaMap* tmap_at(const std::vector<TmaMap>& v, int b) { return b < int(v.si
 template <class T>
 struct Gemm;
 
-void attention_ctx(swf_ctx* c, const AttnParams& ap);
+void attention_ctx(swf_ctx* c, const AttnParams& ap, bool training);
 
 // FP32-context linear layer. In the BF16 training mode (swf_set_backward_precision(BF16)) the
 // forwards of the training entry points (activations saved) and the backward's recomputation run
@@ -1129,7 +1129,7 @@ void run_block(swf_ctx* c, int b, int cur, const LayMap& L, const LayMap& Lnext,
     {
         ProfScope ps(c, K_ATTN);
         if constexpr (sizeof(T) == 4)
-            attention_ctx(c, ap);
+            attention_ctx(c, ap, c->save_x);
         else
             attention_bf16(ap, c->st);
     }
@@ -1302,8 +1302,16 @@ void alloc_bwd_tc(swf_ctx* c) {
     c->bt_b = dalloc<__nv_bfloat16>(c, n);
     c->bt_c_n = M * wide;
     c->bt_c = dalloc<float>(c, c->bt_c_n);
-    if (c->world == 1 && m.d % 8 == 0)
-        c->bt_att = dalloc<char>(c, attention_bwd_tc_scratch(m.w * m.w));
+    if (c->world == 1 && m.d % 8 == 0) {
+        auto& ws = c->bt_ws;
+        ws.n = AttnBwdStreams::kMax;
+        for (int i = 0; i < ws.n; ++i) {
+            SWF_CUDA(cudaStreamCreateWithFlags(&ws.st[i], cudaStreamNonBlocking));
+            ws.scratch[i] = dalloc<char>(c, attention_bwd_tc_scratch(m.w * m.w));
+            ws.sched[i] = dalloc<int>(c, 1);
+        }
+        for (int i = 0; i <= ws.n; ++i) SWF_CUDA(cudaEventCreateWithFlags(&ws.ev[i], cudaEventDisableTiming));
+    }
     if (c->world == 1 && (m.d == 32 || m.d == 64 || m.d == 128)) {
         c->bt_qkv = dalloc<__nv_bfloat16>(c, size_t(3) * M * m.h);
         c->bt_o = dalloc<__nv_bfloat16>(c, M * size_t(m.hp));
@@ -1324,8 +1332,8 @@ void alloc_bwd_tc(swf_ctx* c) {
 
 // FP32-context attention. The BF16 training mode runs the tensor-core kernel (k_attn_pp) on bf16
 // copies of q, k and V^T and widens its bf16 output; the FP32 validation mode runs the SIMT kernel.
-void attention_ctx(swf_ctx* c, const AttnParams& ap) {
-    if (!(c->bwd_tc && c->save_x && c->bt_qkv)) {
+void attention_ctx(swf_ctx* c, const AttnParams& ap, bool training) {
+    if (!(c->bwd_tc && training && c->bt_qkv)) {
         attention_f32(ap, c->st);
         return;
     }
@@ -1450,7 +1458,7 @@ void backward_core(swf_ctx* c, const float* dout) {
         ap.w = m.w;
         ap.lay = c->lay[par];
         ap.scale = 1.0f / std::sqrt(float(m.d));
-        attention_ctx(c, ap);
+        attention_ctx(c, ap, true);
         SWF_CUDA(cudaMemcpyAsync(bw.xmid, xb, size_t(M) * h * 4, cudaMemcpyDeviceToDevice, st));
         e = ep;
         e.x = bw.xmid;
@@ -1491,10 +1499,10 @@ void backward_core(swf_ctx* c, const float* dout) {
         lin(h, h, int(M), bw.obuf, 1, hp, dxmid, h, 1, ga(base + 1), h, 1.f);  // dW_out
         lin(int(M), h, h, dxmid, h, 1, pa(base + 1), 1, h, bw.dO, hp, 0.f);
         float* dq = bw.dplanes;
-        if (c->bwd_tc && c->bt_att)
+        if (c->bwd_tc && c->bt_ws.n > 0)
             attention_bwd_tc(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h,
                              c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, c->bt_a,
-                             c->bt_b, c->bt_att, c->d_sched, st);
+                             c->bt_b, c->bt_ws, st);
         else
             attention_bwd_f32(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h,
                               bw.stats, c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, st);
@@ -2334,6 +2342,11 @@ void swf_destroy(swf_ctx* c) {
             if (p) cudaIpcCloseMemHandle(p);
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (int i = 0; i < c->bt_ws.n; ++i) {
+        cudaStreamSynchronize(c->bt_ws.st[i]);
+        cudaStreamDestroy(c->bt_ws.st[i]);
+    }
+    for (int i = 0; c->bt_ws.n > 0 && i <= c->bt_ws.n; ++i) cudaEventDestroy(c->bt_ws.ev[i]);
     cudaStreamDestroy(c->st);
     delete c;
 }

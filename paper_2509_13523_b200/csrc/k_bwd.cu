@@ -762,15 +762,10 @@ size_t attention_bwd_tc_scratch(int s) {  // bytes: S / dP fp32 + P / dS bf16 + 
 }
 void attention_bwd_tc(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,
                       float* dq, float* dk, float* dv, int nloc, int heads, int s, int d, int w, const LayMap& lay,
-                      const EpiParams& ep, float* dqkv, __nv_bfloat16* qkv16, __nv_bfloat16* dO16, void* scratch,
-                      int* sched, cudaStream_t st) {
+                      const EpiParams& ep, float* dqkv, __nv_bfloat16* qkv16, __nv_bfloat16* dO16,
+                      const AttnBwdStreams& ws, cudaStream_t st) {
     const i64 M = i64(nloc) * s, hd = i64(heads) * d;
     const int sp = (s + 7) / 8 * 8;
-    float* S = static_cast<float*>(scratch);
-    float* dP = S + size_t(s) * sp;
-    __nv_bfloat16* P = reinterpret_cast<__nv_bfloat16*>(dP + size_t(s) * sp);
-    __nv_bfloat16* dS = P + size_t(s) * sp;
-    float* D = reinterpret_cast<float*>(dS + size_t(s) * sp);
     to_bf16(q, M * hd, qkv16, st);  // q, k, v planes [nloc][heads][s][d]
     to_bf16(k, M * hd, qkv16 + M * hd, st);
     to_bf16(v, M * hd, qkv16 + 2 * M * hd, st);
@@ -781,24 +776,41 @@ void attention_bwd_tc(const float* q, const float* k, const float* v, const floa
     SWF_CUDA(cudaMemcpyAsync(gw.data(), lay.loc2glob, size_t(nloc) * 4, cudaMemcpyDeviceToHost, st));
     SWF_CUDA(cudaStreamSynchronize(st));
     const int split = (w - lay.g.shift) * w;
+    // planes round-robin over the worker streams (a plane's GEMMs are 15 x 1 tiles for N = d: several
+    // planes in flight fill the GPU), each with its own scratch and tile counter
+    SWF_CUDA(cudaEventRecord(ws.ev[0], st));
+    for (int i = 0; i < ws.n; ++i) SWF_CUDA(cudaStreamWaitEvent(ws.st[i], ws.ev[0], 0));
+    int pl_i = 0;
     for (int lw = 0; lw < nloc; ++lw) {
         const int masked = lay.g.shift > 0 && gw[size_t(lw)] / lay.g.nx == lay.g.ny - 1;
-        for (int hh = 0; hh < heads; ++hh) {
+        for (int hh = 0; hh < heads; ++hh, ++pl_i) {
+            const int wi = pl_i % ws.n;
+            cudaStream_t ss = ws.st[wi];
+            int* sched = ws.sched[wi];
+            float* S = static_cast<float*>(ws.scratch[wi]);
+            float* dP = S + size_t(s) * sp;
+            __nv_bfloat16* P = reinterpret_cast<__nv_bfloat16*>(dP + size_t(s) * sp);
+            __nv_bfloat16* dS = P + size_t(s) * sp;
+            float* D = reinterpret_cast<float*>(dS + size_t(s) * sp);
             const i64 pl = (i64(lw) * heads + hh) * s * d;
             const __nv_bfloat16 *q16 = qkv16 + pl, *k16 = qkv16 + M * hd + pl, *v16 = qkv16 + 2 * M * hd + pl;
             const i64 orow = i64(lw) * s * ldo + i64(hh) * d;
-            gemm_bf16_general(q16, false, d, k16, false, d, s, s, d, S, sp, false, sched, st);  // S = Q K^T
-            k_attn_bwd_softmax<<<unsigned((s + 7) / 8), 256, 0, st>>>(S, sp, s, scale, split, masked, o + orow,
+            gemm_bf16_general(q16, false, d, k16, false, d, s, s, d, S, sp, false, sched, ss);  // S = Q K^T
+            k_attn_bwd_softmax<<<unsigned((s + 7) / 8), 256, 0, ss>>>(S, sp, s, scale, split, masked, o + orow,
                                                                       dO + orow, ldo, d, P, D);
             SWF_LAUNCH_CHECK();
-            gemm_bf16_general(P, true, sp, dO16 + orow, true, ldo, s, d, s, dv + pl, d, false, sched, st);  // P^T dO
-            gemm_bf16_general(dO16 + orow, false, ldo, v16, false, d, s, s, d, dP, sp, false, sched, st);  // dO V^T
-            k_attn_bwd_ds<<<unsigned(std::min<i64>((i64(s) * sp + 255) / 256, 148 * 16)), 256, 0, st>>>(dP, P, sp, s,
+            gemm_bf16_general(P, true, sp, dO16 + orow, true, ldo, s, d, s, dv + pl, d, false, sched, ss);  // P^T dO
+            gemm_bf16_general(dO16 + orow, false, ldo, v16, false, d, s, s, d, dP, sp, false, sched, ss);  // dO V^T
+            k_attn_bwd_ds<<<unsigned(std::min<i64>((i64(s) * sp + 255) / 256, 148 * 16)), 256, 0, ss>>>(dP, P, sp, s,
                                                                                                    D, scale, dS);
             SWF_LAUNCH_CHECK();
-            gemm_bf16_general(dS, false, sp, k16, true, d, s, d, s, dq + pl, d, false, sched, st);  // dS K
-            gemm_bf16_general(dS, true, sp, q16, true, d, s, d, s, dk + pl, d, false, sched, st);   // dS^T Q
+            gemm_bf16_general(dS, false, sp, k16, true, d, s, d, s, dq + pl, d, false, sched, ss);  // dS K
+            gemm_bf16_general(dS, true, sp, q16, true, d, s, d, s, dk + pl, d, false, sched, ss);   // dS^T Q
         }
+    }
+    for (int i = 0; i < ws.n; ++i) {
+        SWF_CUDA(cudaEventRecord(ws.ev[1 + i], ws.st[i]));
+        SWF_CUDA(cudaStreamWaitEvent(st, ws.ev[1 + i], 0));
     }
     EpiParams e = ep;
     e.cur = lay;

@@ -322,6 +322,10 @@ __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, i
 #pragma unroll
         for (int rr = 0; rr < 32; ++rr)
             if (rr < mrem && col_ok) ep.x[(row0 + rr) * h + n] = stg[rr * 33 + lane] + b;
+    } else if constexpr (MODE == EPI_STORE) {
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr)
+            if (rr < mrem && col_ok) ep.x[(row0 + rr) * h + n] = stg[rr * 33 + lane];
     } else {
         // all 32 row reads in flight before any dependent store (latency hiding with 4 warps)
         float xv[32];
@@ -606,7 +610,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     normed(u, n_blk * BN + BN / 2 + ch * 32);
                     epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u, pol_out);
                 }
-            } else if constexpr (MODE == EPI_DOWN || MODE == EPI_RESID) {
+            } else if constexpr (MODE == EPI_DOWN || MODE == EPI_RESID || MODE == EPI_STORE) {
                 float* drow = nullptr;
                 __nv_bfloat16* dbrow = nullptr;
                 float* dsrow = nullptr;
@@ -784,7 +788,9 @@ void preload_bn(cudaFuncAttributes& a) {
     const void* k[] = {(const void*)k_gemm_tc<BN, EPI_ENCODE>, (const void*)k_gemm_tc<BN, EPI_QKV>,
                        (const void*)k_gemm_tc<BN, EPI_RESID>, (const void*)k_gemm_tc<BN, EPI_SWIGLU>,
                        (const void*)k_gemm_tc<BN, EPI_DOWN>, (const void*)k_gemm_tc<BN, EPI_DECODE>,
-                       (const void*)k_gemm_tc<BN, EPI_RESID, 3>, (const void*)k_gemm_tc<BN, EPI_RESID, 2>};
+                       (const void*)k_gemm_tc<BN, EPI_RESID, 3>, (const void*)k_gemm_tc<BN, EPI_RESID, 2>,
+                       (const void*)k_gemm_tc<BN, EPI_STORE, 0>, (const void*)k_gemm_tc<BN, EPI_STORE, 3>,
+                       (const void*)k_gemm_tc<BN, EPI_STORE, 2>};
     for (const void* f : k) {
         SWF_CUDA(cudaFuncGetAttributes(&a, f));
         SWF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem));
@@ -812,11 +818,25 @@ void make_tma_bf16_pitch(TmaMap* m, const void* base, i64 rows, i64 inner, i64 p
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (pitch) failed: " + std::to_string(int(r)));
 }
 
+template <int MODE>
+void general_launch(int BN, int mn, const TmaMap& ta, const TmaMap& tb, i64 M, int Np, int Kp, const EpiParams& ep,
+                    cudaStream_t st) {
+    if (BN == 256) {
+        if (mn == 3) launch<256, MODE, 3>(ta, tb, M, Np, Kp, ep, st);
+        else if (mn == 2) launch<256, MODE, 2>(ta, tb, M, Np, Kp, ep, st);
+        else launch<256, MODE, 0>(ta, tb, M, Np, Kp, ep, st);
+    } else {
+        if (mn == 3) launch<128, MODE, 3>(ta, tb, M, Np, Kp, ep, st);
+        else if (mn == 2) launch<128, MODE, 2>(ta, tb, M, Np, Kp, ep, st);
+        else launch<128, MODE, 0>(ta, tb, M, Np, Kp, ep, st);
+    }
+}
+
 void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bfloat16* B, bool b_mn, i64 ldb, i64 M,
                        i64 N, i64 K, float* C, i64 ldc, bool accumulate, int* sched, cudaStream_t st) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     if (a_mn && !b_mn) throw CudaError("gemm_bf16_general: A MN-major with B K-major is not instantiated");
-    if (!accumulate) SWF_CUDA(cudaMemset2DAsync(C, size_t(ldc) * 4, 0, size_t(N) * 4, size_t(M), st));
+
     const int BN = N > 128 ? 256 : 128;
     TmaMap ta, tb;
     if (a_mn)
@@ -838,15 +858,10 @@ void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bf
     const int Kp = int((K + BK - 1) / BK * BK);
     const int Np = int((N + BN - 1) / BN * BN);
     const int mn = (a_mn ? 1 : 0) | (b_mn ? 2 : 0);
-    if (BN == 256) {
-        if (mn == 3) launch<256, EPI_RESID, 3>(ta, tb, M, Np, Kp, ep, st);
-        else if (mn == 2) launch<256, EPI_RESID, 2>(ta, tb, M, Np, Kp, ep, st);
-        else launch<256, EPI_RESID, 0>(ta, tb, M, Np, Kp, ep, st);
-    } else {
-        if (mn == 3) launch<128, EPI_RESID, 3>(ta, tb, M, Np, Kp, ep, st);
-        else if (mn == 2) launch<128, EPI_RESID, 2>(ta, tb, M, Np, Kp, ep, st);
-        else launch<128, EPI_RESID, 0>(ta, tb, M, Np, Kp, ep, st);
-    }
+    if (accumulate)
+        general_launch<EPI_RESID>(BN, mn, ta, tb, M, Np, Kp, ep, st);
+    else
+        general_launch<EPI_STORE>(BN, mn, ta, tb, M, Np, Kp, ep, st);
 }
 
 void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int BN, int mode, const EpiParams& ep,

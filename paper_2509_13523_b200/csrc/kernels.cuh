@@ -83,6 +83,7 @@ enum EpiMode : int {
     EPI_SWIGLU = 3,  // s[m][j] = silu(gate) * up from interleaved columns          (swin.hpp:230-232)
     EPI_DOWN = 4,    // xdst[dest(m)][n] = xsrc[m][n] + acc, dest = next layout     (swin.hpp:324, 356-358)
     EPI_DECODE = 5,  // out[m][n] = (acc + bias[n]) * out_scale, n < cout (local L0 order) (swin.hpp:364-366)
+    EPI_STORE = 6,   // x[m][n] = acc, n < N (the backward's plain products; tensor-core kernel only)
 };
 
 struct EpiParams {
@@ -187,10 +188,18 @@ void vt_bf16(const float* v, i64 planes, int s, int d, __nv_bfloat16* vt, cudaSt
 // GEMMs and two row passes; scratch of attention_bwd_tc_scratch(s) bytes, qkv16 3 M h and dO16 M ldo
 // bf16 elements; d % 8 == 0
 size_t attention_bwd_tc_scratch(int s);
+struct AttnBwdStreams {  // worker streams of the per-plane loop, each with scratch and a GEMM tile counter
+    static constexpr int kMax = 4;
+    int n = 0;
+    cudaStream_t st[kMax];
+    cudaEvent_t ev[kMax + 1];
+    void* scratch[kMax];
+    int* sched[kMax];
+};
 void attention_bwd_tc(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,
                       float* dq, float* dk, float* dv, int nloc, int heads, int s, int d, int w, const LayMap& lay,
-                      const EpiParams& ep, float* dqkv, __nv_bfloat16* qkv16, __nv_bfloat16* dO16, void* scratch,
-                      int* sched, cudaStream_t st);
+                      const EpiParams& ep, float* dqkv, __nv_bfloat16* qkv16, __nv_bfloat16* dO16,
+                      const AttnBwdStreams& ws, cudaStream_t st);
 void gemm_strided_tc(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj, float* C,
                      i64 ldc, float beta, __nv_bfloat16* ta, __nv_bfloat16* tb, int* sched, cudaStream_t st);
 // prenorm_modulate_bwd / prenorm_plain_bwd (a, b, gate null): dX += ..., per-channel grads +=
