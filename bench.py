@@ -481,6 +481,9 @@ def run_train(args, rank: int, world: int, local_rank: int):
     cfg = swf.ModelConfig(**CFG)
     dn = swf.Denoiser(cfg, TH, TW, device=local_rank, precision=swf.PREC_FP32)
     dn.init_params(SEED, mode=2, scale=0.02 / math.sqrt(CFG["time_dim"]))
+    bf16 = args.train_precision == "bf16"
+    if bf16:  # BF16 training mode: linears and attention (fwd + bwd) on the tensor cores
+        dn.set_backward_precision(swf.PREC_BF16)
     rng = np.random.default_rng(SEED + rank)
     cp, cf = CFG["out_channels"], CFG["in_channels"] - 2 * CFG["out_channels"]
     fields = [(rng.standard_normal((TH * TW, cp), dtype=np.float32),
@@ -526,16 +529,23 @@ def run_train(args, rank: int, world: int, local_rank: int):
     fp32_peak = 148 * 128 * 2 * 1965e6 / 1e12  # FFMA lanes x 2 x max SM clock (no measured FP32 peak)
     if rank == 0:
         tf = model_flops / (ms * 1e-3) / world / 1e12
+        if bf16:
+            mp = measured_peaks()
+            peak, peak_kind, bound = mp["bf16_sus"], f"bf16 sustained ({mp['src']})", "tensor"
+        else:
+            peak, bound = fp32_peak, "fp32"
+            peak_kind = "computed: 148 SMs x 128 FFMA lanes x 2 x 1965 MHz (no measured FP32 peak)"
         print(json.dumps({
             "metric": "training samples/sec", "value": samples / (ms * 1e-3), "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "f3 training step (reference_train_step, FP32 validation mode), "
-                                   "AERIS-1.3B widths / 20 blocks on a grid slice",
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if bf16 else "f32", "data": "synthetic",
+            "config": {"workload": "f3 training step (reference_train_step, "
+                                   + ("BF16 training mode" if bf16 else "FP32 validation mode")
+                                   + "), AERIS-1.3B widths / 20 blocks on a grid slice",
                        "grid": [TH, TW], "gas": gas, "parallelism": f"dp{world}", "model": "swin-dit-1.3B (C2)",
                        "l2": "inputs far larger than L2 (weights 5.3 GB fp32 + activations)"},
-            "roofline": {"bound": "fp32", "achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s", "frac": tf / fp32_peak,
-                         "peak_kind": "computed: 148 SMs x 128 FFMA lanes x 2 x 1965 MHz (no measured FP32 peak)",
+            "roofline": {"bound": bound, "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                         "peak_kind": peak_kind,
                          "traffic": None, "flops": "3 x forward per sample (perf_model.cpp:63-74), recompute excluded"},
             "e2e": {"value": samples / (ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": int(sum(a.nbytes for a in fields[0])) * samples, "d2h_bytes_per_step": 8 * samples},
@@ -564,6 +574,8 @@ def main():
     ap.add_argument("--solver-steps", type=int, default=10, help="c5: DPM-Solver++ 2S steps (2 evaluations each)")
     ap.add_argument("--gas", type=int, default=1, help="train: microbatches per rank")
     ap.add_argument("--train-grid", type=int, nargs=2, default=[120, 240], help="train: grid slice (H W)")
+    ap.add_argument("--train-precision", choices=["fp32", "bf16"], default="fp32",
+                    help="train: FP32 validation mode or the BF16 training mode (tensor cores)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
