@@ -98,7 +98,7 @@ struct swf_ctx {
     float* xbuf[2] = {nullptr, nullptr};
     void *xm = nullptr, *qkv = nullptr, *sbuf = nullptr, *a_in = nullptr;
     float* out_loc = nullptr;
-    float *rope_row = nullptr, *rope_col = nullptr, *feat = nullptr, *emb = nullptr, *six = nullptr;
+    float *rope_row = nullptr, *rope_col = nullptr, *rope_row_pm = nullptr, *rope_col_pm = nullptr, *feat = nullptr, *emb = nullptr, *six = nullptr;
     int* flags = nullptr;
     int* h_flags = nullptr;
     float* h_feat = nullptr;
@@ -419,6 +419,19 @@ void build_rope(swf_ctx* c) {
     c->rope_col = dalloc<float>(c, tc.size());
     h2d_sync(c, c->rope_row, tr.data(), tr.size() * 4);
     h2d_sync(c, c->rope_col, tc.data(), tc.size() * 4);
+    // position-major copies for the tensor-core QKV epilogue: a row's 16 pairs are one 128-B line
+    auto pm = [&](const std::vector<float>& t, int npos) {
+        std::vector<float> o(t.size());
+        for (int j = 0; j < q4; ++j)
+            for (int pos = 0; pos < npos; ++pos)
+                for (int k = 0; k < 2; ++k) o[(size_t(pos) * q4 + j) * 2 + k] = t[(size_t(j) * npos + pos) * 2 + k];
+        return o;
+    };
+    const auto trp = pm(tr, c->H + m.w), tcp = pm(tc, c->W + m.w);
+    c->rope_row_pm = dalloc<float>(c, trp.size());
+    c->rope_col_pm = dalloc<float>(c, tcp.size());
+    h2d_sync(c, c->rope_row_pm, trp.data(), trp.size() * 4);
+    h2d_sync(c, c->rope_col_pm, tcp.data(), tcp.size() * 4);
 }
 
 void allocate(swf_ctx* c) {
@@ -990,6 +1003,8 @@ EpiParams base_ep(swf_ctx* c) {
     ep.sched = c->d_sched;
     ep.rope_row = reinterpret_cast<const float2*>(c->rope_row);
     ep.rope_col = reinterpret_cast<const float2*>(c->rope_col);
+    ep.rope_row_pm = reinterpret_cast<const float2*>(c->rope_row_pm);
+    ep.rope_col_pm = reinterpret_cast<const float2*>(c->rope_col_pm);
     ep.rope_nrow = c->H + c->m.w;
     ep.rope_ncol = c->W + c->m.w;
     ep.cur = c->lay[0];

@@ -272,6 +272,64 @@ __device__ __forceinline__ float epi32(const EpiParams& ep, i64 m, int n0, float
     return 0.f;
 }
 
+// QKV epilogue with the row's window / token / RoPE positions resolved once per tile (not per
+// 32-column chunk): RoPE pairs from the position-major tables (a chunk's 16 pairs are one line, read
+// as 8 float4), q / k rows as 16-byte stores, V^T as 64-byte warp-wide rows.
+struct QkvRow {
+    bool ok;
+    int lw, tok;
+    const float2 *rr, *rc;  // this row's RoPE (cos, sin) for the row / column halves
+};
+__device__ __forceinline__ QkvRow qkv_row(const EpiParams& ep, i64 m) {
+    QkvRow r;
+    r.ok = m < ep.M;
+    if (!r.ok) return r;
+    int gw;
+    ep.cur.loc_to_wtok(m, gw, r.tok, r.lw);
+    const int w = ep.cur.g.w, q4 = ep.d >> 2;
+    const int wy = gw / ep.cur.g.nx, wx = gw - wy * ep.cur.g.nx;
+    const int prow = wy * w + ep.cur.g.shift + r.tok / w;  // unwrapped RoPE position (window.hpp:54-56)
+    const int pcol = wx * w + ep.cur.g.shift + r.tok % w;
+    r.rr = ep.rope_row_pm + i64(prow) * q4;
+    r.rc = ep.rope_col_pm + i64(pcol) * q4;
+    return r;
+}
+__device__ __forceinline__ void epi_qkv32(const EpiParams& ep, const QkvRow& qr, int n0, float* v) {
+    if (!qr.ok || n0 >= ep.N) return;
+    const int h = ep.h, s = ep.cur.g.w * ep.cur.g.w, q4 = ep.d >> 2;
+    const int which = n0 / h;
+    const int e = n0 - which * h;
+    const int head = e / ep.d;
+    const int dd = e - head * ep.d;
+    const int hg = head / ep.heads_loc, hl = head - hg * ep.heads_loc;
+    __nv_bfloat16* base =
+        reinterpret_cast<__nv_bfloat16*>(ep.qkv_dst[ep.wp_rank * ep.cur.sp + hg]) + which * ep.plane;
+    if (which == 2) {  // V^T [window][head][d][token]: the warp's 32 lanes are consecutive tokens
+        __nv_bfloat16* vt = base + ((i64(qr.lw) * ep.heads_loc + hl) * ep.d + dd) * s + qr.tok;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) vt[i64(j) * s] = __float2bfloat16_rn(v[j]);
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // pairs j, j + 1 lie in the same half (q4 is even)
+        const int j = (dd >> 1) + 2 * k;
+        const float4 cs = j < q4 ? *reinterpret_cast<const float4*>(qr.rr + j)
+                                 : *reinterpret_cast<const float4*>(qr.rc + (j - q4));
+        float x = v[4 * k], y = v[4 * k + 1];
+        v[4 * k] = cs.x * x - cs.y * y;
+        v[4 * k + 1] = cs.y * x + cs.x * y;
+        x = v[4 * k + 2];
+        y = v[4 * k + 3];
+        v[4 * k + 2] = cs.z * x - cs.w * y;
+        v[4 * k + 3] = cs.w * x + cs.z * y;
+    }
+    uint4* d4 = reinterpret_cast<uint4*>(base + ((i64(qr.lw) * ep.heads_loc + hl) * s + qr.tok) * ep.d + dd);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        d4[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                           pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+}
+
 __device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0, const float* g, const float* u,
                                              uint64_t pol) {
     if (m >= ep.M || j0 >= ep.N) return;
@@ -642,12 +700,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             } else {
                 constexpr int NCH = BN / 32;
                 float ssum = 0.f;
+                [[maybe_unused]] QkvRow qr;
+                if constexpr (MODE == EPI_QKV) qr = qkv_row(ep, row);
 #pragma unroll 1
                 for (int ch = half * NCH / 2; ch < (half + 1) * NCH / 2; ++ch) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
                     normed(v, n_blk * BN + ch * 32);
-                    ssum += epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
+                    if constexpr (MODE == EPI_QKV)
+                        epi_qkv32(ep, qr, n_blk * BN + ch * 32, v);
+                    else
+                        ssum += epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
                 }
                 if constexpr (MODE == EPI_ENCODE)
                     if (ep.nss && row < ep.M) ep.x[ep.off_ss + row * ep.nss + 2 * n_blk + half] = ssum;

@@ -100,6 +100,8 @@ struct EpiParams {
     int G;           // SWIGLU interleave granularity
     const float2* rope_row;  // [d/4][H+w] (cos, sin)
     const float2* rope_col;  // [d/4][W+w]
+    const float2* rope_row_pm;  // the same tables position-major: [H+w][d/4], [W+w][d/4]
+    const float2* rope_col_pm;
     int rope_nrow, rope_ncol;
     LayMap cur, nxt;
     float out_scale;

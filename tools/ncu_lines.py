@@ -1,6 +1,6 @@
 """Per-CUDA-source-line stall breakdown of one kernel in an ncu report (--import-source on):
 warp-stall samples, executed instructions and the top stall reasons per line.
-usage: python tools/ncu_lines.py REPORT.ncu-rep [N_LINES]"""
+usage: python tools/ncu_lines.py REPORT.ncu-rep [N_LINES] [LAUNCH_INDEX]"""
 import collections
 import csv
 import io
@@ -9,7 +9,8 @@ import sys
 
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
+sel = ["--launch-skip", sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"] + sel,
                      capture_output=True, text=True).stdout
 
 
