@@ -1435,9 +1435,9 @@ void backward_core(swf_ctx* c, const float* dout) {
     // decode head (swin.hpp:430-436): n3 = prenorm_plain(x_final); dW_dec, db_dec, dN3, prenorm_plain_bwd
     const float* xf = c->xsave + size_t(nb) * M * h;
     rms_modulate<float>(xf, M, h, hp, c->g_dec, nullptr, nullptr, nullptr, bw.xm1, nullptr, 0, st);
-    gemm_strided_f32(h, m.cout, int(M), bw.xm1, 1, hp, dout, m.cout, 1, ga(tail + 3), m.cout, 1.f, st);
+    lin(h, m.cout, int(M), bw.xm1, 1, hp, dout, m.cout, 1, ga(tail + 3), m.cout, 1.f);
     colsum_f32(dout, m.cout, M, m.cout, ga(tail + 4), st);
-    gemm_strided_f32(int(M), h, m.cout, dout, m.cout, 1, pa(tail + 3), 1, m.cout, bw.dtmp, h, 0.f, st);
+    lin(int(M), h, m.cout, dout, m.cout, 1, pa(tail + 3), 1, m.cout, bw.dtmp, h, 0.f);
     SWF_CUDA(cudaMemsetAsync(bw.dx[0], 0, size_t(M) * h * 4, st));
     norm_bwd(xf, h, bw.dtmp, h, M, h, c->g_dec, nullptr, nullptr, nullptr, bw.dx[0], h, bw.rms, ga(tail + 2), nullptr,
              nullptr, nullptr, bw.npart, st);
@@ -1531,9 +1531,9 @@ void backward_core(swf_ctx* c, const float* dout) {
     }
     // encode (swin.hpp:458-461) and the shared time projection (:463-466)
     const float* dx = bw.dx[cur];
-    gemm_strided_f32(m.cin, h, int(M), static_cast<const float*>(c->a_in), 1, m.cinp, dx, h, 1, ga(0), h, 1.f, st);
+    lin(m.cin, h, int(M), static_cast<const float*>(c->a_in), 1, m.cinp, dx, h, 1, ga(0), h, 1.f);
     colsum_f32(dx, h, M, h, ga(1), st);
-    gemm_strided_f32(int(M), m.cin, h, dx, h, 1, pa(0), 1, h, bw.din, m.cin, 0.f, st);
+    lin(int(M), m.cin, h, dx, h, 1, pa(0), 1, h, bw.din, m.cin, 0.f);
     time_bwd(bw.demb, c->feat, pa(tail + 0), pa(tail + 1), td, ga(tail + 0), ga(tail + 1), st);
 }
 

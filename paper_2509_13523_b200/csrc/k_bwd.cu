@@ -637,14 +637,38 @@ void vt_bf16(const float* v, i64 planes, int s, int d, __nv_bfloat16* vt, cudaSt
 // tb (same layout) and multiplied by one tcgen05 GEMM with FP32 accumulation. The backward's linears
 // take this path when it runs in BF16 (swf_set_backward_precision): data gradients with both operands
 // K-major, weight gradients (K = tokens) with both MN-major, straight from the row-major activations.
+// rows x cols of a row-major fp32 matrix (pitch ld) into bf16 rows of pitch ldo (ldo >= cols; the
+// pad columns are zeroed)
+__global__ void k_to_bf16_2d(const float* __restrict__ x, i64 rows, int cols, i64 ld, __nv_bfloat16* __restrict__ y,
+                             int ldo) {
+    const i64 n = rows * ldo;
+    for (i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += i64(gridDim.x) * blockDim.x) {
+        const i64 r = t / ldo;
+        const int c = int(t - r * ldo);
+        y[t] = __float2bfloat16_rn(c < cols ? x[r * ld + c] : 0.f);
+    }
+}
 void gemm_strided_tc(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj, float* C,
                      i64 ldc, float beta, __nv_bfloat16* ta, __nv_bfloat16* tb, int* sched, cudaStream_t st) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const bool a_mn = sai == 1 && sak != 1, b_mn = sbj == 1 && sbk != 1;
     const i64 lda = a_mn ? sak : sai, ldb = b_mn ? sbk : sbj;
-    to_bf16(A, a_mn ? i64(K) * lda : i64(M) * lda, ta, st);
-    to_bf16(B, b_mn ? i64(K) * ldb : i64(N) * ldb, tb, st);
-    gemm_bf16_general(ta, a_mn, lda, tb, b_mn, ldb, M, N, K, C, ldc, beta != 0.f, sched, st);
+    // the bf16 copies keep the layout; pitches rounded up to 8 elements (16-byte TMA rows)
+    auto conv = [&](const float* x, i64 rows, int cols, i64 ld, __nv_bfloat16* y) -> i64 {
+        const i64 ldo = (ld % 8 == 0) ? ld : (cols + 7) / 8 * 8;
+        if (ldo == ld) {
+            to_bf16(x, rows * ld, y, st);
+        } else {
+            const i64 n = rows * ldo;
+            k_to_bf16_2d<<<unsigned(std::min<i64>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(x, rows, cols, ld, y,
+                                                                                              int(ldo));
+            SWF_LAUNCH_CHECK();
+        }
+        return ldo;
+    };
+    const i64 pa = a_mn ? conv(A, K, M, lda, ta) : conv(A, M, K, lda, ta);
+    const i64 pb = b_mn ? conv(B, K, N, ldb, tb) : conv(B, N, K, ldb, tb);
+    gemm_bf16_general(ta, a_mn, pa, tb, b_mn, pb, M, N, K, C, ldc, beta != 0.f, sched, st);
 }
 void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h, const float* g, const float* a,
               const float* b, const float* gate, float* dX, int lddx, float* rms, float* dg, float* da, float* db,
