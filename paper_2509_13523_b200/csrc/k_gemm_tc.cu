@@ -384,6 +384,26 @@ __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, i
 #pragma unroll
         for (int rr = 0; rr < 32; ++rr)
             if (rr < mrem && col_ok) ep.x[(row0 + rr) * h + n] = stg[rr * 33 + lane];
+    } else if (MODE == EPI_RESID && mrem >= 32 && n0 + 32 <= ep.N) {
+        // out projection, full 32 x 32 chunk (the common case): in place, so the bf16 copy's rows are
+        // addressed directly (no pointer shuffles) and no per-row predicates
+        float* xs = ep.x + row0 * h + n;
+        float xv[32];
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) xv[rr] = xs[i64(rr) * h];
+        if (ep.nss) {
+            __nv_bfloat16* db = reinterpret_cast<__nv_bfloat16*>(ep.x + ep.off_xb) + row0 * ep.hp + n;
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+                const float o = xv[rr] + stg[rr * 33 + lane];
+                xs[i64(rr) * h] = o;
+                db[i64(rr) * ep.hp] = __float2bfloat16_rn(o);
+                stg[rr * 33 + lane] = o;
+            }
+        } else {
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) xs[i64(rr) * h] = xv[rr] + stg[rr * 33 + lane];
+        }
     } else {
         // all 32 row reads in flight before any dependent store (latency hiding with 4 warps)
         float xv[32];
