@@ -177,6 +177,7 @@ def cpu_sample(windows: int, blocks: int) -> dict:
     """Oracle (fp32, all host threads) on `windows` 60x60 windows x `blocks` blocks at the C2
     widths; returns pixels/s extrapolated per FLOP to the full 20-block 720x1440 step."""
     from oracle import pyoracle as o
+    o.use_all_cores()
     c = dict(CFG, n_layers=1, blocks_per_layer=blocks)
     oc = o.ModelConfig(**c)
     p = o.init_params(oc, SEED, random=False, dtype=np.float32)
@@ -199,6 +200,7 @@ def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
     from oracle import pyoracle as o
+    o.use_all_cores()  # all host threads, also under torchrun (which exports OMP_NUM_THREADS=1)
     c = dict(CFG, n_layers=1, blocks_per_layer=1)
     oc = o.ModelConfig(**c)
     p = o.init_params(oc, SEED, random=False, dtype=np.float32)

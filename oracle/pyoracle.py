@@ -521,3 +521,10 @@ def shift_transfer_total(H, W, w, s_from, s_to, a, b, sp=1):
 
 def num_threads() -> int:
     return lib().orc_num_threads()
+
+
+def use_all_cores() -> int:
+    """OpenMP threads = the host cores this process may run on (torchrun sets OMP_NUM_THREADS=1)."""
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    lib().orc_set_num_threads(n)
+    return num_threads()

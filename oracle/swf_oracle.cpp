@@ -1282,4 +1282,12 @@ int orc_num_threads() {
 #endif
 }
 
+void orc_set_num_threads(int n) {  // torchrun exports OMP_NUM_THREADS=1: the CPU baselines undo it
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 }  // extern "C"
