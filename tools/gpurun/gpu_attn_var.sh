@@ -1,5 +1,5 @@
 # Attention build variants (paper_2509_13523_b200/_build/var/lib_*.so via SWF_LIB): kernel isolation
-# time and energy, repeated twice in alternating order. usage: bash tools/gpu_attn_var.sh TAG
+# time and energy, repeated twice in alternating order. usage: bash tools/gpurun/gpu_attn_var.sh TAG
 T=${1:-av}
 for rep in 1 2; do
   for lib in paper_2509_13523_b200/_build/var/lib_*.so; do

@@ -1,5 +1,5 @@
 # Round-end validation on a 2-GPU box: GPU tests, smoke, the default bench, and the C5 / training
-# workloads on 2 GPUs. usage: bash tools/gpu_final.sh TAG
+# workloads on 2 GPUs. usage: bash tools/gpurun/gpu_final.sh TAG
 T=${1:-final}
 timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/${T}_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?"

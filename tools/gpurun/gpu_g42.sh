@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_c2_spot.py tests/test_gpu_group.py -x -q > gpurun_out/g42_t.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/g42_t.log
-bash tools/gpu_var_cycles.sh g42 qkv_gemm k_gemm_tc
+bash tools/gpurun/gpu_var_cycles.sh g42 qkv_gemm k_gemm_tc

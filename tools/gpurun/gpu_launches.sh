@@ -1,5 +1,5 @@
 # GPU test suite + smoke + default bench + ncu launch list of the same bench command.
-# usage: bash tools/gpu_launches.sh TAG
+# usage: bash tools/gpurun/gpu_launches.sh TAG
 T=${1:-launch}
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?"

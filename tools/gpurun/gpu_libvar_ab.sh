@@ -1,5 +1,5 @@
 # A/B of library build variants (paper_2509_13523_b200/_build/var/lib_*.so via SWF_LIB): kernel
-# isolation of the GEMM classes and ncu tensor-pipe activity. usage: bash tools/gpu_libvar_ab.sh TAG
+# isolation of the GEMM classes and ncu tensor-pipe activity. usage: bash tools/gpurun/gpu_libvar_ab.sh TAG
 T=${1:-var}
 for lib in paper_2509_13523_b200/_build/var/lib_*.so; do
   v=$(basename $lib .so)

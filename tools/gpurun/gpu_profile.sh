@@ -1,5 +1,5 @@
 # ncu evidence for profiles/: launch list of the default bench command, and a full capture of the
-# attention kernel and of the GEMMs (one step). usage: bash tools/gpu_profile.sh TAG
+# attention kernel and of the GEMMs (one step). usage: bash tools/gpurun/gpu_profile.sh TAG
 T=${1:-prof}
 timeout 900 python bench.py > gpurun_out/${T}_plain.log 2>&1; rc=$?; echo "plain bench rc=$rc"
 [ $rc -eq 0 ] || exit 1

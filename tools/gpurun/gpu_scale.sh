@@ -1,4 +1,4 @@
-# WP scaling lines (contiguous ownership) on 2 and 4 GPUs of one box; usage: bash tools/gpu_scale.sh TAG
+# WP scaling lines (contiguous ownership) on 2 and 4 GPUs of one box; usage: bash tools/gpurun/gpu_scale.sh TAG
 T=${1:-scale}
 for n in 2 4; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2964$n \

@@ -1,6 +1,6 @@
 # Variant A/B at locked base clocks: for every paper_2509_13523_b200/_build_variants/*.so, ncu
 # --clock-control base over kbench's kernel classes (median of the launches), then kernel isolation
-# at free clocks (ms, J/launch). usage: bash tools/gpu_var_cycles.sh TAG CLASSES KERNEL_REGEX
+# at free clocks (ms, J/launch). usage: bash tools/gpurun/gpu_var_cycles.sh TAG CLASSES KERNEL_REGEX
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 T=${1:-var}; CL=${2:-out_gemm,down_gemm}; KR=${3:-k_gemm_tc}

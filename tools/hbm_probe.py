@@ -1,7 +1,7 @@
 """HBM-bound kernels of the C2 sampler / forward path (for ncu): one forecast_step (1 solver step = 2
 denoiser evaluations, churn on) through the C-ABI host-buffer call on the 720x1440 grid, after one
 warm-up call. Run under ncu with the metrics gpu__time_duration.sum, dram__bytes_read.sum and
-dram__bytes_write.sum and a kernel filter for the elementwise / gather kernels (tools/gpu_hbm.sh)."""
+dram__bytes_write.sum and a kernel filter for the elementwise / gather kernels (tools/gpurun/gpu_hbm.sh)."""
 import os
 import sys
 
