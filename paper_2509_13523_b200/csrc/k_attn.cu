@@ -76,7 +76,7 @@ constexpr int BKV = 128;  // keys per tile
 // softmax threads per query row (each takes BKV / kSplit keys of every tile); 4 control warps +
 // 4 * kSplit softmax warps. 2 is the default: with 4 (640 threads) the C2 launch is ~5% slower --
 // the softmax is bound by its sub-partition's issue / MUFU throughput, not by per-thread latency
-// (tools/gpu_attn_ab.sh).
+// (tools/gpurun/gpu_attn_ab.sh).
 #ifndef SWF_ATTN_SPLIT
 #define SWF_ATTN_SPLIT 2
 #endif
@@ -85,7 +85,7 @@ constexpr int kSplit = SWF_ATTN_SPLIT;
 #define SWF_ATTN_POLY8 2
 #endif
 // exponentials per 8 evaluated by the FMA-pipe polynomial: 0..2 of 8 measured equal within noise and
-// ~5% faster / ~25% less energy than 4 of 8 (tools/gpu_attn_poly.sh)
+// ~5% faster / ~25% less energy than 4 of 8 (tools/gpurun/gpu_attn_poly.sh)
 constexpr int kPoly8 = SWF_ATTN_POLY8;
 constexpr int kKPT = 128 / kSplit;  // keys per thread per tile
 constexpr int kThreads = 128 + 128 * kSplit;
