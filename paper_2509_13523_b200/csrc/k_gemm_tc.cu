@@ -649,13 +649,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + c * 32) : "memory");
                 }
 #endif
-            mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
-            tc_fence_after();
-            const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
-            // fused RMSNorm + AdaLN of operand A's rows (consumers): 1 / rms from the producer partials
+            // row-only epilogue inputs load while the accumulator is computed: 1 / rms from the producer
+            // partials (fused RMSNorm + AdaLN of operand A's rows) and the QKV row's window / RoPE positions
             float inv_r = 1.f;
             if constexpr (MODE == EPI_QKV || MODE == EPI_SWIGLU || MODE == EPI_DECODE)
                 if (ep.inv_r && row < ep.M) inv_r = ep.inv_r[row];
+            [[maybe_unused]] QkvRow qr;
+            if constexpr (MODE == EPI_QKV) qr = qkv_row(ep, row);
+            mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
             auto normed = [&](float* v, int col) {
                 if constexpr (MODE == EPI_QKV || MODE == EPI_SWIGLU || MODE == EPI_DECODE) {
                     if (ep.inv_r) {
@@ -720,8 +723,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             } else {
                 constexpr int NCH = BN / 32;
                 float ssum = 0.f;
-                [[maybe_unused]] QkvRow qr;
-                if constexpr (MODE == EPI_QKV) qr = qkv_row(ep, row);
 #pragma unroll 1
                 for (int ch = half * NCH / 2; ch < (half + 1) * NCH / 2; ++ch) {
                     float v[32];
