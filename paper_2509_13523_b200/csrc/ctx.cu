@@ -3162,6 +3162,7 @@ int swf_set_backward_precision(swf_ctx* c, int precision) {
         if (tc)
             require(c->m.h % 8 == 0 && c->m.f % 8 == 0,
                     "BF16 backward: hidden_dim and ffn_dim must be multiples of 8 (16-byte operand rows)");
+        SWF_CUDA(cudaSetDevice(c->dev));
         SWF_CUDA(cudaStreamSynchronize(c->st));
         c->bwd_tc = tc;
         if (tc && c->bw_alloc) alloc_bwd_tc(c);  // work buffers exist already: add the operand copies
