@@ -8,6 +8,11 @@ namespace {
 
 constexpr int kThreads = 256;
 
+inline bool aligned16(const void* a, const void* b, const void* c, const void* d) {
+    return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(c) |
+             reinterpret_cast<uintptr_t>(d)) & 15) == 0;
+}
+
 inline int grid_for(i64 n, int per_block = kThreads) {
     i64 g = (n + per_block - 1) / per_block;
     if (g > 148 * 64) g = 148 * 64;
@@ -124,6 +129,9 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const float* __restrict__ 
         if (C % 4 == 0)
             for (int q = lane; q < C / 4; q += 32)
                 reinterpret_cast<float4*>(o)[q] = __ldg(reinterpret_cast<const float4*>(r) + q);
+        else if (C % 2 == 0)  // e.g. the decode output's 70 channels: 8-byte vectors
+            for (int q = lane; q < C / 2; q += 32)
+                reinterpret_cast<float2*>(o)[q] = __ldg(reinterpret_cast<const float2*>(r) + q);
         else
             for (int c = lane; c < C; c += 32) o[c] = __ldg(r + c);
     }
@@ -186,16 +194,78 @@ __global__ void __launch_bounds__(256) k_rms_mod(const float* __restrict__ x, i6
 // ---------------------------------------------------------------- sampler
 // xa and y may alias (stage 2 updates the state in place): no __restrict__ on either; each element is
 // read and written by one thread, in that order
+// VEC: 16-byte accesses (all pointers 16-byte aligned, checked by the launcher) plus a scalar tail
+template <bool VEC>
 __global__ void k_sampler_update(const float* xa, const float* __restrict__ xd, const float* __restrict__ v, i64 n,
                                  float cs, float sn, float c1, float c2, float* y, int* flags, int slot) {
     bool bad = false;
-    for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
-        const float d = cs * xd[i] - sn * v[i];
-        const float r = c1 * xa[i] - c2 * d;
-        y[i] = r;
+    auto one = [&](float a, float d0, float w) {
+        const float d = cs * d0 - sn * w;
+        const float r = c1 * a - c2 * d;
         bad |= !isfinite(r);
+        return r;
+    };
+    const i64 stride = i64(gridDim.x) * blockDim.x, t0 = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+    i64 done = 0;
+    if constexpr (VEC) {
+        const i64 n4 = n >> 2;
+        for (i64 i = t0; i < n4; i += stride) {
+            const float4 a = reinterpret_cast<const float4*>(xa)[i], d = __ldg(reinterpret_cast<const float4*>(xd) + i),
+                         w = __ldg(reinterpret_cast<const float4*>(v) + i);
+            reinterpret_cast<float4*>(y)[i] =
+                make_float4(one(a.x, d.x, w.x), one(a.y, d.y, w.y), one(a.z, d.z, w.z), one(a.w, d.w, w.w));
+        }
+        done = 4 * n4;
     }
+    for (i64 i = done + t0; i < n; i += stride) y[i] = one(xa[i], xd[i], v[i]);
     if (flags && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_nonfinite(flags, slot);
+}
+
+template <class T>
+__device__ __forceinline__ void store_cvt2(T* p, float a, float b);
+template <>
+__device__ __forceinline__ void store_cvt2<float>(float* p, float a, float b) {
+    *reinterpret_cast<float2*>(p) = make_float2(a, b);
+}
+template <>
+__device__ __forceinline__ void store_cvt2<__nv_bfloat16>(__nv_bfloat16* p, float a, float b) {
+    *reinterpret_cast<uint32_t*>(p) = pack_bf16x2(a, b);
+}
+// The sampler's input assembly, one warp per row and channel pairs (cp, cf, cin, kp even; checked by
+// the launchers, which fall back to the element-wise kernels below otherwise).
+template <class T>
+__global__ void __launch_bounds__(256) k_build_static_rows(const float* __restrict__ xp, const float* __restrict__ fo,
+                                                           const float* __restrict__ pe, i64 M, int cp, int cf,
+                                                           int cin, int kp, T* __restrict__ a_in) {
+    const int lane = threadIdx.x & 31;
+    for (i64 i = i64(blockIdx.x) * 8 + (threadIdx.x >> 5); i < M; i += i64(gridDim.x) * 8) {
+        for (int c = cp + 2 * lane; c < kp; c += 64) {  // channels [cp, kp): x_prev, forcings, zero pad
+            float2 v = make_float2(0.f, 0.f);
+            if (c < 2 * cp) {
+                const float2 a = __ldg(reinterpret_cast<const float2*>(xp + i * cp + (c - cp)));
+                const float2 p = __ldg(reinterpret_cast<const float2*>(pe + i * cin + c));
+                v = make_float2(a.x + p.x, a.y + p.y);
+            } else if (c < cin) {
+                const float2 a = __ldg(reinterpret_cast<const float2*>(fo + i * cf + (c - 2 * cp)));
+                const float2 p = __ldg(reinterpret_cast<const float2*>(pe + i * cin + c));
+                v = make_float2(a.x + p.x, a.y + p.y);
+            }
+            store_cvt2<T>(a_in + i * kp + c, v.x, v.y);
+        }
+    }
+}
+template <class T>
+__global__ void __launch_bounds__(256) k_assemble_state_rows(const float* __restrict__ x, const float* __restrict__ pe,
+                                                             i64 M, int cp, int cin, int kp, float sd,
+                                                             T* __restrict__ a_in) {
+    const int lane = threadIdx.x & 31;
+    for (i64 i = i64(blockIdx.x) * 8 + (threadIdx.x >> 5); i < M; i += i64(gridDim.x) * 8) {
+        for (int c = 2 * lane; c < cp; c += 64) {
+            const float2 a = __ldg(reinterpret_cast<const float2*>(x + i * cp + c));
+            const float2 p = __ldg(reinterpret_cast<const float2*>(pe + i * cin + c));
+            store_cvt2<T>(a_in + i * kp + c, a.x / sd + p.x, a.y / sd + p.y);
+        }
+    }
 }
 
 template <class T>
@@ -265,22 +335,52 @@ __global__ void k_churn(float* __restrict__ x, LayMap lay, i64 M, int C, const u
     }
 }
 
+// per-channel affine maps over [M][C] rows; VEC: 16-byte accesses, one channel modulo per 4 elements
+template <bool VEC>
 __global__ void k_standardize(const float* __restrict__ x, i64 M, int C, const float* __restrict__ mean,
                               const float* __restrict__ sd, float* __restrict__ y) {
-    const i64 total = M * C;
-    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
-        const int c = int(e % C);
-        y[e] = (x[e] - mean[c]) / sd[c];
+    const i64 total = M * C, stride = i64(gridDim.x) * blockDim.x, t0 = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+    auto f = [&](float v, int c) { return (v - mean[c]) / sd[c]; };
+    i64 done = 0;
+    if constexpr (VEC) {
+        for (i64 i = t0; i < (total >> 2); i += stride) {
+            int c = int((4 * i) % C);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+            float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                o[k] = f(o[k], c);
+                if (++c == C) c = 0;
+            }
+            reinterpret_cast<float4*>(y)[i] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        done = total & ~i64(3);
     }
+    for (i64 e = done + t0; e < total; e += stride) y[e] = f(x[e], int(e % C));
 }
 
+template <bool VEC>
 __global__ void k_destd_add(const float* __restrict__ r, const float* __restrict__ base, i64 M, int C,
                             const float* __restrict__ mean, const float* __restrict__ sd, float* __restrict__ y) {
-    const i64 total = M * C;
-    for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
-        const int c = int(e % C);
-        y[e] = base[e] + (r[e] * sd[c] + mean[c]);
+    const i64 total = M * C, stride = i64(gridDim.x) * blockDim.x, t0 = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+    auto f = [&](float b, float v, int c) { return b + (v * sd[c] + mean[c]); };
+    i64 done = 0;
+    if constexpr (VEC) {
+        for (i64 i = t0; i < (total >> 2); i += stride) {
+            int c = int((4 * i) % C);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(r) + i),
+                         b = __ldg(reinterpret_cast<const float4*>(base) + i);
+            float o[4] = {v.x, v.y, v.z, v.w}, bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                o[k] = f(bb[k], o[k], c);
+                if (++c == C) c = 0;
+            }
+            reinterpret_cast<float4*>(y)[i] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        done = total & ~i64(3);
     }
+    for (i64 e = done + t0; e < total; e += stride) y[e] = f(base[e], r[e], int(e % C));
 }
 
 __global__ void k_check_finite(const float* __restrict__ x, i64 n, int* flags, int slot) {
@@ -432,14 +532,20 @@ template void rms_modulate<__nv_bfloat16>(const float*, i64, int, int, const flo
 
 void sampler_update(const float* xa, const float* xd, const float* v, i64 n, float cs, float sn, float c1, float c2,
                     float* y, int* flags, int slot, cudaStream_t st) {
-    k_sampler_update<<<grid_for(n), kThreads, 0, st>>>(xa, xd, v, n, cs, sn, c1, c2, y, flags, slot);
+    if (aligned16(xa, xd, v, y))
+        k_sampler_update<true><<<grid_for((n + 3) / 4), kThreads, 0, st>>>(xa, xd, v, n, cs, sn, c1, c2, y, flags, slot);
+    else
+        k_sampler_update<false><<<grid_for(n), kThreads, 0, st>>>(xa, xd, v, n, cs, sn, c1, c2, y, flags, slot);
     SWF_LAUNCH_CHECK();
 }
 
 template <class T>
 void build_static_input(const float* xprev, const float* forc, const float* pe, i64 M, int cp, int cf, int cin,
                         int kp, T* a_in, cudaStream_t st) {
-    k_build_static<T><<<grid_for(M * (kp - cp)), kThreads, 0, st>>>(xprev, forc, pe, M, cp, cf, cin, kp, a_in);
+    if (cp % 2 == 0 && cf % 2 == 0 && cin % 2 == 0 && kp % 2 == 0 && aligned16(xprev, forc, pe, a_in))
+        k_build_static_rows<T><<<grid_for(M, 8), kThreads, 0, st>>>(xprev, forc, pe, M, cp, cf, cin, kp, a_in);
+    else
+        k_build_static<T><<<grid_for(M * (kp - cp)), kThreads, 0, st>>>(xprev, forc, pe, M, cp, cf, cin, kp, a_in);
     SWF_LAUNCH_CHECK();
 }
 template void build_static_input<float>(const float*, const float*, const float*, i64, int, int, int, int, float*,
@@ -450,7 +556,10 @@ template void build_static_input<__nv_bfloat16>(const float*, const float*, cons
 template <class T>
 void assemble_state(const float* x, const float* pe, i64 M, int cp, int cin, int kp, float sd, T* a_in,
                     cudaStream_t st) {
-    k_assemble_state<T><<<grid_for(M * cp), kThreads, 0, st>>>(x, pe, M, cp, cin, kp, sd, a_in);
+    if (cp % 2 == 0 && cin % 2 == 0 && kp % 2 == 0 && aligned16(x, pe, a_in, a_in))
+        k_assemble_state_rows<T><<<grid_for(M, 8), kThreads, 0, st>>>(x, pe, M, cp, cin, kp, sd, a_in);
+    else
+        k_assemble_state<T><<<grid_for(M * cp), kThreads, 0, st>>>(x, pe, M, cp, cin, kp, sd, a_in);
     SWF_LAUNCH_CHECK();
 }
 template void assemble_state<float>(const float*, const float*, i64, int, int, int, float, float*, cudaStream_t);
@@ -470,13 +579,19 @@ void churn_rotate(float* x, const LayMap& lay0, i64 M, int C, const u64* key, u6
 }
 
 void standardize(const float* x, i64 M, int C, const float* mean, const float* stdv, float* y, cudaStream_t st) {
-    k_standardize<<<grid_for(M * C), kThreads, 0, st>>>(x, M, C, mean, stdv, y);
+    if (aligned16(x, y, x, y) && C >= 4)
+        k_standardize<true><<<grid_for((M * C + 3) / 4), kThreads, 0, st>>>(x, M, C, mean, stdv, y);
+    else
+        k_standardize<false><<<grid_for(M * C), kThreads, 0, st>>>(x, M, C, mean, stdv, y);
     SWF_LAUNCH_CHECK();
 }
 
 void destandardize_add(const float* r, const float* base, i64 M, int C, const float* mean, const float* stdv,
                        float* y, cudaStream_t st) {
-    k_destd_add<<<grid_for(M * C), kThreads, 0, st>>>(r, base, M, C, mean, stdv, y);
+    if (aligned16(r, base, y, y) && C >= 4)
+        k_destd_add<true><<<grid_for((M * C + 3) / 4), kThreads, 0, st>>>(r, base, M, C, mean, stdv, y);
+    else
+        k_destd_add<false><<<grid_for(M * C), kThreads, 0, st>>>(r, base, M, C, mean, stdv, y);
     SWF_LAUNCH_CHECK();
 }
 
@@ -491,10 +606,14 @@ void preload_elem_kernels() {
     const void* k[] = {
         (const void*)k_time_features, (const void*)k_time_embed, (const void*)k_ada,
         (const void*)k_gather_rows<float>, (const void*)k_gather_rows<__nv_bfloat16>, (const void*)k_scatter_rows,
-        (const void*)k_rms_mod<float>, (const void*)k_rms_mod<__nv_bfloat16>, (const void*)k_sampler_update,
+        (const void*)k_rms_mod<float>, (const void*)k_rms_mod<__nv_bfloat16>, (const void*)k_sampler_update<true>,
+        (const void*)k_sampler_update<false>,
         (const void*)k_build_static<float>, (const void*)k_build_static<__nv_bfloat16>,
+        (const void*)k_build_static_rows<float>, (const void*)k_build_static_rows<__nv_bfloat16>,
+        (const void*)k_assemble_state_rows<float>, (const void*)k_assemble_state_rows<__nv_bfloat16>,
         (const void*)k_assemble_state<float>, (const void*)k_assemble_state<__nv_bfloat16>, (const void*)k_noise,
-        (const void*)k_churn, (const void*)k_standardize, (const void*)k_destd_add, (const void*)k_check_finite,
+        (const void*)k_churn, (const void*)k_standardize<true>, (const void*)k_standardize<false>,
+        (const void*)k_destd_add<true>, (const void*)k_destd_add<false>, (const void*)k_check_finite,
         (const void*)k_prep_residual, (const void*)k_rows_at_pixels, (const void*)k_fold_adaln, (const void*)k_inv_rms};
     for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
 }
