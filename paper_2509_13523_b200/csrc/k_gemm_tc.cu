@@ -8,6 +8,8 @@
 #include <cuda.h>
 
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -436,17 +438,17 @@ __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, i
     return ss;
 }
 
-// Dynamic tile schedule: the leader CTA's producer thread takes tile indices from a global counter
-// (atomicAdd, one per tile) and publishes them through a kQ-slot ring in both CTAs' shared memory;
-// every consumer role (the peer's producer, the MMA thread, the 16 epilogue warps) reads its next
-// tile from the ring. Clusters then take tiles in index order as they free up, so the clusters
+// Dynamic tile schedule: a scheduler thread of the leader CTA (warp 3) takes tile indices from a
+// global counter (atomicAdd, one per tile) and publishes them through a kQ-slot ring in both CTAs'
+// shared memory; every consumer role (both producers, the MMA thread, the 16 epilogue warps) reads
+// its next tile from the ring, with CTA-scope synchronisation in the scheduler's CTA. Clusters then take tiles in index order as they free up, so the clusters
 // sharing an A row block (consecutive indices) start it together and its K slices are fetched from
 // HBM once, instead of drifting apart over the static round-robin schedule (which re-read A ~3x).
 constexpr int kQ = 4;
 #ifndef SWF_GEMM_XPF
 #define SWF_GEMM_XPF 1
 #endif
-constexpr uint32_t kQConsumers = 1 /*peer producer*/ + 1 /*MMA*/ + 2 * kEpiWarps;
+constexpr uint32_t kQConsumers = 2 /*producers*/ + 1 /*MMA*/ + 2 * kEpiWarps;
 struct TileQueue {
     uint64_t* full;  // [kQ], one arrival (the scheduler) per round, in each CTA
     uint64_t* empty; // [kQ], kQConsumers arrivals per round, leader CTA only
@@ -454,8 +456,9 @@ struct TileQueue {
     int* counter;    // global; nullptr -> static round-robin schedule
     i64 total;
     int cluster_id, n_clusters;
-    // scheduler (leader producer): publish the i-th tile of this cluster
-    __device__ void publish(int i) {
+    bool local;      // this thread runs in the leader CTA (the scheduler's): CTA-scope synchronisation
+    // scheduler (leader CTA, its own thread): publish the i-th tile of this cluster; returns it
+    __device__ int publish(int i) {
         const int slot = i % kQ;
         const uint32_t round = uint32_t(i / kQ);
         mbar_wait_acquire_cluster(smem_u32(&empty[slot]), (round & 1) ^ 1);
@@ -465,6 +468,7 @@ struct TileQueue {
         st_cluster_u32(map_to_rank(smem_u32(&tile[slot]), 1), uint32_t(v));
         mbar_arrive_release_cluster(map_to_rank(smem_u32(&full[slot]), 1));
         mbar_arrive_release_cluster(smem_u32(&full[slot]));
+        return v;
     }
     // consumer: the i-th tile (-1: done); arrive = whether this thread signals the slot free
     __device__ i64 next(int i, bool arrive) {
@@ -473,6 +477,12 @@ struct TileQueue {
             return t < total ? t : -1;
         }
         const int slot = i % kQ;
+        if (local) {  // same CTA as the scheduler: CTA-scope acquire / release (no cluster-wide fence)
+            mbar_wait(smem_u32(&full[slot]), uint32_t(i / kQ) & 1);
+            const int v = *reinterpret_cast<volatile int*>(&tile[slot]);
+            if (arrive) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[slot])) : "memory");
+            return v;
+        }
         mbar_wait_acquire_cluster(smem_u32(&full[slot]), uint32_t(i / kQ) & 1);
         const int v = *reinterpret_cast<volatile int*>(&tile[slot]);
         if (arrive) mbar_arrive_release_cluster(map_to_rank(smem_u32(&empty[slot]), 0));
@@ -480,6 +490,18 @@ struct TileQueue {
     }
 };
 
+#ifdef SWF_GEMM_TRACE
+// development build only: clock64 stamps of cluster 0's MMA thread per tile: [0] before the tile-queue
+// read, [1] after it, [2] after the accumulator-free wait, [3] after the tile's last commit, [4] cycles
+// spent waiting for operand stages within the tile
+constexpr int kGTr = 2048;
+__device__ unsigned long long g_gtrace[5][kGTr];
+inline void* g_gtrace_ptr() {
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, g_gtrace);
+    return p;
+}
+#endif
 // ---------------------------------------------------------------- the kernel
 // MN: operand majors, bit 0 = A MN-major (A stored [K][M]), bit 1 = B MN-major (B stored [K][N]); 0 =
 // both K-major (the forward's layout)
@@ -538,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    TileQueue tq{q_full, q_empty, q_tile, sched, total, cluster_id, n_clusters};
+    TileQueue tq{q_full, q_empty, q_tile, sched, total, cluster_id, n_clusters, leader};
 
     if (warp == 0) {
         // ===== TMA producer (both CTAs; each loads its A half and B half, signalling the leader)
@@ -547,10 +569,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
-            const bool sched_here = sched && leader;
-            if (sched_here) tq.publish(0);
+
             for (int i = 0;; ++i) {
-                const i64 t = tq.next(i, !leader);
+                const i64 t = tq.next(i, true);
                 if (t < 0) break;
                 int m_blk, n_blk;
                 tile_coords(t, n_tiles, m_tiles, group_m, m_blk, n_blk);
@@ -576,9 +597,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     } else {
                         tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK, row_b, pol_b);
                     }
-                    // the next tile is taken once this tile's first stage is in flight, so the
-                    // atomic's round trip overlaps the loads (one tile ahead of every consumer)
-                    if (sched_here && kb == 0) tq.publish(i + 1);
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -586,6 +604,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
         }
+    } else if (warp == 3) {
+        // ===== tile scheduler (leader CTA, one thread): takes tile indices from the global counter and
+        // publishes them up to kQ tiles ahead, off the producer's path (the atomic's round trip had
+        // stalled the operand loads ~2 K cycles per tile)
+        if (leader && lane == 0 && sched)
+            for (int i = 0;; ++i)
+                if (tq.publish(i) < 0) break;
     } else if (warp == 1) {
         // ===== MMA issuer (leader CTA, one thread)
         if (leader && lane == 0) {
@@ -594,12 +619,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int i = 0;; ++i) {
+#ifdef SWF_GEMM_TRACE
+                const bool tr = blockIdx.x == 0 && i < kGTr;
+                unsigned long long fw = 0;
+                if (tr) g_gtrace[0][i] = clock64();
+#endif
                 if (tq.next(i, true) < 0) break;
+#ifdef SWF_GEMM_TRACE
+                if (tr) g_gtrace[1][i] = clock64();
+#endif
                 mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
                 tc_fence_after();
+#ifdef SWF_GEMM_TRACE
+                if (tr) g_gtrace[2][i] = clock64();
+#endif
                 const uint32_t dtm = tmem_base + uint32_t(acc * BN);
                 for (int kb = 0; kb < num_k; ++kb) {
+#ifdef SWF_GEMM_TRACE
+                    const unsigned long long w0 = clock64();
                     mbar_wait(smem_u32(&full_bar[stage]), phase);
+                    fw += clock64() - w0;
+#else
+                    mbar_wait(smem_u32(&full_bar[stage]), phase);
+#endif
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * C::kStageA);
                     const uint32_t b0 = smem_u32(sB + stage * C::kStageB);
@@ -616,6 +658,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
                 umma_commit_mc(smem_u32(&tfull_bar[acc]), 0x3);
+#ifdef SWF_GEMM_TRACE
+                if (tr) {
+                    g_gtrace[3][i] = clock64();
+                    g_gtrace[4][i] = fw;
+                }
+#endif
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -820,6 +868,20 @@ void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiP
     static const int env_gm = getenv("SWF_GEMM_GROUPM") ? std::max(1, atoi(getenv("SWF_GEMM_GROUPM"))) : 0;
     const int group_m = env_gm ? env_gm : 1;
     SWF_CUDA(cudaLaunchKernelEx(&cfg, kern, *a, *b, M, n_tiles, K / BK, ep, sched, group_m));
+#ifdef SWF_GEMM_TRACE
+    if (const char* path = getenv("SWF_GEMM_TRACE_OUT")) {  // appends: mode, then the five rows
+        static unsigned long long h[5][kGTr];
+        SWF_CUDA(cudaStreamSynchronize(st));
+        SWF_CUDA(cudaMemcpyFromSymbol(h, g_gtrace, sizeof(h)));
+        if (FILE* f = fopen(path, "ab")) {
+            const unsigned long long tag = (unsigned long long)(MODE * 1000 + BN);
+            fwrite(&tag, 8, 1, f);
+            fwrite(h, sizeof(h), 1, f);
+            fclose(f);
+        }
+        SWF_CUDA(cudaMemset(g_gtrace_ptr(), 0, sizeof(h)));
+    }
+#endif
 }
 
 template <int BN>
