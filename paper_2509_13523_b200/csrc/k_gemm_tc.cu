@@ -27,14 +27,22 @@ constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, each draining half of the columns
 
-template <int BN>
+// The gate/up GEMM (SwiGLU epilogue, no shared-memory transposes) gives the epilogue staging space to a
+// 7th operand stage at BN = 256: 55.9 -> 55.0 M cycles at base clock (the QKV GEMM measured 1% slower
+// with 7, so every other mode keeps 6; SWF_GEMM_DEEP=0: 6 stages everywhere)
+#ifndef SWF_GEMM_DEEP
+#define SWF_GEMM_DEEP 1
+#endif
+constexpr bool uses_stg(int mode) { return mode != EPI_SWIGLU; }
+
+template <int BN, bool STG = true>
 struct Cfg {
     static constexpr int kStageA = BM * BK * 2;
     static constexpr int kStageB = (BN / 2) * BK * 2;
     static constexpr int kStage = kStageA + kStageB;
-    static constexpr int kStages = (BN == 256) ? 6 : 8;
+    static constexpr int kStages = (BN == 256) ? ((STG || !SWF_GEMM_DEEP) ? 6 : 7) : 8;
     static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
-    static constexpr int kStageFloats = kEpiWarps * 32 * 33;  // epilogue transpose buffers (32x33 per warp)
+    static constexpr int kStageFloats = (STG || !SWF_GEMM_DEEP) ? kEpiWarps * 32 * 33 : 0;  // epilogue transposes
     static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/ + kStageFloats * 4;
     static constexpr uint32_t kIdesc = (1u << 4)                 // D = F32
                                        | (1u << 7) | (1u << 10)  // A, B = BF16
@@ -509,7 +517,7 @@ template <int BN, int MODE, int MN = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, i64 M, int n_tiles,
               int num_k, EpiParams ep, int* sched, int group_m) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, uses_stg(MODE)>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -834,7 +842,7 @@ int* sched_counter() {
 
 template <int BN, int MODE, int MN = 0>
 void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiParams& ep, cudaStream_t st) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, uses_stg(MODE)>;
     auto kern = k_gemm_tc<BN, MODE, MN>;  // shared-memory limit set per device by preload_gemm_kernels
     const int n_tiles = Npad / BN;
     const i64 m_tiles = (M + 2 * BM - 1) / (2 * BM);
@@ -931,16 +939,22 @@ void make_tma_bf16_2d(TmaMap* m, const void* base, i64 rows, i64 inner, int box_
 
 template <int BN>
 void preload_bn(cudaFuncAttributes& a) {
-    const void* k[] = {(const void*)k_gemm_tc<BN, EPI_ENCODE>, (const void*)k_gemm_tc<BN, EPI_QKV>,
-                       (const void*)k_gemm_tc<BN, EPI_RESID>, (const void*)k_gemm_tc<BN, EPI_SWIGLU>,
-                       (const void*)k_gemm_tc<BN, EPI_DOWN>, (const void*)k_gemm_tc<BN, EPI_DECODE>,
-                       (const void*)k_gemm_tc<BN, EPI_RESID, 3>, (const void*)k_gemm_tc<BN, EPI_RESID, 2>,
-                       (const void*)k_gemm_tc<BN, EPI_STORE, 0>, (const void*)k_gemm_tc<BN, EPI_STORE, 3>,
-                       (const void*)k_gemm_tc<BN, EPI_STORE, 2>};
-    for (const void* f : k) {
+    auto set = [&](const void* f, int smem) {
         SWF_CUDA(cudaFuncGetAttributes(&a, f));
-        SWF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem));
-    }
+        SWF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    };
+    constexpr int kS = Cfg<BN, true>::kSmem, kN = Cfg<BN, false>::kSmem;
+    set((const void*)k_gemm_tc<BN, EPI_ENCODE>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_QKV>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_SWIGLU>, kN);
+    set((const void*)k_gemm_tc<BN, EPI_DECODE>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_RESID>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_DOWN>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_RESID, 3>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_RESID, 2>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_STORE, 0>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_STORE, 3>, kS);
+    set((const void*)k_gemm_tc<BN, EPI_STORE, 2>, kS);
 }
 void preload_gemm_kernels() {
     cudaFuncAttributes a;

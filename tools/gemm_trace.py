@@ -12,7 +12,7 @@ names = {1: "QKV", 2: "out", 3: "gate/up", 4: "down", 0: "encode", 5: "decode"}
 for k in range(len(raw) // rec):
     r = raw[k * rec:(k + 1) * rec]
     tag, t = int(r[0]), r[1:].reshape(5, N)
-    n = int(np.count_nonzero(t[3]))
+    n = int(np.argmin(t[3] > 0)) if (t[3] == 0).any() else N  # tiles recorded (contiguous from 0)
     if n < 4:
         continue
     i = np.arange(1, n)
