@@ -8,6 +8,7 @@
 #include <cuda.h>
 
 #include <cstring>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -493,7 +494,12 @@ struct TileQueue {
         }
         mbar_wait_acquire_cluster(smem_u32(&full[slot]), uint32_t(i / kQ) & 1);
         const int v = *reinterpret_cast<volatile int*>(&tile[slot]);
-        if (arrive) mbar_arrive_release_cluster(map_to_rank(smem_u32(&empty[slot]), 0));
+        // a relaxed arrive (no cluster-wide fence): the branch on the loaded value orders the slot's
+        // read before the arrive that lets the scheduler overwrite it (v is never INT_MIN)
+        if (arrive && v != INT_MIN)
+            asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                             map_to_rank(smem_u32(&empty[slot]), 0))
+                         : "memory");
         return v;
     }
 };
