@@ -1223,12 +1223,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             pp::quad_sync(wq);
             const float m0 = red[r], m1 = red[BQ + r], l0 = red[2 * BQ + r], l1 = red[3 * BQ + r];
             pp::quad_sync(wq);  // both read before the next item's epilogue overwrites
+            if (warp == 4 && lane == 0) SWF_TR(2, n);
             const float M = fmaxf(m0, m1);
             const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
             const float inv = 1.f / (l0 * f0 + l1 * f1);
             const bool has1 = rg.ntiles >= 2;  // item-uniform: O1 holds this item's odd tiles
             mbar_wait(bar(pp::OD + 0), (cnt0 - 1) & 1);
             if (has1) mbar_wait(bar(pp::OD + 1), (cnt1 - 1) & 1);
+            if (warp == 4 && lane == 0) SWF_TR(3, n);
             fence_after();
             const uint32_t tO0 = lane_off + pp::kTO + uint32_t(grp * C::kOC), tO1 = tO0 + uint32_t(D);
             const int qb = n & 1;
@@ -1271,9 +1273,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
                                           pack_bf16x2(__uint_as_float(o[8 * v + 6]), __uint_as_float(o[8 * v + 7])));
                     }
                 }
+                if (warp == 4 && lane == 0) SWF_TR(4, n);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 fence_before();
                 pp::all_softmax_sync();
+                if (warp == 4 && lane == 0) SWF_TR(5, n);
                 if (leader) {
                     for (int bx = 0; bx < D / 64; ++bx)
                         tma_store_2d(&tmO, smem_u32(stg + bx * (BQ * 128)), (p.head0 + it.head) * D + bx * 64,

@@ -50,6 +50,9 @@ print(f"softmax: P(g) done -> S(g+2) ready med {med(w[wg2, g2 + 2] - w[16 + wg2,
 busy = np.maximum(0, w[wg2, g2 + 2] - w[16 + wg2, g2])
 print(f"softmax per own tile: work {med(p_done - s_regs) + med(s_regs - s_ready):.0f}, wait for S {np.mean(busy):.0f} (mean)")
 for n in range(1, 7):
+    if t[5, n]:
+        print(f"  epilogue item {n}: stats exchange {t[2, n] - t[8, n]}, last P V wait {t[3, n] - t[2, n]}, "
+              f"O read / merge / stage {t[4, n] - t[3, n]}, sync {t[5, n] - t[4, n]}, store issue + rest {t[9, n] - t[5, n]}")
     print(f"item {n}: epilogue {t[9, n] - t[8, n]} cyc; PV issuer saw O free {t[7, n] - t[9, n - 1] if n else 0} after "
           f"prev epilogue end; first S ready of item {w[0, starts[n]] - t[8, n - 1]} after prev epilogue start; tiles {starts[n + 1] - starts[n]}")
 # per-quadrant skew of S ready / P done for one tile
