@@ -386,11 +386,18 @@ __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, i
     const bool col_ok = n < ep.N;
     const int h = ep.h;
     const i64 mrem = ep.M - row0;  // rows of this 32-row group that exist
-    if constexpr (MODE == EPI_ENCODE) {
+    if constexpr (MODE == EPI_ENCODE) {  // x = acc + bias, plus the bf16 copy for the first block's norm
         const float b = col_ok ? ep.bias[n] : 0.f;
+        __nv_bfloat16* db = ep.nss ? reinterpret_cast<__nv_bfloat16*>(ep.x + ep.off_xb) + row0 * ep.hp + n : nullptr;
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr)
-            if (rr < mrem && col_ok) ep.x[(row0 + rr) * h + n] = stg[rr * 33 + lane] + b;
+        for (int rr = 0; rr < 32; ++rr) {
+            const float o = stg[rr * 33 + lane] + b;
+            if (rr < mrem && col_ok) {
+                ep.x[(row0 + rr) * h + n] = o;
+                if (ep.nss) db[i64(rr) * ep.hp] = __float2bfloat16_rn(o);
+            }
+            if (ep.nss) stg[rr * 33 + lane] = col_ok ? o : 0.f;
+        }
     } else if constexpr (MODE == EPI_STORE) {
 #pragma unroll
         for (int rr = 0; rr < 32; ++rr)
@@ -753,7 +760,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     normed(u, n_blk * BN + BN / 2 + ch * 32);
                     epi_swiglu32(ep, row, n_blk * (BN / 2) + ch * 32, g, u, pol_out);
                 }
-            } else if constexpr (MODE == EPI_DOWN || MODE == EPI_RESID || MODE == EPI_STORE) {
+            } else if constexpr (MODE == EPI_DOWN || MODE == EPI_RESID || MODE == EPI_STORE || MODE == EPI_ENCODE) {
                 float* drow = nullptr;
                 __nv_bfloat16* dbrow = nullptr;
                 float* dsrow = nullptr;
