@@ -1317,7 +1317,9 @@ void alloc_bwd_tc(swf_ctx* c) {
     c->bt_b = dalloc<__nv_bfloat16>(c, n);
     c->bt_c_n = M * wide;
     c->bt_c = dalloc<float>(c, c->bt_c_n);
-    if (c->world == 1 && m.d % 8 == 0) {
+    // the tensor-core attention pieces need the rank's own O rows (no sequence parallelism); window
+    // parallelism is fine -- attention is per window, every rank on its own windows
+    if (c->sp == 1 && m.d % 8 == 0) {
         auto& ws = c->bt_ws;
         ws.n = AttnBwdStreams::kMax;
         for (int i = 0; i < ws.n; ++i) {
@@ -1327,12 +1329,14 @@ void alloc_bwd_tc(swf_ctx* c) {
         }
         for (int i = 0; i <= ws.n; ++i) SWF_CUDA(cudaEventCreateWithFlags(&ws.ev[i], cudaEventDisableTiming));
     }
-    if (c->world == 1 && (m.d == 32 || m.d == 64 || m.d == 128)) {
+    if (c->sp == 1 && (m.d == 32 || m.d == 64 || m.d == 128)) {
         c->bt_qkv = dalloc<__nv_bfloat16>(c, size_t(3) * M * m.h);
         c->bt_o = dalloc<__nv_bfloat16>(c, M * size_t(m.hp));
-        c->d_bt_o = dalloc<void*>(c, 1);
-        void* o = c->bt_o;
-        h2d_sync(c, c->d_bt_o, &o, sizeof(void*));
+        // the kernel indexes the output table by the owning rank (wp_rank under window parallelism):
+        // every entry is this rank's buffer, its O rows are always its own tokens' (sp == 1)
+        c->d_bt_o = dalloc<void*>(c, 8);
+        std::vector<void*> o(8, c->bt_o);
+        h2d_sync(c, c->d_bt_o, o.data(), 8 * sizeof(void*));
         const int sw = m.d >= 64 ? 128 : 2 * m.d;
         const i64 rows = i64(c->lay[0].nloc) * m.heads * m.w * m.w;
         const __nv_bfloat16* qb = c->bt_qkv;

@@ -875,7 +875,10 @@ void preload_bwd_kernels() {
                        (const void*)k_colsum, (const void*)k_swiglu_bwd, (const void*)k_relayout,
                        (const void*)k_relayout_push, (const void*)k_attn_bwd_q, (const void*)k_attn_bwd_kv,
                        (const void*)k_attn_bwd_pack, (const void*)k_ada_bwd, (const void*)k_time_bwd,
-                       (const void*)k_train_prep, (const void*)k_train_loss, (const void*)k_axpy};
+                       (const void*)k_train_prep, (const void*)k_train_loss, (const void*)k_axpy,
+                       (const void*)k_norm_bwd_cols_sum, (const void*)k_to_bf16, (const void*)k_to_bf16_2d,
+                       (const void*)k_to_f32, (const void*)k_vt_bf16, (const void*)k_attn_bwd_softmax,
+                       (const void*)k_attn_bwd_ds};
     for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
     int dev = 0, mx = 0;
     SWF_CUDA(cudaGetDevice(&dev));

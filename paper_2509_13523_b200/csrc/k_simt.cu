@@ -248,7 +248,9 @@ void preload_simt_kernels() {
     const void* k[] = {(const void*)k_gemm_f32<EPI_ENCODE>, (const void*)k_gemm_f32<EPI_QKV>,
                        (const void*)k_gemm_f32<EPI_RESID>, (const void*)k_gemm_f32<EPI_SWIGLU>,
                        (const void*)k_gemm_f32<EPI_DOWN>, (const void*)k_gemm_f32<EPI_DECODE>,
-                       (const void*)k_attn_f32};
+                       (const void*)k_attn_f32, (const void*)k_epi_rows<EPI_ENCODE>, (const void*)k_epi_rows<EPI_QKV>,
+                       (const void*)k_epi_rows<EPI_RESID>, (const void*)k_epi_rows<EPI_SWIGLU>,
+                       (const void*)k_epi_rows<EPI_DOWN>, (const void*)k_epi_rows<EPI_DECODE>};
     for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
     int dev = 0, mx = 0;
     SWF_CUDA(cudaGetDevice(&dev));

@@ -111,6 +111,31 @@ def test_train_step_bf16_backward():
         assert float(np.abs(x - y).max()) <= TOL_GRAD_BF16 * max(float(np.abs(x).max()), 1e-30), name
 
 
+def test_train_step_bf16_wp_group_matches_single():
+    """The BF16 training mode on a window-parallel group (WP 1x2, one process, ranks on devices
+    [0, 1 % n]): per-rank partial gradients over their own windows, summed by the group, equal the
+    single-device BF16 training mode's within fp32 summation-order noise; losses identical."""
+    import torch
+    oc, sc = o.ModelConfig(**C1), swf.ModelConfig(**C1)
+    H, W = 32, 64
+    p = o.init_params(oc, 58, random=True, scale=0.03, dtype=np.float32)
+    data = swf.DataSet(*[[o.random_field(c, H * W, 700 + 3 * i + j).astype(np.float32) for i in range(3)]
+                         for j, c in ((0, 3), (1, 2), (2, 3))])
+    w = swf.LossWeights.make(H, [1.0, 0.6, 1.7])
+    n = max(1, torch.cuda.device_count())
+    res = {}
+    for grp in (False, True):
+        kw = dict(topology=(1, 2, 1, swf.OWN_CONTIGUOUS), devices=[0, 1 % n]) if grp else {}
+        dn = swf.Denoiser(sc, H, W, precision=swf.PREC_FP32, **kw)
+        dn.load_params(p)
+        dn.set_backward_precision(swf.PREC_BF16)
+        res[grp] = dn.train_step(data, 3, 2, 2, w, swf.DiffusionConfig(), 31)
+        dn.close()
+    a, b = res[False], res[True]
+    assert np.allclose(a.mb_losses, b.mb_losses, rtol=1e-5, atol=0)
+    assert float(np.abs(a.grads - b.grads).max()) <= 1e-3 * float(np.abs(a.grads).max())
+
+
 def test_backward_precision_config_errors():
     cfg = dict(TINY, hidden_dim=12, n_heads=3, ffn_dim=24)  # rows of 12 bf16 = 24 B: not 16-byte aligned
     dn = swf.Denoiser(swf.ModelConfig(**cfg), 12, 12, precision=swf.PREC_FP32)
