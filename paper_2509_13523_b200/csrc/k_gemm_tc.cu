@@ -286,6 +286,14 @@ __device__ __forceinline__ float epi32(const EpiParams& ep, i64 m, int n0, float
 // QKV epilogue with the row's window / token / RoPE positions resolved once per tile (not per
 // 32-column chunk): RoPE pairs from the position-major tables (a chunk's 16 pairs are one line, read
 // as 8 float4), q / k rows as 16-byte stores, V^T as 64-byte warp-wide rows.
+// The column half's pairs are read from the frequency-major table (entry j at rcf[j * ncol]): the 32
+// lanes of a warp are consecutive tokens, i.e. mostly consecutive columns, so one load instruction
+// touches 2-3 lines instead of 32 (the position-major row of a lane is its own line). The row half
+// stays position-major: the lanes share 1-2 image rows. ncu: the q/k tiles' epilogue was bound by
+// L1 wavefronts (~12.8 K per tile against 12.3 K cycles of MMA per tile).
+#ifndef SWF_QKV_ROPE_FM
+#define SWF_QKV_ROPE_FM 1
+#endif
 struct QkvRow {
     bool ok;
     int lw, tok;
@@ -302,11 +310,19 @@ __device__ __forceinline__ QkvRow qkv_row(const EpiParams& ep, i64 m) {
     const int prow = wy * w + ep.cur.g.shift + r.tok / w;  // unwrapped RoPE position (window.hpp:54-56)
     const int pcol = wx * w + ep.cur.g.shift + r.tok % w;
     r.rr = ep.rope_row_pm + i64(prow) * q4;
-    r.rc = ep.rope_col_pm + i64(pcol) * q4;
+    r.rc = SWF_QKV_ROPE_FM ? ep.rope_col + pcol : ep.rope_col_pm + i64(pcol) * q4;
     return r;
 }
-__device__ __forceinline__ void epi_qkv32(const EpiParams& ep, const QkvRow& qr, int n0, float* v) {
-    if (!qr.ok || n0 >= ep.N) return;
+// q / k rows leave through the warp's shared-memory staging: a lane holds 64 B of its own row (the
+// rows are 256 B apart in the destination plane), so a direct 16-byte store touches 32 lines per
+// instruction; transposed, 4 lanes write one row's 64 B and an instruction touches 8 lines (pieces
+// XOR-swizzled by row so both shared-memory passes are conflict-free).
+#ifndef SWF_QKV_STS
+#define SWF_QKV_STS 1
+#endif
+__device__ __forceinline__ void epi_qkv32(const EpiParams& ep, const QkvRow& qr, int n0, float* v, float* stg,
+                                          int lane) {
+    if (n0 >= ep.N) return;  // warp-uniform
     const int h = ep.h, s = ep.cur.g.w * ep.cur.g.w, q4 = ep.d >> 2;
     const int which = n0 / h;
     const int e = n0 - which * h;
@@ -316,29 +332,60 @@ __device__ __forceinline__ void epi_qkv32(const EpiParams& ep, const QkvRow& qr,
     __nv_bfloat16* base =
         reinterpret_cast<__nv_bfloat16*>(ep.qkv_dst[ep.wp_rank * ep.cur.sp + hg]) + which * ep.plane;
     if (which == 2) {  // V^T [window][head][d][token]: the warp's 32 lanes are consecutive tokens
+        if (!qr.ok) return;
         __nv_bfloat16* vt = base + ((i64(qr.lw) * ep.heads_loc + hl) * ep.d + dd) * s + qr.tok;
 #pragma unroll
         for (int j = 0; j < 32; ++j) vt[i64(j) * s] = __float2bfloat16_rn(v[j]);
         return;
     }
+    __nv_bfloat16* dst = nullptr;
+    if (qr.ok) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {  // pairs j, j + 1 lie in the same half (q4 is even)
-        const int j = (dd >> 1) + 2 * k;
-        const float4 cs = j < q4 ? *reinterpret_cast<const float4*>(qr.rr + j)
-                                 : *reinterpret_cast<const float4*>(qr.rc + (j - q4));
-        float x = v[4 * k], y = v[4 * k + 1];
-        v[4 * k] = cs.x * x - cs.y * y;
-        v[4 * k + 1] = cs.y * x + cs.x * y;
-        x = v[4 * k + 2];
-        y = v[4 * k + 3];
-        v[4 * k + 2] = cs.z * x - cs.w * y;
-        v[4 * k + 3] = cs.w * x + cs.z * y;
+        for (int k = 0; k < 8; ++k) {  // pairs j, j + 1 lie in the same half (q4 is even); warp-uniform branch
+            const int j = (dd >> 1) + 2 * k;
+            float4 cs;
+            if (j < q4) {
+                cs = *reinterpret_cast<const float4*>(qr.rr + j);
+            } else if (SWF_QKV_ROPE_FM) {
+                const float2 a = qr.rc[i64(j - q4) * ep.rope_ncol], b = qr.rc[i64(j + 1 - q4) * ep.rope_ncol];
+                cs = make_float4(a.x, a.y, b.x, b.y);
+            } else {
+                cs = *reinterpret_cast<const float4*>(qr.rc + (j - q4));
+            }
+            float x = v[4 * k], y = v[4 * k + 1];
+            v[4 * k] = cs.x * x - cs.y * y;
+            v[4 * k + 1] = cs.y * x + cs.x * y;
+            x = v[4 * k + 2];
+            y = v[4 * k + 3];
+            v[4 * k + 2] = cs.z * x - cs.w * y;
+            v[4 * k + 3] = cs.w * x + cs.z * y;
+        }
+        dst = base + ((i64(qr.lw) * ep.heads_loc + hl) * s + qr.tok) * ep.d + dd;
     }
-    uint4* d4 = reinterpret_cast<uint4*>(base + ((i64(qr.lw) * ep.heads_loc + hl) * s + qr.tok) * ep.d + dd);
+    uint4 u[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-        d4[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                           pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+        u[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                          pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+#if SWF_QKV_STS
+    uint4* st4 = reinterpret_cast<uint4*>(stg);  // [32 rows][4 pieces of 16 B]
+    __syncwarp();                                // the previous chunk's reads are done
+#pragma unroll
+    for (int p = 0; p < 4; ++p) st4[lane * 4 + (p ^ ((lane >> 1) & 3))] = u[p];
+    __syncwarp();
+    const int p = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = 8 * i + (lane >> 2);
+        const uint4 val = st4[r * 4 + (p ^ ((r >> 1) & 3))];
+        auto* rd = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), r));
+        if (rd) rd[p] = val;
+    }
+#else
+    if (dst)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) reinterpret_cast<uint4*>(dst)[j] = u[j];
+#endif
 }
 
 __device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0, const float* g, const float* u,
@@ -373,7 +420,7 @@ __device__ __forceinline__ void tile_coords(i64 t, int n_tiles, i64 m_tiles, int
     m_blk = int(g * group_m + r % gm);
 }
 
-// fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)// fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)
+// fp32 row-major outputs (encode / residual / down): the 32x32 chunk a warp holds (thread = row)
 // is transposed through shared memory so each global access is one contiguous 128-byte row segment.
 template <int MODE>
 __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, int n0, const float* v, float* stg,
@@ -798,7 +845,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tmem_ld32(tbase + ch * 32, v);
                     normed(v, n_blk * BN + ch * 32);
                     if constexpr (MODE == EPI_QKV)
-                        epi_qkv32(ep, qr, n_blk * BN + ch * 32, v);
+                        epi_qkv32(ep, qr, n_blk * BN + ch * 32, v, stg, lane);
                     else
                         ssum += epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
                 }
