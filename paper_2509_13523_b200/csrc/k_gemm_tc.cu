@@ -431,6 +431,15 @@ __device__ __forceinline__ void tile_coords(i64 t, int n_tiles, i64 m_tiles, int
 #ifndef SWF_RESID_V4
 #define SWF_RESID_V4 1
 #endif
+// the 16-byte path needs 16-byte fp32 rows and 8-byte bf16-copy rows (the general GEMM's accumulate
+// mode runs EPI_RESID on any caller matrix, e.g. a 70-column gradient)
+template <int MODE>
+__device__ __forceinline__ bool v4_aligned(const EpiParams& ep) {
+    uintptr_t a = reinterpret_cast<uintptr_t>(ep.x) | (uintptr_t(ep.h) * 4);
+    if (MODE == EPI_ENCODE) a |= reinterpret_cast<uintptr_t>(ep.bias);
+    uintptr_t b = ep.nss ? reinterpret_cast<uintptr_t>(ep.x + ep.off_xb) | (uintptr_t(ep.hp) * 2) : 0;
+    return (a & 15) == 0 && (b & 7) == 0;
+}
 template <int MODE>  // EPI_RESID: x += acc in place; EPI_ENCODE: x = acc + bias
 __device__ __forceinline__ float epi32_v4(const EpiParams& ep, i64 row0, int n0, const float* v, float* stg, int lane) {
     float4* s4 = reinterpret_cast<float4*>(stg);  // [32 rows][8 pieces], piece p of row r at slot p ^ (r & 7)
@@ -484,7 +493,8 @@ template <int MODE>
 __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, int n0, const float* v, float* stg,
                                                  float* drow, __nv_bfloat16* dbrow, int lane) {
     if constexpr ((MODE == EPI_RESID || MODE == EPI_ENCODE) && SWF_RESID_V4)
-        if (ep.M - (row - lane) >= 32 && n0 + 32 <= ep.N) return epi32_v4<MODE>(ep, row - lane, n0, v, stg, lane);
+        if (ep.M - (row - lane) >= 32 && n0 + 32 <= ep.N && v4_aligned<MODE>(ep))
+            return epi32_v4<MODE>(ep, row - lane, n0, v, stg, lane);
 #pragma unroll
     for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
     __syncwarp();

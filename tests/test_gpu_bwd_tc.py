@@ -33,7 +33,7 @@ def bf16(a):
     return u.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
-@pytest.mark.parametrize("M,N,K", [(300, 200, 100), (1000, 384, 2048), (256, 64, 16), (129, 1000, 777)])
+@pytest.mark.parametrize("M,N,K", [(300, 200, 100), (1000, 384, 2048), (256, 64, 16), (129, 1000, 777), (200, 70, 96)])
 @pytest.mark.parametrize("mn", [False, True])
 def test_gemm_bf16_general(M, N, K, mn):
     rng = np.random.default_rng(M * 7 + N + K + mn)
