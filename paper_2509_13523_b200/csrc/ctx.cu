@@ -161,6 +161,7 @@ struct swf_ctx {
     size_t bt_c_n = 0;
     // tensor-core attention of the BF16 training mode: bf16 q / k planes + V^T, bf16 output rows
     __nv_bfloat16 *bt_qkv = nullptr, *bt_o = nullptr;
+    float *bt_lse = nullptr, *bt_D = nullptr;  // attention rows' log2-sum-exp (forward) and D (backward)
     AttnBwdStreams bt_ws;  // worker streams / scratch of the tensor-core attention backward
     void** d_bt_o = nullptr;
     TmaMap bt_tm_q, bt_tm_k, bt_tm_k2, bt_tm_vt, bt_tm_o;
@@ -1332,6 +1333,8 @@ void alloc_bwd_tc(swf_ctx* c) {
     if (c->sp == 1 && (m.d == 32 || m.d == 64 || m.d == 128)) {
         c->bt_qkv = dalloc<__nv_bfloat16>(c, size_t(3) * M * m.h);
         c->bt_o = dalloc<__nv_bfloat16>(c, M * size_t(m.hp));
+        c->bt_lse = dalloc<float>(c, M * size_t(m.heads));  // [nloc][heads][s], nloc s = M
+        c->bt_D = dalloc<float>(c, M * size_t(m.heads));
         // the kernel indexes the output table by the owning rank (wp_rank under window parallelism):
         // every entry is this rank's buffer, its O rows are always its own tokens' (sp == 1)
         c->d_bt_o = dalloc<void*>(c, 8);
@@ -1373,6 +1376,7 @@ void attention_ctx(swf_ctx* c, const AttnParams& ap, bool training) {
     b.tmk2 = &c->bt_tm_k2;
     b.tmv = &c->bt_tm_vt;
     b.tmo = &c->bt_tm_o;
+    b.lse = c->bt_lse;  // the backward's P comes from these row statistics
     attention_bf16(b, c->st);
     to_f32(c->bt_o, M * m.hp, static_cast<float*>(ap.o), c->st);
     c->launches += 4;
@@ -1518,10 +1522,10 @@ void backward_core(swf_ctx* c, const float* dout) {
         lin(h, h, int(M), bw.obuf, 1, hp, dxmid, h, 1, ga(base + 1), h, 1.f);  // dW_out
         lin(int(M), h, h, dxmid, h, 1, pa(base + 1), 1, h, bw.dO, hp, 0.f);
         float* dq = bw.dplanes;
-        if (c->bwd_tc && c->bt_ws.n > 0)
+        if (c->bwd_tc && c->bt_ws.n > 0 && c->bt_lse)  // the recompute above ran the tensor-core kernel
             attention_bwd_tc(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h,
                              c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, c->bt_a,
-                             c->bt_b, c->bt_ws, st);
+                             c->bt_b, c->bt_lse, c->bt_D, c->bt_ws, st);
         else
             attention_bwd_f32(q, kk, v, bw.obuf, bw.dO, hp, dq, dq + size_t(M) * h, dq + size_t(2) * M * h,
                               bw.stats, c->lay[par].nloc, m.heads, m.w * m.w, m.d, m.w, c->lay[par], ep, bw.dqkv, st);

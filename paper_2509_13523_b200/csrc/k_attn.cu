@@ -1227,6 +1227,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::kThreads, 1)
             const float M = fmaxf(m0, m1);
             const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
             const float inv = 1.f / (l0 * f0 + l1 * f1);
+            if (p.lse && grp == 0 && q < s)  // BF16 training mode: the row's log2-sum-exp for the backward
+                p.lse[(i64(it.lw) * p.heads + it.head) * s + q] = M + __log2f(l0 * f0 + l1 * f1);
             const bool has1 = rg.ntiles >= 2;  // item-uniform: O1 holds this item's odd tiles
             mbar_wait(bar(pp::OD + 0), (cnt0 - 1) & 1);
             if (has1) mbar_wait(bar(pp::OD + 1), (cnt1 - 1) & 1);
@@ -1387,6 +1389,7 @@ void preload_attn_kernels() {
 void attention_bf16(const AttnParams& p, cudaStream_t st) {
     if (!p.tmq || !p.tmk || !p.tmv) throw CudaError("attention_bf16: TMA descriptors missing");
     if (!use_split_kernel() && !p.tmk2) throw CudaError("attention_bf16: the K map with 32-row boxes is missing");
+    if (use_split_kernel() && p.lse) throw CudaError("attention_bf16: the row statistics need the ping-pong kernel");
     switch (p.d) {
         case 32: launch<32>(p, st); break;
         case 64: launch<64>(p, st); break;

@@ -741,53 +741,36 @@ void attention_bwd_f32(const float* q, const float* k, const float* v, const flo
     k_attn_bwd_pack<<<unsigned((n + 255) / 256), 256, 0, st>>>(dq, dk, dv, e, nloc, dqkv);
     SWF_LAUNCH_CHECK();
 }
-// ---- attention backward on the tensor cores (BF16 training mode), one (window, head) plane at a time:
-// S = Q K^T, P = softmax (seam mask as key ranges), dV = P^T dO, dP = dO V^T, dS = P (dP - D) / sqrt(d),
-// dQ = dS K, dK = dS^T Q -- five tcgen05 GEMMs (K-major or MN-major operands, no transposes) and two
-// row passes over the s x s plane (head_attention_bwd, swin.hpp:189-226).
-// One warp per query row: P (bf16) and D_i = dO_i . O_i.
-__global__ void k_attn_bwd_softmax(const float* __restrict__ S, int lds, int s, float scale, int split, int masked,
-                                   const float* __restrict__ O, const float* __restrict__ dO, int ldo, int d,
-                                   __nv_bfloat16* __restrict__ P, float* __restrict__ D) {
-    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (i >= s) return;
-    const int lo = (masked && i >= split) ? split : 0, hi = (masked && i < split) ? split : s;
-    const float* row = S + i64(i) * lds;
-    float mx = -INFINITY;
-    for (int k = lo + lane; k < hi; k += 32) mx = fmaxf(mx, row[k]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.f;
-    for (int k = lo + lane; k < hi; k += 32) sum += __expf((row[k] - mx) * scale);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const float inv = 1.f / sum;
-    __nv_bfloat16* prow = P + i64(i) * lds;
-    for (int k = lane; k < s; k += 32)
-        prow[k] = __float2bfloat16_rn(k >= lo && k < hi ? __expf((row[k] - mx) * scale) * inv : 0.f);
+// ---- attention backward on the tensor cores (BF16 training mode), one (window, head) plane at a time
+// (head_attention_bwd, swin.hpp:189-226): P = 2^(S log2e / sqrt(d) - lse) in the epilogue of S = Q K^T
+// (lse = the forward kernel's per-row log2-sum-exp, seam mask as key ranges), dV = P^T dO, dS =
+// P (dP - D) / sqrt(d) in the epilogue of dP = dO V^T, dQ = dS K, dK = dS^T Q -- five tcgen05 GEMMs
+// (K-major or MN-major operands, no transposes); the s x s plane exists only as bf16 P and dS.
+// D_i = dO_i . O_i for every row of every plane ([nloc][heads][s]), one warp per row.
+__global__ void k_attn_bwd_D(const float* __restrict__ O, const float* __restrict__ dO, int ldo, int heads, int s,
+                             int d, i64 rows, float* __restrict__ D) {
+    const i64 t = i64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= rows) return;
+    const i64 lh = t / s;
+    const int i = int(t - lh * s);
+    const i64 lw = lh / heads;
+    const int hh = int(lh - lw * heads);
+    const i64 off = (lw * s + i) * ldo + i64(hh) * d;
     float dd = 0.f;
-    for (int e = lane; e < d; e += 32) dd = fmaf(O[i64(i) * ldo + e], dO[i64(i) * ldo + e], dd);
+    for (int e = lane; e < d; e += 32) dd = fmaf(O[off + e], dO[off + e], dd);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
-    if (lane == 0) D[i] = dd;
+    if (lane == 0) D[t] = dd;
 }
-// dS = P (dP - D_i) * scale (bf16)
-__global__ void k_attn_bwd_ds(const float* __restrict__ dP, const __nv_bfloat16* __restrict__ P, int ld, int s,
-                              const float* __restrict__ D, float scale, __nv_bfloat16* __restrict__ dS) {
-    const i64 n = i64(s) * ld;
-    for (i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += i64(gridDim.x) * blockDim.x) {
-        const i64 i = t / ld;
-        dS[t] = __float2bfloat16_rn(__bfloat162float(P[t]) * (dP[t] - D[i]) * scale);
-    }
-}
-size_t attention_bwd_tc_scratch(int s) {  // bytes: S / dP fp32 + P / dS bf16 + D, row pitch s rounded to 8
+size_t attention_bwd_tc_scratch(int s) {  // bytes: P / dS bf16, row pitch s rounded to 8
     const size_t sp = size_t((s + 7) / 8 * 8);
-    return size_t(s) * sp * (4 + 4 + 2 + 2) + size_t(s) * 4 + 1024;
+    return size_t(s) * sp * (2 + 2) + 1024;
 }
 void attention_bwd_tc(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,
                       float* dq, float* dk, float* dv, int nloc, int heads, int s, int d, int w, const LayMap& lay,
                       const EpiParams& ep, float* dqkv, __nv_bfloat16* qkv16, __nv_bfloat16* dO16,
-                      const AttnBwdStreams& ws, cudaStream_t st) {
+                      const float* lse, float* Dbuf, const AttnBwdStreams& ws, cudaStream_t st) {
     const i64 M = i64(nloc) * s, hd = i64(heads) * d;
     const int sp = (s + 7) / 8 * 8;
     to_bf16(q, M * hd, qkv16, st);  // q, k, v planes [nloc][heads][s][d]
@@ -795,6 +778,10 @@ void attention_bwd_tc(const float* q, const float* k, const float* v, const floa
     to_bf16(v, M * hd, qkv16 + 2 * M * hd, st);
     to_bf16(dO, M * ldo, dO16, st);
     const float scale = 1.0f / sqrtf(float(d));
+    if (s % 8 != 0) throw CudaError("attention backward (tensor cores): s must be a multiple of 8");
+    const i64 rows = i64(nloc) * heads * s;
+    k_attn_bwd_D<<<unsigned((rows + 7) / 8), 256, 0, st>>>(o, dO, ldo, heads, s, d, rows, Dbuf);
+    SWF_LAUNCH_CHECK();
     // host copy of the window ids (seam windows), one small read per call
     std::vector<int> gw(static_cast<size_t>(nloc));
     SWF_CUDA(cudaMemcpyAsync(gw.data(), lay.loc2glob, size_t(nloc) * 4, cudaMemcpyDeviceToHost, st));
@@ -811,23 +798,17 @@ void attention_bwd_tc(const float* q, const float* k, const float* v, const floa
             const int wi = pl_i % ws.n;
             cudaStream_t ss = ws.st[wi];
             int* sched = ws.sched[wi];
-            float* S = static_cast<float*>(ws.scratch[wi]);
-            float* dP = S + size_t(s) * sp;
-            __nv_bfloat16* P = reinterpret_cast<__nv_bfloat16*>(dP + size_t(s) * sp);
+            __nv_bfloat16* P = static_cast<__nv_bfloat16*>(ws.scratch[wi]);
             __nv_bfloat16* dS = P + size_t(s) * sp;
-            float* D = reinterpret_cast<float*>(dS + size_t(s) * sp);
-            const i64 pl = (i64(lw) * heads + hh) * s * d;
+            const i64 prow = (i64(lw) * heads + hh) * s;  // this plane's rows of lse / D
+            const i64 pl = prow * d;
             const __nv_bfloat16 *q16 = qkv16 + pl, *k16 = qkv16 + M * hd + pl, *v16 = qkv16 + 2 * M * hd + pl;
             const i64 orow = i64(lw) * s * ldo + i64(hh) * d;
-            gemm_bf16_general(q16, false, d, k16, false, d, s, s, d, S, sp, false, sched, ss);  // S = Q K^T
-            k_attn_bwd_softmax<<<unsigned((s + 7) / 8), 256, 0, ss>>>(S, sp, s, scale, split, masked, o + orow,
-                                                                      dO + orow, ldo, d, P, D);
-            SWF_LAUNCH_CHECK();
+            gemm_bf16_attn_rows(EPI_SMAX, q16, d, k16, d, s, d, P, sp, lse + prow, nullptr, split, masked,
+                                scale * 1.4426950408889634f, sched, ss);  // P from S = Q K^T
             gemm_bf16_general(P, true, sp, dO16 + orow, true, ldo, s, d, s, dv + pl, d, false, sched, ss);  // P^T dO
-            gemm_bf16_general(dO16 + orow, false, ldo, v16, false, d, s, s, d, dP, sp, false, sched, ss);  // dO V^T
-            k_attn_bwd_ds<<<unsigned(std::min<i64>((i64(s) * sp + 255) / 256, 148 * 16)), 256, 0, ss>>>(dP, P, sp, s,
-                                                                                                   D, scale, dS);
-            SWF_LAUNCH_CHECK();
+            gemm_bf16_attn_rows(EPI_DSM, dO16 + orow, ldo, v16, d, s, d, dS, sp, Dbuf + prow, P, split, masked, scale,
+                                sched, ss);  // dS from dP = dO V^T
             gemm_bf16_general(dS, false, sp, k16, true, d, s, d, s, dq + pl, d, false, sched, ss);  // dS K
             gemm_bf16_general(dS, true, sp, q16, true, d, s, d, s, dk + pl, d, false, sched, ss);   // dS^T Q
         }
@@ -877,8 +858,7 @@ void preload_bwd_kernels() {
                        (const void*)k_attn_bwd_pack, (const void*)k_ada_bwd, (const void*)k_time_bwd,
                        (const void*)k_train_prep, (const void*)k_train_loss, (const void*)k_axpy,
                        (const void*)k_norm_bwd_cols_sum, (const void*)k_to_bf16, (const void*)k_to_bf16_2d,
-                       (const void*)k_to_f32, (const void*)k_vt_bf16, (const void*)k_attn_bwd_softmax,
-                       (const void*)k_attn_bwd_ds};
+                       (const void*)k_to_f32, (const void*)k_vt_bf16, (const void*)k_attn_bwd_D};
     for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
     int dev = 0, mx = 0;
     SWF_CUDA(cudaGetDevice(&dev));

@@ -313,6 +313,27 @@ __device__ __forceinline__ QkvRow qkv_row(const EpiParams& ep, i64 m) {
     r.rc = SWF_QKV_ROPE_FM ? ep.rope_col + pcol : ep.rope_col_pm + i64(pcol) * q4;
     return r;
 }
+// 32 rows x 64 B of bf16 (lane = row, u = its 4 16-byte pieces) stored through the warp's shared-memory
+// staging so that 4 lanes write one row's 64 B and an instruction touches 8 lines instead of 32 (pieces
+// XOR-swizzled by row: both shared-memory passes are conflict-free); rows with dst == nullptr and
+// pieces >= npieces are skipped.
+__device__ __forceinline__ void store_rows_bf16x32(const uint4* u, __nv_bfloat16* dst, int npieces, float* stg,
+                                                   int lane) {
+    uint4* st4 = reinterpret_cast<uint4*>(stg);  // [32 rows][4 pieces of 16 B]
+    __syncwarp();                                // the previous chunk's reads are done
+#pragma unroll
+    for (int p = 0; p < 4; ++p) st4[lane * 4 + (p ^ ((lane >> 1) & 3))] = u[p];
+    __syncwarp();
+    const int p = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = 8 * i + (lane >> 2);
+        const uint4 val = st4[r * 4 + (p ^ ((r >> 1) & 3))];
+        auto* rd = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), r));
+        if (rd && p < npieces) rd[p] = val;
+    }
+}
+
 // q / k rows leave through the warp's shared-memory staging: a lane holds 64 B of its own row (the
 // rows are 256 B apart in the destination plane), so a direct 16-byte store touches 32 lines per
 // instruction; transposed, 4 lanes write one row's 64 B and an instruction touches 8 lines (pieces
@@ -368,24 +389,57 @@ __device__ __forceinline__ void epi_qkv32(const EpiParams& ep, const QkvRow& qr,
         u[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
                           pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
 #if SWF_QKV_STS
-    uint4* st4 = reinterpret_cast<uint4*>(stg);  // [32 rows][4 pieces of 16 B]
-    __syncwarp();                                // the previous chunk's reads are done
-#pragma unroll
-    for (int p = 0; p < 4; ++p) st4[lane * 4 + (p ^ ((lane >> 1) & 3))] = u[p];
-    __syncwarp();
-    const int p = lane & 3;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int r = 8 * i + (lane >> 2);
-        const uint4 val = st4[r * 4 + (p ^ ((r >> 1) & 3))];
-        auto* rd = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), r));
-        if (rd) rd[p] = val;
-    }
+    store_rows_bf16x32(u, dst, 4, stg, lane);
 #else
     if (dst)
 #pragma unroll
         for (int j = 0; j < 4; ++j) reinterpret_cast<uint4*>(dst)[j] = u[j];
 #endif
+}
+
+// Attention backward (EPI_SMAX / EPI_DSM): 32 columns of one row of the s x s plane -> bf16 P or dS.
+template <int MODE>
+__device__ __forceinline__ void epi_attn_rows32(const EpiParams& ep, i64 m, int n0, const float* v, float* stg,
+                                                int lane) {
+    if (n0 >= ep.N) return;  // warp-uniform
+    const bool ok = m < ep.M;
+    uint4 u[4];
+    __nv_bfloat16* dst = nullptr;
+    if (ok) {
+        float o[32];
+        const float rv = ep.rowv[m];
+        if constexpr (MODE == EPI_SMAX) {
+            const int lo = (ep.masked && m >= ep.split) ? ep.split : 0;
+            const int hi = (ep.masked && m < ep.split) ? ep.split : ep.N;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                o[j] = (n0 + j >= lo && n0 + j < hi) ? exp2f(fmaf(v[j], ep.out_scale, -rv)) : 0.f;
+        } else {
+            const uint4* pr = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.pin) +
+                                                             m * ep.ld_out + n0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 pp = n0 + 8 * q < ep.N ? pr[q] : make_uint4(0, 0, 0, 0);
+                const uint32_t w[4] = {pp.x, pp.y, pp.z, pp.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[t]));
+                    o[8 * q + 2 * t] = f.x * (v[8 * q + 2 * t] - rv) * ep.out_scale;
+                    o[8 * q + 2 * t + 1] = f.y * (v[8 * q + 2 * t + 1] - rv) * ep.out_scale;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            u[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]), pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                              pack_bf16x2(o[8 * j + 4], o[8 * j + 5]), pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+        dst = static_cast<__nv_bfloat16*>(ep.out) + m * ep.ld_out + n0;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) u[j] = make_uint4(0, 0, 0, 0);
+    }
+    const int npieces = min(4, (ep.N - n0) >> 3);  // 8-column pieces inside N (N % 8 == 0)
+    store_rows_bf16x32(u, dst, npieces, stg, lane);
 }
 
 __device__ __forceinline__ void epi_swiglu32(const EpiParams& ep, i64 m, int j0, const float* g, const float* u,
@@ -916,6 +970,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     normed(v, n_blk * BN + ch * 32);
                     if constexpr (MODE == EPI_QKV)
                         epi_qkv32(ep, qr, n_blk * BN + ch * 32, v, stg, lane);
+                    else if constexpr (MODE == EPI_SMAX || MODE == EPI_DSM)
+                        epi_attn_rows32<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, lane);
                     else
                         ssum += epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
                 }
@@ -1085,6 +1141,10 @@ void preload_bn(cudaFuncAttributes& a) {
     set((const void*)k_gemm_tc<BN, EPI_STORE, 0>, kS);
     set((const void*)k_gemm_tc<BN, EPI_STORE, 3>, kS);
     set((const void*)k_gemm_tc<BN, EPI_STORE, 2>, kS);
+    if constexpr (BN == 256) {
+        set((const void*)k_gemm_tc<BN, EPI_SMAX, 0>, kS);
+        set((const void*)k_gemm_tc<BN, EPI_DSM, 0>, kS);
+    }
 }
 void preload_gemm_kernels() {
     cudaFuncAttributes a;
@@ -1152,6 +1212,35 @@ void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bf
         general_launch<EPI_RESID>(BN, mn, ta, tb, M, Np, Kp, ep, st);
     else
         general_launch<EPI_STORE>(BN, mn, ta, tb, M, Np, Kp, ep, st);
+}
+
+void gemm_bf16_attn_rows(int mode, const __nv_bfloat16* A, i64 lda, const __nv_bfloat16* B, i64 ldb, int s, int K,
+                         __nv_bfloat16* out, int ldo, const float* rowv, const __nv_bfloat16* pin, int split,
+                         int masked, float scale, int* sched, cudaStream_t st) {
+    if (s <= 0 || K <= 0) return;
+    if (s % 8 != 0) throw CudaError("gemm_bf16_attn_rows: s must be a multiple of 8");
+    TmaMap ta, tb;
+    make_tma_bf16_pitch(&ta, A, s, K, lda, BM);
+    make_tma_bf16_pitch(&tb, B, s, K, ldb, 128);
+    EpiParams ep;
+    std::memset(&ep, 0, sizeof ep);
+    ep.M = s;
+    ep.N = s;
+    ep.out = out;
+    ep.ld_out = ldo;
+    ep.out_scale = scale;
+    ep.rowv = rowv;
+    ep.pin = pin;
+    ep.split = split;
+    ep.masked = masked;
+    ep.sched = sched;
+    const int Kp = (K + BK - 1) / BK * BK, Np = (s + 255) / 256 * 256;
+    if (mode == EPI_SMAX)
+        launch<256, EPI_SMAX, 0>(ta, tb, s, Np, Kp, ep, st);
+    else if (mode == EPI_DSM)
+        launch<256, EPI_DSM, 0>(ta, tb, s, Np, Kp, ep, st);
+    else
+        throw CudaError("gemm_bf16_attn_rows: bad mode");
 }
 
 void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int BN, int mode, const EpiParams& ep,

@@ -84,6 +84,11 @@ enum EpiMode : int {
     EPI_DOWN = 4,    // xdst[dest(m)][n] = xsrc[m][n] + acc, dest = next layout     (swin.hpp:324, 356-358)
     EPI_DECODE = 5,  // out[m][n] = (acc + bias[n]) * out_scale, n < cout (local L0 order) (swin.hpp:364-366)
     EPI_STORE = 6,   // x[m][n] = acc, n < N (the backward's plain products; tensor-core kernel only)
+    // attention backward on the tensor cores (head_attention_bwd, swin.hpp:189-226), bf16 out[m][n] with
+    // row pitch ld_out, n < N (N % 8 == 0); the row's key range: [0, N), or with `masked` [0, split)
+    // for rows < split and [split, N) for the others (the seam mask, window.hpp:107-122)
+    EPI_SMAX = 7,    // P = 2^(acc * out_scale - rowv[m]) in the key range, else 0 (rowv = log2-sum-exp)
+    EPI_DSM = 8,     // dS = P[m][n] * (acc - rowv[m]) * out_scale, P = pin (bf16, pitch ld_out), rowv = D
 };
 
 struct EpiParams {
@@ -124,6 +129,10 @@ struct EpiParams {
     // tile counter of the persistent GEMM's dynamic schedule, owned by the context (GEMMs of one
     // context are stream-ordered); nullptr -> a per-device counter (single-stream callers only)
     int* sched;
+    // EPI_SMAX / EPI_DSM
+    const float* rowv;
+    const void* pin;
+    int split, masked;
 };
 // inv_r[m] = 1 / sqrt(sum_i ss[m][i] / h + 1e-8) over the nss partials; non-finite rows flag
 // flags[slot] (check_finite, swin.hpp:295-300)
@@ -154,6 +163,11 @@ void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int 
 // MN-major (B[k * ldb + n]) -- not A MN-major with B K-major; pitches multiples of 8 elements.
 void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bfloat16* B, bool b_mn, i64 ldb, i64 M,
                        i64 N, i64 K, float* C, i64 ldc, bool accumulate, int* sched, cudaStream_t st);
+// The attention backward's row-wise products (both operands K-major, s x s output in bf16, pitch ldo):
+// mode EPI_SMAX: out = P from S = A . B^T; EPI_DSM: out = dS from dP = A . B^T (see EpiMode)
+void gemm_bf16_attn_rows(int mode, const __nv_bfloat16* A, i64 lda, const __nv_bfloat16* B, i64 ldb, int s, int K,
+                         __nv_bfloat16* out, int ldo, const float* rowv, const __nv_bfloat16* pin, int split,
+                         int masked, float scale, int* sched, cudaStream_t st);
 
 // ------------------------------------------------------------------ attention
 struct AttnParams {
@@ -175,6 +189,8 @@ struct AttnParams {
     const TmaMap* tmo;  // BF16 path, sp == 1: map of the own output buffer (box 64 x 128, SW128) for TMA
                         // stores of whole query tiles; nullptr = per-row stores
     int dbg = 0;        // test only (swf_selftest_attention negative control): bit 0 skips the O rescale
+    float* lse = nullptr;  // BF16 training mode, ping-pong kernel: per query row [nloc][heads][s] the
+                           // log2-sum-exp of the scaled logits (s log2e / sqrt(d)), for the backward's P
 };
 void attention_f32(const AttnParams& p, cudaStream_t st);
 void attention_bf16(const AttnParams& p, cudaStream_t st);
@@ -187,8 +203,10 @@ void to_bf16(const float* x, i64 n, __nv_bfloat16* y, cudaStream_t st);
 void to_f32(const __nv_bfloat16* x, i64 n, float* y, cudaStream_t st);
 void vt_bf16(const float* v, i64 planes, int s, int d, __nv_bfloat16* vt, cudaStream_t st);
 // attention backward on the tensor cores (BF16 training mode): per (window, head) plane, five tcgen05
-// GEMMs and two row passes; scratch of attention_bwd_tc_scratch(s) bytes, qkv16 3 M h and dO16 M ldo
-// bf16 elements; d % 8 == 0
+// GEMMs -- P from S = Q K^T in the GEMM's epilogue with the forward's log2-sum-exp `lse`, dS from
+// dP = dO V^T in the next one's with D = rowsum(dO . O) (one pass over all planes into `Dbuf`,
+// [nloc][heads][s]); scratch of attention_bwd_tc_scratch(s) bytes, qkv16 3 M h and dO16 M ldo bf16
+// elements; d % 8 == 0, s % 8 == 0
 size_t attention_bwd_tc_scratch(int s);
 struct AttnBwdStreams {  // worker streams of the per-plane loop, each with scratch and a GEMM tile counter
     static constexpr int kMax = 4;
@@ -201,7 +219,7 @@ struct AttnBwdStreams {  // worker streams of the per-plane loop, each with scra
 void attention_bwd_tc(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,
                       float* dq, float* dk, float* dv, int nloc, int heads, int s, int d, int w, const LayMap& lay,
                       const EpiParams& ep, float* dqkv, __nv_bfloat16* qkv16, __nv_bfloat16* dO16,
-                      const AttnBwdStreams& ws, cudaStream_t st);
+                      const float* lse, float* Dbuf, const AttnBwdStreams& ws, cudaStream_t st);
 void gemm_strided_tc(int M, int N, int K, const float* A, i64 sai, i64 sak, const float* B, i64 sbk, i64 sbj, float* C,
                      i64 ldc, float beta, __nv_bfloat16* ta, __nv_bfloat16* tb, int* sched, cudaStream_t st);
 // prenorm_modulate_bwd / prenorm_plain_bwd (a, b, gate null): dX += ..., per-channel grads +=
