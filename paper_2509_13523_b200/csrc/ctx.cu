@@ -1444,7 +1444,7 @@ void backward_core(swf_ctx* c, const float* dout) {
     const float* xf = c->xsave + size_t(nb) * M * h;
     rms_modulate<float>(xf, M, h, hp, c->g_dec, nullptr, nullptr, nullptr, bw.xm1, nullptr, 0, st);
     lin(h, m.cout, int(M), bw.xm1, 1, hp, dout, m.cout, 1, ga(tail + 3), m.cout, 1.f);
-    colsum_f32(dout, m.cout, M, m.cout, ga(tail + 4), st);
+    colsum_f32(dout, m.cout, M, m.cout, ga(tail + 4), bw.npart, st);
     lin(int(M), h, m.cout, dout, m.cout, 1, pa(tail + 3), 1, m.cout, bw.dtmp, h, 0.f);
     SWF_CUDA(cudaMemsetAsync(bw.dx[0], 0, size_t(M) * h * 4, st));
     norm_bwd(xf, h, bw.dtmp, h, M, h, c->g_dec, nullptr, nullptr, nullptr, bw.dx[0], h, bw.rms, ga(tail + 2), nullptr,
@@ -1494,7 +1494,11 @@ void backward_core(swf_ctx* c, const float* dout) {
         e.ld_out = m.np_gu;
         e.N = m.np_gu;
         e.bias = bw.zero;
-        gemm_f32_ctx(c, bw.x2m, static_cast<const float*>(c->w_gu[b]), M, m.np_gu, hp, EPI_DECODE, e);
+        if (c->bwd_tc && c->bt_c && hp % 8 == 0)  // tensor cores: the plain product is the result (no epilogue pass)
+            gemm_strided_tc(int(M), m.np_gu, hp, bw.x2m, hp, 1, static_cast<const float*>(c->w_gu[b]), 1, hp, bw.gu,
+                            m.np_gu, 0.f, c->bt_a, c->bt_b, c->d_sched, st);
+        else
+            gemm_f32_ctx(c, bw.x2m, static_cast<const float*>(c->w_gu[b]), M, m.np_gu, hp, EPI_DECODE, e);
         // ---- backward (block_window_backward, swin.hpp:370-417)
         float* dXp = bw.dtmp;  // output gradient in this block's layout
         if (c->world > 1) {    // WP: owners change between the layouts -> peer stores, then a barrier
@@ -1540,7 +1544,7 @@ void backward_core(swf_ctx* c, const float* dout) {
     // encode (swin.hpp:458-461) and the shared time projection (:463-466)
     const float* dx = bw.dx[cur];
     lin(m.cin, h, int(M), static_cast<const float*>(c->a_in), 1, m.cinp, dx, h, 1, ga(0), h, 1.f);
-    colsum_f32(dx, h, M, h, ga(1), st);
+    colsum_f32(dx, h, M, h, ga(1), bw.npart, st);
     lin(int(M), m.cin, h, dx, h, 1, pa(0), 1, h, bw.din, m.cin, 0.f);
     time_bwd(bw.demb, c->feat, pa(tail + 0), pa(tail + 1), td, ga(tail + 0), ga(tail + 1), st);
 }

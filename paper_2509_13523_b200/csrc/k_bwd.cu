@@ -177,12 +177,23 @@ __global__ void k_norm_bwd_cols_sum(const float* __restrict__ part, int S, int h
     if (dgate) dgate[i] += s[3];
 }
 
-// column sums (bias gradients): out[i] += sum_j X[j][i]
-__global__ void k_colsum(const float* __restrict__ X, int ldx, i64 M, int n, float* __restrict__ out) {
+// column sums (bias gradients): out[i] += sum_j X[j][i]. One thread per (column, token slice) into
+// part[sl][n], then the slices added in order (deterministic; one thread per column over all M rows
+// had left 1-12 blocks for 148 SMs: 6.9 ms per call at 240x480)
+__global__ void k_colsum(const float* __restrict__ X, int ldx, i64 M, int n, int S, float* __restrict__ part) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int sl = blockIdx.y;
+    if (i >= n) return;
+    float s = 0.f;
+    const i64 j1 = M * (sl + 1) / S;
+    for (i64 j = M * sl / S; j < j1; ++j) s += X[j * ldx + i];
+    part[size_t(sl) * n + i] = s;
+}
+__global__ void k_colsum_sum(const float* __restrict__ part, int S, int n, float* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float s = 0.f;
-    for (i64 j = 0; j < M; ++j) s += X[j * ldx + i];
+    for (int sl = 0; sl < S; ++sl) s += part[size_t(sl) * n + i];
     out[i] += s;
 }
 
@@ -683,8 +694,12 @@ void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h
     k_norm_bwd_cols_sum<<<unsigned(cb), 128, 0, st>>>(part, S, h, dg, da, db, dgate);
     SWF_LAUNCH_CHECK();
 }
-void colsum_f32(const float* X, int ldx, i64 M, int n, float* out, cudaStream_t st) {
-    k_colsum<<<unsigned((n + 127) / 128), 128, 0, st>>>(X, ldx, M, n, out);
+void colsum_f32(const float* X, int ldx, i64 M, int n, float* out, float* part, cudaStream_t st) {
+    const int cb = (n + 127) / 128;
+    const int S = int(std::max<i64>(1, std::min<i64>({i64(kNormSlices), (M + 63) / 64, i64(148 * 4 / cb + 1)})));
+    k_colsum<<<dim3(unsigned(cb), unsigned(S)), 128, 0, st>>>(X, ldx, M, n, S, part);
+    SWF_LAUNCH_CHECK();
+    k_colsum_sum<<<unsigned(cb), 128, 0, st>>>(part, S, n, out);
     SWF_LAUNCH_CHECK();
 }
 void swiglu_bwd(const float* gu, int ldgu, const float* dS, int ldds, i64 M, int f, int G, float* act, float* dG,
@@ -857,7 +872,7 @@ void preload_bwd_kernels() {
                        (const void*)k_relayout_push, (const void*)k_attn_bwd_q, (const void*)k_attn_bwd_kv,
                        (const void*)k_attn_bwd_pack, (const void*)k_ada_bwd, (const void*)k_time_bwd,
                        (const void*)k_train_prep, (const void*)k_train_loss, (const void*)k_axpy,
-                       (const void*)k_norm_bwd_cols_sum, (const void*)k_to_bf16, (const void*)k_to_bf16_2d,
+                       (const void*)k_norm_bwd_cols_sum, (const void*)k_colsum_sum, (const void*)k_to_bf16, (const void*)k_to_bf16_2d,
                        (const void*)k_to_f32, (const void*)k_vt_bf16, (const void*)k_attn_bwd_D};
     for (const void* f : k) SWF_CUDA(cudaFuncGetAttributes(&a, f));
     int dev = 0, mx = 0;

@@ -228,7 +228,7 @@ constexpr int kNormSlices = 256;
 void norm_bwd(const float* X, int ldx, const float* dXM, int lddxm, i64 M, int h, const float* g, const float* a,
               const float* b, const float* gate, float* dX, int lddx, float* rms, float* dg, float* da, float* db,
               float* dgate, float* part, cudaStream_t st);
-void colsum_f32(const float* X, int ldx, i64 M, int n, float* out, cudaStream_t st);
+void colsum_f32(const float* X, int ldx, i64 M, int n, float* out, float* part, cudaStream_t st);  // part: kNormSlices * n
 void swiglu_bwd(const float* gu, int ldgu, const float* dS, int ldds, i64 M, int f, int G, float* act, float* dG,
                 float* dU, cudaStream_t st);
 // WP: row i of A's local order -> dst[owner rank][B-local index] (peer stores)
