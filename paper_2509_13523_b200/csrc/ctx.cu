@@ -161,7 +161,8 @@ struct swf_ctx {
     size_t bt_c_n = 0;
     // tensor-core attention of the BF16 training mode: bf16 q / k planes + V^T, bf16 output rows
     __nv_bfloat16 *bt_qkv = nullptr, *bt_o = nullptr;
-    float *bt_lse = nullptr, *bt_D = nullptr;  // attention rows' log2-sum-exp (forward) and D (backward)
+    float *bt_lse = nullptr, *bt_D = nullptr;
+    void** bench_otab = nullptr;  // swf_bench_kernel's attention output table  // attention rows' log2-sum-exp (forward) and D (backward)
     AttnBwdStreams bt_ws;  // worker streams / scratch of the tensor-core attention backward
     void** d_bt_o = nullptr;
     TmaMap bt_tm_q, bt_tm_k, bt_tm_k2, bt_tm_vt, bt_tm_o;
@@ -3100,7 +3101,7 @@ int swf_bench_kernel(swf_ctx* c, int kclass, int blk, int reps, double* ms) {
                     ap.head0 = c->band * (m.heads / c->sp);
                     ap.wp_rank = c->wp_rank;
                     {
-                        static void** scratch_tab = nullptr;  // o_dst table pointing at sbuf (scratch)
+                        void**& scratch_tab = c->bench_otab;  // o_dst table pointing at sbuf (scratch), per context
                         if (!scratch_tab) {
                             scratch_tab = dalloc<void*>(c, 8);
                             std::vector<void*> t(8, c->sbuf);
