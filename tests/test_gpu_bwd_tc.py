@@ -84,6 +84,36 @@ def test_backward_bf16_matches_oracle(cfg, H, W):
     assert float((np.abs(din - dref).max(axis=0) / scale).max()) <= TOL_GRAD_BF16
 
 
+def test_backward_bf16_c2_widths_matches_fp32_mode():
+    """C2 widths (h 1536, 12 heads, d 128, f 9216, 60 x 60 windows: s = 3600, 15 key tiles per GEMM with a
+    partial last one, the shifted block's windows all seam-masked) on a 60 x 120 grid, 2 blocks: the BF16
+    training mode (P / dS built in the tensor-core GEMMs' epilogues from the forward kernel's row
+    log2-sum-exp) against the FP32 validation mode, which the tests above pin to the oracle at the
+    small widths; per parameter array and for the input gradient."""
+    cfg = swf.ModelConfig(hidden_dim=1536, n_heads=12, ffn_dim=9216, n_layers=1, blocks_per_layer=2,
+                          window_px=60, in_channels=144, out_channels=70, time_dim=1536)
+    H, W = 60, 120
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((H * W, cfg.in_channels)).astype(np.float32)
+    R = rng.standard_normal((H * W, cfg.out_channels)).astype(np.float32)
+    dn = swf.Denoiser(cfg, H, W, precision=swf.PREC_FP32)
+    dn.init_params(2024, mode=1, scale=0.01)
+    g32, d32 = dn.backward(x, 0.8, R)
+    dn.set_backward_precision(swf.PREC_BF16)
+    g, din = dn.backward(x, 0.8, R)
+    dn.close()
+    assert not np.array_equal(g, g32)  # the BF16 path ran
+    off = 0
+    for name, r, c in swf.param_arrays(cfg):
+        a, b = g[off:off + r * c], g32[off:off + r * c]
+        off += r * c
+        scale = max(float(np.abs(b).max()), 1e-30)
+        assert float(np.abs(a - b).max()) / scale <= TOL_GRAD_BF16, name
+    assert off == g.size
+    scale = np.maximum(np.abs(d32).max(axis=0), 1e-30)
+    assert float((np.abs(din - d32).max(axis=0) / scale).max()) <= TOL_GRAD_BF16
+
+
 def test_train_step_bf16_backward():
     """reference_train_step in the BF16 training mode (the forward's and the backward's linears on the
     tensor cores, attention / norms in FP32): losses and accumulated gradients within the BF16 bar of
