@@ -1326,7 +1326,7 @@ void alloc_bwd_tc(swf_ctx* c) {
         ws.n = AttnBwdStreams::kMax;
         for (int i = 0; i < ws.n; ++i) {
             SWF_CUDA(cudaStreamCreateWithFlags(&ws.st[i], cudaStreamNonBlocking));
-            ws.scratch[i] = dalloc<char>(c, attention_bwd_tc_scratch(m.w * m.w));
+            ws.scratch[i] = dalloc<char>(c, attention_bwd_tc_scratch(m.w * m.w, m.heads));
             ws.sched[i] = dalloc<int>(c, 1);
         }
         for (int i = 0; i <= ws.n; ++i) SWF_CUDA(cudaEventCreateWithFlags(&ws.ev[i], cudaEventDisableTiming));

@@ -778,9 +778,9 @@ __global__ void k_attn_bwd_D(const float* __restrict__ O, const float* __restric
     for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
     if (lane == 0) D[t] = dd;
 }
-size_t attention_bwd_tc_scratch(int s) {  // bytes: P / dS bf16, row pitch s rounded to 8
-    const size_t sp = size_t((s + 7) / 8 * 8);
-    return size_t(s) * sp * (2 + 2) + 1024;
+size_t attention_bwd_tc_scratch(int s, int heads) {  // bytes: P / dS bf16 of a window's heads, zero K-tail rows
+    const size_t sp = size_t((s + 7) / 8 * 8), spad = size_t((s + 63) / 64 * 64);
+    return size_t(heads) * spad * sp * (2 + 2) + 1024;
 }
 void attention_bwd_tc(const float* q, const float* k, const float* v, const float* o, const float* dO, int ldo,
                       float* dq, float* dk, float* dv, int nloc, int heads, int s, int d, int w, const LayMap& lay,
@@ -802,31 +802,43 @@ void attention_bwd_tc(const float* q, const float* k, const float* v, const floa
     SWF_CUDA(cudaMemcpyAsync(gw.data(), lay.loc2glob, size_t(nloc) * 4, cudaMemcpyDeviceToHost, st));
     SWF_CUDA(cudaStreamSynchronize(st));
     const int split = (w - lay.g.shift) * w;
-    // planes round-robin over the worker streams (a plane's GEMMs are 15 x 1 tiles for N = d: several
-    // planes in flight fill the GPU), each with its own scratch and tile counter
+    // one window's heads per launch (plane-batched GEMMs: a plane's d-wide products are only 15 tiles),
+    // windows round-robin over the worker streams, each with its own scratch and tile counter. The P / dS
+    // planes of a window sit spad (s rounded up to 64) rows apart with zero pad rows, so the K tails of
+    // the MN-major products (P^T dO, dS^T Q) read zeros on the P / dS side; the K-major ones stay
+    // inside the maps' inner extent.
+    const int spad = (s + 63) / 64 * 64;
+    const i64 pst = i64(spad) * sp;  // elements per P / dS plane
     SWF_CUDA(cudaEventRecord(ws.ev[0], st));
     for (int i = 0; i < ws.n; ++i) SWF_CUDA(cudaStreamWaitEvent(ws.st[i], ws.ev[0], 0));
-    int pl_i = 0;
     for (int lw = 0; lw < nloc; ++lw) {
         const int masked = lay.g.shift > 0 && gw[size_t(lw)] / lay.g.nx == lay.g.ny - 1;
-        for (int hh = 0; hh < heads; ++hh, ++pl_i) {
-            const int wi = pl_i % ws.n;
-            cudaStream_t ss = ws.st[wi];
-            int* sched = ws.sched[wi];
-            __nv_bfloat16* P = static_cast<__nv_bfloat16*>(ws.scratch[wi]);
-            __nv_bfloat16* dS = P + size_t(s) * sp;
-            const i64 prow = (i64(lw) * heads + hh) * s;  // this plane's rows of lse / D
-            const i64 pl = prow * d;
-            const __nv_bfloat16 *q16 = qkv16 + pl, *k16 = qkv16 + M * hd + pl, *v16 = qkv16 + 2 * M * hd + pl;
-            const i64 orow = i64(lw) * s * ldo + i64(hh) * d;
-            gemm_bf16_attn_rows(EPI_SMAX, q16, d, k16, d, s, d, P, sp, lse + prow, nullptr, split, masked,
-                                scale * 1.4426950408889634f, sched, ss);  // P from S = Q K^T
-            gemm_bf16_general(P, true, sp, dO16 + orow, true, ldo, s, d, s, dv + pl, d, false, sched, ss);  // P^T dO
-            gemm_bf16_attn_rows(EPI_DSM, dO16 + orow, ldo, v16, d, s, d, dS, sp, Dbuf + prow, P, split, masked, scale,
-                                sched, ss);  // dS from dP = dO V^T
-            gemm_bf16_general(dS, false, sp, k16, true, d, s, d, s, dq + pl, d, false, sched, ss);  // dS K
-            gemm_bf16_general(dS, true, sp, q16, true, d, s, d, s, dk + pl, d, false, sched, ss);   // dS^T Q
-        }
+        const int wi = lw % ws.n;
+        cudaStream_t ss = ws.st[wi];
+        int* sched = ws.sched[wi];
+        __nv_bfloat16* P = static_cast<__nv_bfloat16*>(ws.scratch[wi]);
+        __nv_bfloat16* dS = P + size_t(heads) * pst;
+        const i64 prow = i64(lw) * heads * s;  // rows of head 0 of this window in lse / D / the q, k, v planes
+        const i64 pl = prow * d;
+        const __nv_bfloat16 *q16 = qkv16 + pl, *k16 = qkv16 + M * hd + pl, *v16 = qkv16 + 2 * M * hd + pl;
+        const __nv_bfloat16* dOw = dO16 + i64(lw) * s * ldo;  // head hh at column hh d
+        const i64 prows = i64(heads) * s;                      // q / k / v plane rows of the window
+        // P from S = Q K^T
+        gemm_bf16_attn_rows(EPI_SMAX, q16, d, k16, d, s, d, P, sp, lse + prow, nullptr, split, masked,
+                            scale * 1.4426950408889634f, sched, ss, heads, s, 0, s, pst);
+        // dV = P^T dO: A = P MN-major (K = queries: spad rows per plane), B = dO MN-major (head columns)
+        gemm_bf16_batched(P, true, sp, i64(heads) * spad, s, dOw, true, ldo, s, i64(heads) * d, s, d, s, dv + pl, d,
+                          heads, 0, spad, d, 0, i64(s) * d, sched, ss);
+        // dS from dP = dO V^T
+        gemm_bf16_attn_rows(EPI_DSM, dOw, ldo, v16, d, s, d, dS, sp, Dbuf + prow, P, split, masked, scale, sched, ss,
+                            heads, 0, d, s, pst);
+        // dQ = dS K: A = dS K-major (inner = keys, s), B = K MN-major (K = keys: the next plane's rows meet
+        // dS's zero-filled columns)
+        gemm_bf16_batched(dS, false, sp, (i64(heads) - 1) * spad + s, s, k16, true, d, prows, d, s, d, s, dq + pl, d,
+                          heads, 0, spad, 0, s, i64(s) * d, sched, ss);
+        // dK = dS^T Q: A = dS MN-major (K = queries: zero pad rows), B = Q MN-major
+        gemm_bf16_batched(dS, true, sp, i64(heads) * spad, s, q16, true, d, prows, d, s, d, s, dk + pl, d, heads, 0,
+                          spad, 0, s, i64(s) * d, sched, ss);
     }
     for (int i = 0; i < ws.n; ++i) {
         SWF_CUDA(cudaEventRecord(ws.ev[1 + i], ws.st[i]));

@@ -400,14 +400,14 @@ __device__ __forceinline__ void epi_qkv32(const EpiParams& ep, const QkvRow& qr,
 // Attention backward (EPI_SMAX / EPI_DSM): 32 columns of one row of the s x s plane -> bf16 P or dS.
 template <int MODE>
 __device__ __forceinline__ void epi_attn_rows32(const EpiParams& ep, i64 m, int n0, const float* v, float* stg,
-                                                int lane) {
+                                                int lane, int bb) {
     if (n0 >= ep.N) return;  // warp-uniform
     const bool ok = m < ep.M;
     uint4 u[4];
     __nv_bfloat16* dst = nullptr;
     if (ok) {
         float o[32];
-        const float rv = ep.rowv[m];
+        const float rv = ep.rowv[i64(bb) * ep.bst_rv + m];
         if constexpr (MODE == EPI_SMAX) {
             const int lo = (ep.masked && m >= ep.split) ? ep.split : 0;
             const int hi = (ep.masked && m < ep.split) ? ep.split : ep.N;
@@ -416,7 +416,7 @@ __device__ __forceinline__ void epi_attn_rows32(const EpiParams& ep, i64 m, int 
                 o[j] = (n0 + j >= lo && n0 + j < hi) ? exp2f(fmaf(v[j], ep.out_scale, -rv)) : 0.f;
         } else {
             const uint4* pr = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.pin) +
-                                                             m * ep.ld_out + n0);
+                                                             i64(bb) * ep.bst_p + m * ep.ld_out + n0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint4 pp = n0 + 8 * q < ep.N ? pr[q] : make_uint4(0, 0, 0, 0);
@@ -433,7 +433,7 @@ __device__ __forceinline__ void epi_attn_rows32(const EpiParams& ep, i64 m, int 
         for (int j = 0; j < 4; ++j)
             u[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]), pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
                               pack_bf16x2(o[8 * j + 4], o[8 * j + 5]), pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
-        dst = static_cast<__nv_bfloat16*>(ep.out) + m * ep.ld_out + n0;
+        dst = static_cast<__nv_bfloat16*>(ep.out) + i64(bb) * ep.bst_c + m * ep.ld_out + n0;
     } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) u[j] = make_uint4(0, 0, 0, 0);
@@ -545,7 +545,7 @@ __device__ __forceinline__ float epi32_v4(const EpiParams& ep, i64 row0, int n0,
 
 template <int MODE>
 __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, int n0, const float* v, float* stg,
-                                                 float* drow, __nv_bfloat16* dbrow, int lane) {
+                                                 float* drow, __nv_bfloat16* dbrow, int lane, float* xstore) {
     if constexpr ((MODE == EPI_RESID || MODE == EPI_ENCODE) && SWF_RESID_V4)
         if (ep.M - (row - lane) >= 32 && n0 + 32 <= ep.N && v4_aligned<MODE>(ep))
             return epi32_v4<MODE>(ep, row - lane, n0, v, stg, lane);
@@ -569,10 +569,10 @@ __device__ __forceinline__ float epi32_coalesced(const EpiParams& ep, i64 row, i
             }
             if (ep.nss) stg[rr * 33 + lane] = col_ok ? o : 0.f;
         }
-    } else if constexpr (MODE == EPI_STORE) {
+    } else if constexpr (MODE == EPI_STORE) {  // xstore: this problem's C (plane-batched launches)
 #pragma unroll
         for (int rr = 0; rr < 32; ++rr)
-            if (rr < mrem && col_ok) ep.x[(row0 + rr) * h + n] = stg[rr * 33 + lane];
+            if (rr < mrem && col_ok) xstore[(row0 + rr) * h + n] = stg[rr * 33 + lane];
     } else if (MODE == EPI_RESID && mrem >= 32 && n0 + 32 <= ep.N) {
         // out projection, full 32 x 32 chunk (the common case): in place, so the bf16 copy's rows are
         // addressed directly (no pointer shuffles) and no per-row predicates
@@ -722,7 +722,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool leader = crank == 0;
     const int cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
     const i64 m_tiles = (M + 2 * BM - 1) / (2 * BM);
-    const i64 total = m_tiles * n_tiles;
+    // plane-batched products (the attention backward's): tile t of problem t / per_b
+    constexpr bool kBatched = MODE == EPI_STORE || MODE == EPI_SMAX || MODE == EPI_DSM;
+    const i64 per_b = m_tiles * n_tiles;
+    const i64 total = kBatched ? per_b * max(1, ep.nbatch) : per_b;
 
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
@@ -765,10 +768,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int i = 0;; ++i) {
                 const i64 t = tq.next(i, true);
                 if (t < 0) break;
-                int m_blk, n_blk;
-                tile_coords(t, n_tiles, m_tiles, group_m, m_blk, n_blk);
-                const int row_a = m_blk * 2 * BM + int(crank) * BM;
-                const int row_b = n_blk * BN + int(crank) * (BN / 2);
+                int m_blk, n_blk, bb = 0;
+                if constexpr (kBatched) bb = int(t / per_b);
+                tile_coords(kBatched ? t - i64(bb) * per_b : t, n_tiles, m_tiles, group_m, m_blk, n_blk);
+                int row_a = m_blk * 2 * BM + int(crank) * BM, row_b = n_blk * BN + int(crank) * (BN / 2);
+                int ka = 0, kbo = 0;  // problem offsets along the operands' K coordinate
+                if constexpr (kBatched) {
+                    if constexpr (MN & 1) row_a += bb * ep.adx, ka = bb * ep.ady;
+                    else row_a += bb * ep.ady, ka = bb * ep.adx;
+                    if constexpr (MN & 2) row_b += bb * ep.bdx, kbo = bb * ep.bdy;
+                    else row_b += bb * ep.bdy, kbo = bb * ep.bdx;
+                }
                 for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = map_to_rank(smem_u32(&full_bar[stage]), 0);
@@ -777,17 +787,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int c = 0; c < BM / 64; ++c)
                             tma_load_2cta(smem_u32(sA + stage * C::kStageA + c * BK * 128), &tmA, fb, row_a + 64 * c,
-                                          kb * BK, pol_a);
+                                          kb * BK + ka, pol_a);
                     } else {
-                        tma_load_2cta(smem_u32(sA + stage * C::kStageA), &tmA, fb, kb * BK, row_a, pol_a);
+                        tma_load_2cta(smem_u32(sA + stage * C::kStageA), &tmA, fb, kb * BK + ka, row_a, pol_a);
                     }
                     if constexpr (MN & 2) {
 #pragma unroll
                         for (int c = 0; c < BN / 128; ++c)
                             tma_load_2cta(smem_u32(sB + stage * C::kStageB + c * BK * 128), &tmB, fb, row_b + 64 * c,
-                                          kb * BK, pol_b);
+                                          kb * BK + kbo, pol_b);
                     } else {
-                        tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK, row_b, pol_b);
+                        tma_load_2cta(smem_u32(sB + stage * C::kStageB), &tmB, fb, kb * BK + kbo, row_b, pol_b);
                     }
                     if (++stage == C::kStages) {
                         stage = 0;
@@ -874,9 +884,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int i = 0;; ++i) {
             const i64 t = tq.next(i, lane == 0);
             if (t < 0) break;
-            int m_blk, n_blk;
-            tile_coords(t, n_tiles, m_tiles, group_m, m_blk, n_blk);
-            const i64 row = i64(m_blk) * 2 * BM + crank * BM + q * 32 + lane;
+            int m_blk, n_blk, bb = 0;
+            if constexpr (kBatched) bb = int(t / per_b);
+            tile_coords(kBatched ? t - i64(bb) * per_b : t, n_tiles, m_tiles, group_m, m_blk, n_blk);
+            const i64 row = i64(m_blk) * 2 * BM + crank * BM + q * 32 + lane;  // row of problem bb
 #if SWF_GEMM_XPF
             // out projection (short K): pull this tile's rows of the residual x (this warp's half: BN/2
             // floats per row) into L2 while the accumulator is computed, so the epilogue's loads hit L2
@@ -957,7 +968,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int ch = half * NCH / 2; ch < (half + 1) * NCH / 2; ++ch) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
-                    ssum += epi32_coalesced<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, drow, dbrow, lane);
+                    ssum += epi32_coalesced<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, drow, dbrow, lane,
+                                                  MODE == EPI_STORE ? ep.x + i64(bb) * ep.bst_c : ep.x);
                 }
                 if (dsrow) dsrow[2 * n_blk + half] = ssum;
             } else {
@@ -971,7 +983,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if constexpr (MODE == EPI_QKV)
                         epi_qkv32(ep, qr, n_blk * BN + ch * 32, v, stg, lane);
                     else if constexpr (MODE == EPI_SMAX || MODE == EPI_DSM)
-                        epi_attn_rows32<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, lane);
+                        epi_attn_rows32<MODE>(ep, row, n_blk * BN + ch * 32, v, stg, lane, bb);
                     else
                         ssum += epi32<MODE>(ep, row, n_blk * BN + ch * 32, v);
                 }
@@ -1032,7 +1044,7 @@ void launch(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, const EpiP
     auto kern = k_gemm_tc<BN, MODE, MN>;  // shared-memory limit set per device by preload_gemm_kernels
     const int n_tiles = Npad / BN;
     const i64 m_tiles = (M + 2 * BM - 1) / (2 * BM);
-    const i64 total = m_tiles * n_tiles;
+    const i64 total = m_tiles * n_tiles * std::max(1, ep.nbatch);  // plane-batched launches: all problems
     int sms = 148;
     int clusters = int(std::min<i64>(total, sms / 2));
     // Rounds of the static schedule (tile t on cluster t mod clusters) cover whole M blocks when the
@@ -1214,16 +1226,55 @@ void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bf
         general_launch<EPI_STORE>(BN, mn, ta, tb, M, Np, Kp, ep, st);
 }
 
-void gemm_bf16_attn_rows(int mode, const __nv_bfloat16* A, i64 lda, const __nv_bfloat16* B, i64 ldb, int s, int K,
-                         __nv_bfloat16* out, int ldo, const float* rowv, const __nv_bfloat16* pin, int split,
-                         int masked, float scale, int* sched, cudaStream_t st) {
-    if (s <= 0 || K <= 0) return;
-    if (s % 8 != 0) throw CudaError("gemm_bf16_attn_rows: s must be a multiple of 8");
+void gemm_bf16_batched(const __nv_bfloat16* A, bool a_mn, i64 lda, i64 a_rows, i64 a_inner, const __nv_bfloat16* B,
+                       bool b_mn, i64 ldb, i64 b_rows, i64 b_inner, i64 M, i64 N, i64 K, float* C, i64 ldc, int nbatch,
+                       int adx, int ady, int bdx, int bdy, i64 bst_c, int* sched, cudaStream_t st) {
+    if (M <= 0 || N <= 0 || K <= 0 || nbatch <= 0) return;
+    if (a_mn && !b_mn) throw CudaError("gemm_bf16_batched: A MN-major with B K-major is not instantiated");
+    const int BN = N > 128 ? 256 : 128;
     TmaMap ta, tb;
-    make_tma_bf16_pitch(&ta, A, s, K, lda, BM);
-    make_tma_bf16_pitch(&tb, B, s, K, ldb, 128);
+    make_tma_bf16_pitch(&ta, A, a_rows, a_inner, lda, a_mn ? BK : BM);
+    make_tma_bf16_pitch(&tb, B, b_rows, b_inner, ldb, b_mn ? BK : BN / 2);
     EpiParams ep;
     std::memset(&ep, 0, sizeof ep);
+    ep.M = M;
+    ep.N = int(N);
+    ep.x = C;
+    ep.h = int(ldc);
+    ep.out_scale = 1.f;
+    ep.sched = sched;
+    ep.nbatch = nbatch;
+    ep.adx = adx;
+    ep.ady = ady;
+    ep.bdx = bdx;
+    ep.bdy = bdy;
+    ep.bst_c = bst_c;
+    const int Kp = int((K + BK - 1) / BK * BK);
+    const int Np = int((N + BN - 1) / BN * BN);
+    general_launch<EPI_STORE>(BN, (a_mn ? 1 : 0) | (b_mn ? 2 : 0), ta, tb, M, Np, Kp, ep, st);
+}
+
+void gemm_bf16_attn_rows(int mode, const __nv_bfloat16* A, i64 lda, const __nv_bfloat16* B, i64 ldb, int s, int K,
+                         __nv_bfloat16* out, int ldo, const float* rowv, const __nv_bfloat16* pin, int split,
+                         int masked, float scale, int* sched, cudaStream_t st, int nbatch, i64 a_rows_b,
+                         int a_col_b, i64 b_rows_b, i64 bst_out) {
+    if (s <= 0 || K <= 0) return;
+    if (s % 8 != 0) throw CudaError("gemm_bf16_attn_rows: s must be a multiple of 8");
+    nbatch = std::max(1, nbatch);
+    TmaMap ta, tb;
+    // K-major operands: A [rows][K (+ a_col_b per problem)], B [rows][K]; maps over all problems
+    make_tma_bf16_pitch(&ta, A, nbatch > 1 && a_rows_b ? (nbatch - 1) * a_rows_b + s : s,
+                        K + i64(nbatch - 1) * a_col_b, lda, BM);
+    make_tma_bf16_pitch(&tb, B, nbatch > 1 ? (nbatch - 1) * b_rows_b + s : s, K, ldb, 128);
+    EpiParams ep;
+    std::memset(&ep, 0, sizeof ep);
+    ep.nbatch = nbatch;
+    ep.adx = a_col_b;
+    ep.ady = int(a_rows_b);
+    ep.bdy = int(b_rows_b);
+    ep.bst_c = bst_out;
+    ep.bst_p = bst_out;
+    ep.bst_rv = s;
     ep.M = s;
     ep.N = s;
     ep.out = out;

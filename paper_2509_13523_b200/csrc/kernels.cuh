@@ -133,6 +133,12 @@ struct EpiParams {
     const float* rowv;
     const void* pin;
     int split, masked;
+    // plane-batched launches (EPI_STORE / EPI_SMAX / EPI_DSM only): nbatch problems of one shape; problem
+    // b shifts the A / B TMA coordinates by b (adx, ady) / (bdx, bdy) and the output (x or out), rowv and
+    // pin by b times bst_c, bst_rv, bst_p elements (nbatch 0 = 1)
+    int nbatch;
+    int adx, ady, bdx, bdy;
+    i64 bst_c, bst_rv, bst_p;
 };
 // inv_r[m] = 1 / sqrt(sum_i ss[m][i] / h + 1e-8) over the nss partials; non-finite rows flag
 // flags[slot] (check_finite, swin.hpp:295-300)
@@ -163,11 +169,21 @@ void gemm_bf16_tc(const TmaMap& A, const TmaMap& B, i64 M, int Npad, int K, int 
 // MN-major (B[k * ldb + n]) -- not A MN-major with B K-major; pitches multiples of 8 elements.
 void gemm_bf16_general(const __nv_bfloat16* A, bool a_mn, i64 lda, const __nv_bfloat16* B, bool b_mn, i64 ldb, i64 M,
                        i64 N, i64 K, float* C, i64 ldc, bool accumulate, int* sched, cudaStream_t st);
+// Plane-batched plain products: nbatch GEMMs C_b[M][N] = op(A_b) op(B_b) (fp32, pitch ldc), operand maps
+// over [a_rows][a_inner] / [b_rows][b_inner] (all problems), problem b at coordinate offsets b (adx, ady),
+// b (bdx, bdy) and C_b = C + b bst_c. No K-tail zero fill inside the maps: the caller keeps the K tails
+// of one operand zero (or inside the map's inner extent).
+void gemm_bf16_batched(const __nv_bfloat16* A, bool a_mn, i64 lda, i64 a_rows, i64 a_inner, const __nv_bfloat16* B,
+                       bool b_mn, i64 ldb, i64 b_rows, i64 b_inner, i64 M, i64 N, i64 K, float* C, i64 ldc, int nbatch,
+                       int adx, int ady, int bdx, int bdy, i64 bst_c, int* sched, cudaStream_t st);
 // The attention backward's row-wise products (both operands K-major, s x s output in bf16, pitch ldo):
 // mode EPI_SMAX: out = P from S = A . B^T; EPI_DSM: out = dS from dP = A . B^T (see EpiMode)
+// nbatch > 1: problems b = 0.. at A / B row offsets b a_rows_b / b b_rows_b (maps over nbatch of them),
+// out / pin + b bst_out, rowv + b s; a_col_b: A column offset per problem instead (dO's head columns)
 void gemm_bf16_attn_rows(int mode, const __nv_bfloat16* A, i64 lda, const __nv_bfloat16* B, i64 ldb, int s, int K,
                          __nv_bfloat16* out, int ldo, const float* rowv, const __nv_bfloat16* pin, int split,
-                         int masked, float scale, int* sched, cudaStream_t st);
+                         int masked, float scale, int* sched, cudaStream_t st, int nbatch = 1, i64 a_rows_b = 0,
+                         int a_col_b = 0, i64 b_rows_b = 0, i64 bst_out = 0);
 
 // ------------------------------------------------------------------ attention
 struct AttnParams {
@@ -205,9 +221,9 @@ void vt_bf16(const float* v, i64 planes, int s, int d, __nv_bfloat16* vt, cudaSt
 // attention backward on the tensor cores (BF16 training mode): per (window, head) plane, five tcgen05
 // GEMMs -- P from S = Q K^T in the GEMM's epilogue with the forward's log2-sum-exp `lse`, dS from
 // dP = dO V^T in the next one's with D = rowsum(dO . O) (one pass over all planes into `Dbuf`,
-// [nloc][heads][s]); scratch of attention_bwd_tc_scratch(s) bytes, qkv16 3 M h and dO16 M ldo bf16
+// [nloc][heads][s]); one window's heads per (plane-batched) launch; scratch of attention_bwd_tc_scratch(s, heads) bytes, qkv16 3 M h and dO16 M ldo bf16
 // elements; d % 8 == 0, s % 8 == 0
-size_t attention_bwd_tc_scratch(int s);
+size_t attention_bwd_tc_scratch(int s, int heads);
 struct AttnBwdStreams {  // worker streams of the per-plane loop, each with scratch and a GEMM tile counter
     static constexpr int kMax = 4;
     int n = 0;
