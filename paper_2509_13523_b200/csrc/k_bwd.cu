@@ -117,6 +117,7 @@ __global__ void k_norm_bwd_rows(const float* __restrict__ X, int ldx, const floa
     const float* x = X + j * ldx;
     const float* dxm = dXM + j * lddxm;
     float ss = 0.f, xdu = 0.f;
+#pragma unroll 4
     for (int i = lane; i < h; i += 32) {
         ss = fmaf(x[i], x[i], ss);
         const float du = dxm[i] * (gate ? gate[i] : 1.f) * (a ? 1.f + a[i] : 1.f) * g[i];
@@ -127,6 +128,7 @@ __global__ void k_norm_bwd_rows(const float* __restrict__ X, int ldx, const floa
     const float r = sqrtf(ss / float(h) + 1e-8f);
     const float c = xdu / (float(h) * r * r * r);
     float* dx = dX + j * lddx;
+#pragma unroll 4
     for (int i = lane; i < h; i += 32) {
         const float du = dxm[i] * (gate ? gate[i] : 1.f) * (a ? 1.f + a[i] : 1.f) * g[i];
         dx[i] += du / r - x[i] * c;
@@ -148,15 +150,27 @@ __global__ void k_norm_bwd_cols(const float* __restrict__ X, int ldx, const floa
     const float gi = g[i], ai = a ? a[i] : 0.f, bi = b ? b[i] : 0.f, qi = gate ? gate[i] : 1.f;
     float sg = 0.f, sa = 0.f, sb = 0.f, sq = 0.f;
     const i64 j1 = M * (sl + 1) / S;
-    for (i64 j = M * sl / S; j < j1; ++j) {
-        const float u = X[j * ldx + i] / rms[j];
-        const float dxm = dXM[j * lddxm + i];
+    auto acc = [&](float xv, float r, float dxm) {
+        const float u = xv / r;
         const float gu = gi * u;
         sa = fmaf(dxm * qi, gu, sa);
         sb = fmaf(dxm, qi, sb);
         sq = fmaf(dxm, gu * (1.f + ai) + bi, sq);
         sg = fmaf(dxm * qi * (1.f + ai), u, sg);
+    };
+    i64 j = M * sl / S;
+    for (; j + 4 <= j1; j += 4) {  // 4 tokens' loads in flight, accumulated in token order
+        float xv[4], r[4], dv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            xv[e] = X[(j + e) * ldx + i];
+            r[e] = rms[j + e];
+            dv[e] = dXM[(j + e) * lddxm + i];
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc(xv[e], r[e], dv[e]);
     }
+    for (; j < j1; ++j) acc(X[j * ldx + i], rms[j], dXM[j * lddxm + i]);
     float* pt = part + size_t(sl) * 4 * h;
     pt[i] = sg;
     pt[h + i] = sa;
@@ -186,7 +200,15 @@ __global__ void k_colsum(const float* __restrict__ X, int ldx, i64 M, int n, int
     if (i >= n) return;
     float s = 0.f;
     const i64 j1 = M * (sl + 1) / S;
-    for (i64 j = M * sl / S; j < j1; ++j) s += X[j * ldx + i];
+    i64 j = M * sl / S;
+    for (; j + 4 <= j1; j += 4) {  // 4 loads in flight, summed in token order
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = X[(j + e) * ldx + i];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s += v[e];
+    }
+    for (; j < j1; ++j) s += X[j * ldx + i];
     part[size_t(sl) * n + i] = s;
 }
 __global__ void k_colsum_sum(const float* __restrict__ part, int S, int n, float* __restrict__ out) {
